@@ -1,0 +1,393 @@
+// TEST INFRASTRUCTURE ONLY -- never linked into the product.
+//
+// C-ABI adapter (include/slos_planner.h) over the UNMODIFIED reference planner.
+// Built by oracle/Makefile together with the reference's own sources, read in
+// place from /root/reference/proj/src, into oracle/_ref/libslos_ref.so. It is the
+// parity anchor for the C restatement (oracle/slos_oracle.c) and the
+// `cpu_baseline.kind = "reference"` arm of bench.py.
+//
+// Each entry point forwards to the reference function it is named after:
+//   slos_plan            -> SloScheduler::schedule / schedule_throughput  dp_scheduler.cpp:360-362
+//   slos_tile_gap_batch  -> BatchPlanner::tile_gap_ar / tile_gap / prefill_budget
+//                           batch_planner.cpp:152, 315, 408
+//   slos_time2bs_batch   -> PerfModel::time2bs  perf_model.cpp:116
+//   slos_predict_batch   -> PerfModel::predict  perf_model.cpp:106
+//   slos_solve_spec_lengths -> solve_spec_lengths batch_planner.cpp:51
+//   slos_expected_accepted  -> expected_accepted  batch_planner.cpp:32
+
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "slos_planner.h"
+#include "slosim/batch_planner.hpp"
+#include "slosim/common.hpp"
+#include "slosim/dp_scheduler.hpp"
+#include "slosim/perf_model.hpp"
+#include "slosim/workload.hpp"
+
+using namespace slosim;
+
+struct slos_planner {
+  PerfModel model;
+  SloConfig slo;
+  PlannerConfig cfg;
+  std::unique_ptr<BatchPlanner> planner;
+  std::unique_ptr<SloScheduler> sched;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int status_of(const Error& e) {
+  if (e.code() == "invalid-parameters") return SLOS_ERR_INVALID_PARAMETERS;
+  if (e.code() == "internal-inconsistency") return SLOS_ERR_INTERNAL_INCONSISTENCY;
+  if (e.code() == "infeasible-budget") return SLOS_ERR_INFEASIBLE_BUDGET;
+  return SLOS_ERR_INVALID_PARAMETERS;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return status_of(e);
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SLOS_ERR_INVALID_PARAMETERS;
+  }
+}
+
+ScheduleInput to_input(const slos_input* in) {
+  ScheduleInput s;
+  s.now = in->now;
+  s.memory_total = in->memory_total;
+  s.memory_standard_resident = in->memory_standard_resident;
+  s.tail_horizon_s = in->tail_horizon_s;
+  s.running.reserve(in->n_running);
+  for (int i = 0; i < in->n_running; ++i) {
+    const slos_running& r = in->running[i];
+    RunningRequest rr;
+    rr.id = r.id;
+    rr.prefill_remaining = r.prefill_remaining;
+    rr.prefill_deadline = r.prefill_deadline;
+    rr.decode_tier = r.decode_tier;
+    rr.next_due_s = r.next_due_s;
+    rr.backlog = r.backlog;
+    rr.decode_remaining = r.decode_remaining;
+    s.running.push_back(std::move(rr));
+  }
+  s.pending.reserve(in->n_pending);
+  for (int i = 0; i < in->n_pending; ++i) {
+    const slos_pending& p = in->pending[i];
+    PendingRequest pp;
+    pp.id = p.id;
+    pp.prefill_deadline = p.prefill_deadline;
+    pp.prefill_tokens = p.prefill_tokens;
+    pp.decode_tier = p.decode_tier;
+    pp.memory_units = p.memory_units;
+    pp.value = p.value;
+    s.pending.push_back(std::move(pp));
+  }
+  return s;
+}
+
+// One malloc per result; every array points into it.
+void fill_result(const slos_input* in, const ScheduleResult& res, slos_result* out) {
+  std::unordered_map<std::string, int32_t> ref;
+  for (int i = 0; i < in->n_running; ++i) ref.emplace(in->running[i].id, i);
+  for (int i = 0; i < in->n_pending; ++i) ref.emplace(in->pending[i].id, SLOS_PENDING_REF(i));
+  size_t n_entries = 0;
+  for (const auto& b : res.plan.batches) n_entries += b.entries.size();
+  const size_t n_adm = res.admitted.size(), n_dec = res.declined.size(),
+               n_def = res.deferred.size(), n_b = res.plan.batches.size();
+  size_t bytes = sizeof(slos_batch) * n_b + sizeof(slos_entry) * n_entries +
+                 sizeof(int32_t) * (n_adm + n_dec + n_def) + 64;
+  char* mem = static_cast<char*>(std::calloc(1, bytes));
+  slos_batch* batches = reinterpret_cast<slos_batch*>(mem);
+  slos_entry* entries = reinterpret_cast<slos_entry*>(batches + n_b);
+  int32_t* ids = reinterpret_cast<int32_t*>(entries + n_entries);
+  auto pidx = [&](const std::string& id) { return -ref.at(id) - 1; };
+  for (size_t k = 0; k < n_adm; ++k) ids[k] = pidx(res.admitted[k]);
+  for (size_t k = 0; k < n_dec; ++k) ids[n_adm + k] = pidx(res.declined[k]);
+  for (size_t k = 0; k < n_def; ++k) ids[n_adm + n_dec + k] = pidx(res.deferred[k]);
+  size_t e = 0;
+  for (size_t k = 0; k < n_b; ++k) {
+    const PlanBatch& b = res.plan.batches[k];
+    batches[k].start_s = b.start_s;
+    batches[k].end_s = b.end_s;
+    batches[k].capacity_tokens = b.capacity_tokens;
+    batches[k].spec_step = b.spec_step;
+    batches[k].prefill_budget_left = b.prefill_budget_left;
+    batches[k].first_entry = (int64_t)e;
+    batches[k].n_entries = (int64_t)b.entries.size();
+    for (const PlanEntry& pe : b.entries) {
+      entries[e].req = ref.at(pe.id);
+      entries[e].spec_len = pe.spec_len;
+      entries[e].prefill_tokens = pe.prefill_tokens;
+      entries[e].decode_tokens = pe.decode_tokens;
+      ++e;
+    }
+  }
+  out->status = SLOS_OK;
+  out->running_set_infeasible = res.running_set_infeasible ? 1 : 0;
+  out->admitted_value = res.admitted_value;
+  out->n_admitted = (int32_t)n_adm;
+  out->n_declined = (int32_t)n_dec;
+  out->n_deferred = (int32_t)n_def;
+  out->admitted = ids;
+  out->declined = ids + n_adm;
+  out->deferred = ids + n_adm + n_dec;
+  out->n_batches = (int64_t)n_b;
+  out->batches = batches;
+  out->n_entries = (int64_t)n_entries;
+  out->entries = entries;
+  out->exact_until_s = res.plan.exact_until_s;
+  std::memset(&out->counters, 0, sizeof(out->counters));
+  out->owner_ = mem;
+}
+
+DecodeCensus to_census(const slos_gap_query& q, int num_tiers) {
+  DecodeCensus c;
+  c.counts_per_tier.assign(q.counts_per_tier, q.counts_per_tier + num_tiers);
+  if (q.mode != SLOS_GAP_PREFILL_BUDGET) {
+    for (int i = 0; i < q.n_exact; ++i) {
+      DecodeMember m;
+      m.tier = q.exact[i].tier;
+      m.owner = q.exact[i].owner;
+      m.phase_s = q.exact[i].phase_s;
+      m.backlog = q.exact[i].backlog;
+      m.remaining = q.exact[i].remaining;
+      c.exact.push_back(m);
+    }
+  }
+  return c;
+}
+
+void fill_gap(const std::optional<GapPlan>& gp, int num_tiers, slos_gap_result* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->status = SLOS_OK;
+  if (!gp) return;
+  out->feasible = 1;
+  out->prefill_budget = gp->prefill_budget;
+  out->n_spec_lengths = (int32_t)gp->spec_lengths.size();
+  for (size_t l = 0; l < gp->spec_lengths.size() && l < SLOS_MAX_TIERS; ++l)
+    out->spec_lengths[l] = gp->spec_lengths[l];
+  size_t pairs = 0;
+  for (const auto& b : gp->batches) pairs += b.decode_by_owner.size();
+  const size_t n_b = gp->batches.size();
+  char* mem = static_cast<char*>(
+      std::calloc(1, sizeof(slos_gap_batch) * n_b + sizeof(int64_t) * 2 * pairs + 64));
+  slos_gap_batch* bs = reinterpret_cast<slos_gap_batch*>(mem);
+  int64_t* own = reinterpret_cast<int64_t*>(bs + n_b);
+  size_t p = 0;
+  for (size_t k = 0; k < n_b; ++k) {
+    const PlannedBatch& b = gp->batches[k];
+    bs[k].start_s = b.start_s;
+    bs[k].end_s = b.end_s;
+    bs[k].capacity_tokens = b.capacity_tokens;
+    bs[k].spec_step = b.spec_step;
+    bs[k].decode_tokens = b.decode_tokens;
+    bs[k].prefill_budget = b.prefill_budget;
+    for (size_t l = 0; l < b.decode_per_tier.size() && l < (size_t)num_tiers; ++l)
+      bs[k].decode_per_tier[l] = b.decode_per_tier[l];
+    bs[k].first_owner = (int64_t)p;
+    bs[k].n_owners = (int64_t)b.decode_by_owner.size();
+    for (const auto& [o, t] : b.decode_by_owner) {
+      own[2 * p] = o;
+      own[2 * p + 1] = t;
+      ++p;
+    }
+  }
+  out->n_batches = (int64_t)n_b;
+  out->batches = bs;
+  out->n_owner_pairs = (int64_t)pairs;
+  out->owner_tokens = own;
+  out->owner_ = mem;
+}
+
+}  // namespace
+
+extern "C" {
+
+void slos_planner_config_default(slos_planner_config* cfg) {
+  PlannerConfig d;
+  cfg->max_chunk_tokens = d.max_chunk_tokens;
+  cfg->max_batch_tokens = d.max_batch_tokens;
+  cfg->speculative = d.speculative ? 1 : 0;
+  cfg->spec_max_len = d.spec_max_len;
+  cfg->spec_alpha = d.spec_alpha;
+  cfg->plan_margin = d.plan_margin;
+}
+
+int slos_planner_create(const slos_perf_term* terms, int32_t n_terms, const double* tpot,
+                        const double* slow, int32_t n_tiers, int32_t tpot_window,
+                        const slos_planner_config* cfg, slos_planner** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto p = std::make_unique<slos_planner>();
+    std::vector<PerfTerm> t;
+    for (int i = 0; i < n_terms; ++i) t.push_back({terms[i].k1, terms[i].k2, terms[i].b});
+    p->model = PerfModel(t);
+    p->slo.tpot_tiers_s.assign(tpot, tpot + n_tiers);
+    p->slo.ttft_slowdowns.assign(slow, slow + n_tiers);
+    p->slo.tpot_window = tpot_window;
+    slos_planner_config c;
+    if (cfg) c = *cfg; else slos_planner_config_default(&c);
+    p->cfg.max_chunk_tokens = c.max_chunk_tokens;
+    p->cfg.max_batch_tokens = c.max_batch_tokens;
+    p->cfg.speculative = c.speculative != 0;
+    p->cfg.spec_alpha = c.spec_alpha;
+    p->cfg.spec_max_len = c.spec_max_len;
+    p->cfg.plan_margin = c.plan_margin;
+    p->planner = std::make_unique<BatchPlanner>(p->model, p->slo, p->cfg);
+    p->sched = std::make_unique<SloScheduler>(*p->planner);
+    *out = p.release();
+    return SLOS_OK;
+  });
+}
+
+void slos_planner_destroy(slos_planner* p) { delete p; }
+
+int slos_plan(slos_planner* p, const slos_input* in, int32_t unit_value, slos_result* out) {
+  std::memset(out, 0, sizeof(*out));
+  int st = guarded([&] {
+    ScheduleInput s = to_input(in);
+    ScheduleResult r = unit_value ? p->sched->schedule_throughput(s) : p->sched->schedule(s);
+    fill_result(in, r, out);
+    return SLOS_OK;
+  });
+  out->status = st;
+  return st;
+}
+
+// Reference CPU batch: a std::thread pool over all host cores, one planner per
+// instance handle. Handles shared between instances are
+// serialised by giving each worker its own private copy of the planner.
+int slos_plan_batch(slos_planner* const* planners, int32_t n, const slos_input* inputs,
+                    int32_t unit_value, slos_result* outs, void* /*stream*/) {
+  const char* env = std::getenv("SLOS_REF_THREADS");
+  int workers = env ? std::atoi(env) : (int)std::thread::hardware_concurrency();
+  if (workers < 1) workers = 1;
+  std::vector<std::thread> pool;
+  std::atomic<int> next{0};
+  for (int w = 0; w < workers; ++w) {
+    pool.emplace_back([&] {
+      std::unordered_map<const slos_planner*, std::unique_ptr<slos_planner>> own;
+      for (int k = next.fetch_add(1); k < n; k = next.fetch_add(1)) {
+        const slos_planner* src = planners[k];
+        auto& mine = own[src];
+        if (!mine) {
+          mine = std::make_unique<slos_planner>();
+          mine->model = src->model;
+          mine->slo = src->slo;
+          mine->cfg = src->cfg;
+          mine->planner = std::make_unique<BatchPlanner>(mine->model, mine->slo, mine->cfg);
+          mine->sched = std::make_unique<SloScheduler>(*mine->planner);
+        }
+        slos_plan(mine.get(), &inputs[k], unit_value, &outs[k]);
+      }
+    });
+  }
+  for (auto& t : pool) t.join();
+  return SLOS_OK;
+}
+
+void slos_result_free(slos_result* r) {
+  if (r && r->owner_) std::free(r->owner_);
+  if (r) std::memset(r, 0, sizeof(*r));
+}
+
+int slos_tile_gap_batch(slos_planner* p, int32_t n, const slos_gap_query* q,
+                        slos_gap_result* outs) {
+  const int L = p->slo.num_tiers();
+  for (int k = 0; k < n; ++k) {
+    int st = guarded([&] {
+      DecodeCensus c = to_census(q[k], L);
+      if (q[k].mode == SLOS_GAP_TILE_AR) {
+        fill_gap(p->planner->tile_gap_ar(q[k].gap_s, c, q[k].due_horizon_s), L, &outs[k]);
+      } else if (q[k].mode == SLOS_GAP_TILE) {
+        fill_gap(p->planner->tile_gap(q[k].gap_s, c, q[k].due_horizon_s), L, &outs[k]);
+      } else {
+        auto b = p->planner->prefill_budget(q[k].gap_s, c.counts_per_tier);
+        std::memset(&outs[k], 0, sizeof(outs[k]));
+        outs[k].feasible = b.has_value();
+        outs[k].prefill_budget = b ? *b : 0;
+      }
+      return SLOS_OK;
+    });
+    if (st != SLOS_OK) {
+      std::memset(&outs[k], 0, sizeof(outs[k]));
+      outs[k].status = st;
+    }
+  }
+  return SLOS_OK;
+}
+
+void slos_gap_result_free(slos_gap_result* r) {
+  if (r && r->owner_) std::free(r->owner_);
+  if (r) std::memset(r, 0, sizeof(*r));
+}
+
+int slos_time2bs_batch(slos_planner* p, int32_t n, const double* budget, const int64_t* spec,
+                       int64_t max_tokens, int64_t* out, int32_t* status) {
+  for (int k = 0; k < n; ++k) {
+    out[k] = 0;
+    status[k] = guarded([&] {
+      out[k] = p->model.time2bs(budget[k], spec ? spec[k] : 0, max_tokens);
+      return SLOS_OK;
+    });
+  }
+  return SLOS_OK;
+}
+
+int slos_predict_batch(slos_planner* p, int32_t n, const int64_t* tokens, const int64_t* spec,
+                       double* out) {
+  return guarded([&] {
+    for (int k = 0; k < n; ++k) out[k] = p->model.predict(tokens[k], spec ? spec[k] : 0);
+    return SLOS_OK;
+  });
+}
+
+int slos_solve_spec_lengths(slos_planner* p, const int64_t* counts, int32_t n_tiers, double alpha,
+                            int32_t max_len, slos_spec_plan* out) {
+  std::memset(out, 0, sizeof(*out));
+  return guarded([&] {
+    std::vector<int64_t> c(counts, counts + n_tiers);
+    auto sp = solve_spec_lengths(c, alpha, max_len, p->model, p->slo, p->cfg);
+    if (sp) {
+      out->feasible = 1;
+      for (size_t l = 0; l < sp->lengths.size() && l < SLOS_MAX_TIERS; ++l)
+        out->lengths[l] = sp->lengths[l];
+      out->batch_time_s = sp->batch_time_s;
+      out->batch_capacity = sp->batch_capacity;
+      out->decode_tokens = sp->decode_tokens;
+      out->prefill_throughput = sp->prefill_throughput;
+    }
+    return SLOS_OK;
+  });
+}
+
+double slos_expected_accepted(double alpha, int32_t sl) { return expected_accepted(alpha, sl); }
+
+const char* slos_status_slug(int s) {
+  switch (s) {
+    case SLOS_OK: return "ok";
+    case SLOS_ERR_INVALID_PARAMETERS: return "invalid-parameters";
+    case SLOS_ERR_INTERNAL_INCONSISTENCY: return "internal-inconsistency";
+    case SLOS_ERR_INFEASIBLE_BUDGET: return "infeasible-budget";
+    default: return "error";
+  }
+}
+
+const char* slos_last_error(void) { return g_last_error.c_str(); }
+const char* slos_backend(void) { return "reference-cpp"; }
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// TEST INFRASTRUCTURE ONLY -- never linked into the product.
+//
+// Extra exports of oracle/_ref/libslos_ref.so used to generate and pin golden
+// fixtures (tests/golden/, written by oracle/make_golden.py):
+//   slos_ref_uniforms          std::mt19937_64 + std::uniform_real_distribution<double>(0,1),
+//                              the draw sequence of the reference's stress generator
+//                              (acceptance_main.cpp:577-605); pins our C generator.
+//   slos_ref_oracle_instances  the reference's brute-force instance generator
+//                              (tests/oracle.cpp:67-102) serialised as int64 records.
+//   slos_ref_oracle_best_value / slos_ref_oracle_subset_feasible
+//                              tests/oracle.cpp:8-65 on such a record.
+
+#include <cstdint>
+#include <random>
+#include <vector>
+
+#include "oracle.hpp"
+
+using namespace slosim;
+
+namespace {
+
+constexpr int kRec = 41;  // see encode()
+
+void encode(const oracle::Instance& in, int64_t* r) {
+  for (int k = 0; k < kRec; ++k) r[k] = 0;
+  r[0] = in.cap;
+  r[1] = (int64_t)in.tpots.size();
+  for (size_t l = 0; l < in.tpots.size() && l < 2; ++l) r[2 + l] = in.tpots[l];
+  r[4] = (int64_t)in.runners.size();
+  for (size_t j = 0; j < in.runners.size() && j < 3; ++j) r[5 + j] = in.runners[j].tier;
+  r[8] = (int64_t)in.candidates.size();
+  for (size_t i = 0; i < in.candidates.size() && i < 6; ++i) {
+    const auto& c = in.candidates[i];
+    r[9 + 5 * i + 0] = c.deadline;
+    r[9 + 5 * i + 1] = c.prefill;
+    r[9 + 5 * i + 2] = c.tier;
+    r[9 + 5 * i + 3] = c.memory;
+    r[9 + 5 * i + 4] = (int64_t)c.value;
+  }
+  r[39] = in.memory_total;
+  r[40] = in.horizon;
+}
+
+oracle::Instance decode(const int64_t* r) {
+  oracle::Instance in;
+  in.cap = (int)r[0];
+  for (int l = 0; l < r[1]; ++l) in.tpots.push_back((int)r[2 + l]);
+  for (int j = 0; j < r[4]; ++j) in.runners.push_back({(int)r[5 + j]});
+  for (int i = 0; i < r[8]; ++i) {
+    oracle::Instance::Candidate c;
+    c.deadline = (int)r[9 + 5 * i];
+    c.prefill = (int)r[9 + 5 * i + 1];
+    c.tier = (int)r[9 + 5 * i + 2];
+    c.memory = r[9 + 5 * i + 3];
+    c.value = (double)r[9 + 5 * i + 4];
+    in.candidates.push_back(c);
+  }
+  in.memory_total = r[39];
+  in.horizon = (int)r[40];
+  return in;
+}
+
+}  // namespace
+
+extern "C" {
+
+int slos_ref_oracle_record_len(void) { return kRec; }
+
+void slos_ref_uniforms(uint64_t seed, int32_t n, double* out) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u(0.0, 1.0);
+  for (int i = 0; i < n; ++i) out[i] = u(rng);
+}
+
+void slos_ref_oracle_instances(uint64_t seed, int32_t count, int64_t* records) {
+  std::mt19937_64 rng(seed);
+  for (int i = 0; i < count; ++i) encode(oracle::random_instance(rng), records + (size_t)i * kRec);
+}
+
+double slos_ref_oracle_best_value(const int64_t* record) {
+  return oracle::best_value(decode(record));
+}
+
+int32_t slos_ref_oracle_subset_feasible(const int64_t* record, const int32_t* admitted,
+                                        int32_t n) {
+  std::vector<int> a(admitted, admitted + n);
+  return oracle::subset_feasible(decode(record), a) ? 1 : 0;
+}
+
+}  // extern "C"

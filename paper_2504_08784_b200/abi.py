@@ -1,0 +1,350 @@
+"""ctypes mirror of include/slos_planner.h (the C-ABI drop-in boundary).
+
+The same declarations bind all three libraries that export the ABI:
+  * the product ``libslos_b200.so`` (CUDA kernels + C++ host shim),
+  * the test-only C oracle ``oracle/liboracle_slos.so``,
+  * the test-only reference adapter ``oracle/_ref/libslos_ref.so``.
+Only tests/, bench.py's cpu_baseline leg and __graft_entry__.smoke() ever load
+the latter two.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.dirname(os.path.abspath(__file__))
+
+PRODUCT_LIB = os.path.join(PKG, "libslos_b200.so")
+WORKLOAD_LIB = os.path.join(PKG, "libslos_workload.so")
+ORACLE_LIB = os.path.join(ROOT, "oracle", "liboracle_slos.so")
+REF_LIB = os.path.join(ROOT, "oracle", "_ref", "libslos_ref.so")
+
+MAX_TIERS = 8
+
+SLOS_OK = 0
+SLOS_ERR_INVALID_PARAMETERS = 1
+SLOS_ERR_INTERNAL_INCONSISTENCY = 2
+SLOS_ERR_INFEASIBLE_BUDGET = 3
+SLOS_ERR_CUDA = 10
+SLOS_ERR_CAPACITY = 11
+SLOS_ERR_NO_DEVICE = 12
+SLOS_ERR_ALLOC = 13
+SLOS_ERR_RANGE = 14
+
+SLUGS = {
+    SLOS_ERR_INVALID_PARAMETERS: "invalid-parameters",
+    SLOS_ERR_INTERNAL_INCONSISTENCY: "internal-inconsistency",
+    SLOS_ERR_INFEASIBLE_BUDGET: "infeasible-budget",
+}
+
+GAP_TILE_AR, GAP_TILE, GAP_PREFILL_BUDGET = 0, 1, 2
+
+
+class PerfTerm(C.Structure):
+    _fields_ = [("k1", C.c_double), ("k2", C.c_double), ("b", C.c_double)]
+
+
+class PlannerConfigC(C.Structure):
+    _fields_ = [
+        ("max_chunk_tokens", C.c_int64),
+        ("max_batch_tokens", C.c_int64),
+        ("speculative", C.c_int32),
+        ("spec_max_len", C.c_int32),
+        ("spec_alpha", C.c_double),
+        ("plan_margin", C.c_double),
+    ]
+
+
+class Running(C.Structure):
+    _fields_ = [
+        ("id", C.c_char_p),
+        ("prefill_remaining", C.c_int64),
+        ("prefill_deadline", C.c_double),
+        ("decode_tier", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("next_due_s", C.c_double),
+        ("backlog", C.c_int64),
+        ("decode_remaining", C.c_int64),
+    ]
+
+
+class Pending(C.Structure):
+    _fields_ = [
+        ("id", C.c_char_p),
+        ("prefill_deadline", C.c_double),
+        ("prefill_tokens", C.c_int64),
+        ("decode_tier", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("memory_units", C.c_int64),
+        ("value", C.c_double),
+    ]
+
+
+class Input(C.Structure):
+    _fields_ = [
+        ("now", C.c_double),
+        ("running", C.POINTER(Running)),
+        ("n_running", C.c_int32),
+        ("n_pending", C.c_int32),
+        ("pending", C.POINTER(Pending)),
+        ("memory_total", C.c_int64),
+        ("memory_standard_resident", C.c_int64),
+        ("tail_horizon_s", C.c_double),
+    ]
+
+
+class Entry(C.Structure):
+    _fields_ = [
+        ("req", C.c_int32),
+        ("spec_len", C.c_int32),
+        ("prefill_tokens", C.c_int64),
+        ("decode_tokens", C.c_int64),
+    ]
+
+
+class Batch(C.Structure):
+    _fields_ = [
+        ("start_s", C.c_double),
+        ("end_s", C.c_double),
+        ("capacity_tokens", C.c_int64),
+        ("spec_step", C.c_int64),
+        ("prefill_budget_left", C.c_int64),
+        ("first_entry", C.c_int64),
+        ("n_entries", C.c_int64),
+    ]
+
+
+class Counters(C.Structure):
+    _fields_ = [
+        ("transitions", C.c_int64),
+        ("gap_evals", C.c_int64),
+        ("dues", C.c_int64),
+        ("slots", C.c_int64),
+        ("states", C.c_int64),
+    ]
+
+
+class Result(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32),
+        ("running_set_infeasible", C.c_int32),
+        ("admitted_value", C.c_double),
+        ("n_admitted", C.c_int32),
+        ("n_declined", C.c_int32),
+        ("n_deferred", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("admitted", C.POINTER(C.c_int32)),
+        ("declined", C.POINTER(C.c_int32)),
+        ("deferred", C.POINTER(C.c_int32)),
+        ("n_batches", C.c_int64),
+        ("batches", C.POINTER(Batch)),
+        ("n_entries", C.c_int64),
+        ("entries", C.POINTER(Entry)),
+        ("exact_until_s", C.c_double),
+        ("counters", Counters),
+        ("owner_", C.c_void_p),
+    ]
+
+
+class DecodeMemberC(C.Structure):
+    _fields_ = [
+        ("tier", C.c_int32),
+        ("owner", C.c_int32),
+        ("phase_s", C.c_double),
+        ("backlog", C.c_int64),
+        ("remaining", C.c_int64),
+    ]
+
+
+class GapQuery(C.Structure):
+    _fields_ = [
+        ("mode", C.c_int32),
+        ("n_exact", C.c_int32),
+        ("gap_s", C.c_double),
+        ("due_horizon_s", C.c_double),
+        ("counts_per_tier", C.c_int64 * MAX_TIERS),
+        ("exact", C.POINTER(DecodeMemberC)),
+    ]
+
+
+class GapBatch(C.Structure):
+    _fields_ = [
+        ("start_s", C.c_double),
+        ("end_s", C.c_double),
+        ("capacity_tokens", C.c_int64),
+        ("spec_step", C.c_int64),
+        ("decode_tokens", C.c_int64),
+        ("prefill_budget", C.c_int64),
+        ("decode_per_tier", C.c_int64 * MAX_TIERS),
+        ("first_owner", C.c_int64),
+        ("n_owners", C.c_int64),
+    ]
+
+
+class GapResult(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32),
+        ("feasible", C.c_int32),
+        ("prefill_budget", C.c_int64),
+        ("n_spec_lengths", C.c_int32),
+        ("spec_lengths", C.c_int32 * MAX_TIERS),
+        ("n_batches", C.c_int64),
+        ("batches", C.POINTER(GapBatch)),
+        ("n_owner_pairs", C.c_int64),
+        ("owner_tokens", C.POINTER(C.c_int64)),
+        ("owner_", C.c_void_p),
+    ]
+
+
+class SpecPlanC(C.Structure):
+    _fields_ = [
+        ("feasible", C.c_int32),
+        ("lengths", C.c_int32 * MAX_TIERS),
+        ("batch_time_s", C.c_double),
+        ("batch_capacity", C.c_int64),
+        ("decode_tokens", C.c_int64),
+        ("prefill_throughput", C.c_double),
+    ]
+
+
+# numpy views of the input structs (used to build large batches without
+# per-request Python objects: ids are pointers into one bytes blob).
+RUNNING_DTYPE = np.dtype(
+    {
+        "names": ["id", "prefill_remaining", "prefill_deadline", "decode_tier", "reserved0",
+                  "next_due_s", "backlog", "decode_remaining"],
+        "formats": [np.uint64, np.int64, np.float64, np.int32, np.int32, np.float64, np.int64,
+                    np.int64],
+        "offsets": [Running.id.offset, Running.prefill_remaining.offset,
+                    Running.prefill_deadline.offset, Running.decode_tier.offset,
+                    Running.reserved0.offset, Running.next_due_s.offset, Running.backlog.offset,
+                    Running.decode_remaining.offset],
+        "itemsize": C.sizeof(Running),
+    }
+)
+PENDING_DTYPE = np.dtype(
+    {
+        "names": ["id", "prefill_deadline", "prefill_tokens", "decode_tier", "reserved0",
+                  "memory_units", "value"],
+        "formats": [np.uint64, np.float64, np.int64, np.int32, np.int32, np.int64, np.float64],
+        "offsets": [Pending.id.offset, Pending.prefill_deadline.offset,
+                    Pending.prefill_tokens.offset, Pending.decode_tier.offset,
+                    Pending.reserved0.offset, Pending.memory_units.offset, Pending.value.offset],
+        "itemsize": C.sizeof(Pending),
+    }
+)
+INPUT_DTYPE = np.dtype(
+    {
+        "names": ["now", "running", "n_running", "n_pending", "pending", "memory_total",
+                  "memory_standard_resident", "tail_horizon_s"],
+        "formats": [np.float64, np.uint64, np.int32, np.int32, np.uint64, np.int64, np.int64,
+                    np.float64],
+        "offsets": [Input.now.offset, Input.running.offset, Input.n_running.offset,
+                    Input.n_pending.offset, Input.pending.offset, Input.memory_total.offset,
+                    Input.memory_standard_resident.offset, Input.tail_horizon_s.offset],
+        "itemsize": C.sizeof(Input),
+    }
+)
+ENTRY_DTYPE = np.dtype(
+    {
+        "names": ["req", "spec_len", "prefill_tokens", "decode_tokens"],
+        "formats": [np.int32, np.int32, np.int64, np.int64],
+        "offsets": [0, 4, 8, 16],
+        "itemsize": C.sizeof(Entry),
+    }
+)
+BATCH_DTYPE = np.dtype(
+    {
+        "names": ["start_s", "end_s", "capacity_tokens", "spec_step", "prefill_budget_left",
+                  "first_entry", "n_entries"],
+        "formats": [np.float64, np.float64, np.int64, np.int64, np.int64, np.int64, np.int64],
+        "offsets": [0, 8, 16, 24, 32, 40, 48],
+        "itemsize": C.sizeof(Batch),
+    }
+)
+
+_LIBS: dict[str, C.CDLL] = {}
+
+
+def _bind(lib: C.CDLL) -> C.CDLL:
+    P = C.POINTER
+    lib.slos_planner_config_default.argtypes = [P(PlannerConfigC)]
+    lib.slos_planner_config_default.restype = None
+    lib.slos_planner_create.argtypes = [P(PerfTerm), C.c_int32, P(C.c_double), P(C.c_double),
+                                        C.c_int32, C.c_int32, P(PlannerConfigC), P(C.c_void_p)]
+    lib.slos_planner_create.restype = C.c_int
+    lib.slos_planner_destroy.argtypes = [C.c_void_p]
+    lib.slos_planner_destroy.restype = None
+    lib.slos_plan.argtypes = [C.c_void_p, P(Input), C.c_int32, P(Result)]
+    lib.slos_plan.restype = C.c_int
+    lib.slos_plan_batch.argtypes = [P(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32, P(Result),
+                                    C.c_void_p]
+    lib.slos_plan_batch.restype = C.c_int
+    lib.slos_result_free.argtypes = [P(Result)]
+    lib.slos_result_free.restype = None
+    lib.slos_tile_gap_batch.argtypes = [C.c_void_p, C.c_int32, P(GapQuery), P(GapResult)]
+    lib.slos_tile_gap_batch.restype = C.c_int
+    lib.slos_gap_result_free.argtypes = [P(GapResult)]
+    lib.slos_gap_result_free.restype = None
+    lib.slos_time2bs_batch.argtypes = [C.c_void_p, C.c_int32, P(C.c_double), P(C.c_int64),
+                                       C.c_int64, P(C.c_int64), P(C.c_int32)]
+    lib.slos_time2bs_batch.restype = C.c_int
+    lib.slos_predict_batch.argtypes = [C.c_void_p, C.c_int32, P(C.c_int64), P(C.c_int64),
+                                       P(C.c_double)]
+    lib.slos_predict_batch.restype = C.c_int
+    lib.slos_solve_spec_lengths.argtypes = [C.c_void_p, P(C.c_int64), C.c_int32, C.c_double,
+                                            C.c_int32, P(SpecPlanC)]
+    lib.slos_solve_spec_lengths.restype = C.c_int
+    lib.slos_expected_accepted.argtypes = [C.c_double, C.c_int32]
+    lib.slos_expected_accepted.restype = C.c_double
+    lib.slos_status_slug.argtypes = [C.c_int]
+    lib.slos_status_slug.restype = C.c_char_p
+    lib.slos_last_error.argtypes = []
+    lib.slos_last_error.restype = C.c_char_p
+    lib.slos_backend.argtypes = []
+    lib.slos_backend.restype = C.c_char_p
+    return lib
+
+
+def load(path: str) -> C.CDLL:
+    """Load (once) and bind a library exporting include/slos_planner.h."""
+    path = os.path.abspath(path)
+    if path not in _LIBS:
+        if not os.path.exists(path):
+            raise FileNotFoundError(
+                f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        _LIBS[path] = _bind(C.CDLL(path))
+    return _LIBS[path]
+
+
+def product() -> C.CDLL:
+    """The product library. There is deliberately no CPU fallback: a missing
+    libslos_b200.so is an error, not a reason to use the oracle."""
+    return load(PRODUCT_LIB)
+
+
+def oracle() -> C.CDLL:  # test infrastructure only
+    return load(ORACLE_LIB)
+
+
+def reference() -> C.CDLL:  # test infrastructure only
+    return load(REF_LIB)
+
+
+def workload() -> C.CDLL:
+    path = os.path.abspath(WORKLOAD_LIB)
+    if path not in _LIBS:
+        lib = C.CDLL(path)
+        P = C.POINTER
+        lib.slos_wl_uniforms.argtypes = [C.c_uint64, C.c_int32, P(C.c_double)]
+        lib.slos_wl_uniforms.restype = None
+        lib.slos_wl_stress.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, P(C.c_double),
+                                       C.c_double, P(C.c_int32), P(C.c_double), P(C.c_int64),
+                                       P(C.c_double), P(C.c_int64), P(C.c_int32), P(C.c_int64),
+                                       P(C.c_double)]
+        lib.slos_wl_stress.restype = None
+        _LIBS[path] = lib
+    return _LIBS[path]
