@@ -1,0 +1,83 @@
+"""In-tree build of the native libraries (no JIT cache: the .so files travel to
+the GPU box with the repo snapshot).
+
+  libslos_b200.so      product: sm_100a kernels + C++ host shim (C-ABI)
+  libslos_workload.so  synthetic instance generator (benchmark/test input)
+Test infrastructure (oracle/Makefile): liboracle_slos.so, oracle/_ref/libslos_ref.so.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# -fmad=false: no FMA contraction (bit-exact fp64 vs the -O2 x86 reference)
+NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC",
+           "-Xcompiler", "-ffp-contract=off", "-diag-suppress", "550"]
+
+
+def _run(cmd, cwd=None):
+    r = subprocess.run(cmd, cwd=cwd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("build failed: " + " ".join(cmd))
+    return r
+
+
+def _stale(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build_product(force: bool = False, verbose: bool = False) -> str:
+    out = os.path.join(PKG, "libslos_b200.so")
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "slos_planner.h")]
+    if not force and not _stale(out, deps):
+        return out
+    bdir = os.path.join(PKG, "build")
+    os.makedirs(bdir, exist_ok=True)
+    ko = os.path.join(bdir, "slos_kernels.o")
+    ho = os.path.join(bdir, "slos_host.o")
+    k = _run([NVCC, *ARCH, *NVFLAGS, "-Xptxas", "-v", "-c", os.path.join(CSRC, "slos_kernels.cu"), "-o", ko])
+    if verbose:
+        sys.stderr.write(k.stderr)
+    _run([NVCC, *ARCH, *NVFLAGS, "-x", "cu", "-c", os.path.join(CSRC, "slos_host.cpp"), "-o", ho])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xlinker", "-Bsymbolic", ko, ho, "-o", out,
+          "-lpthread", "-ldl", "-lrt"])
+    return out
+
+
+def build_workload(force: bool = False) -> str:
+    out = os.path.join(PKG, "libslos_workload.so")
+    src = os.path.join(CSRC, "slos_workload.c")
+    if force or _stale(out, [src]):
+        _run(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", out, src, "-lm"])
+    return out
+
+
+def build_oracle(force: bool = False) -> str:
+    """Test-only checkers: the C restatement always, the compiled reference when
+    /root/reference is present (on the GPU box the prebuilt copy is used)."""
+    odir = os.path.join(ROOT, "oracle")
+    _run(["make", "-s", "-C", odir, "oracle"])
+    if os.path.isdir(os.environ.get("SLOS_REF", "/root/reference/proj")):
+        _run(["make", "-s", "-j8", "-C", odir, "ref"])
+    return os.path.join(odir, "liboracle_slos.so")
+
+
+def build_all(force: bool = False, verbose: bool = False) -> None:
+    build_workload(force)
+    build_oracle(force)
+    build_product(force, verbose)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, verbose=True)

@@ -1,0 +1,574 @@
+// Plan reconstruction kernel (K4): build_plan (dp_scheduler.cpp:196-354) and the
+// EDF fallback (:96-188), one CTA per instance, after the DP kernel.
+// Gaps are sequential (chain lines carry decode_assigned from gap to gap, :244,
+// :287); inside a gap everything is block-parallel (slos_gapblock.cuh).
+// Output batches are written in slos_batch layout and entries in slos_entry
+// layout so the host hands them to the caller without conversion.
+#pragma once
+
+#include "slos_gapblock.cuh"
+
+namespace slos {
+
+struct BuildParams {
+  BatchArgs a;
+};
+
+struct BuildShared {
+  BlockShared bs;
+  GapPlanBuf o, tmp;
+  PlannerDev P;
+  InstDev I;
+  double bounds[SLOS_MAX_CHAIN + 2];
+  int64_t m_left[SLOS_MAX_CHAIN + 1];
+  unsigned long long m_asg[SLOS_MAX_CHAIN + 1];
+  int32_t m_item[SLOS_MAX_CHAIN + 1];
+  int nb, nsel, edf, fill_late, err, m1;
+  int64_t n_batch, n_entry;
+  double tail_len;
+};
+
+// members_at(running, now, at, pull) compacted in decoder (= owner) order.
+__device__ inline int build_members_at(const BatchArgs& A, BuildShared& sh, double at, double pull,
+                                       const MemBuf& E) {
+  const InstDev& I = sh.I;
+  int64_t carry = 0;
+  for (int base = 0; base < I.n_dec; base += kBT) {
+    const int k = base + threadIdx.x;
+    Member m;
+    m.valid = false;
+    if (k < I.n_dec) {
+      const int64_t o = I.off_dec + k;
+      m = member_at(sh.P, A.dec_next[o], A.dec_backlog[o], A.dec_rem[o], A.dec_tier[o], I.now, at, pull);
+    }
+    int64_t tot;
+    const int64_t ex = blk_excl(sh.bs, m.valid ? 1 : 0, &tot);
+    if (m.valid) {
+      const int64_t d = carry + ex;
+      E.ph[d] = m.phase;
+      E.bl[d] = m.backlog;
+      E.rm[d] = m.rem;
+      E.tr[d] = m.tier;
+      E.ow[d] = A.dec_idx[I.off_dec + k];
+    }
+    carry += tot;
+  }
+  return (int)carry;
+}
+
+// chain_member lambda (dp_scheduler.cpp:238-252) for selected member mi.
+__device__ inline void chain_member(const BatchArgs& A, BuildShared& sh, int mi, double a,
+                                    double span, double pull, const MemBuf& E, int at) {
+  const PlannerDev& P = sh.P;
+  const int ci = sh.m_item[mi];
+  const int64_t o = sh.I.off_chain + ci;
+  const int tier = A.ch_tier[o];
+  const double tpot = P.tpot[tier];
+  const int64_t remaining = (int64_t)ceil(span / tpot) + 2;
+  double next = A.ch_deadline[o] + (double)((int64_t)sh.m_asg[mi] + 1) * tpot;
+  int64_t backlog = 0;
+  while (backlog < remaining && time_lt(next - a, pull)) {
+    backlog += 1;
+    next += tpot;
+  }
+  E.ph[at] = next - a;
+  E.bl[at] = backlog;
+  E.rm[at] = remaining;
+  E.tr[at] = tier;
+  E.ow[at] = sh.I.R_total + mi;
+}
+
+__device__ __forceinline__ int32_t owner_ref(const BatchArgs& A, const BuildShared& sh, int64_t owner) {
+  if (owner < sh.I.R_total) return (int32_t)owner;
+  return A.ch_ref[sh.I.off_chain + sh.m_item[owner - sh.I.R_total]];
+}
+__device__ __forceinline__ int owner_tier(const BatchArgs& A, const BuildShared& sh, int64_t owner) {
+  if (owner < sh.I.R_total) return A.run_tier[sh.I.off_run + owner];
+  return A.ch_tier[sh.I.off_chain + sh.m_item[owner - sh.I.R_total]];
+}
+
+// Emit one tiled gap (offset `a`): decode entries per owner, then EDF prefill
+// fill (fill_prefill, dp_scheduler.cpp:220-232). track=true updates
+// decode_assigned of chain owners (the gap loop, :287; not the tail, :341-344).
+__device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bool track) {
+  const int tid = threadIdx.x;
+  const InstDev& I = sh.I;
+  GapPlanBuf& o = sh.o;
+  slos_batch* OB = A.batches + I.off_batch;
+  slos_entry* OE = A.entries + I.off_entry;
+  for (int k = 0; k < o.n_b; ++k) {
+    const GapBatchOut& gb = o.b[k];
+    const bool spec_batch = gb.spec_step > 0 && o.n_spec > 0;
+    const int64_t e0 = sh.n_entry;
+    // decode entries (parallel copy)
+    for (int q = tid; q < gb.n_owner; q += kBT) {
+      const int64_t owner = o.own[2 * (gb.first_owner + q)];
+      const int64_t t = o.own[2 * (gb.first_owner + q) + 1];
+      const int64_t at = e0 + q;
+      if (at < I.cap_entry) {
+        slos_entry e;
+        e.req = owner_ref(A, sh, owner);
+        e.spec_len = spec_batch ? o.spec[owner_tier(A, sh, owner)] : 0;
+        e.prefill_tokens = 0;
+        e.decode_tokens = t;
+        OE[at] = e;
+      }
+      if (track && owner >= I.R_total) atomicAdd(&sh.m_asg[owner - I.R_total], (unsigned long long)t);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int64_t ne = e0 + gb.n_owner;
+      const double end_abs = a + gb.end_s;
+      int64_t budget = gb.prefill_budget;
+      while (budget > 0) {  // fill_prefill
+        while (sh.edf < sh.nsel && sh.m_left[sh.edf] == 0) ++sh.edf;
+        if (sh.edf == sh.nsel) break;
+        const int mi = sh.edf;
+        const int64_t spend = imin(budget, sh.m_left[mi]);
+        sh.m_left[mi] -= spend;
+        budget -= spend;
+        const int64_t o2 = I.off_chain + sh.m_item[mi];
+        if (sh.m_left[mi] == 0 && end_abs > A.ch_deadline[o2] + kTimeEps) sh.fill_late = 1;
+        if (ne < I.cap_entry) {
+          slos_entry e;
+          e.req = A.ch_ref[o2];
+          e.spec_len = 0;
+          e.prefill_tokens = spend;
+          e.decode_tokens = 0;
+          OE[ne] = e;
+        }
+        ++ne;
+      }
+      if (sh.n_batch < I.cap_batch) {
+        slos_batch b;
+        b.start_s = a + gb.start_s;
+        b.end_s = a + gb.end_s;
+        b.capacity_tokens = gb.capacity;
+        b.spec_step = gb.spec_step;
+        b.prefill_budget_left = budget;
+        b.first_entry = e0;
+        b.n_entries = ne - e0;
+        OB[sh.n_batch] = b;
+      }
+      sh.n_batch++;
+      sh.n_entry = ne;
+    }
+    __syncthreads();
+  }
+  return 0;
+}
+
+// edf_fallback dp_scheduler.cpp:96-188 (block-parallel over decoders/prefills).
+__device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena ar, OutHdr* out) {
+  const int tid = threadIdx.x;
+  const InstDev& I = sh.I;
+  const PlannerDev& P = sh.P;
+  const int nd = I.n_dec, np = I.n_pre;
+  double* dnext = (double*)ar.take(sizeof(double) * (nd + 1));
+  int64_t* dbl = (int64_t*)ar.take(sizeof(int64_t) * (nd + 1));
+  int64_t* dleft = (int64_t*)ar.take(sizeof(int64_t) * (nd + 1));
+  int64_t* pleft = (int64_t*)ar.take(sizeof(int64_t) * (np + 1));
+  if (ar.used > ar.cap) {
+    if (tid == 0) { sh.err = SLOS_ERR_CAPACITY; out->need_work = 2 * ar.used; }
+    __syncthreads();
+    return;
+  }
+  double tmin = INFINITY;
+  for (int k = tid; k < nd; k += kBT) {
+    const int64_t o = I.off_dec + k;
+    dnext[k] = A.dec_next[o];
+    dleft[k] = A.dec_rem[o];
+    dbl[k] = imin(A.dec_backlog[o], A.dec_rem[o]);
+    tmin = dmin(tmin, P.tpot[A.dec_tier[o]]);
+  }
+  for (int k = tid; k < np; k += kBT) pleft[k] = A.pre_left[I.off_pre + k];
+  const double t0 = nd > 0 ? blk_min(sh.bs, tmin) : 0.0;
+  slos_batch* OB = A.batches + I.off_batch;
+  slos_entry* OE = A.entries + I.off_entry;
+  const int64_t chunk_cap = P.max_chunk;
+  if (tid == 0) { sh.n_batch = 0; sh.n_entry = 0; }
+  __syncthreads();
+  double t = I.now;
+  for (int guard = 0; guard < 100000; ++guard) {
+    int any_d = 0, any_p = 0;
+    for (int k = tid; k < nd; k += kBT) if (dleft[k] > 0) any_d = 1;
+    for (int k = tid; k < np; k += kBT) if (pleft[k] > 0) any_p = 1;
+    const int fl = blk_or(sh.bs, any_d | (any_p << 1));
+    const bool decodes = fl & 1, prefills = (fl >> 1) & 1;
+    if (!prefills && !decodes) break;
+    const int64_t e0 = sh.n_entry;
+    int64_t ne = e0;
+    slos_batch b;
+    b.start_s = t;
+    b.spec_step = 0;
+    b.first_entry = e0;
+    int64_t free = 0;
+    int64_t dtok = 0, cap = 0;
+    if (decodes) {
+      const double slot_end = t + t0;
+      int64_t carry = 0;
+      for (int base = 0; base < nd; base += kBT) {
+        const int k = base + tid;
+        int64_t due = 0;
+        bool emit = false;
+        if (k < nd && dleft[k] > 0) {
+          due = imin(dbl[k], dleft[k]);
+          dbl[k] -= due;
+          const double tpot = P.tpot[A.dec_tier[I.off_dec + k]];
+          while (dleft[k] - due > 0 && time_le(dnext[k], slot_end)) {
+            ++due;
+            dnext[k] += tpot;
+          }
+          if (due > 0) { dleft[k] -= due; emit = true; }
+        }
+        int64_t tot;
+        const int64_t ex = blk_excl(sh.bs, emit ? 1 : 0, &tot);
+        if (emit) {
+          const int64_t at = ne + carry + ex;
+          if (at < I.cap_entry) {
+            slos_entry e;
+            e.req = A.dec_idx[I.off_dec + k];
+            e.spec_len = 0;
+            e.prefill_tokens = 0;
+            e.decode_tokens = due;
+            OE[at] = e;
+          }
+        }
+        carry += tot;
+        dtok += emit ? due : 0;
+      }
+      ne += carry;
+      dtok = blk_sum64(sh.bs, dtok);
+      cap = plan_time2bs(P, t0, 0);
+      if (cap < 0) {
+        if (tid == 0) sh.err = SLOS_ERR_INFEASIBLE_BUDGET;
+        __syncthreads();
+        return;
+      }
+      free = imax(0, imin(cap - dtok, chunk_cap));
+    } else {
+      free = chunk_cap;
+    }
+    // EDF prefill: take_k = min(left_k, max(0, free - sum_{k'<k} left_k'))
+    int64_t carry = 0, spent = 0;
+    for (int base = 0; base < np; base += kBT) {
+      const int k = base + tid;
+      const int64_t lk = (k < np && pleft[k] > 0) ? pleft[k] : 0;
+      int64_t tot;
+      const int64_t before = carry + blk_excl(sh.bs, lk, &tot);
+      const int64_t take = imin(lk, imax(0, free - before));
+      int64_t t2;
+      const int64_t ex = blk_excl(sh.bs, take > 0 ? 1 : 0, &t2);
+      if (take > 0) {
+        pleft[k] -= take;
+        const int64_t at = ne + ex;
+        if (at < I.cap_entry) {
+          slos_entry e;
+          e.req = A.pre_idx[I.off_pre + k];
+          e.spec_len = 0;
+          e.prefill_tokens = take;
+          e.decode_tokens = 0;
+          OE[at] = e;
+        }
+      }
+      ne += t2;
+      spent += take;
+      carry += tot;
+    }
+    spent = blk_sum64(sh.bs, spent);
+    if (decodes) {
+      const int64_t total = dtok + spent;
+      const double dur = dmax(t0, total > 0 ? plan_predict(P, total, 0) : 0.0);
+      b.end_s = t + dur;
+      b.capacity_tokens = imax(cap, total);
+      b.prefill_budget_left = imax(0, free - spent);
+    } else {
+      b.end_s = t + plan_predict(P, spent, 0);
+      b.capacity_tokens = spent;
+      b.prefill_budget_left = 0;
+    }
+    b.n_entries = ne - e0;
+    if (tid == 0) {
+      if (sh.n_batch < I.cap_batch) OB[sh.n_batch] = b;
+      sh.n_batch++;
+      sh.n_entry = ne;
+    }
+    t = b.end_s;
+    __syncthreads();
+  }
+  if (tid == 0) out->exact_until = t;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
+  __shared__ BuildShared sh;
+  const BatchArgs& A = prm.a;
+  const int tid = threadIdx.x;
+  const int inst = A.order[blockIdx.x];
+  OutHdr* out = &A.out[inst];
+  if (out->status != 0) return;
+  if (tid == 0) {
+    sh.P = A.planners[A.inst[inst].planner];
+    sh.I = A.inst[inst];
+    sh.err = 0;
+    sh.n_batch = 0;
+    sh.n_entry = 0;
+    sh.edf = 0;
+    sh.fill_late = 0;
+  }
+  __syncthreads();
+  const InstDev& I = sh.I;
+  const PlannerDev& P = sh.P;
+  const double pull = plan_predict(P, 1, 0);
+  Arena ar;
+  ar.base = A.work + I.off_work;
+  ar.cap = I.cap_work;
+  ar.used = 0;
+  const int Mmax = I.n_dec + I.N + 1;
+  MemBuf E;
+  E.ph = (double*)ar.take(sizeof(double) * Mmax);
+  E.bl = (int64_t*)ar.take(sizeof(int64_t) * Mmax);
+  E.rm = (int64_t*)ar.take(sizeof(int64_t) * Mmax);
+  E.tr = (int32_t*)ar.take(sizeof(int32_t) * Mmax);
+  E.ow = (int32_t*)ar.take(sizeof(int32_t) * Mmax);
+  GapBatchOut* gb = (GapBatchOut*)ar.take(sizeof(GapBatchOut) * I.cap_gb);
+  int64_t* go = (int64_t*)ar.take(sizeof(int64_t) * 2 * I.cap_go);
+  GapBatchOut* tb = (GapBatchOut*)ar.take(sizeof(GapBatchOut) * I.cap_gb);
+  if (ar.used > ar.cap) {
+    if (tid == 0) { out->status = SLOS_ERR_CAPACITY; out->need_work = 2 * ar.used; }
+    return;
+  }
+  if (tid == 0) {
+    sh.o.b = gb; sh.o.cap_b = (int32_t)I.cap_gb; sh.o.own = go; sh.o.cap_own = (int32_t)I.cap_go;
+    sh.tmp.b = tb; sh.tmp.cap_b = (int32_t)I.cap_gb; sh.tmp.own = nullptr; sh.tmp.cap_own = 0;
+  }
+  int64_t zero[kMaxTiers];
+  for (int l = 0; l < kMaxTiers; ++l) zero[l] = 0;
+  bool fallback = out->best < 0;
+  if (!fallback) {
+    const int32_t* sel = A.sel + I.off_sel;
+    if (tid == 0) {
+      sh.nsel = out->n_sel;
+      for (int k = 0; k < sh.nsel; ++k) {
+        sh.m_item[k] = sel[k];
+        sh.m_left[k] = A.ch_prefill[I.off_chain + sel[k]];
+        sh.m_asg[k] = 0;
+      }
+      int nb = 0;
+      sh.bounds[nb++] = I.now;
+      for (int k = 0; k < sh.nsel; ++k) {
+        const double dl = A.ch_deadline[I.off_chain + sel[k]];
+        if (dl > sh.bounds[nb - 1] + kTimeEps) sh.bounds[nb++] = dl;
+      }
+      sh.nb = nb;
+    }
+    __syncthreads();
+    for (int k = 0; k + 1 < sh.nb && !fallback; ++k) {  // :262-293
+      const double a = sh.bounds[k];
+      const double raw = sh.bounds[k + 1] - a;
+      const double len = quantize_gap(raw);
+      int m = build_members_at(A, sh, a, pull, E);
+      if (tid == 0) {
+        int mm = m;
+        for (int mi = 0; mi < sh.nsel; ++mi)
+          if (A.ch_deadline[I.off_chain + sh.m_item[mi]] <= a + kTimeEps)
+            chain_member(A, sh, mi, a, raw + pull, pull, E, mm++);
+        sh.m1 = mm;
+      }
+      __syncthreads();
+      MemBuf EE = E;
+      EE.M = sh.m1;
+      Arena ar2 = ar;
+      block_tile_gap(P, sh.bs, len, raw + pull, zero, EE, true, ar2, sh.o, sh.tmp);
+      if (sh.o.status) {
+        if (tid == 0) { out->status = sh.o.status; out->need_work = sh.o.need_work; }
+        return;
+      }
+      if (sh.o.n_b > sh.o.cap_b || sh.o.n_own > sh.o.cap_own) {
+        if (tid == 0) { out->status = SLOS_ERR_CAPACITY; out->need_work = 2 * ar.cap; }
+        return;
+      }
+      if (!sh.o.feasible) { fallback = true; break; }
+      emit_gap(A, sh, a, true);
+    }
+    if (!fallback) {
+      if (tid == 0) {  // :294-300
+        int shortfall = sh.fill_late;
+        for (int k = 0; k < sh.nsel; ++k) if (sh.m_left[k] > 0) shortfall = 1;
+        sh.err = shortfall;
+      }
+      __syncthreads();
+      if (sh.err) fallback = true;
+      __syncthreads();
+      if (tid == 0) sh.err = 0;
+    }
+    if (!fallback) {  // decode tail :302-349
+      const double t_last = sh.bounds[sh.nb - 1];
+      const int m = build_members_at(A, sh, t_last, pull, E);
+      double tl = 0.0, capv = 0.0;
+      for (int q = tid; q < m; q += kBT) {
+        const double tpot = P.tpot[E.tr[q]];
+        tl = dmax(tl, E.ph[q] + (double)E.rm[q] * tpot);
+        if (E.rm[q] > 0) capv = dmax(capv, E.ph[q] + tpot);
+      }
+      double tail_len = blk_max(sh.bs, tl);
+      const double capm = blk_max(sh.bs, capv);
+      if (sh.nsel > 0 || I.tail_horizon > kTimeEps) {
+        double max_tpot = 0.0;
+        for (int l = 0; l < P.L; ++l) max_tpot = dmax(max_tpot, P.tpot[l]);
+        double cp = dmax(2.0 * max_tpot, I.tail_horizon);
+        cp = dmax(cp, capm);
+        tail_len = dmin(tail_len, cp);
+      }
+      if (tid == 0) {
+        int mm = m;
+        for (int mi = 0; mi < sh.nsel; ++mi) chain_member(A, sh, mi, t_last, tail_len, pull, E, mm++);
+        sh.m1 = mm;
+      }
+      __syncthreads();
+      const double tlen = quantize_gap(tail_len);
+      if (tlen > kTimeEps && sh.m1 > 0) {
+        MemBuf EE = E;
+        EE.M = sh.m1;
+        Arena ar2 = ar;
+        block_tile_gap(P, sh.bs, tlen, tail_len, zero, EE, true, ar2, sh.o, sh.tmp);
+        if (sh.o.status) {
+          if (tid == 0) { out->status = sh.o.status; out->need_work = sh.o.need_work; }
+          return;
+        }
+        if (sh.o.n_b > sh.o.cap_b || sh.o.n_own > sh.o.cap_own) {
+          if (tid == 0) { out->status = SLOS_ERR_CAPACITY; out->need_work = 2 * ar.cap; }
+          return;
+        }
+        if (!sh.o.feasible) fallback = true;
+        else emit_gap(A, sh, t_last, false);
+      }
+    }
+    if (!fallback && tid == 0) {
+      const slos_batch* OB = A.batches + I.off_batch;
+      out->exact_until = sh.n_batch == 0 ? I.now
+                         : (sh.n_batch <= I.cap_batch ? OB[sh.n_batch - 1].end_s : 0.0);
+    }
+  }
+  if (fallback) {  // :525-530 / :546-556
+    if (tid == 0) {
+      out->infeasible = 1;
+      out->n_admitted = 0;
+      out->value = 0.0;
+      int32_t* dec = A.ids + I.off_ids + I.n_pending;
+      for (int q = 0; q < I.n_pending; ++q) dec[q] = q;
+      out->n_declined = I.n_pending;
+    }
+    __syncthreads();
+    edf_fallback(A, sh, ar, out);
+    if (sh.err) {
+      if (tid == 0) out->status = sh.err;
+      return;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    out->n_batches = sh.n_batch;
+    out->n_entries = sh.n_entry;
+    if (sh.n_batch > I.cap_batch || sh.n_entry > I.cap_entry) {
+      out->status = SLOS_ERR_CAPACITY;
+      out->need_batch = 2 * sh.n_batch;
+      out->need_entry = 2 * sh.n_entry;
+    }
+  }
+}
+
+// ---- standalone gap queries (slos_tile_gap_batch) ----------------------------
+struct GapParams {
+  const PlannerDev* planner;
+  const GapQueryDev* q;
+  const double* ph;
+  const int64_t* bl;
+  const int64_t* rm;
+  const int32_t* tr;
+  const int32_t* ow;
+  GapBatchOut* ob;
+  int64_t* oo;
+  unsigned char* work;
+  GapOutDev* out;
+};
+
+__global__ void __launch_bounds__(kBT) gap_kernel(GapParams prm) {
+  __shared__ BlockShared bs;
+  __shared__ GapPlanBuf o, tmp;
+  __shared__ PlannerDev P;
+  const int tid = threadIdx.x;
+  const GapQueryDev q = prm.q[blockIdx.x];
+  if (tid == 0) P = *prm.planner;
+  __syncthreads();
+  Arena ar;
+  ar.base = prm.work + q.off_work;
+  ar.cap = q.cap_work;
+  ar.used = 0;
+  MemBuf E;
+  E.ph = const_cast<double*>(prm.ph) + q.off_exact;
+  E.bl = const_cast<int64_t*>(prm.bl) + q.off_exact;
+  E.rm = const_cast<int64_t*>(prm.rm) + q.off_exact;
+  E.tr = const_cast<int32_t*>(prm.tr) + q.off_exact;
+  E.ow = const_cast<int32_t*>(prm.ow) + q.off_exact;
+  E.M = q.n_exact;
+  GapBatchOut* tb = (GapBatchOut*)ar.take(sizeof(GapBatchOut) * q.cap_batch);
+  if (tid == 0) {
+    o.b = prm.ob + q.off_out_batch; o.cap_b = (int32_t)q.cap_batch;
+    o.own = prm.oo + 2 * q.off_out_owner; o.cap_own = (int32_t)q.cap_owner;
+    tmp.b = tb; tmp.cap_b = (int32_t)q.cap_batch; tmp.own = nullptr; tmp.cap_own = 0;
+  }
+  __syncthreads();
+  int64_t c[kMaxTiers];
+  for (int l = 0; l < kMaxTiers; ++l) c[l] = q.counts[l];
+  bool sorted = true;
+  for (int m = 1; m < E.M; ++m) if (E.ow[m] <= E.ow[m - 1]) { sorted = false; break; }
+  if (q.mode == SLOS_GAP_TILE_AR) {
+    block_tile_gap_ar(P, bs, q.gap_s, q.horizon, c, E, sorted, ar, o);
+  } else if (q.mode == SLOS_GAP_TILE) {
+    block_tile_gap(P, bs, q.gap_s, q.horizon, c, E, sorted, ar, o, tmp);
+  } else {  // prefill_budget: quantised gap, canonical census, due_horizon 0
+    MemBuf none = E;
+    none.M = 0;
+    block_tile_gap(P, bs, quantize_gap(q.gap_s), 0.0, c, none, true, ar, o, tmp);
+  }
+  if (tid == 0) {
+    GapOutDev r;
+    r.status = o.status;
+    r.feasible = o.feasible;
+    r.budget = o.budget;
+    r.n_spec = o.n_spec;
+    for (int l = 0; l < kMaxTiers; ++l) r.spec_lengths[l] = o.spec[l];
+    r.n_batches = o.n_b;
+    r.n_owner_pairs = o.n_own;
+    r.need_batch = o.n_b;
+    r.need_owner = o.n_own;
+    r.need_work = o.need_work;
+    if (!r.status && (o.n_b > o.cap_b || o.n_own > o.cap_own)) r.status = SLOS_ERR_CAPACITY;
+    prm.out[blockIdx.x] = r;
+  }
+}
+
+// ---- PerfModel primitives (slos_time2bs_batch / slos_predict_batch) --------
+__global__ void time2bs_kernel(const PlannerDev* P, int n, const double* budget, const int64_t* spec,
+                               int64_t max_tokens, int64_t* out, int32_t* status) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t s = spec ? spec[k] : 0;
+  if (max_tokens < 1 || s < 0) { out[k] = 0; status[k] = SLOS_ERR_INVALID_PARAMETERS; return; }
+  const int64_t r = time2bs(*P, budget[k], s, max_tokens);
+  out[k] = r < 0 ? 0 : r;
+  status[k] = r < 0 ? SLOS_ERR_INFEASIBLE_BUDGET : SLOS_OK;
+}
+
+__global__ void predict_kernel(const PlannerDev* P, int n, const int64_t* tokens, const int64_t* spec,
+                               double* out, int32_t* status) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t s = spec ? spec[k] : 0;
+  if (tokens[k] < 0 || s < 0) { out[k] = 0.0; status[k] = SLOS_ERR_INVALID_PARAMETERS; return; }
+  out[k] = predict(*P, tokens[k], s);
+  status[k] = SLOS_OK;
+}
+
+}  // namespace slos

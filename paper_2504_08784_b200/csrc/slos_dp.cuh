@@ -1,0 +1,813 @@
+// Admission DP kernel (K3 + terminal selection of K4): SloScheduler::run's DP,
+// dp_scheduler.cpp:438-544, one CTA per planning instance.
+//
+// The reference walks (item i, source item j, surviving source state) in order,
+// memoising gap budgets and inserting candidates into eps-Pareto buckets one by
+// one. Here each chain item i is one block-synchronous LEVEL:
+//   1. enumerate the level's candidates (j ascending, then source creation order:
+//      exactly the reference traversal, dp_scheduler.cpp:467-478);
+//   2. find-or-insert every memo key (a_us, raw_us, counts) in a per-instance HBM
+//      hash table; a key new to this level keeps its FIRST candidate (atomicMin),
+//      i.e. the reference's first-computed value under µs key collisions (:423-435);
+//   3. evaluate the new keys grouped by anchor j, one warp per group, with the
+//      warp Δpb engine (slos_gapwarp.cuh) sharing the exact census across counts;
+//   4. form candidate states (:479-498);
+//   5. group candidates by Pareto bucket (item, counts) with a stable multi-split,
+//      then one thread per bucket replays try_insert (:445-465) in candidate order;
+//   6. arena ids = rank among accepted candidates (creation order), survivors =
+//      accepted and not later pruned, stored level by level (states_at).
+// Terminal selection (:504-522) is a parallel lexicographic argmax when every
+// value is integral (eps ties impossible), otherwise the reference's sequential
+// scan; backtracking and the admitted/declined lists follow :532-544.
+#pragma once
+
+#include "slos_gapwarp.cuh"
+
+namespace slos {
+
+constexpr int kDpThreads = 256;
+constexpr int kDpWarps = kDpThreads / 32;
+
+struct DpParams {
+  BatchArgs a;
+  int Sc;              // per-warp slot capacity
+  int Lmax;            // max tiers over planners
+  int dec_smem_max;    // stage decoders in smem when n_dec <= this
+  unsigned char* wscr_global;  // per-CTA-slot warp scratch when not in smem (nullptr = smem)
+  size_t wscr_stride;  // bytes per warp in wscr_global
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdULL; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ULL; x ^= x >> 33;
+  return x;
+}
+
+// ---- block-wide helpers (kDpThreads threads) --------------------------------
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* wsum, int64_t* total) {
+  const int lane = lane_id(), w = warp_id();
+  const int64_t inc = warp_incl_scan(v);
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int64_t x = lane < kDpWarps ? wsum[lane] : 0;
+    const int64_t xi = warp_incl_scan(x);
+    if (lane < kDpWarps) wsum[lane] = xi - x;
+    if (lane == kDpWarps - 1) wsum[kDpWarps] = xi;
+  }
+  __syncthreads();
+  const int64_t r = inc - v + wsum[w];
+  *total = wsum[kDpWarps];
+  __syncthreads();
+  return r;
+}
+
+// memo find-or-insert; returns slot or -1 on overflow.
+__device__ inline int memo_find_insert(MemoEnt* T, int64_t cap, uint64_t k0, uint64_t k1,
+                                       uint64_t k2, int c, int32_t* new_list, int* n_new,
+                                       int* n_used, int* overflow) {
+  uint64_t h = mix64(k0 * 0x9E3779B97F4A7C15ULL ^ mix64(k1 + 0x632BE59BD9B4E019ULL) ^
+                     mix64(k2 ^ 0x85EBCA77C2B2AE63ULL)) & (uint64_t)(cap - 1);
+  for (int64_t probe = 0; probe < cap; ++probe) {
+    MemoEnt* e = &T[h];
+    int st = atomicAdd(&e->state, 0);
+    if (st == 0) {
+      if (atomicCAS(&e->state, 0, 1) == 0) {
+        e->k0 = k0; e->k1 = k1; e->k2 = k2;
+        e->first = c; e->has = 0; e->val = 0;
+        __threadfence();
+        atomicExch(&e->state, 2);
+        if (atomicAdd(n_used, 1) * 2 >= cap) atomicExch(overflow, 1);
+        const int idx = atomicAdd(n_new, 1);
+        new_list[idx] = (int32_t)h;
+        return (int)h;
+      }
+      st = atomicAdd(&e->state, 0);
+    }
+    while (st == 1) st = atomicAdd(&e->state, 0);
+    __threadfence();
+    const volatile MemoEnt* ve = e;
+    if (ve->k0 == k0 && ve->k1 == k1 && ve->k2 == k2) {
+      if (st == 2) atomicMin(&e->first, c);
+      return (int)h;
+    }
+    h = (h + 1) & (uint64_t)(cap - 1);
+  }
+  atomicExch(overflow, 1);
+  return -1;
+}
+
+// Evaluate one memo key (counts c) of a group: tile_gap(gap, census, dh).prefill_budget.
+__device__ inline EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D, GapGroup& g,
+                                           Variant& v, const WarpScr& w, const int64_t* c,
+                                           double min_slot) {
+  EvalOut o;
+  o.status = 0; o.has = false; o.budget = 0; o.dues = 0; o.slots = 0;
+  const int L = P.L;
+  unsigned cmask = 0;
+  for (int l = 0; l < L; ++l) if (c[l] > 0) cmask |= 1u << l;
+  // ---------------- tile_gap_ar (budget) ----------------
+  bool ar_has = false;
+  int64_t ar_budget = 0;
+  if (g.gap <= kTimeEps) {
+    ar_has = !g.any_due;
+  } else {
+    const unsigned present = g.exact_mask | cmask;
+    if (!present) {
+      if (g.po_state == 0) {
+        int st = 0;
+        int64_t b = 0;
+        if (lane_id() == 0) b = prefill_only_budget(P, g.gap, min_slot, &st);
+        st = __shfl_sync(0xffffffffu, st, 0);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        g.po_state = st ? 2 : 1;
+        g.po_budget = b;
+      }
+      if (g.po_state == 2) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return o; }
+      ar_has = true;
+      ar_budget = g.po_budget;
+    } else {
+      const double t0 = P.tpot[__ffs(present) - 1];
+      if (!v.valid || v.t0 != t0) warp_build_variant(P, D, g, t0, min_slot, w, v);
+      int64_t Dtot = v.Dx;
+      for (int l = 0; l < L; ++l) Dtot += c[l] * (int64_t)v.q[l];
+      o.dues += Dtot;
+      if (Dtot == 0) {
+        if (g.po_state == 0) {
+          int st = 0;
+          int64_t b = 0;
+          if (lane_id() == 0) b = prefill_only_budget(P, g.gap, min_slot, &st);
+          st = __shfl_sync(0xffffffffu, st, 0);
+          b = __shfl_sync(0xffffffffu, b, 0);
+          g.po_state = st ? 2 : 1;
+          g.po_budget = b;
+        }
+        if (g.po_state == 2) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return o; }
+        ar_has = true;
+        ar_budget = g.po_budget;
+      } else if (min_slot > t0 + kTimeEps) {
+        ar_has = false;
+      } else {
+        o.slots += v.S;
+        if (v.S == 0) {
+          ar_has = false;
+        } else if (v.S > w.Sc) {
+          o.status = SLOS_ERR_CAPACITY;
+          return o;
+        } else if (v.cap_err) {
+          o.status = SLOS_ERR_INFEASIBLE_BUDGET;
+          return o;
+        } else if (v.exact_fail || (v.cfail & cmask)) {
+          ar_has = false;
+        } else {
+          ar_has = warp_place_budget(P, v, w.ends, w.cap, w.nx, w.hc, w.tmp, c, &ar_budget) != 0;
+        }
+      }
+    }
+  }
+  o.has = ar_has;
+  o.budget = ar_budget;
+  // ---------------- tile_gap speculative branch (batch_planner.cpp:318-405) -----
+  if (!P.speculative) return o;
+  if (g.n_exact == 0 && cmask == 0) return o;  // census.empty()
+  const bool spill = v.valid ? v.spill : false;
+  if (g.has_backlog) return o;
+  if (g.dh > g.gap + kTimeEps && spill) return o;
+  int64_t merged[kMaxTiers];
+  for (int l = 0; l < L; ++l) merged[l] = c[l] + g.exact_per_tier[l];
+  SpecSol sp;
+  if (lane_id() == 0) sp = solve_spec(P, merged);
+  sp.ok = __shfl_sync(0xffffffffu, sp.ok, 0);
+  if (!sp.ok) return o;
+  sp.bt = __shfl_sync(0xffffffffu, sp.bt, 0);
+  sp.cap = __shfl_sync(0xffffffffu, sp.cap, 0);
+  for (int l = 0; l < kMaxTiers; ++l) sp.lengths[l] = __shfl_sync(0xffffffffu, sp.lengths[l], 0);
+  if (g.n_exact > 0 && g.min_phase < sp.bt - kTimeEps) return o;
+  const int full = (int)floor(g.gap / sp.bt + kTimeEps);
+  if (full == 0) return o;
+  if (full + 2 > w.Sc + 2) { o.status = SLOS_ERR_CAPACITY; return o; }
+  int64_t canon_dec = 0;
+  for (int l = 0; l < L; ++l) canon_dec += c[l] * (int64_t)sp.lengths[l];
+  for (int k = lane_id(); k <= full; k += 32) w.kh[k] = 0;
+  __syncwarp();
+  if (g.exact) {
+    for (int k = lane_id(); k < D.n; k += 32) {
+      const Member m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], g.now, g.a, g.pull);
+      if (!m.valid || m.rem <= 0) continue;
+      const int64_t sl = sp.lengths[m.tier];
+      const int64_t q = m.rem / sl, r = m.rem % sl;
+      atomicAdd((unsigned long long*)&w.kh[0], (unsigned long long)sl);
+      if (q < full) {
+        atomicAdd((unsigned long long*)&w.kh[q], (unsigned long long)(r - sl));
+        atomicAdd((unsigned long long*)&w.kh[q + 1], (unsigned long long)(-r));
+      }
+    }
+  }
+  __syncwarp();
+  int64_t spec_budget = 0, carry = 0;
+  for (int base = 0; base < full; base += 32) {
+    const int k = base + lane_id();
+    const int64_t x = k < full ? w.kh[k] : 0;
+    const int64_t e = warp_incl_scan(x) + carry;
+    carry = __shfl_sync(0xffffffffu, e, 31);
+    if (k < full) {
+      const int64_t decode = canon_dec + e;
+      spec_budget += imax(0, imin(sp.cap - decode, P.max_chunk));
+    }
+  }
+  spec_budget = warp_sum(spec_budget);
+  const double used = full * sp.bt;
+  if (g.gap - used > kTimeEps) {
+    const double gap2 = g.gap - used;
+    unsigned pm = 0;
+    for (int l = 0; l < L; ++l) if (merged[l] > 0) pm |= 1u << l;
+    bool tail_has = false;
+    int64_t tail_budget = 0;
+    // tile_gap_ar(gap2, rest): gap2 > eps; rest is canonical only
+    if (!pm) {
+      int st = 0;
+      if (lane_id() == 0) tail_budget = prefill_only_budget(P, gap2, min_slot, &st);
+      st = __shfl_sync(0xffffffffu, st, 0);
+      tail_budget = __shfl_sync(0xffffffffu, tail_budget, 0);
+      if (st) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return o; }
+      tail_has = true;
+    } else {
+      const double t0 = P.tpot[__ffs(pm) - 1];
+      Variant v2;
+      warp_build_canon_variant(P, gap2, t0, min_slot, w.ends2, w.cap2, w.hc2, w.Sc, v2);
+      int64_t Dt = 0;
+      for (int l = 0; l < L; ++l) Dt += merged[l] * (int64_t)v2.q[l];
+      o.dues += Dt;
+      if (Dt == 0) {
+        int st = 0;
+        if (lane_id() == 0) tail_budget = prefill_only_budget(P, gap2, min_slot, &st);
+        st = __shfl_sync(0xffffffffu, st, 0);
+        tail_budget = __shfl_sync(0xffffffffu, tail_budget, 0);
+        if (st) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return o; }
+        tail_has = true;
+      } else if (min_slot > t0 + kTimeEps) {
+        tail_has = false;
+      } else {
+        o.slots += v2.S;
+        if (v2.S == 0) tail_has = false;
+        else if (v2.S > w.Sc) { o.status = SLOS_ERR_CAPACITY; return o; }
+        else if (v2.cap_err) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return o; }
+        else if (v2.cfail & pm) tail_has = false;
+        else tail_has = warp_place_budget(P, v2, w.ends2, w.cap2, nullptr, w.hc2, w.tmp, merged,
+                                          &tail_budget) != 0;
+      }
+    }
+    if (!tail_has) return o;
+    spec_budget += tail_budget;
+  }
+  if (o.has && o.budget >= spec_budget) return o;
+  o.has = true;
+  o.budget = spec_budget;
+  return o;
+}
+
+__global__ void __launch_bounds__(kDpThreads) dp_kernel(DpParams prm) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ PlannerDev sP;
+  __shared__ InstDev sI;
+  __shared__ int64_t lvl_off[SLOS_MAX_CHAIN + 2];
+  __shared__ int32_t lvl_cnt[SLOS_MAX_CHAIN + 2];
+  __shared__ int32_t s_pre[SLOS_MAX_CHAIN + 2];
+  __shared__ int32_t s_jcnt[SLOS_MAX_CHAIN + 2];
+  __shared__ int32_t s_joff[SLOS_MAX_CHAIN + 2];
+  __shared__ int64_t s_wsum[kDpWarps + 1];
+  __shared__ unsigned long long s_ctr[5];
+  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_next_grp, s_best;
+  __shared__ int64_t s_next_free, s_arena_next;
+
+  const BatchArgs& A = prm.a;
+  const int tid = threadIdx.x;
+  const int inst = A.order[blockIdx.x];
+  OutHdr* out = &A.out[inst];
+  if (tid == 0) {
+    sP = A.planners[A.inst[inst].planner];
+    sI = A.inst[inst];
+    s_err = 0;
+    s_ovf = 0;
+    s_n_used = 0;
+    for (int k = 0; k < 5; ++k) s_ctr[k] = 0;
+  }
+  __syncthreads();
+  const PlannerDev& P = sP;
+  const InstDev& I = sI;
+  const int N = I.N;
+  const int L = P.L;
+  const double min_slot = plan_predict(P, 1, 0);  // BatchPlanner::min_slot_s
+  const double pull = min_slot;
+
+  // ---- dynamic smem: chain, decoders, warp scratch ----
+  unsigned char* p = dsm;
+  double* ch_dl = (double*)p; p += sizeof(double) * (N + 1);
+  int64_t* ch_pf = (int64_t*)p; p += sizeof(int64_t) * (N + 1);
+  int64_t* ch_mm = (int64_t*)p; p += sizeof(int64_t) * (N + 1);
+  double* ch_vl = (double*)p; p += sizeof(double) * (N + 1);
+  int64_t* ch_sf = (int64_t*)p; p += sizeof(int64_t) * (N + 2);
+  int32_t* ch_tr = (int32_t*)p; p += sizeof(int32_t) * (N + 2);
+  int32_t* ch_fc = (int32_t*)p; p += sizeof(int32_t) * (N + 2);
+  int32_t* ch_fl = (int32_t*)p; p += sizeof(int32_t) * (N + 2);
+  p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+  for (int k = tid; k < N; k += kDpThreads) {
+    const int64_t o = I.off_chain + k;
+    ch_dl[k] = A.ch_deadline[o];
+    ch_pf[k] = A.ch_prefill[o];
+    ch_mm[k] = A.ch_memory[o];
+    ch_vl[k] = A.ch_value[o];
+    ch_tr[k] = A.ch_tier[o];
+    ch_fc[k] = A.ch_forced[o];
+    ch_fl[k] = A.ch_floor[o];
+  }
+  for (int k = tid; k <= N; k += kDpThreads) ch_sf[k] = A.ch_suffix[I.off_chain + k];
+  DecView D;
+  D.n = I.have_running_decode ? I.n_dec : 0;
+  if (I.n_dec <= prm.dec_smem_max) {
+    double* dn = (double*)p; p += sizeof(double) * I.n_dec;
+    int64_t* db = (int64_t*)p; p += sizeof(int64_t) * I.n_dec;
+    int64_t* dr = (int64_t*)p; p += sizeof(int64_t) * I.n_dec;
+    int32_t* dt = (int32_t*)p; p += sizeof(int32_t) * I.n_dec;
+    p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    for (int k = tid; k < I.n_dec; k += kDpThreads) {
+      dn[k] = A.dec_next[I.off_dec + k];
+      db[k] = A.dec_backlog[I.off_dec + k];
+      dr[k] = A.dec_rem[I.off_dec + k];
+      dt[k] = A.dec_tier[I.off_dec + k];
+    }
+    D.next = dn; D.backlog = db; D.rem = dr; D.tier = dt;
+  } else {
+    D.next = A.dec_next + I.off_dec;
+    D.backlog = A.dec_backlog + I.off_dec;
+    D.rem = A.dec_rem + I.off_dec;
+    D.tier = A.dec_tier + I.off_dec;
+  }
+  unsigned char* wbase;
+  if (prm.wscr_global) {
+    wbase = prm.wscr_global + ((size_t)blockIdx.x * kDpWarps + warp_id()) * prm.wscr_stride;
+  } else {
+    wbase = p + (size_t)warp_id() * prm.wscr_stride;
+  }
+  const WarpScr W = warp_scr_carve(wbase, prm.Sc, prm.Lmax);
+
+  // ---- scratch slices ----
+  uint64_t* Sc_ = A.s_counts + I.off_surv;
+  int64_t* Sm_ = A.s_mem + I.off_surv;
+  int64_t* Sp_ = A.s_pb + I.off_surv;
+  double* Sv_ = A.s_value + I.off_surv;
+  int32_t* Sn_ = A.s_nadm + I.off_surv;
+  int32_t* Spar = A.s_parent + I.off_surv;
+  int32_t* Sar = A.s_arena + I.off_surv;
+  int32_t* Sit = A.s_level + I.off_surv;
+  int32_t* Csrc = A.c_src + I.off_cand;
+  int32_t* Cj = A.c_j + I.off_cand;
+  int32_t* Cme = A.c_memo + I.off_cand;
+  int32_t* Cfl = A.c_flag + I.off_cand;
+  int32_t* Cbk = A.c_bucket + I.off_cand;
+  int32_t* Cps = A.c_pos + I.off_cand;
+  int32_t* Caux = A.c_aux + I.off_cand;
+  uint64_t* Ccn = A.c_counts + I.off_cand;
+  int64_t* Cmm = A.c_mem + I.off_cand;
+  int64_t* Cpb = A.c_pb + I.off_cand;
+  double* Cvl = A.c_value + I.off_cand;
+  int32_t* Cna = A.c_nadm + I.off_cand;
+  uint64_t* Bkey = A.c_bkey + 2 * I.off_cand;
+  int32_t* Bval = A.c_bval + 2 * I.off_cand;
+  MemoEnt* Memo = A.memo + I.off_memo;
+  const int64_t capC = I.cap_cand;
+  const int64_t capB = 2 * I.cap_cand;
+  // generic int scratch: reuse bucket value space halves
+  int32_t* X0 = Cps;  // new list / bucket lists
+
+  if (tid == 0) {
+    Sc_[0] = 0; Sm_[0] = 0; Sp_[0] = 0; Sv_[0] = 0.0; Sn_[0] = 0; Spar[0] = -1; Sar[0] = 0; Sit[0] = -1;
+    lvl_off[0] = 0;
+    lvl_cnt[0] = 1;
+    s_next_free = 1;
+    s_arena_next = 1;
+  }
+  __syncthreads();
+
+  for (int i = 0; i < N && !s_err; ++i) {
+    const int jlo = ch_fl[i];
+    const int nlev = i - jlo;  // levels jlo+1 .. i
+    if (tid == 0) {
+      int acc = 0;
+      for (int k = 0; k < nlev; ++k) { s_pre[k] = acc; acc += lvl_cnt[jlo + 1 + k]; }
+      s_pre[nlev] = acc;
+      s_n_new = 0;
+      s_nb = 0;
+      s_next_grp = 0;
+      if (acc > capC) { s_err = SLOS_ERR_CAPACITY; out->need_cand = acc; }
+    }
+    __syncthreads();
+    if (s_err) break;
+    const int T = s_pre[nlev];
+    if (tid == 0) s_ctr[0] += (unsigned long long)T;
+    const double t_i = ch_dl[i];
+    // ---- 1+2: candidates and memo keys ----
+    for (int c = tid; c < T; c += kDpThreads) {
+      int lo = 0, hi = nlev - 1;
+      while (lo < hi) {  // last k with s_pre[k] <= c
+        const int mid = (lo + hi + 1) / 2;
+        if (s_pre[mid] <= c) lo = mid; else hi = mid - 1;
+      }
+      const int lv = jlo + 1 + lo;
+      const int src = (int)(lvl_off[lv] + (c - s_pre[lo]));
+      const int j = lv - 1;
+      Csrc[c] = src;
+      Cj[c] = j;
+      const double a = (j < 0) ? I.now : ch_dl[j];
+      const double raw = dmax(0.0, t_i - a);
+      uint64_t k0, k1;
+      if (I.have_running_decode) {
+        k0 = (uint64_t)llround(a * 1e6);
+        k1 = (uint64_t)llround(raw * 1e6);
+      } else {
+        const double gap = quantize_gap(quantize_gap(raw));
+        k0 = 0xFFFFFFFFFFFFFFFFULL;
+        k1 = (uint64_t)llround(gap * 1000.0);
+      }
+      Cme[c] = memo_find_insert(Memo, I.cap_memo, k0, k1, Sc_[src], c, X0, &s_n_new, &s_n_used, &s_ovf);
+    }
+    __syncthreads();
+    if (s_ovf) {
+      if (tid == 0) { s_err = SLOS_ERR_CAPACITY; out->need_memo = 2 * I.cap_memo; }
+      __syncthreads();
+      break;
+    }
+    const int n_new = s_n_new;
+    // ---- 3: group new keys by anchor j and evaluate ----
+    for (int k = tid; k <= nlev; k += kDpThreads) s_jcnt[k] = 0;
+    __syncthreads();
+    for (int q = tid; q < n_new; q += kDpThreads) {
+      const int c = Memo[X0[q]].first;
+      atomicAdd(&s_jcnt[Cj[c] - jlo], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int k = 0; k < nlev; ++k) { s_joff[k] = acc; acc += s_jcnt[k]; s_jcnt[k] = 0; }
+      s_ctr[1] += (unsigned long long)n_new;
+    }
+    __syncthreads();
+    int32_t* G = Cbk;  // grouped key slots
+    for (int q = tid; q < n_new; q += kDpThreads) {
+      const int slot = X0[q];
+      const int k = Cj[Memo[slot].first] - jlo;
+      const int pos = s_joff[k] + atomicAdd(&s_jcnt[k], 1);
+      G[pos] = slot;
+    }
+    __syncthreads();
+    {
+      const int lane = lane_id();
+      unsigned long long wd = 0, ws = 0;
+      for (;;) {
+        int grp = 0;
+        if (lane == 0) grp = atomicAdd(&s_next_grp, 1);
+        grp = __shfl_sync(0xffffffffu, grp, 0);
+        if (grp >= nlev || s_err) break;
+        const int cnt = s_jcnt[grp];
+        if (cnt == 0) continue;
+        const int j = jlo + grp;
+        GapGroup g;
+        g.a = (j < 0) ? I.now : ch_dl[j];
+        const double raw = dmax(0.0, t_i - g.a);
+        const double len = quantize_gap(raw);
+        g.now = I.now;
+        g.pull = pull;
+        g.exact = I.have_running_decode != 0;
+        if (g.exact) { g.gap = len; g.dh = raw + pull; }
+        else { g.gap = quantize_gap(len); g.dh = 0.0; }
+        g.horizon = dmax(g.gap, g.dh);
+        warp_group_setup(P, D, g);
+        Variant v;
+        v.valid = false;
+        for (int q = 0; q < cnt; ++q) {
+          MemoEnt* e = &Memo[G[s_joff[grp] + q]];
+          const uint64_t cw = e->k2;
+          int64_t cv[kMaxTiers];
+          for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
+          const EvalOut r = warp_eval_counts(P, D, g, v, W, cv, min_slot);
+          wd += (unsigned long long)r.dues;
+          ws += (unsigned long long)r.slots;
+          if (r.status) {
+            if (lane == 0) {
+              atomicCAS(&s_err, 0, r.status);
+              if (r.status == SLOS_ERR_CAPACITY) out->need_work = 2 * prm.Sc;
+            }
+            break;
+          }
+          if (lane == 0) {
+            e->has = r.has ? 1 : 0;
+            e->val = r.budget;
+          }
+        }
+      }
+      if (lane == 0) {
+        atomicAdd(&s_ctr[2], wd);
+        atomicAdd(&s_ctr[3], ws);
+      }
+    }
+    __syncthreads();
+    if (s_err) break;
+    for (int q = tid; q < n_new; q += kDpThreads) Memo[X0[q]].state = 3;
+    // ---- 4: candidate states ----
+    const int tier_i = ch_tr[i];
+    const bool forced = ch_fc[i] != 0;
+    for (int c = tid; c < T; c += kDpThreads) {
+      const MemoEnt* e = &Memo[Cme[c]];
+      int flag = 0;
+      const int src = Csrc[c];
+      if (e->has) {
+        const int64_t avail = Sp_[src] + e->val;
+        if (avail >= ch_pf[i]) {
+          const uint64_t nc = pack_add(Sc_[src], tier_i);
+          if (pack_get(nc, tier_i) > 250) atomicCAS(&s_err, 0, SLOS_ERR_INTERNAL_INCONSISTENCY);
+          int64_t mem = Sm_[src];
+          bool ok = true;
+          if (!forced) {
+            mem = mem + ch_mm[i];
+            if (mem > I.mem_budget) ok = false;
+          }
+          if (ok) {
+            flag = 1;
+            Ccn[c] = nc;
+            Cmm[c] = mem;
+            Cpb[c] = imin(avail - ch_pf[i], ch_sf[i + 1]);
+            Cvl[c] = Sv_[src] + (forced ? 0.0 : ch_vl[i]);
+            Cna[c] = Sn_[src] + (forced ? 0 : 1);
+          }
+        }
+      }
+      Cfl[c] = flag;
+    }
+    __syncthreads();
+    if (s_err) break;
+    // ---- 5: Pareto buckets ----
+    for (int c = tid; c < T; c += kDpThreads) {
+      int b = -1;
+      if (Cfl[c] & 1) {
+        const uint64_t key = Ccn[c];
+        uint64_t h = mix64(key) & (uint64_t)(capB - 1);
+        for (;;) {
+          const unsigned long long old = atomicCAS((unsigned long long*)&Bkey[h], 0ull,
+                                                   (unsigned long long)key);
+          if (old == 0ull) {
+            b = atomicAdd(&s_nb, 1);
+            Caux[b] = (int32_t)h;
+            atomicExch(&Bval[h], b);
+            break;
+          }
+          if (old == key) {
+            int x;
+            do { x = atomicAdd(&Bval[h], 0); } while (x < 0);
+            b = x;
+            break;
+          }
+          h = (h + 1) & (uint64_t)(capB - 1);
+        }
+      }
+      Cbk[c] = b;
+    }
+    __syncthreads();
+    const int NB = s_nb;
+    int32_t* cntB = Cj;   // anchors are no longer needed this level
+    int32_t* offB = Cme;  // memo slots are no longer needed after step 4
+    for (int b = tid; b < NB; b += kDpThreads) cntB[b] = 0;
+    __syncthreads();
+    for (int c = tid; c < T; c += kDpThreads)
+      if (Cbk[c] >= 0) atomicAdd(&cntB[Cbk[c]], 1);
+    __syncthreads();
+    {
+      int64_t carry = 0;
+      for (int base = 0; base < NB; base += kDpThreads) {
+        const int b = base + tid;
+        const int64_t x = b < NB ? cntB[b] : 0;
+        int64_t tot;
+        const int64_t ex = block_excl_scan(x, s_wsum, &tot);
+        if (b < NB) { offB[b] = (int32_t)(carry + ex); cntB[b] = 0; }
+        carry += tot;
+      }
+    }
+    __syncthreads();
+    // stable multi-split: chunk by chunk, warp by warp, candidate order preserved
+    for (int base = 0; base < T; base += kDpThreads) {
+      const int c = base + tid;
+      const int b = c < T ? Cbk[c] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      const int lane = lane_id();
+      const int rank = __popc(peers & ((1u << lane) - 1));
+      const int leader = __ffs(peers) - 1;
+      for (int w = 0; w < kDpWarps; ++w) {
+        if (warp_id() == w) {
+          int basepos = 0;
+          if (b >= 0 && lane == leader) {
+            basepos = cntB[b];
+            cntB[b] = basepos + __popc(peers);
+          }
+          basepos = __shfl_sync(0xffffffffu, basepos, leader);
+          if (b >= 0) X0[offB[b] + basepos + rank] = c;
+        }
+        __syncthreads();
+      }
+    }
+    // one thread per bucket: try_insert replay (dp_scheduler.cpp:445-465)
+    for (int b = tid; b < NB; b += kDpThreads) {
+      int32_t* lst = X0 + offB[b];
+      const int n = cntB[b];
+      int f = 0;  // frontier lst[0..f)
+      for (int q = 0; q < n; ++q) {
+        const int c = lst[q];
+        const double sv = Cvl[c];
+        const int64_t sm = Cmm[c], sp = Cpb[c];
+        const int sn = Cna[c];
+        bool reject = false;
+        for (int r = 0; r < f; ++r) {
+          const int e = lst[r];
+          if (Cvl[e] >= sv - kValueEps && Cmm[e] <= sm && Cpb[e] >= sp) {
+            const bool equal = fabs(Cvl[e] - sv) <= kValueEps && Cmm[e] == sm && Cpb[e] == sp;
+            if (!equal || Cna[e] >= sn) { reject = true; break; }
+          }
+        }
+        if (reject) continue;
+        int wq = 0;
+        for (int r = 0; r < f; ++r) {
+          const int e = lst[r];
+          if (sv >= Cvl[e] - kValueEps && sm <= Cmm[e] && sp >= Cpb[e]) Cfl[e] |= 4;  // pruned
+          else lst[wq++] = e;
+        }
+        lst[wq++] = c;
+        f = wq;
+        Cfl[c] |= 2;  // accepted
+      }
+    }
+    __syncthreads();
+    // reset the bucket hash slots claimed by this level (table returns to empty)
+    for (int b = tid; b < NB; b += kDpThreads) {
+      Bkey[Caux[b]] = 0ull;
+      Bval[Caux[b]] = -1;
+    }
+    __syncthreads();
+    // ---- 6: arena ids and survivors ----
+    {
+      int64_t carry_acc = 0, carry_sv = 0;
+      const int64_t base_free = s_next_free;
+      for (int base = 0; base < T; base += kDpThreads) {
+        const int c = base + tid;
+        const int fl = c < T ? Cfl[c] : 0;
+        const int acc = (fl & 2) ? 1 : 0;
+        const int sv = ((fl & 2) && !(fl & 4)) ? 1 : 0;
+        int64_t tot_acc, tot_sv;
+        const int64_t r_acc = block_excl_scan(acc, s_wsum, &tot_acc);
+        const int64_t r_sv = block_excl_scan(sv, s_wsum, &tot_sv);
+        if (sv) {
+          const int64_t dst = base_free + carry_sv + r_sv;
+          if (dst < I.cap_surv) {
+            Sc_[dst] = Ccn[c];
+            Sm_[dst] = Cmm[c];
+            Sp_[dst] = Cpb[c];
+            Sv_[dst] = Cvl[c];
+            Sn_[dst] = Cna[c];
+            Spar[dst] = Csrc[c];
+            Sar[dst] = (int32_t)(s_arena_next + carry_acc + r_acc);
+            Sit[dst] = i;
+          }
+        }
+        carry_acc += tot_acc;
+        carry_sv += tot_sv;
+      }
+      if (tid == 0) {
+        lvl_off[i + 1] = base_free;
+        lvl_cnt[i + 1] = (int32_t)carry_sv;
+        s_next_free = base_free + carry_sv;
+        s_arena_next += carry_acc;
+        if (s_next_free > I.cap_surv) { s_err = SLOS_ERR_CAPACITY; out->need_surv = 2 * s_next_free; }
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) out->status = s_err;
+    return;
+  }
+  // ---- terminal selection (dp_scheduler.cpp:504-522) ----
+  const int lv0 = I.last_forced + 1;
+  const int64_t t_lo = lvl_off[lv0];
+  const int64_t t_hi = s_next_free;
+  if (I.values_integral) {
+    // total order: value desc, n_admitted desc, mem asc, pb desc, arena asc
+    int64_t best = -1;
+    for (int64_t x = t_lo + tid; x < t_hi; x += kDpThreads) {
+      if (best < 0) { best = x; continue; }
+      const double vx = Sv_[x], vb = Sv_[best];
+      bool bt;
+      if (vx != vb) bt = vx > vb;
+      else if (Sn_[x] != Sn_[best]) bt = Sn_[x] > Sn_[best];
+      else if (Sm_[x] != Sm_[best]) bt = Sm_[x] < Sm_[best];
+      else if (Sp_[x] != Sp_[best]) bt = Sp_[x] > Sp_[best];
+      else bt = Sar[x] < Sar[best];
+      if (bt) best = x;
+    }
+    // block argmax under the same order
+    for (int o = 16; o; o >>= 1) {
+      const int64_t y = __shfl_xor_sync(0xffffffffu, best, o);
+      if (y >= 0) {
+        bool bt;
+        if (best < 0) bt = true;
+        else {
+          const double vy = Sv_[y], vb = Sv_[best];
+          if (vy != vb) bt = vy > vb;
+          else if (Sn_[y] != Sn_[best]) bt = Sn_[y] > Sn_[best];
+          else if (Sm_[y] != Sm_[best]) bt = Sm_[y] < Sm_[best];
+          else if (Sp_[y] != Sp_[best]) bt = Sp_[y] > Sp_[best];
+          else bt = Sar[y] < Sar[best];
+        }
+        if (bt) best = y;
+      }
+    }
+    if (lane_id() == 0) s_wsum[warp_id()] = best;
+    __syncthreads();
+    if (tid == 0) {
+      int64_t b = -1;
+      for (int w = 0; w < kDpWarps; ++w) {
+        const int64_t y = s_wsum[w];
+        if (y < 0) continue;
+        bool bt;
+        if (b < 0) bt = true;
+        else {
+          const double vy = Sv_[y], vb = Sv_[b];
+          if (vy != vb) bt = vy > vb;
+          else if (Sn_[y] != Sn_[b]) bt = Sn_[y] > Sn_[b];
+          else if (Sm_[y] != Sm_[b]) bt = Sm_[y] < Sm_[b];
+          else if (Sp_[y] != Sp_[b]) bt = Sp_[y] > Sp_[b];
+          else bt = Sar[y] < Sar[b];
+        }
+        if (bt) b = y;
+      }
+      s_best = (int)b;
+    }
+  } else if (tid == 0) {
+    int64_t b = -1;
+    for (int64_t x = t_lo; x < t_hi; ++x) {
+      bool bt;
+      if (b < 0) bt = true;
+      else if (fabs(Sv_[x] - Sv_[b]) > kValueEps) bt = Sv_[x] > Sv_[b];
+      else if (Sn_[x] != Sn_[b]) bt = Sn_[x] > Sn_[b];
+      else if (Sm_[x] != Sm_[b]) bt = Sm_[x] < Sm_[b];
+      else if (Sp_[x] != Sp_[b]) bt = Sp_[x] > Sp_[b];
+      else bt = Sar[x] < Sar[b];
+      if (bt) b = x;
+    }
+    s_best = (int)b;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int best = s_best;
+    int32_t* sel = A.sel + I.off_sel;
+    int32_t* adm = A.ids + I.off_ids;
+    int32_t* dec = adm + I.n_pending;
+    out->best = best;
+    out->ctr[0] = (int64_t)s_ctr[0];
+    out->ctr[1] = (int64_t)s_ctr[1];
+    out->ctr[2] = (int64_t)s_ctr[2];
+    out->ctr[3] = (int64_t)s_ctr[3];
+    out->ctr[4] = s_arena_next - 1;
+    if (best < 0) {  // dp_scheduler.cpp:525-530
+      out->infeasible = 1;
+      out->n_sel = 0;
+      out->n_admitted = 0;
+      out->n_declined = I.n_pending;
+      for (int q = 0; q < I.n_pending; ++q) dec[q] = q;
+      out->value = 0.0;
+    } else {  // :532-544
+      int n = 0;
+      for (int s = best; s > 0; s = Spar[s]) sel[n++] = Sit[s];
+      for (int a = 0, b = n - 1; a < b; ++a, --b) { const int t = sel[a]; sel[a] = sel[b]; sel[b] = t; }
+      double value = 0.0;
+      int na = 0, nd = 0;
+      int k = 0;
+      for (int q = 0; q < n; ++q) {
+        const int ci = sel[q];
+        if (!ch_fc[ci]) {
+          adm[na++] = -A.ch_ref[I.off_chain + ci] - 1;
+          value += ch_vl[ci];
+        }
+      }
+      for (int ci = 0; ci < N; ++ci) {  // sel is ascending: merge-walk
+        while (k < n && sel[k] < ci) ++k;
+        const bool in_chain = k < n && sel[k] == ci;
+        if (!ch_fc[ci] && !in_chain) dec[nd++] = -A.ch_ref[I.off_chain + ci] - 1;
+      }
+      out->infeasible = 0;
+      out->n_sel = n;
+      out->n_admitted = na;
+      out->n_declined = nd;
+      out->value = value;
+    }
+    out->status = 0;
+  }
+}
+
+}  // namespace slos

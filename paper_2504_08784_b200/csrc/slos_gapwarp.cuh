@@ -1,0 +1,397 @@
+// Warp-level Δpb engine: the leftover prefill budget of one gap for MANY canonical
+// count vectors sharing the same exact census (the admission DP's inner primitive,
+// dp_scheduler.cpp:418-436 -> BatchPlanner::tile_gap batch_planner.cpp:315-406 ->
+// tile_gap_ar :152-313, budget only).
+//
+// Re-design (not a port): the reference materialises every due, sorts them and
+// places them one by one into per-owner std::map bins. For the DP only the budget
+// matters, so a gap is reduced to per-slot counts:
+//   * exact members (the running decoders at the gap start, members_at) are
+//     enumerated ONCE per (chain item i, anchor j, tightest tier) "variant", lanes
+//     over members, into a per-slot histogram nx[s] (same repeated-addition due
+//     times and the same jit binary search as the reference, so bit-identical);
+//   * canonical members contribute c_l * hc_l[s] where hc_l is the per-slot
+//     histogram of tier-l canonical dues (independent of the counts);
+//   * late dues fill slots first-fit, and latest-fit placement of the jit groups
+//     leaves free capacity G(s) - G(s-1) with G(s) = min_{u>=s}(F(u) - D(u))
+//     (F = prefix free capacity after late dues, D = prefix due counts); the gap
+//     is infeasible iff min_u (F(u) - D(u)) < 0. Warp scans over slots give the
+//     budget sum_s min(free_s, max_chunk) in O(S/32) per count vector.
+// All fp64 is evaluated in the reference's order (see slos_common.cuh).
+#pragma once
+
+#include "slos_common.cuh"
+
+namespace slos {
+
+// Per-warp scratch (shared or global memory), sized by the host-chosen slot cap Sc.
+struct WarpScr {
+  double* ends;   // Sc
+  int64_t* cap;   // Sc
+  int32_t* nx;    // Sc   exact non-late dues per slot
+  int32_t* hc;    // L*Sc canonical dues per slot per tier
+  int64_t* tmp;   // Sc   placement temporaries
+  double* ends2;  // Sc   spec-tail canonical variant
+  int64_t* cap2;  // Sc
+  int32_t* hc2;   // L*Sc
+  int64_t* kh;    // Sc+2 spec per-batch exact decode histogram
+  int Sc;
+  int L;
+};
+
+__device__ __forceinline__ size_t warp_scr_bytes(int Sc, int L) {
+  return (size_t)Sc * (8 + 8 + 4 + 4 * L + 8 + 8 + 8 + 4 * L) + (size_t)(Sc + 2) * 8 + 64;
+}
+
+__device__ __forceinline__ WarpScr warp_scr_carve(unsigned char* base, int Sc, int L) {
+  WarpScr w;
+  unsigned char* p = base;
+  w.ends = (double*)p; p += (size_t)Sc * 8;
+  w.cap = (int64_t*)p; p += (size_t)Sc * 8;
+  w.tmp = (int64_t*)p; p += (size_t)Sc * 8;
+  w.ends2 = (double*)p; p += (size_t)Sc * 8;
+  w.cap2 = (int64_t*)p; p += (size_t)Sc * 8;
+  w.kh = (int64_t*)p; p += (size_t)(Sc + 2) * 8;
+  w.nx = (int32_t*)p; p += (size_t)Sc * 4;
+  w.hc = (int32_t*)p; p += (size_t)Sc * 4 * L;
+  w.hc2 = (int32_t*)p; p += (size_t)Sc * 4 * L;
+  w.Sc = Sc;
+  w.L = L;
+  return w;
+}
+
+// Running decoders of one instance (SoA; shared memory when staged).
+struct DecView {
+  const double* next;
+  const int64_t* backlog;
+  const int64_t* rem;
+  const int32_t* tier;
+  int n;
+};
+
+// One gap (chain item i, anchor j): the exact census is members_at(a).
+struct GapGroup {
+  double a;        // gap start (t_j)
+  double gap;      // tile_gap gap_s (len, or quantize(len) without running decoders)
+  double dh;       // due_horizon_s (raw + pull, or 0)
+  double horizon;  // max(gap, dh)  (batch_planner.cpp:155)
+  double now, pull;
+  bool exact;      // census has exact members (have_running_decode)
+  // filled by warp_group_setup (group-level facts, independent of counts)
+  unsigned exact_mask;        // tiers with an exact member of remaining > 0
+  int64_t exact_per_tier[kMaxTiers];  // merged_counts contribution (batch_planner.cpp:28)
+  int n_exact;                // valid members
+  bool any_due;               // gap<=eps branch (batch_planner.cpp:156-164)
+  bool has_backlog;           // spec: any exact backlog > 0 (:321-322)
+  double min_phase;           // spec: min phase over members with remaining > 0 (:341-346)
+  // prefill-only cache
+  int po_state;               // 0 unknown, 1 ok, 2 error
+  int64_t po_budget;
+};
+
+struct Variant {
+  double t0;
+  double t0_first;
+  int S;            // number of slots (may exceed Sc -> overflow)
+  int64_t Lx;       // exact late dues
+  int64_t Dx;       // exact dues materialised
+  int q[kMaxTiers]; // canonical due times per tier
+  bool exact_fail;  // an exact non-late due with jit < 0
+  unsigned cfail;   // tiers whose canonical dues have jit < 0
+  bool cap_err;     // plan_time2bs threw on some slot
+  bool spill;       // spec: an exact due past gap (within due_horizon)
+  bool valid;
+};
+
+struct EvalOut {
+  int status;     // 0 ok, else SLOS_ERR_*
+  bool has;       // optional<int64_t>
+  int64_t budget;
+  int64_t dues;   // reference work counters (D, S)
+  int64_t slots;
+};
+
+// ---- group setup: one pass over members (lanes over decoders) ----------------
+__device__ inline void warp_group_setup(const PlannerDev& P, const DecView& D, GapGroup& g) {
+  const int lane = lane_id();
+  unsigned mask = 0;
+  int64_t per[kMaxTiers];
+  for (int l = 0; l < kMaxTiers; ++l) per[l] = 0;
+  int n_valid = 0, any_due = 0, bl = 0;
+  double minph = INFINITY;
+  if (g.exact) {
+    for (int k = lane; k < D.n; k += 32) {
+      const Member m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], g.now, g.a, g.pull);
+      if (!m.valid) continue;
+      ++n_valid;
+      per[m.tier] += 1;
+      if (m.backlog > 0) bl = 1;
+      if (m.rem > 0) {
+        mask |= 1u << m.tier;
+        if (m.backlog > 0) any_due = 1;
+        if (g.horizon > kTimeEps && time_le(m.phase, g.horizon)) any_due = 1;
+        minph = dmin(minph, m.phase);
+      }
+    }
+  }
+  g.exact_mask = __reduce_or_sync(0xffffffffu, mask);
+  for (int l = 0; l < P.L; ++l) g.exact_per_tier[l] = warp_sum(per[l]);
+  g.n_exact = warp_sum(n_valid);
+  g.any_due = warp_or(any_due) != 0;
+  g.has_backlog = warp_or(bl) != 0;
+  g.min_phase = warp_min(minph);
+  g.po_state = 0;
+  g.po_budget = 0;
+}
+
+// Ordered t0_first scan (batch_planner.cpp:234-239) without serialising the warp:
+// cur only decreases, so each round finds the first lane (in member order) that
+// still qualifies against the current value.
+__device__ inline double warp_t0_first(const PlannerDev& P, const DecView& D, const GapGroup& g,
+                                       double t0, double min_slot) {
+  const int lane = lane_id();
+  double cur = t0;
+  if (!g.exact) return cur;
+  for (int base = 0; base < D.n; base += 32) {
+    const int k = base + lane;
+    double ph = 0.0;
+    bool ok = false;
+    if (k < D.n) {
+      const Member m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], g.now, g.a, g.pull);
+      ok = m.valid && m.rem > 0 && m.phase > kTimeEps;
+      ph = m.phase;
+    }
+    unsigned above = 0xffffffffu;
+    for (;;) {
+      const unsigned q = __ballot_sync(0xffffffffu, ok && ph < cur - kTimeEps) & above;
+      if (!q) break;
+      const int f = __ffs(q) - 1;
+      const double pf = __shfl_sync(0xffffffffu, ph, f);
+      cur = dmax(pf, min_slot);
+      above = (f == 31) ? 0u : (0xffffffffu << (f + 1));
+    }
+  }
+  return cur;
+}
+
+// Slot ends (batch_planner.cpp:240-248) on lane 0; returns S (may exceed Sc).
+__device__ inline int warp_slot_ends(double* ends, int Sc, double t0_first, double t0, double gap,
+                                     double min_slot) {
+  int S = 0;
+  if (lane_id() == 0) {
+    double last = 0.0;
+    for (double e = t0_first; time_le(e, gap); e += t0) {
+      if (S < Sc) ends[S] = e;
+      last = e;
+      ++S;
+    }
+    if (S == 0) {
+      if (time_le(min_slot, gap)) { if (S < Sc) ends[S] = gap; ++S; }
+    } else if (gap - last >= min_slot - kTimeEps) {
+      if (S < Sc) ends[S] = gap;
+      ++S;
+    }
+  }
+  S = __shfl_sync(0xffffffffu, S, 0);
+  __syncwarp();
+  return S;
+}
+
+// Build the exact-member variant for tightest tier t0 (lanes over members).
+__device__ inline void warp_build_variant(const PlannerDev& P, const DecView& D, const GapGroup& g,
+                                          double t0, double min_slot, const WarpScr& w, Variant& v) {
+  const int lane = lane_id();
+  v.t0 = t0;
+  v.t0_first = warp_t0_first(P, D, g, t0, min_slot);
+  v.S = warp_slot_ends(w.ends, w.Sc, v.t0_first, t0, g.gap, min_slot);
+  v.valid = true;
+  const int S = v.S;
+  const bool fits = S <= w.Sc;
+  int cap_err = 0;
+  if (fits) {
+    for (int s = lane; s < S; s += 32) {
+      const double dur = w.ends[s] - (s == 0 ? 0.0 : w.ends[s - 1]);
+      const int64_t c = plan_time2bs(P, dur, 0);
+      if (c < 0) cap_err = 1;
+      w.cap[s] = imin(c, P.max_batch);
+      w.nx[s] = 0;
+    }
+    for (int x = lane; x < S * P.L; x += 32) w.hc[x] = 0;  // layout hc[l*S + s]
+  }
+  v.cap_err = warp_or(cap_err) != 0;
+  __syncwarp();
+  int64_t late = 0, dues = 0;
+  int fail = 0, spill = 0;
+  if (g.exact) {
+    for (int k = lane; k < D.n; k += 32) {
+      const Member m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], g.now, g.a, g.pull);
+      if (!m.valid || m.rem <= 0) continue;
+      int64_t issued = m.backlog > 0 ? imin(m.backlog, m.rem) : 0;
+      late += issued;
+      const double tpot = P.tpot[m.tier];
+      for (double d = dmax(m.phase, 0.0); time_le(d, g.horizon) && issued < m.rem; d += tpot, ++issued) {
+        if (!time_le(d, g.gap)) spill = 1;
+        if (d <= kTimeEps) {
+          ++late;
+        } else {
+          ++dues;
+          if (fits) {
+            const int jit = jit_search(w.ends, S, d);
+            if (jit < 0) fail = 1; else atomicAdd(&w.nx[jit], 1);
+          }
+        }
+      }
+    }
+  }
+  v.Lx = warp_sum(late);
+  v.Dx = warp_sum(dues) + v.Lx;
+  v.exact_fail = warp_or(fail) != 0;
+  v.spill = warp_or(spill) != 0;
+  // canonical dues per tier (batch_planner.cpp:214-220): lane l owns tier l
+  int q = 0, cf = 0;
+  if (lane < P.L) {
+    const double tpot = P.tpot[lane];
+    for (double d = tpot; time_le(d, g.gap); d += tpot) {
+      ++q;
+      if (fits) {
+        const int jit = jit_search(w.ends, S, d);
+        if (jit < 0) cf = 1; else w.hc[lane * S + jit] += 1;
+      }
+    }
+  }
+  for (int l = 0; l < P.L; ++l) v.q[l] = __shfl_sync(0xffffffffu, q, l);
+  v.cfail = __ballot_sync(0xffffffffu, cf != 0);
+  __syncwarp();
+}
+
+// Canonical-only variant (no exact members) for the speculative remainder
+// tile_gap_ar(gap - used, rest) (batch_planner.cpp:390-395).
+__device__ inline void warp_build_canon_variant(const PlannerDev& P, double gap, double t0,
+                                                double min_slot, double* ends, int64_t* cap,
+                                                int32_t* hc, int Sc, Variant& v) {
+  const int lane = lane_id();
+  v.t0 = t0;
+  v.t0_first = t0;
+  v.S = warp_slot_ends(ends, Sc, t0, t0, gap, min_slot);
+  v.valid = true;
+  const int S = v.S;
+  const bool fits = S <= Sc;
+  int cap_err = 0;
+  if (fits) {
+    for (int s = lane; s < S; s += 32) {
+      const double dur = ends[s] - (s == 0 ? 0.0 : ends[s - 1]);
+      const int64_t c = plan_time2bs(P, dur, 0);
+      if (c < 0) cap_err = 1;
+      cap[s] = imin(c, P.max_batch);
+    }
+    for (int x = lane; x < S * P.L; x += 32) hc[x] = 0;
+  }
+  v.cap_err = warp_or(cap_err) != 0;
+  v.Lx = 0;
+  v.Dx = 0;
+  v.exact_fail = false;
+  v.spill = false;
+  __syncwarp();
+  int q = 0, cf = 0;
+  if (lane < P.L) {
+    const double tpot = P.tpot[lane];
+    for (double d = tpot; time_le(d, gap); d += tpot) {
+      ++q;
+      if (fits) {
+        const int jit = jit_search(ends, S, d);
+        if (jit < 0) cf = 1; else hc[lane * S + jit] += 1;
+      }
+    }
+  }
+  for (int l = 0; l < P.L; ++l) v.q[l] = __shfl_sync(0xffffffffu, q, l);
+  v.cfail = __ballot_sync(0xffffffffu, cf != 0);
+  __syncwarp();
+}
+
+// prefill_only lambda (batch_planner.cpp:177-195), budget only. status!=0 on throw.
+__device__ inline int64_t prefill_only_budget(const PlannerDev& P, double gap, double min_slot,
+                                              int* status) {
+  double t = 0.0;
+  int64_t budget = 0;
+  for (long guard = 0; gap - t >= min_slot - kTimeEps; ++guard) {
+    int64_t size = plan_time2bs(P, gap - t, 0);
+    if (size < 0) { *status = SLOS_ERR_INFEASIBLE_BUDGET; return 0; }
+    if (guard > 100000000L) { *status = SLOS_ERR_INTERNAL_INCONSISTENCY; return 0; }
+    size = imin(size, P.max_chunk);
+    const double dur = plan_predict(P, size, 0);
+    budget += size;
+    t += dur;
+  }
+  *status = 0;
+  return budget;
+}
+
+// Latest-fit placement budget for counts c over a built variant (warp, lanes over
+// slots). Returns 1 = feasible (*budget set), 0 = nullopt.
+__device__ inline int warp_place_budget(const PlannerDev& P, const Variant& v, const double* ends,
+                                        const int64_t* cap, const int32_t* nx, const int32_t* hc,
+                                        int64_t* tmp, const int64_t* c, int64_t* budget) {
+  (void)ends;
+  const int lane = lane_id();
+  const int S = v.S;
+  const int L = P.L;
+  // forward pass: free capacity after late dues, F - D prefix
+  int64_t carry_cap = 0, carry_F = 0, carry_D = 0, min_diff = INT64_MAX;
+  for (int base = 0; base < S; base += 32) {
+    const int s = base + lane;
+    int64_t capv = 0, n = 0;
+    if (s < S) {
+      capv = cap[s];
+      n = nx ? nx[s] : 0;
+      for (int l = 0; l < L; ++l)
+        if (c[l] > 0) n += c[l] * (int64_t)hc[l * S + s];
+    }
+    const int64_t cc = warp_incl_scan(capv) + carry_cap;
+    const int64_t before = cc - capv;
+    int64_t used = v.Lx - before;
+    used = used < 0 ? 0 : (used > capv ? capv : used);
+    const int64_t free0 = capv - used;
+    const int64_t F = warp_incl_scan(free0) + carry_F;
+    const int64_t Dn = warp_incl_scan(n) + carry_D;
+    const int64_t diff = F - Dn;
+    if (s < S) tmp[s] = diff;
+    min_diff = imin(min_diff, s < S ? diff : INT64_MAX);
+    carry_cap = __shfl_sync(0xffffffffu, cc, 31);
+    carry_F = __shfl_sync(0xffffffffu, F, 31);
+    carry_D = __shfl_sync(0xffffffffu, Dn, 31);
+  }
+  min_diff = warp_min(min_diff);
+  if (v.Lx > carry_cap) return 0;  // a late due finds every slot full
+  if (min_diff < 0) return 0;      // some jit group overflows
+  __syncwarp();
+  // suffix minima G(s) = min_{u>=s} diff(u), stored in place (backwards chunks)
+  int64_t carry_min = INT64_MAX;
+  const int nch = (S + 31) / 32;
+  for (int ch = nch - 1; ch >= 0; --ch) {
+    const int s = ch * 32 + lane;
+    int64_t x = s < S ? tmp[s] : INT64_MAX;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {  // suffix min within the chunk
+      const int64_t y = __shfl_down_sync(0xffffffffu, x, o);
+      if (lane + o < 32) x = imin(x, y);
+    }
+    x = imin(x, carry_min);
+    __syncwarp();
+    if (s < S) tmp[s] = x;
+    carry_min = __shfl_sync(0xffffffffu, x, 0);
+  }
+  __syncwarp();
+  int64_t b = 0;
+  for (int base = 0; base < S; base += 32) {
+    const int s = base + lane;
+    if (s < S) {
+      const int64_t f = tmp[s] - (s > 0 ? tmp[s - 1] : 0);
+      b += imin(f, P.max_chunk);
+    }
+  }
+  *budget = warp_sum(b);
+  __syncwarp();
+  return 1;
+}
+
+}  // namespace slos

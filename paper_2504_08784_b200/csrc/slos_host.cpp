@@ -1,0 +1,1194 @@
+// C-ABI implementation (include/slos_planner.h) of the product planner.
+//
+// Host side = the work the reference does before/around its DP that is host-
+// trivial or string-typed (SURVEY.md §7 hard part 6): validation
+// (dp_scheduler.cpp:367-392), the chain std::stable_sort with its eps/forced/id
+// comparator (:393-397, run here with libstdc++ so eps-tie behaviour is identical),
+// floor_at / suffix_prefill (:399-408), edf_fallback's prefill order (:121-124),
+// packing instances into SoA blobs, one H2D copy, the kernel pipeline
+// (dp_kernel -> build_kernel -> compact_kernel), one D2H copy of the packed
+// results, and capacity regrowth for the rare instance whose scratch estimate
+// was too small. There is no CPU fallback: without an sm_100 device every entry
+// point returns SLOS_ERR_NO_DEVICE.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "slos_dev.h"
+#include "slos_launch.h"
+#include "../../include/slos_planner.h"
+
+namespace slos {
+struct DpParams {
+  BatchArgs a;
+  int Sc;
+  int Lmax;
+  int dec_smem_max;
+  unsigned char* wscr_global;
+  size_t wscr_stride;
+};
+struct BuildParams {
+  BatchArgs a;
+};
+struct GapBatchOut {
+  double start_s, end_s;
+  int64_t capacity, spec_step, decode_tokens, prefill_budget;
+  int64_t per_tier[kMaxTiers];
+  int32_t first_owner, n_owner;
+};
+struct GapParams {
+  const PlannerDev* planner;
+  const GapQueryDev* q;
+  const double* ph;
+  const int64_t* bl;
+  const int64_t* rm;
+  const int32_t* tr;
+  const int32_t* ow;
+  GapBatchOut* ob;
+  int64_t* oo;
+  unsigned char* work;
+  GapOutDev* out;
+};
+struct SpecSolH {
+  bool ok;
+  int lengths[kMaxTiers];
+  double bt;
+  int64_t cap;
+  int64_t decode;
+  double tpt;
+};
+}  // namespace slos
+
+using namespace slos;
+
+// ------------------------------------------------------------------ state ---
+
+struct slos_planner {
+  PlannerDev dev;
+  std::vector<slos_perf_term> terms;
+  std::vector<double> tpot, slow;
+  int L = 0;
+  int tpot_window = 10;
+  slos_planner_config cfg{};
+  bool device_ok = true;  // representable on device (terms, tiers, spec length)
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = std::string(slos_status_slug(code)) + ": " + msg;
+  return code;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max(bytes, (size_t)1 << 20);
+    want = want + want / 4;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+};
+
+struct PinBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max(bytes, (size_t)1 << 20);
+    want = want + want / 4;
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocDefault);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+};
+
+// Pinned result arenas, reference counted by the slos_result objects that point
+// into them; recycled through a small pool.
+struct ResultArena {
+  std::atomic<int> refs{0};
+  void* p = nullptr;
+  size_t cap = 0;
+  bool pinned = true;
+};
+
+struct Ctx {
+  std::mutex mu;
+  bool init = false;
+  int status = SLOS_OK;
+  std::string why;
+  cudaStream_t stream = nullptr;
+  DevBuf d_in, d_scr, d_out, d_pack, d_wscr, d_small;
+  PinBuf h_in, h_small;
+  std::mutex pool_mu;
+  std::vector<ResultArena*> pool;
+};
+
+Ctx& ctx() {
+  static Ctx* c = new Ctx();  // never destroyed: results may outlive static teardown
+  return *c;
+}
+
+int ensure_device(Ctx& c) {
+  if (c.init) return c.status;
+  c.init = true;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    c.status = SLOS_ERR_NO_DEVICE;
+    c.why = "no CUDA device (the product has no CPU fallback)";
+    return c.status;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, dev);
+  if (prop.major != 10) {
+    c.status = SLOS_ERR_NO_DEVICE;
+    c.why = std::string("device ") + prop.name + " is not sm_100 (B200)";
+    return c.status;
+  }
+  e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    c.status = SLOS_ERR_CUDA;
+    c.why = cudaGetErrorString(e);
+    return c.status;
+  }
+  c.status = SLOS_OK;
+  return SLOS_OK;
+}
+
+ResultArena* arena_get(Ctx& c, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> g(c.pool_mu);
+    for (size_t i = 0; i < c.pool.size(); ++i) {
+      if (c.pool[i]->cap >= bytes) {
+        ResultArena* a = c.pool[i];
+        c.pool.erase(c.pool.begin() + (long)i);
+        return a;
+      }
+    }
+  }
+  ResultArena* a = new ResultArena();
+  size_t want = std::max(bytes, (size_t)1 << 16);
+  if (cudaHostAlloc(&a->p, want, cudaHostAllocDefault) != cudaSuccess) {
+    a->p = std::malloc(want);  // pageable is still correct, only slower to fill
+    if (!a->p) { delete a; return nullptr; }
+    a->cap = want;
+    a->pinned = false;
+    return a;
+  }
+  a->cap = want;
+  return a;
+}
+
+void arena_release(ResultArena* a) {
+  Ctx& c = ctx();
+  if (--a->refs != 0) return;
+  if (!a->pinned) {
+    std::free(a->p);
+    delete a;
+    return;
+  }
+  {
+    std::lock_guard<std::mutex> g(c.pool_mu);
+    if (c.pool.size() < 4) {
+      c.pool.push_back(a);
+    } else {
+      cudaFreeHost(a->p);
+      delete a;
+    }
+  }
+}
+
+void arena_addref(ResultArena* a) { ++a->refs; }
+
+// ------------------------------------------------------------ blob layout ---
+
+struct Blob {
+  size_t bytes = 0;
+  template <typename T>
+  size_t add(size_t count) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    const size_t o = bytes;
+    bytes += sizeof(T) * std::max<size_t>(count, 1);
+    return o;
+  }
+};
+
+bool integral(double v) { return std::isfinite(v) && v == std::floor(v) && std::fabs(v) < 4.0e15; }
+
+struct Prep {  // host-side per-instance preparation
+  int status = SLOS_OK;
+  std::string why;
+  int planner = 0;
+  int N = 0, n_dec = 0, n_pre = 0;
+  int last_forced = -1;
+  bool have_rd = false;
+  bool values_integral = true;
+  std::vector<int> chain;  // encoded: >=0 running idx (forced), <0 -(pending+1)
+  std::vector<int> pre;    // running indices, EDF order
+  double span = 0.0;       // max gap bound for slot capacity
+  double tail_bound = 0.0;
+  int64_t max_rem = 0;
+};
+
+struct ChainKey {
+  bool forced;
+  const char* id;
+  double deadline;
+  int enc;
+};
+
+int prep_instance(const slos_planner* P, const slos_input* in, int unit_value, Prep& pr) {
+  const int L = P->L;
+  if (L > 8) return set_err(SLOS_ERR_INVALID_PARAMETERS, "at most 8 SLO tiers supported");
+  if (!P->device_ok) return set_err(SLOS_ERR_RANGE, "planner not representable on device");
+  std::vector<ChainKey> ch;
+  ch.reserve((size_t)in->n_running + (size_t)in->n_pending);
+  for (int i = 0; i < in->n_running; ++i) {
+    const slos_running& r = in->running[i];
+    if (r.prefill_remaining <= 0) continue;
+    ch.push_back({true, r.id ? r.id : "", r.prefill_deadline, i});
+  }
+  for (int i = 0; i < in->n_pending; ++i) {
+    const slos_pending& p = in->pending[i];
+    ch.push_back({false, p.id ? p.id : "", p.prefill_deadline, -(i + 1)});
+  }
+  if (ch.size() > 250) return set_err(SLOS_ERR_INVALID_PARAMETERS, "admission chain too large");
+  for (const ChainKey& k : ch) {
+    const int tier = k.enc >= 0 ? in->running[k.enc].decode_tier : in->pending[-k.enc - 1].decode_tier;
+    if (tier < 0 || tier >= L) return set_err(SLOS_ERR_INVALID_PARAMETERS, "bad SLO tier");
+  }
+  for (int i = 0; i < in->n_running; ++i) {
+    const slos_running& r = in->running[i];
+    if (r.prefill_remaining <= 0 && r.decode_remaining > 0 && (r.decode_tier < 0 || r.decode_tier >= L))
+      return set_err(SLOS_ERR_INVALID_PARAMETERS, "vector::_M_range_check: running decode tier");
+  }
+  std::stable_sort(ch.begin(), ch.end(), [](const ChainKey& a, const ChainKey& b) {
+    if (std::abs(a.deadline - b.deadline) > kTimeEps) return a.deadline < b.deadline;
+    if (a.forced != b.forced) return a.forced;
+    return std::strcmp(a.id, b.id) < 0;
+  });
+  pr.N = (int)ch.size();
+  pr.chain.resize(ch.size());
+  double maxdl = in->now, mindl = in->now;
+  for (size_t k = 0; k < ch.size(); ++k) {
+    pr.chain[k] = ch[k].enc;
+    if (ch[k].forced) pr.last_forced = (int)k;
+    maxdl = std::max(maxdl, ch[k].deadline);
+    mindl = std::min(mindl, ch[k].deadline);
+    const double v = ch[k].forced ? 0.0 : (unit_value ? 1.0 : in->pending[-ch[k].enc - 1].value);
+    if (!integral(v)) pr.values_integral = false;
+  }
+  pr.span = std::max(0.0, maxdl - mindl);
+  struct PreKey { int idx; double ddl; const char* id; };
+  std::vector<PreKey> pre;
+  double tb = 0.0;
+  for (int i = 0; i < in->n_running; ++i) {
+    const slos_running& r = in->running[i];
+    if (r.prefill_remaining > 0) {
+      pre.push_back({i, r.prefill_deadline, r.id ? r.id : ""});
+    } else if (r.decode_remaining > 0) {
+      pr.n_dec++;
+      pr.have_rd = true;
+      const double tp = P->tpot[r.decode_tier];
+      tb = std::max(tb, (r.next_due_s - in->now) + tp);
+      pr.max_rem = std::max(pr.max_rem, r.decode_remaining + std::max<int64_t>(0, r.backlog));
+    }
+  }
+  std::stable_sort(pre.begin(), pre.end(), [](const PreKey& a, const PreKey& b) {
+    if (std::abs(a.ddl - b.ddl) > kTimeEps) return a.ddl < b.ddl;
+    return std::strcmp(a.id, b.id) < 0;
+  });
+  pr.n_pre = (int)pre.size();
+  pr.pre.resize(pre.size());
+  for (size_t k = 0; k < pre.size(); ++k) pr.pre[k] = pre[k].idx;
+  double max_tpot = 0.0;
+  for (int l = 0; l < L; ++l) max_tpot = std::max(max_tpot, P->tpot[l]);
+  pr.tail_bound = std::max({2.0 * max_tpot, in->tail_horizon_s, tb, 0.0});
+  return SLOS_OK;
+}
+
+// capacities (scratch) per instance; `grow` multiplies them after an overflow
+struct Caps {
+  int64_t surv, cand, memo, batch, entry, work, gb, go;
+};
+
+int64_t pow2_at_least(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+Caps estimate_caps(const slos_planner* P, const slos_input* in, const Prep& pr, int grow) {
+  Caps c;
+  const double t0 = P->tpot[0];
+  const int64_t S_gap = (int64_t)std::ceil(pr.span / t0) + 6;
+  const int64_t S_tail = (int64_t)std::ceil(pr.tail_bound / t0) + 6;
+  const int64_t S = std::max<int64_t>({S_gap, S_tail, 16});
+  const int64_t M = pr.n_dec + pr.N + 1;
+  const int64_t g = (int64_t)1 << (2 * grow);
+  c.surv = std::max<int64_t>(1024, 64 * (int64_t)(pr.N + 1)) * g;
+  c.cand = pow2_at_least(std::max<int64_t>(512, 16 * (int64_t)(pr.N + 1)) * g);
+  c.memo = pow2_at_least(std::max<int64_t>(2048, 64 * (int64_t)(pr.N + 1)) * g);
+  c.gb = (S + 8) * (grow + 1);
+  c.go = M * c.gb;
+  // plan output: gaps + tail, or the fallback (until every line completes)
+  double max_tpot = 0.0;
+  for (int l = 0; l < P->L; ++l) max_tpot = std::max(max_tpot, P->tpot[l]);
+  int64_t pre_tokens = 0;
+  for (int i = 0; i < in->n_running; ++i)
+    if (in->running[i].prefill_remaining > 0) pre_tokens += in->running[i].prefill_remaining;
+  const int64_t fb_batches = pr.max_rem * ((int64_t)std::ceil(max_tpot / t0) + 1) +
+                             pre_tokens / std::max<int64_t>(1, P->cfg.max_chunk_tokens) + pr.n_pre + 16;
+  c.batch = std::max<int64_t>((pr.N + 2) * (S + 4), std::min<int64_t>(fb_batches, 100000)) * (grow + 1) + 64;
+  c.entry = std::max<int64_t>(c.batch * (pr.n_dec + pr.N + 1) / 2, 1024) * (grow + 1);
+  const int64_t engine = S * (M + 1) * 4 + S * (64 + 8 * P->L) + M * 48 + 64 * M + (1 << 16);
+  c.work = (M * 32 + 2 * c.gb * (int64_t)sizeof(GapBatchOut) + 16 * c.go + engine) * (grow + 1);
+  return c;
+}
+
+void fill_planner_dev(slos_planner* p) {
+  PlannerDev& d = p->dev;
+  std::memset(&d, 0, sizeof d);
+  p->device_ok = p->terms.size() <= (size_t)kMaxTerms && p->L <= kMaxTiers &&
+                 (!p->cfg.speculative || p->cfg.spec_max_len <= kMaxSpecLen);
+  d.n_terms = (int32_t)std::min<size_t>(p->terms.size(), kMaxTerms);
+  for (int t = 0; t < d.n_terms; ++t) {
+    d.k1[t] = p->terms[t].k1;
+    d.k2[t] = p->terms[t].k2;
+    d.b[t] = p->terms[t].b;
+  }
+  d.L = std::min(p->L, kMaxTiers);
+  for (int l = 0; l < d.L; ++l) d.tpot[l] = p->tpot[l];
+  d.margin1 = 1.0 + p->cfg.plan_margin;
+  d.spec_alpha = p->cfg.spec_alpha;
+  d.max_chunk = p->cfg.max_chunk_tokens;
+  d.max_batch = p->cfg.max_batch_tokens;
+  d.speculative = p->cfg.speculative ? 1 : 0;
+  d.spec_max_len = std::min(p->cfg.spec_max_len, kMaxSpecLen);
+  for (int sl = 1; sl <= d.spec_max_len; ++sl) d.acc[sl] = slos_expected_accepted(p->cfg.spec_alpha, sl);
+}
+
+// ---------------------------------------------------------- batch runner ---
+
+struct Job {
+  int k;      // index into the caller's arrays
+  int grow;   // capacity growth step
+};
+
+struct Layout {
+  size_t planners, inst, order, dec_idx, dec_tier, dec_next, dec_backlog, dec_rem;
+  size_t ch_deadline, ch_prefill, ch_tier, ch_memory, ch_value, ch_forced, ch_ref, ch_floor, ch_suffix;
+  size_t pre_idx, pre_left, run_tier;
+  size_t in_bytes;
+  size_t s_counts, s_mem, s_pb, s_value, s_nadm, s_parent, s_arena, s_level;
+  size_t c_src, c_j, c_memo, c_flag, c_bucket, c_pos, c_aux, c_counts, c_mem, c_pb, c_value, c_nadm;
+  size_t c_bkey, c_bval, memo, work, scr_bytes;
+  size_t out, sel, ids, batches, entries, out_bytes;
+};
+
+int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, int unit_value,
+             const std::vector<Job>& jobs, slos_result* outs, std::vector<Job>& retry) {
+  const int n = (int)jobs.size();
+  if (n == 0) return SLOS_OK;
+  // ---- host preparation ----
+  std::vector<Prep> prep(n);
+  std::vector<const slos_planner*> plist;
+  std::vector<int> valid;
+  int64_t TD = 0, TC = 0, TP = 0, TR = 0, TS = 0, TCd = 0, TM = 0, TW = 0, TSel = 0, TIds = 0, TB = 0, TE = 0;
+  std::vector<Caps> caps(n);
+  int maxN = 0, maxDec = 0, Lmax = 1;
+  double S_need = 16;
+  for (int q = 0; q < n; ++q) {
+    const int k = jobs[q].k;
+    const slos_planner* P = planners[k];
+    Prep& pr = prep[q];
+    pr.status = prep_instance(P, &inputs[k], unit_value, pr);
+    if (pr.status != SLOS_OK) {
+      std::memset(&outs[k], 0, sizeof(outs[k]));
+      outs[k].status = pr.status;
+      continue;
+    }
+    int pi = -1;
+    for (size_t x = 0; x < plist.size(); ++x) if (plist[x] == P) { pi = (int)x; break; }
+    if (pi < 0) { pi = (int)plist.size(); plist.push_back(P); }
+    pr.planner = pi;
+    valid.push_back(q);
+    caps[q] = estimate_caps(P, &inputs[k], pr, jobs[q].grow);
+    TD += pr.n_dec;
+    TC += pr.N + 1;
+    TP += pr.n_pre;
+    TR += inputs[k].n_running;
+    TS += caps[q].surv;
+    TCd += caps[q].cand;
+    TM += caps[q].memo;
+    TW += (caps[q].work + 255) & ~(int64_t)255;
+    TSel += pr.N + 1;
+    TIds += 2 * (int64_t)inputs[k].n_pending + 1;
+    TB += caps[q].batch;
+    TE += caps[q].entry;
+    maxN = std::max(maxN, pr.N);
+    maxDec = std::max(maxDec, pr.n_dec);
+    Lmax = std::max(Lmax, P->L);
+    S_need = std::max(S_need, std::ceil(pr.span / P->tpot[0]) + 8);
+  }
+  const int nv = (int)valid.size();
+  if (nv == 0) return SLOS_OK;
+  Layout Ly;
+  Blob bi;
+  Ly.planners = bi.add<PlannerDev>(plist.size());
+  Ly.inst = bi.add<InstDev>(nv);
+  Ly.order = bi.add<int32_t>(nv);
+  Ly.dec_idx = bi.add<int32_t>(TD);
+  Ly.dec_tier = bi.add<int32_t>(TD);
+  Ly.dec_next = bi.add<double>(TD);
+  Ly.dec_backlog = bi.add<int64_t>(TD);
+  Ly.dec_rem = bi.add<int64_t>(TD);
+  Ly.ch_deadline = bi.add<double>(TC);
+  Ly.ch_prefill = bi.add<int64_t>(TC);
+  Ly.ch_tier = bi.add<int32_t>(TC);
+  Ly.ch_memory = bi.add<int64_t>(TC);
+  Ly.ch_value = bi.add<double>(TC);
+  Ly.ch_forced = bi.add<int32_t>(TC);
+  Ly.ch_ref = bi.add<int32_t>(TC);
+  Ly.ch_floor = bi.add<int32_t>(TC);
+  Ly.ch_suffix = bi.add<int64_t>(TC);
+  Ly.pre_idx = bi.add<int32_t>(TP);
+  Ly.pre_left = bi.add<int64_t>(TP);
+  Ly.run_tier = bi.add<int32_t>(TR);
+  Ly.in_bytes = bi.bytes;
+  Blob bs;
+  Ly.s_counts = bs.add<uint64_t>(TS);
+  Ly.s_mem = bs.add<int64_t>(TS);
+  Ly.s_pb = bs.add<int64_t>(TS);
+  Ly.s_value = bs.add<double>(TS);
+  Ly.s_nadm = bs.add<int32_t>(TS);
+  Ly.s_parent = bs.add<int32_t>(TS);
+  Ly.s_arena = bs.add<int32_t>(TS);
+  Ly.s_level = bs.add<int32_t>(TS);
+  Ly.c_src = bs.add<int32_t>(TCd);
+  Ly.c_j = bs.add<int32_t>(TCd);
+  Ly.c_memo = bs.add<int32_t>(TCd);
+  Ly.c_flag = bs.add<int32_t>(TCd);
+  Ly.c_bucket = bs.add<int32_t>(TCd);
+  Ly.c_pos = bs.add<int32_t>(TCd);
+  Ly.c_aux = bs.add<int32_t>(TCd);
+  Ly.c_counts = bs.add<uint64_t>(TCd);
+  Ly.c_mem = bs.add<int64_t>(TCd);
+  Ly.c_pb = bs.add<int64_t>(TCd);
+  Ly.c_value = bs.add<double>(TCd);
+  Ly.c_nadm = bs.add<int32_t>(TCd);
+  Ly.c_bkey = bs.add<uint64_t>(2 * TCd);
+  Ly.c_bval = bs.add<int32_t>(2 * TCd);
+  Ly.memo = bs.add<MemoEnt>(TM);
+  Ly.work = bs.add<unsigned char>(TW);
+  Ly.scr_bytes = bs.bytes;
+  Blob bo;
+  Ly.out = bo.add<OutHdr>(nv);
+  Ly.sel = bo.add<int32_t>(TSel);
+  Ly.ids = bo.add<int32_t>(TIds);
+  Ly.batches = bo.add<slos_batch>(TB);
+  Ly.entries = bo.add<slos_entry>(TE);
+  Ly.out_bytes = bo.bytes;
+
+  cudaError_t e;
+  if ((e = c.h_in.ensure(Ly.in_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  if ((e = c.d_in.ensure(Ly.in_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  if ((e = c.d_scr.ensure(Ly.scr_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  if ((e = c.d_out.ensure(Ly.out_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  unsigned char* H = (unsigned char*)c.h_in.p;
+  auto hp = [&](size_t off) { return H + off; };
+  PlannerDev* hP = (PlannerDev*)hp(Ly.planners);
+  for (size_t x = 0; x < plist.size(); ++x) hP[x] = plist[x]->dev;
+  InstDev* hI = (InstDev*)hp(Ly.inst);
+  int32_t* h_dec_idx = (int32_t*)hp(Ly.dec_idx);
+  int32_t* h_dec_tier = (int32_t*)hp(Ly.dec_tier);
+  double* h_dec_next = (double*)hp(Ly.dec_next);
+  int64_t* h_dec_bl = (int64_t*)hp(Ly.dec_backlog);
+  int64_t* h_dec_rem = (int64_t*)hp(Ly.dec_rem);
+  double* h_dl = (double*)hp(Ly.ch_deadline);
+  int64_t* h_pf = (int64_t*)hp(Ly.ch_prefill);
+  int32_t* h_tr = (int32_t*)hp(Ly.ch_tier);
+  int64_t* h_mm = (int64_t*)hp(Ly.ch_memory);
+  double* h_vl = (double*)hp(Ly.ch_value);
+  int32_t* h_fc = (int32_t*)hp(Ly.ch_forced);
+  int32_t* h_rf = (int32_t*)hp(Ly.ch_ref);
+  int32_t* h_fl = (int32_t*)hp(Ly.ch_floor);
+  int64_t* h_sf = (int64_t*)hp(Ly.ch_suffix);
+  int32_t* h_pre_idx = (int32_t*)hp(Ly.pre_idx);
+  int64_t* h_pre_left = (int64_t*)hp(Ly.pre_left);
+  int32_t* h_run_tier = (int32_t*)hp(Ly.run_tier);
+  int64_t oD = 0, oC = 0, oP = 0, oR = 0, oS = 0, oCd = 0, oM = 0, oW = 0, oSel = 0, oIds = 0, oB = 0, oE = 0;
+  std::vector<double> cost(nv);
+  for (int v = 0; v < nv; ++v) {
+    const int q = valid[v];
+    const int k = jobs[q].k;
+    const slos_input* in = &inputs[k];
+    const Prep& pr = prep[q];
+    const Caps& cp = caps[q];
+    InstDev& I = hI[v];
+    std::memset(&I, 0, sizeof I);
+    I.now = in->now;
+    I.tail_horizon = in->tail_horizon_s;
+    I.mem_budget = in->memory_total - in->memory_standard_resident;
+    I.planner = pr.planner;
+    I.unit_value = unit_value;
+    I.R_total = in->n_running;
+    I.n_dec = pr.n_dec;
+    I.N = pr.N;
+    I.n_pre = pr.n_pre;
+    I.n_pending = in->n_pending;
+    I.last_forced = pr.last_forced;
+    I.have_running_decode = pr.have_rd ? 1 : 0;
+    I.values_integral = pr.values_integral ? 1 : 0;
+    I.off_dec = oD;
+    I.off_chain = oC;
+    I.off_pre = oP;
+    I.off_run = oR;
+    I.off_surv = oS; I.cap_surv = cp.surv;
+    I.off_cand = oCd; I.cap_cand = cp.cand;
+    I.off_memo = oM; I.cap_memo = cp.memo;
+    I.off_sel = oSel;
+    I.off_ids = oIds;
+    I.off_batch = oB; I.cap_batch = cp.batch;
+    I.off_entry = oE; I.cap_entry = cp.entry;
+    I.off_work = oW; I.cap_work = cp.work;
+    I.cap_gb = cp.gb;
+    I.cap_go = cp.go;
+    for (int i = 0; i < in->n_running; ++i) {
+      const slos_running& r = in->running[i];
+      h_run_tier[oR + i] = r.decode_tier;
+      if (r.prefill_remaining <= 0 && r.decode_remaining > 0) {
+        h_dec_idx[oD] = i;
+        h_dec_tier[oD] = r.decode_tier;
+        h_dec_next[oD] = r.next_due_s;
+        h_dec_bl[oD] = r.backlog;
+        h_dec_rem[oD] = r.decode_remaining;
+        ++oD;
+      }
+    }
+    for (int x = 0; x < pr.n_pre; ++x) {
+      h_pre_idx[oP + x] = pr.pre[x];
+      h_pre_left[oP + x] = in->running[pr.pre[x]].prefill_remaining;
+    }
+    int lf = -1;
+    for (int x = 0; x < pr.N; ++x) {
+      const int enc = pr.chain[x];
+      const int64_t o = oC + x;
+      h_fl[o] = lf;
+      if (enc >= 0) {
+        const slos_running& r = in->running[enc];
+        h_dl[o] = r.prefill_deadline;
+        h_pf[o] = r.prefill_remaining;
+        h_tr[o] = r.decode_tier;
+        h_mm[o] = 0;
+        h_vl[o] = 0.0;
+        h_fc[o] = 1;
+        h_rf[o] = enc;
+        lf = x;
+      } else {
+        const slos_pending& p = in->pending[-enc - 1];
+        h_dl[o] = p.prefill_deadline;
+        h_pf[o] = p.prefill_tokens;
+        h_tr[o] = p.decode_tier;
+        h_mm[o] = p.memory_units;
+        h_vl[o] = unit_value ? 1.0 : p.value;
+        h_fc[o] = 0;
+        h_rf[o] = enc;
+      }
+    }
+    h_sf[oC + pr.N] = 0;
+    for (int x = pr.N - 1; x >= 0; --x) h_sf[oC + x] = h_sf[oC + x + 1] + h_pf[oC + x];
+    cost[v] = (double)(pr.n_dec + 8) * (double)(pr.N + 1) * (double)(pr.N + 1);
+    oD += 0;  // advanced in the loop above
+    oC += pr.N + 1;
+    oP += pr.n_pre;
+    oR += in->n_running;
+    oS += cp.surv;
+    oCd += cp.cand;
+    oM += cp.memo;
+    oW += (cp.work + 255) & ~(int64_t)255;
+    oSel += pr.N + 1;
+    oIds += 2 * (int64_t)in->n_pending + 1;
+    oB += cp.batch;
+    oE += cp.entry;
+  }
+  int32_t* h_order = (int32_t*)hp(Ly.order);
+  {
+    std::vector<int> ord(nv);
+    for (int v = 0; v < nv; ++v) ord[v] = v;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    for (int v = 0; v < nv; ++v) h_order[v] = ord[v];
+  }
+  // ---- device pipeline ----
+  unsigned char* DI = (unsigned char*)c.d_in.p;
+  unsigned char* DS = (unsigned char*)c.d_scr.p;
+  unsigned char* DO = (unsigned char*)c.d_out.p;
+  cudaStream_t s = c.stream;
+  cudaMemcpyAsync(DI, H, Ly.in_bytes, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(DS + Ly.memo, 0, sizeof(MemoEnt) * TM, s);
+  cudaMemsetAsync(DS + Ly.c_bkey, 0, sizeof(uint64_t) * 2 * TCd, s);
+  cudaMemsetAsync(DS + Ly.c_bval, 0xFF, sizeof(int32_t) * 2 * TCd, s);
+  cudaMemsetAsync(DO + Ly.out, 0, sizeof(OutHdr) * nv, s);
+  BatchArgs A;
+  std::memset(&A, 0, sizeof A);
+  A.planners = (const PlannerDev*)(DI + Ly.planners);
+  A.inst = (const InstDev*)(DI + Ly.inst);
+  A.order = (const int32_t*)(DI + Ly.order);
+  A.n_inst = nv;
+  A.dec_idx = (const int32_t*)(DI + Ly.dec_idx);
+  A.dec_tier = (const int32_t*)(DI + Ly.dec_tier);
+  A.dec_next = (const double*)(DI + Ly.dec_next);
+  A.dec_backlog = (const int64_t*)(DI + Ly.dec_backlog);
+  A.dec_rem = (const int64_t*)(DI + Ly.dec_rem);
+  A.ch_deadline = (const double*)(DI + Ly.ch_deadline);
+  A.ch_prefill = (const int64_t*)(DI + Ly.ch_prefill);
+  A.ch_tier = (const int32_t*)(DI + Ly.ch_tier);
+  A.ch_memory = (const int64_t*)(DI + Ly.ch_memory);
+  A.ch_value = (const double*)(DI + Ly.ch_value);
+  A.ch_forced = (const int32_t*)(DI + Ly.ch_forced);
+  A.ch_ref = (const int32_t*)(DI + Ly.ch_ref);
+  A.ch_floor = (const int32_t*)(DI + Ly.ch_floor);
+  A.ch_suffix = (const int64_t*)(DI + Ly.ch_suffix);
+  A.pre_idx = (const int32_t*)(DI + Ly.pre_idx);
+  A.pre_left = (const int64_t*)(DI + Ly.pre_left);
+  A.run_tier = (const int32_t*)(DI + Ly.run_tier);
+  A.s_counts = (uint64_t*)(DS + Ly.s_counts);
+  A.s_mem = (int64_t*)(DS + Ly.s_mem);
+  A.s_pb = (int64_t*)(DS + Ly.s_pb);
+  A.s_value = (double*)(DS + Ly.s_value);
+  A.s_nadm = (int32_t*)(DS + Ly.s_nadm);
+  A.s_parent = (int32_t*)(DS + Ly.s_parent);
+  A.s_arena = (int32_t*)(DS + Ly.s_arena);
+  A.s_level = (int32_t*)(DS + Ly.s_level);
+  A.c_src = (int32_t*)(DS + Ly.c_src);
+  A.c_j = (int32_t*)(DS + Ly.c_j);
+  A.c_memo = (int32_t*)(DS + Ly.c_memo);
+  A.c_flag = (int32_t*)(DS + Ly.c_flag);
+  A.c_bucket = (int32_t*)(DS + Ly.c_bucket);
+  A.c_pos = (int32_t*)(DS + Ly.c_pos);
+  A.c_aux = (int32_t*)(DS + Ly.c_aux);
+  A.c_counts = (uint64_t*)(DS + Ly.c_counts);
+  A.c_mem = (int64_t*)(DS + Ly.c_mem);
+  A.c_pb = (int64_t*)(DS + Ly.c_pb);
+  A.c_value = (double*)(DS + Ly.c_value);
+  A.c_nadm = (int32_t*)(DS + Ly.c_nadm);
+  A.c_bkey = (uint64_t*)(DS + Ly.c_bkey);
+  A.c_bval = (int32_t*)(DS + Ly.c_bval);
+  A.memo = (MemoEnt*)(DS + Ly.memo);
+  A.work = DS + Ly.work;
+  A.out = (OutHdr*)(DO + Ly.out);
+  A.sel = (int32_t*)(DO + Ly.sel);
+  A.ids = (int32_t*)(DO + Ly.ids);
+  A.batches = (slos_batch*)(DO + Ly.batches);
+  A.entries = (slos_entry*)(DO + Ly.entries);
+
+  DpParams dp;
+  dp.a = A;
+  dp.Lmax = Lmax;
+  dp.Sc = (int)std::min<double>(S_need, 1 << 20);
+  const size_t stride = dp_warp_scr_stride(dp.Sc, Lmax);
+  dp.wscr_stride = stride;
+  const size_t kSmemBudget = 100 * 1024;
+  size_t smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, true);
+  if (smem <= kSmemBudget) {
+    dp.wscr_global = nullptr;
+  } else {
+    if ((e = c.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    dp.wscr_global = (unsigned char*)c.d_wscr.p;
+    smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, false);
+  }
+  dp.dec_smem_max = 0;
+  {
+    const size_t with_dec = dp_smem_bytes(maxN, maxDec, dp.Sc, Lmax, dp.wscr_global == nullptr);
+    if (with_dec <= kSmemBudget) { dp.dec_smem_max = maxDec; smem = with_dec; }
+  }
+  if ((e = launch_dp(dp, nv, smem, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  BuildParams bp;
+  bp.a = A;
+  if ((e = launch_build(bp, nv, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  // ---- headers back, capacity check ----
+  if ((e = c.h_small.ensure(sizeof(OutHdr) * nv)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  OutHdr* hO = (OutHdr*)c.h_small.p;
+  cudaMemcpyAsync(hO, DO + Ly.out, sizeof(OutHdr) * nv, cudaMemcpyDeviceToHost, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  std::vector<OutHdr> hdr(hO, hO + nv);
+  // packed offsets
+  std::vector<int64_t> boff(nv, 0), eoff(nv, 0), ioff(nv, 0);
+  size_t packed = 0;
+  std::vector<int> good;
+  for (int v = 0; v < nv; ++v) {
+    const int q = valid[v];
+    const OutHdr& h = hdr[v];
+    if (h.status == SLOS_ERR_CAPACITY && jobs[q].grow < 6) {
+      retry.push_back({jobs[q].k, jobs[q].grow + 1});
+      continue;
+    }
+    if (h.status != SLOS_OK) continue;
+    good.push_back(v);
+    packed = (packed + 15) & ~(size_t)15;
+    boff[v] = (int64_t)packed;
+    packed += sizeof(slos_batch) * (size_t)h.n_batches;
+    packed = (packed + 15) & ~(size_t)15;
+    eoff[v] = (int64_t)packed;
+    packed += sizeof(slos_entry) * (size_t)h.n_entries;
+    packed = (packed + 15) & ~(size_t)15;
+    ioff[v] = (int64_t)packed;
+    packed += sizeof(int32_t) * (size_t)(h.n_admitted + h.n_declined);
+  }
+  ResultArena* ra = nullptr;
+  if (!good.empty()) {
+    const size_t offs_bytes = sizeof(int64_t) * 3 * (size_t)nv;
+    if ((e = c.d_pack.ensure(packed + offs_bytes + 256)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    if ((e = c.h_small.ensure(offs_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    int64_t* ho = (int64_t*)c.h_small.p;
+    std::memcpy(ho, boff.data(), sizeof(int64_t) * nv);
+    std::memcpy(ho + nv, eoff.data(), sizeof(int64_t) * nv);
+    std::memcpy(ho + 2 * nv, ioff.data(), sizeof(int64_t) * nv);
+    unsigned char* DP_ = (unsigned char*)c.d_pack.p;
+    const size_t offs_at = (packed + 255) & ~(size_t)255;
+    cudaMemcpyAsync(DP_ + offs_at, ho, offs_bytes, cudaMemcpyHostToDevice, s);
+    CompactParams cpp;
+    cpp.inst = A.inst;
+    cpp.out = A.out;
+    cpp.batches = A.batches;
+    cpp.entries = A.entries;
+    cpp.ids = A.ids;
+    cpp.boff = (const int64_t*)(DP_ + offs_at);
+    cpp.eoff = cpp.boff + nv;
+    cpp.ioff = cpp.boff + 2 * nv;
+    cpp.dst = DP_;
+    if ((e = launch_compact(cpp, nv, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    ra = arena_get(c, packed + 64);
+    if (!ra) return set_err(SLOS_ERR_ALLOC, "result arena");
+    cudaMemcpyAsync(ra->p, DP_, packed, cudaMemcpyDeviceToHost, s);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  }
+  for (int v = 0; v < nv; ++v) {
+    const int q = valid[v];
+    const int k = jobs[q].k;
+    const OutHdr& h = hdr[v];
+    slos_result& r = outs[k];
+    if (h.status == SLOS_ERR_CAPACITY && jobs[q].grow < 6) continue;  // retried
+    std::memset(&r, 0, sizeof r);
+    r.status = h.status;
+    if (h.status != SLOS_OK) continue;
+    unsigned char* base = (unsigned char*)ra->p;
+    r.running_set_infeasible = h.infeasible;
+    r.admitted_value = h.value;
+    r.n_admitted = h.n_admitted;
+    r.n_declined = h.n_declined;
+    r.n_deferred = 0;
+    r.admitted = (const int32_t*)(base + ioff[v]);
+    r.declined = r.admitted + h.n_admitted;
+    r.deferred = r.declined + h.n_declined;
+    r.n_batches = h.n_batches;
+    r.batches = (const slos_batch*)(base + boff[v]);
+    r.n_entries = h.n_entries;
+    r.entries = (const slos_entry*)(base + eoff[v]);
+    r.exact_until_s = h.exact_until;
+    r.counters.transitions = h.ctr[0];
+    r.counters.gap_evals = h.ctr[1];
+    r.counters.dues = h.ctr[2];
+    r.counters.slots = h.ctr[3];
+    r.counters.states = h.ctr[4];
+    arena_addref(ra);
+    r.owner_ = ra;
+  }
+  return SLOS_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C-ABI ---
+
+extern "C" {
+
+const char* slos_status_slug(int s) {
+  switch (s) {
+    case SLOS_OK: return "ok";
+    case SLOS_ERR_INVALID_PARAMETERS: return "invalid-parameters";
+    case SLOS_ERR_INTERNAL_INCONSISTENCY: return "internal-inconsistency";
+    case SLOS_ERR_INFEASIBLE_BUDGET: return "infeasible-budget";
+    case SLOS_ERR_CUDA: return "cuda-error";
+    case SLOS_ERR_CAPACITY: return "capacity";
+    case SLOS_ERR_NO_DEVICE: return "no-device";
+    case SLOS_ERR_ALLOC: return "alloc";
+    case SLOS_ERR_RANGE: return "range";
+    default: return "error";
+  }
+}
+
+const char* slos_last_error(void) { return g_err.c_str(); }
+const char* slos_backend(void) { return "b200-cuda"; }
+
+double slos_expected_accepted(double alpha, int32_t sl) {  // batch_planner.cpp:32-37
+  if (sl < 1) return NAN;
+  if (alpha >= 1.0) return (double)sl;
+  if (alpha <= 0.0) return 1.0;
+  return (1.0 - std::pow(alpha, sl)) / (1.0 - alpha);
+}
+
+void slos_planner_config_default(slos_planner_config* c) {
+  c->max_chunk_tokens = 2048;
+  c->max_batch_tokens = 16384;
+  c->speculative = 0;
+  c->spec_max_len = 8;
+  c->spec_alpha = 0.8;
+  c->plan_margin = 0.0;
+}
+
+int slos_planner_create(const slos_perf_term* terms, int32_t n_terms, const double* tpot,
+                        const double* slow, int32_t n_tiers, int32_t tpot_window,
+                        const slos_planner_config* cfg, slos_planner** out) {
+  *out = nullptr;
+  if (n_terms < 1) return set_err(SLOS_ERR_INVALID_PARAMETERS, "perf model needs at least one term");
+  for (int i = 0; i < n_terms; ++i)
+    if (terms[i].k1 < 0 || terms[i].k2 < 0 || terms[i].b < 0)
+      return set_err(SLOS_ERR_INVALID_PARAMETERS, "perf model coefficients must be nonnegative");
+  if (n_tiers < 1) return set_err(SLOS_ERR_INVALID_PARAMETERS, "slo config needs at least one tier");
+  for (int i = 0; i < n_tiers; ++i) {
+    if (tpot[i] <= 0) return set_err(SLOS_ERR_INVALID_PARAMETERS, "tpot tiers must be positive");
+    if (i > 0 && tpot[i] < tpot[i - 1])
+      return set_err(SLOS_ERR_INVALID_PARAMETERS, "tpot tiers must ascend from tightest to loosest");
+    if (slow[i] < 1.0) return set_err(SLOS_ERR_INVALID_PARAMETERS, "ttft slowdown multipliers must be >= 1");
+  }
+  if (tpot_window < 1) return set_err(SLOS_ERR_INVALID_PARAMETERS, "tpot window must be >= 1");
+  slos_planner_config c;
+  if (cfg) c = *cfg; else slos_planner_config_default(&c);
+  if (c.max_chunk_tokens < 1 || c.max_batch_tokens < 1)
+    return set_err(SLOS_ERR_INVALID_PARAMETERS, "batch and chunk caps must be positive");
+  if (c.plan_margin < 0) return set_err(SLOS_ERR_INVALID_PARAMETERS, "plan margin must be >= 0");
+  slos_planner* p = new slos_planner();
+  p->terms.assign(terms, terms + n_terms);
+  p->tpot.assign(tpot, tpot + n_tiers);
+  p->slow.assign(slow, slow + n_tiers);
+  p->L = n_tiers;
+  p->tpot_window = tpot_window;
+  p->cfg = c;
+  fill_planner_dev(p);
+  *out = p;
+  return SLOS_OK;
+}
+
+void slos_planner_destroy(slos_planner* p) { delete p; }
+
+int slos_plan_batch(slos_planner* const* planners, int32_t n, const slos_input* inputs,
+                    int32_t unit_value, slos_result* outs, void* stream) {
+  (void)stream;
+  for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  const int st = ensure_device(c);
+  if (st != SLOS_OK) {
+    set_err(st, c.why);
+    for (int k = 0; k < n; ++k) outs[k].status = st;
+    return st;
+  }
+  std::vector<Job> jobs(n), retry;
+  for (int k = 0; k < n; ++k) jobs[k] = {k, 0};
+  for (int round = 0; round < 8 && !jobs.empty(); ++round) {
+    retry.clear();
+    const int r = run_jobs(c, planners, inputs, unit_value, jobs, outs, retry);
+    if (r != SLOS_OK) {
+      for (const Job& j : jobs) outs[j.k].status = r;
+      return r;
+    }
+    jobs.swap(retry);
+  }
+  for (const Job& j : jobs) {
+    std::memset(&outs[j.k], 0, sizeof(outs[j.k]));
+    outs[j.k].status = SLOS_ERR_CAPACITY;
+  }
+  return SLOS_OK;
+}
+
+int slos_plan(slos_planner* p, const slos_input* in, int32_t unit_value, slos_result* out) {
+  slos_planner* const hs[1] = {p};
+  const int st = slos_plan_batch(hs, 1, in, unit_value, out, nullptr);
+  if (st != SLOS_OK) return st;
+  if (out->status != SLOS_OK) {
+    if (g_err.empty() || out->status == SLOS_ERR_CAPACITY) set_err(out->status, "plan failed");
+    return out->status;
+  }
+  return SLOS_OK;
+}
+
+void slos_result_free(slos_result* r) {
+  if (!r) return;
+  if (r->owner_) arena_release((ResultArena*)r->owner_);
+  std::memset(r, 0, sizeof *r);
+}
+
+// ---- tile_gap primitives (K1) ----------------------------------------------
+
+int slos_tile_gap_batch(slos_planner* p, int32_t n, const slos_gap_query* qs, slos_gap_result* outs) {
+  for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
+  if (n <= 0) return SLOS_OK;
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  int st = ensure_device(c);
+  if (st != SLOS_OK) {
+    for (int k = 0; k < n; ++k) outs[k].status = st;
+    return set_err(st, c.why);
+  }
+  if (!p->device_ok || p->L > kMaxTiers) {
+    for (int k = 0; k < n; ++k) outs[k].status = SLOS_ERR_RANGE;
+    return set_err(SLOS_ERR_RANGE, "planner not representable on device");
+  }
+  std::vector<int> todo(n), grow(n, 0);
+  for (int k = 0; k < n; ++k) todo[k] = k;
+  for (int round = 0; round < 8 && !todo.empty(); ++round) {
+    const int m = (int)todo.size();
+    int64_t TM = 0, TB = 0, TO = 0, TW = 0;
+    std::vector<GapQueryDev> qd(m);
+    for (int x = 0; x < m; ++x) {
+      const slos_gap_query& q = qs[todo[x]];
+      GapQueryDev& d = qd[x];
+      std::memset(&d, 0, sizeof d);
+      d.gap_s = q.gap_s;
+      d.horizon = q.due_horizon_s;
+      for (int l = 0; l < kMaxTiers; ++l) d.counts[l] = l < p->L ? q.counts_per_tier[l] : 0;
+      d.mode = q.mode;
+      d.n_exact = q.mode == SLOS_GAP_PREFILL_BUDGET ? 0 : q.n_exact;
+      d.off_exact = TM;
+      TM += d.n_exact;
+      const double span = std::max({q.gap_s, q.due_horizon_s, 0.0});
+      const int64_t S = (int64_t)std::ceil(span / p->tpot[0]) + 8;
+      const int64_t gg = (int64_t)1 << (2 * grow[todo[x]]);
+      d.cap_batch = (S + 8) * gg;
+      d.cap_owner = (int64_t)(d.n_exact + 1) * d.cap_batch;
+      d.off_out_batch = TB;
+      d.off_out_owner = TO;
+      TB += d.cap_batch;
+      TO += d.cap_owner;
+      d.cap_work = ((S + 2) * (d.n_exact + 2) * 4 + S * 128 + (int64_t)d.n_exact * 96 +
+                    d.cap_batch * (int64_t)sizeof(GapBatchOut) + (1 << 16)) * gg;
+      d.off_work = TW;
+      TW += (d.cap_work + 255) & ~(int64_t)255;
+    }
+    Blob b;
+    const size_t o_pl = b.add<PlannerDev>(1), o_q = b.add<GapQueryDev>(m), o_ph = b.add<double>(TM),
+                 o_bl = b.add<int64_t>(TM), o_rm = b.add<int64_t>(TM), o_tr = b.add<int32_t>(TM),
+                 o_ow = b.add<int32_t>(TM), in_bytes = b.bytes;
+    const size_t o_ob = b.add<GapBatchOut>(TB), o_oo = b.add<int64_t>(2 * TO), o_wk = b.add<unsigned char>(TW),
+                 o_out = b.add<GapOutDev>(m);
+    cudaError_t e;
+    if ((e = c.h_in.ensure(b.bytes)) != cudaSuccess || (e = c.d_in.ensure(b.bytes)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    unsigned char* H = (unsigned char*)c.h_in.p;
+    *(PlannerDev*)(H + o_pl) = p->dev;
+    std::memcpy(H + o_q, qd.data(), sizeof(GapQueryDev) * m);
+    double* ph = (double*)(H + o_ph);
+    int64_t* bl = (int64_t*)(H + o_bl);
+    int64_t* rm = (int64_t*)(H + o_rm);
+    int32_t* tr = (int32_t*)(H + o_tr);
+    int32_t* ow = (int32_t*)(H + o_ow);
+    for (int x = 0; x < m; ++x) {
+      const slos_gap_query& q = qs[todo[x]];
+      for (int i = 0; i < qd[x].n_exact; ++i) {
+        const int64_t o = qd[x].off_exact + i;
+        ph[o] = q.exact[i].phase_s;
+        bl[o] = q.exact[i].backlog;
+        rm[o] = q.exact[i].remaining;
+        tr[o] = q.exact[i].tier;
+        ow[o] = q.exact[i].owner;
+        if (q.exact[i].tier < 0 || q.exact[i].tier >= p->L) qd[x].mode = -1;
+      }
+    }
+    unsigned char* D = (unsigned char*)c.d_in.p;
+    cudaMemcpyAsync(D, H, in_bytes, cudaMemcpyHostToDevice, c.stream);
+    GapParams gp;
+    gp.planner = (const PlannerDev*)(D + o_pl);
+    gp.q = (const GapQueryDev*)(D + o_q);
+    gp.ph = (const double*)(D + o_ph);
+    gp.bl = (const int64_t*)(D + o_bl);
+    gp.rm = (const int64_t*)(D + o_rm);
+    gp.tr = (const int32_t*)(D + o_tr);
+    gp.ow = (const int32_t*)(D + o_ow);
+    gp.ob = (GapBatchOut*)(D + o_ob);
+    gp.oo = (int64_t*)(D + o_oo);
+    gp.work = D + o_wk;
+    gp.out = (GapOutDev*)(D + o_out);
+    if ((e = launch_gap(gp, m, c.stream)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    cudaMemcpyAsync(H + o_ob, D + o_ob, b.bytes - o_ob, cudaMemcpyDeviceToHost, c.stream);
+    if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    const GapOutDev* ro = (const GapOutDev*)(H + o_out);
+    const GapBatchOut* rb = (const GapBatchOut*)(H + o_ob);
+    const int64_t* rown = (const int64_t*)(H + o_oo);
+    std::vector<int> next;
+    for (int x = 0; x < m; ++x) {
+      const int k = todo[x];
+      const GapOutDev& r = ro[x];
+      slos_gap_result& o = outs[k];
+      std::memset(&o, 0, sizeof o);
+      if (r.status == SLOS_ERR_CAPACITY && grow[k] < 6) { ++grow[k]; next.push_back(k); continue; }
+      o.status = r.status;
+      if (r.status != SLOS_OK || !r.feasible) continue;
+      o.feasible = 1;
+      o.prefill_budget = r.budget;
+      if (qs[k].mode == SLOS_GAP_PREFILL_BUDGET) continue;
+      o.n_spec_lengths = r.n_spec;
+      for (int l = 0; l < kMaxTiers; ++l) o.spec_lengths[l] = r.spec_lengths[l];
+      const size_t bytes = sizeof(slos_gap_batch) * (size_t)r.n_batches + sizeof(int64_t) * 2 * (size_t)r.n_owner_pairs + 64;
+      char* mem = (char*)std::calloc(1, bytes);
+      slos_gap_batch* bs2 = (slos_gap_batch*)mem;
+      int64_t* own = (int64_t*)(bs2 + r.n_batches);
+      for (int64_t j = 0; j < r.n_batches; ++j) {
+        const GapBatchOut& gb = rb[qd[x].off_out_batch + j];
+        bs2[j].start_s = gb.start_s;
+        bs2[j].end_s = gb.end_s;
+        bs2[j].capacity_tokens = gb.capacity;
+        bs2[j].spec_step = gb.spec_step;
+        bs2[j].decode_tokens = gb.decode_tokens;
+        bs2[j].prefill_budget = gb.prefill_budget;
+        for (int l = 0; l < kMaxTiers; ++l) bs2[j].decode_per_tier[l] = gb.per_tier[l];
+        bs2[j].first_owner = gb.first_owner;
+        bs2[j].n_owners = gb.n_owner;
+      }
+      std::memcpy(own, rown + 2 * qd[x].off_out_owner, sizeof(int64_t) * 2 * (size_t)r.n_owner_pairs);
+      o.n_batches = r.n_batches;
+      o.batches = bs2;
+      o.n_owner_pairs = r.n_owner_pairs;
+      o.owner_tokens = own;
+      o.owner_ = mem;
+    }
+    todo.swap(next);
+  }
+  for (int k : todo) outs[k].status = SLOS_ERR_CAPACITY;
+  return SLOS_OK;
+}
+
+void slos_gap_result_free(slos_gap_result* r) {
+  if (!r) return;
+  std::free(r->owner_);
+  std::memset(r, 0, sizeof *r);
+}
+
+static int small_call(slos_planner* p, int n, size_t in_bytes, const void* hin, size_t out_bytes,
+                      void* hout, int kind, int64_t max_tokens) {
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  int st = ensure_device(c);
+  if (st != SLOS_OK) return set_err(st, c.why);
+  Blob b;
+  const size_t o_p = b.add<PlannerDev>(1), o_in = b.add<unsigned char>(in_bytes),
+               o_out = b.add<unsigned char>(out_bytes);
+  cudaError_t e;
+  if ((e = c.d_small.ensure(b.bytes)) != cudaSuccess || (e = c.h_in.ensure(b.bytes)) != cudaSuccess)
+    return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  unsigned char* H = (unsigned char*)c.h_in.p;
+  unsigned char* D = (unsigned char*)c.d_small.p;
+  *(PlannerDev*)(H + o_p) = p->dev;
+  std::memcpy(H + o_in, hin, in_bytes);
+  cudaMemcpyAsync(D, H, o_out, cudaMemcpyHostToDevice, c.stream);
+  const PlannerDev* dP = (const PlannerDev*)(D + o_p);
+  if (kind == 0) {  // time2bs: in = budgets[n] f64, spec[n] i64; out = res[n] i64, st[n] i32
+    e = launch_time2bs(dP, n, (const double*)(D + o_in), (const int64_t*)(D + o_in + 8 * (size_t)n),
+                       max_tokens, (int64_t*)(D + o_out), (int32_t*)(D + o_out + 8 * (size_t)n), c.stream);
+  } else if (kind == 1) {  // predict
+    e = launch_predict(dP, n, (const int64_t*)(D + o_in), (const int64_t*)(D + o_in + 8 * (size_t)n),
+                       (double*)(D + o_out), (int32_t*)(D + o_out + 8 * (size_t)n), c.stream);
+  } else {  // spec: in = counts[8], out = SpecSol
+    e = launch_spec(dP, (const int64_t*)(D + o_in), D + o_out, c.stream);
+  }
+  if (e != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  cudaMemcpyAsync(hout, D + o_out, out_bytes, cudaMemcpyDeviceToHost, c.stream);
+  if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  return SLOS_OK;
+}
+
+int slos_time2bs_batch(slos_planner* p, int32_t n, const double* budget, const int64_t* spec,
+                       int64_t max_tokens, int64_t* out, int32_t* status) {
+  if (n <= 0) return SLOS_OK;
+  std::vector<unsigned char> in(16 * (size_t)n), res(12 * (size_t)n);
+  std::memcpy(in.data(), budget, 8 * (size_t)n);
+  for (int k = 0; k < n; ++k) {
+    const int64_t s = spec ? spec[k] : 0;
+    std::memcpy(in.data() + 8 * (size_t)n + 8 * (size_t)k, &s, 8);
+  }
+  const int st = small_call(p, n, in.size(), in.data(), res.size(), res.data(), 0, max_tokens);
+  if (st != SLOS_OK) {
+    for (int k = 0; k < n; ++k) { out[k] = 0; status[k] = st; }
+    return st;
+  }
+  std::memcpy(out, res.data(), 8 * (size_t)n);
+  std::memcpy(status, res.data() + 8 * (size_t)n, 4 * (size_t)n);
+  for (int k = 0; k < n; ++k)
+    if (status[k] == SLOS_ERR_INFEASIBLE_BUDGET) set_err(status[k], "budget below single-token latency");
+  return SLOS_OK;
+}
+
+int slos_predict_batch(slos_planner* p, int32_t n, const int64_t* tokens, const int64_t* spec, double* out) {
+  if (n <= 0) return SLOS_OK;
+  std::vector<unsigned char> in(16 * (size_t)n), res(12 * (size_t)n);
+  std::memcpy(in.data(), tokens, 8 * (size_t)n);
+  for (int k = 0; k < n; ++k) {
+    const int64_t s = spec ? spec[k] : 0;
+    std::memcpy(in.data() + 8 * (size_t)n + 8 * (size_t)k, &s, 8);
+  }
+  const int st = small_call(p, n, in.size(), in.data(), res.size(), res.data(), 1, 0);
+  if (st != SLOS_OK) return st;
+  std::memcpy(out, res.data(), 8 * (size_t)n);
+  for (int k = 0; k < n; ++k) {
+    int32_t s;
+    std::memcpy(&s, res.data() + 8 * (size_t)n + 4 * (size_t)k, 4);
+    if (s != SLOS_OK) return set_err(s, "predict needs nonnegative num_tokens and spec_step");
+  }
+  return SLOS_OK;
+}
+
+int slos_solve_spec_lengths(slos_planner* p, const int64_t* counts, int32_t n_tiers, double alpha,
+                            int32_t max_len, slos_spec_plan* out) {
+  std::memset(out, 0, sizeof *out);
+  if (n_tiers != p->L) return set_err(SLOS_ERR_INVALID_PARAMETERS, "census width does not match tier count");
+  if (alpha <= 0.0 || alpha > 1.0) return set_err(SLOS_ERR_INVALID_PARAMETERS, "alpha must be in (0, 1]");
+  if (max_len < 1) return set_err(SLOS_ERR_INVALID_PARAMETERS, "spec_max_len must be >= 1");
+  if (max_len > kMaxSpecLen || p->L > kMaxTiers) return set_err(SLOS_ERR_RANGE, "spec length / tiers");
+  slos_planner tmp = *p;
+  tmp.cfg.spec_alpha = alpha;
+  tmp.cfg.spec_max_len = max_len;
+  tmp.cfg.speculative = 1;
+  fill_planner_dev(&tmp);
+  int64_t c8[kMaxTiers] = {0};
+  for (int l = 0; l < n_tiers; ++l) c8[l] = counts[l];
+  std::vector<unsigned char> res(sizeof(SpecSolH) + 64);
+  const int st = small_call(&tmp, 1, sizeof c8, c8, spec_sol_bytes(), res.data(), 2, 0);
+  if (st != SLOS_OK) return st;
+  SpecSolH sp;
+  std::memcpy(&sp, res.data(), sizeof sp);
+  if (sp.ok) {
+    out->feasible = 1;
+    for (int l = 0; l < kMaxTiers; ++l) out->lengths[l] = sp.lengths[l];
+    out->batch_time_s = sp.bt;
+    out->batch_capacity = sp.cap;
+    out->decode_tokens = sp.decode;
+    out->prefill_throughput = sp.tpt;
+  }
+  return SLOS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// sm_100a kernels of the batched multi-SLO planner and their launchers.
+// Compiled with: -gencode arch=compute_100a,code=sm_100a -fmad=false -lineinfo -O3
+// (-fmad=false is part of the bit-exactness contract, see slos_common.cuh).
+#include <cuda_runtime.h>
+
+#include "slos_build.cuh"
+#include "slos_dp.cuh"
+#include "slos_launch.h"
+
+namespace slos {
+
+// Pack each instance's batches / entries / admitted+declined ids densely so the
+// host copies exactly the bytes of the results (one D2H).
+__global__ void __launch_bounds__(256) compact_kernel(CompactParams p) {
+  const int k = blockIdx.x;
+  const InstDev& I = p.inst[k];
+  const OutHdr& o = p.out[k];
+  if (o.status != 0) return;
+  const int64_t nb = o.n_batches, ne = o.n_entries;
+  slos_batch* db = (slos_batch*)(p.dst + p.boff[k]);
+  slos_entry* de = (slos_entry*)(p.dst + p.eoff[k]);
+  int32_t* di = (int32_t*)(p.dst + p.ioff[k]);
+  for (int64_t x = threadIdx.x; x < nb; x += blockDim.x) db[x] = p.batches[I.off_batch + x];
+  // entries: 24 B each, copy as 8-byte words for coalescing
+  const uint64_t* se = (const uint64_t*)(p.entries + I.off_entry);
+  uint64_t* dw = (uint64_t*)de;
+  for (int64_t x = threadIdx.x; x < ne * 3; x += blockDim.x) dw[x] = se[x];
+  const int32_t* ids = p.ids + I.off_ids;
+  for (int x = threadIdx.x; x < o.n_admitted; x += blockDim.x) di[x] = ids[x];
+  for (int x = threadIdx.x; x < o.n_declined; x += blockDim.x) di[o.n_admitted + x] = ids[I.n_pending + x];
+}
+
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, bool wscr_in_smem) {
+  const size_t N = (size_t)max_N;
+  size_t b = 8 * (N + 1) * 4 + 8 * (N + 2) + 4 * (N + 2) * 3 + 64;
+  b += (size_t)max_dec_staged * 28 + 64;
+  if (wscr_in_smem) b += (size_t)kDpWarps * dp_warp_scr_stride(Sc, L);
+  return b;
+}
+
+size_t dp_warp_scr_stride(int Sc, int L) {
+  const size_t s = (size_t)Sc * (8 + 8 + 4 + 4 * L + 8 + 8 + 8 + 4 * L) + (size_t)(Sc + 2) * 8 + 64;
+  return (s + 127) & ~(size_t)127;
+}
+
+cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(dp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dp_kernel<<<grid, kDpThreads, smem, s>>>(prm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build(const BuildParams& prm, int grid, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
+  build_kernel<<<grid, kBT, 0, s>>>(prm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const CompactParams& prm, int grid, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
+  compact_kernel<<<grid, 256, 0, s>>>(prm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gap(const GapParams& prm, int grid, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
+  gap_kernel<<<grid, kBT, 0, s>>>(prm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_time2bs(const PlannerDev* P, int n, const double* b, const int64_t* sp,
+                           int64_t max_tokens, int64_t* out, int32_t* st, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  time2bs_kernel<<<(n + 255) / 256, 256, 0, s>>>(P, n, b, sp, max_tokens, out, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_predict(const PlannerDev* P, int n, const int64_t* t, const int64_t* sp,
+                           double* out, int32_t* st, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  predict_kernel<<<(n + 255) / 256, 256, 0, s>>>(P, n, t, sp, out, st);
+  return cudaGetLastError();
+}
+
+__global__ void spec_kernel(const PlannerDev* P, const int64_t* counts, SpecSol* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *out = solve_spec(*P, counts);
+}
+
+cudaError_t launch_spec(const PlannerDev* P, const int64_t* counts, void* out, cudaStream_t s) {
+  spec_kernel<<<1, 32, 0, s>>>(P, counts, (SpecSol*)out);
+  return cudaGetLastError();
+}
+
+size_t spec_sol_bytes() { return sizeof(SpecSol); }
+
+}  // namespace slos

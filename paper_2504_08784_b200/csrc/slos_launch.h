@@ -1,0 +1,40 @@
+// Host-visible launch interface of slos_kernels.cu (C++; used by slos_host.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "slos_dev.h"
+
+namespace slos {
+
+struct DpParams;
+struct BuildParams;
+struct GapParams;
+
+struct CompactParams {
+  const InstDev* inst;
+  const OutHdr* out;
+  const slos_batch* batches;
+  const slos_entry* entries;
+  const int32_t* ids;
+  const int64_t* boff;  // byte offsets into dst
+  const int64_t* eoff;
+  const int64_t* ioff;
+  unsigned char* dst;
+};
+
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, bool wscr_in_smem);
+size_t dp_warp_scr_stride(int Sc, int L);
+cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_build(const BuildParams& prm, int grid, cudaStream_t s);
+cudaError_t launch_compact(const CompactParams& prm, int grid, cudaStream_t s);
+cudaError_t launch_gap(const GapParams& prm, int grid, cudaStream_t s);
+cudaError_t launch_time2bs(const PlannerDev* P, int n, const double* b, const int64_t* sp,
+                           int64_t max_tokens, int64_t* out, int32_t* st, cudaStream_t s);
+cudaError_t launch_predict(const PlannerDev* P, int n, const int64_t* t, const int64_t* sp,
+                           double* out, int32_t* st, cudaStream_t s);
+cudaError_t launch_spec(const PlannerDev* P, const int64_t* counts, void* out, cudaStream_t s);
+size_t spec_sol_bytes();
+
+}  // namespace slos

@@ -431,9 +431,9 @@ def _convert(inp: ScheduleInput, r: abi.Result) -> ScheduleResult:
         return inp.running[ref].id if ref >= 0 else inp.pending[-ref - 1].id
 
     out = ScheduleResult()
-    out.admitted = [rid(r.admitted[k]) for k in range(r.n_admitted)]
-    out.declined = [rid(r.declined[k]) for k in range(r.n_declined)]
-    out.deferred = [rid(r.deferred[k]) for k in range(r.n_deferred)]
+    out.admitted = [inp.pending[r.admitted[k]].id for k in range(r.n_admitted)]
+    out.declined = [inp.pending[r.declined[k]].id for k in range(r.n_declined)]
+    out.deferred = [inp.pending[r.deferred[k]].id for k in range(r.n_deferred)]
     out.admitted_value = r.admitted_value
     out.running_set_infeasible = bool(r.running_set_infeasible)
     out.plan.exact_until_s = r.exact_until_s

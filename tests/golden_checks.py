@@ -1,0 +1,56 @@
+"""Golden-fixture checks shared by the oracle pinning tests (CPU) and the product
+parity tests (GPU). Every fixture was produced by the UNMODIFIED reference
+(oracle/make_golden.py); comparisons are bit-exact via canonical-byte digests."""
+import numpy as np
+
+from golden_io import load
+from parity import plan_many, plan_one, summary
+from paper_2504_08784_b200 import workload as W
+from paper_2504_08784_b200.planner import PlannerConfig, _CInput, _Handle
+from fuzz import random_case
+
+
+def _cmp(got, want, what):
+    g, w = summary(got), want
+    if g != w:
+        keys = [k for k in set(g) | set(w) if g.get(k) != w.get(k)]
+        raise AssertionError(f"{what}: mismatch in {sorted(keys)}: got {({k: g.get(k) for k in keys})} "
+                             f"want {({k: w.get(k) for k in keys})}")
+
+
+def check_oracle_instances(lib, batched=False):
+    fams = load("oracle_instances")
+    n = 0
+    for name, fam in fams.items():
+        unit = fam["unit_value"]
+        for idx, item in enumerate(fam["items"]):
+            f = W.oracle_fields(item["rec"])
+            h = _Handle(lib, W.oracle_model(f), W.oracle_slo(f), PlannerConfig())
+            ci = _CInput(W.oracle_input(f))
+            got = plan_one(lib, h.ptr, ci.c, unit_value=unit)
+            _cmp(got, item["ref"], f"oracle family {name} instance {idx}")
+            n += 1
+    return n
+
+
+def check_stress(lib, families=("C1", "LAT", "C2", "C3", "C4")):
+    st = load("stress")
+    for fam in families:
+        F = W.FAMILIES[fam]
+        b = W.InstanceBatch.stress(F["spec"], st[fam]["seeds"])
+        h = _Handle(lib, F["model"], W.TWO_TIER_SLO, F["cfg"])
+        res = plan_many(lib, h.ptr, b)
+        for k, (got, want) in enumerate(zip(res, st[fam]["ref"])):
+            _cmp(got, want, f"{fam} seed {st[fam]['seeds'][k]}")
+
+
+def check_fuzz(lib, seeds=None):
+    fz = load("fuzz")
+    for case in fz:
+        if seeds is not None and case["seed"] not in seeds:
+            continue
+        terms, slo, cfg, inp = random_case(case["seed"])
+        ci = _CInput(inp)
+        h = _Handle(lib, terms, slo, cfg)
+        _cmp(plan_one(lib, h.ptr, ci.c, False), case["value"], f"fuzz {case['seed']} value")
+        _cmp(plan_one(lib, h.ptr, ci.c, True), case["throughput"], f"fuzz {case['seed']} throughput")

@@ -80,3 +80,28 @@ def plan_one(lib, handle, cinput, unit_value=False) -> dict:
     d = canon_c(out)
     lib.slos_result_free(C.byref(out))
     return d
+
+
+def digest(d: dict) -> str:
+    """sha256 over the canonical bytes of a result (used to pin goldens)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(struct.pack("<i", d["status"]))
+    if d["status"] == 0:
+        h.update(struct.pack("<iqq", d["infeasible"], d["value_bits"], d["exact_until_bits"]))
+        for k in ("admitted", "declined", "deferred"):
+            h.update(struct.pack("<i", len(d[k])))
+            h.update(np.asarray(d[k], np.int32).tobytes())
+        h.update(d["batches"].tobytes())
+        h.update(d["entries"].tobytes())
+    return h.hexdigest()
+
+
+def summary(d: dict) -> dict:
+    s = dict(status=d["status"])
+    if d["status"] == 0:
+        s.update(infeasible=d["infeasible"], value_bits=d["value_bits"], admitted=d["admitted"],
+                 declined=d["declined"], n_batches=int(len(d["batches"])),
+                 n_entries=int(len(d["entries"])), exact_until_bits=d["exact_until_bits"],
+                 digest=digest(d))
+    return s

@@ -1,0 +1,73 @@
+"""Product (sm_100a kernels via the C-ABI) vs the reference: bit-exact on every
+output field of plan() -- admitted/declined id sequences, admitted_value bits,
+running_set_infeasible, every batch and entry, exact_until_s."""
+import pytest
+
+from golden_checks import check_fuzz, check_oracle_instances, check_stress
+from parity import diff, plan_many, plan_one
+from paper_2504_08784_b200 import abi
+from paper_2504_08784_b200 import workload as W
+from paper_2504_08784_b200.planner import _CInput, _Handle
+
+pytestmark = pytest.mark.gpu
+
+
+def test_product_is_the_cuda_backend():
+    assert abi.product().slos_backend() == b"b200-cuda"
+
+
+def test_brute_force_families_match_reference():
+    assert check_oracle_instances(abi.product()) == 811
+
+
+@pytest.mark.parametrize("fam", ["C1", "LAT", "C2", "C3", "C4"])
+def test_stress_families_match_reference(fam):
+    check_stress(abi.product(), families=(fam,))
+
+
+def test_fuzz_matches_reference():
+    check_fuzz(abi.product())
+
+
+def test_c2_batch_matches_oracle_with_reference_counters():
+    """The benchmark workload (BASELINE configs[1]) at 64 instances, one launch;
+    the T/G/D/S work counters follow the reference traversal exactly."""
+    F = W.FAMILIES["C2"]
+    b = W.InstanceBatch.stress(F["spec"], range(100, 164))
+    prod, ora = abi.product(), abi.oracle()
+    hp, ho = _Handle(prod, F["model"], W.TWO_TIER_SLO, F["cfg"]), _Handle(ora, F["model"], W.TWO_TIER_SLO, F["cfg"])
+    P = plan_many(prod, hp.ptr, b)
+    O = plan_many(ora, ho.ptr, b)
+    bad = [(k, diff(P[k], O[k], counters=True)) for k in range(b.n) if diff(P[k], O[k], counters=True)]
+    assert not bad, bad[:4]
+
+
+def test_fresh_fuzz_matches_oracle():
+    from fuzz import random_case
+    prod, ora = abi.product(), abi.oracle()
+    for seed in range(20000, 20300):
+        terms, slo, cfg, inp = random_case(seed, max_pending=12)
+        ci = _CInput(inp)
+        hp, ho = _Handle(prod, terms, slo, cfg), _Handle(ora, terms, slo, cfg)
+        for uv in (False, True):
+            a, o = plan_one(prod, hp.ptr, ci.c, uv), plan_one(ora, ho.ptr, ci.c, uv)
+            assert not diff(a, o, counters=True), (seed, uv, diff(a, o, counters=True))
+
+
+def test_errors_are_status_codes():
+    from paper_2504_08784_b200.planner import (BatchPlanner, Error, PendingRequest, PerfModel,
+                                               ScheduleInput, SloConfig, SloScheduler)
+    slo = SloConfig([0.05, 0.1], [3.0, 5.0])
+    sched = SloScheduler(BatchPlanner(PerfModel(W.DESK_MODEL), slo))
+    bad = ScheduleInput(now=0.0, memory_total=100,
+                        pending=[PendingRequest(id="x", prefill_deadline=1.0, prefill_tokens=10,
+                                                decode_tier=5, memory_units=1)])
+    with pytest.raises(Error) as e:
+        sched.schedule(bad)
+    assert e.value.code == "invalid-parameters"
+    many = ScheduleInput(now=0.0, memory_total=100,
+                         pending=[PendingRequest(id=f"p{i}", prefill_deadline=1.0, prefill_tokens=1,
+                                                 decode_tier=0, memory_units=1) for i in range(251)])
+    with pytest.raises(Error) as e:
+        sched.schedule(many)
+    assert e.value.code == "invalid-parameters"
