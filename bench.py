@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark: multi-SLO DP plans/sec (and p50 per-plan latency) on B200.
+
+Workload (BASELINE.json configs[1], SURVEY.md §8 d2 "C2"): Mixed Summarizer+Coder
+SLOs, 240 running decoders + 16 pending requests per instance (256 requests,
+tiers i%2), desk perf model, chunked prefill 2048, batch of 1024 instances per
+GPU. One "step" = one plan() pass over the whole batch. Synthetic inputs from the
+reference's own stress generator (acceptance_main.cpp:577-605).
+
+  value  : device-resident instances, kernel pipeline only (CUDA events on the
+           launching stream), L2 flushed (512 MiB write) before every step.
+  e2e    : the reference-facing C-ABI call slos_plan_batch with HOST inputs:
+           host prep + H2D + kernels + compaction + D2H of every plan.
+  multi-GPU: one process per GPU, weak scaling (1024 instances per rank), one
+           all_gather of 88-byte result records per step (the only collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "multi-SLO DP plans/sec and p50 per-plan latency at 1/2/4/8 B200"
+FAMILY = "C2"
+PER_RANK = 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--instances", type=int, default=PER_RANK)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() in ("active", "1", "yes")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def family():
+    from paper_2504_08784_b200 import workload as W
+    from paper_2504_08784_b200.sweep import ShardSpec
+    F = W.FAMILIES[FAMILY]
+    return ShardSpec(F["spec"], F["model"], F["cfg"]), F
+
+
+def cpu_reference_rate(n_inst: int, seeds_base: int = 0):
+    """The reference CPU planner (oracle/_ref, compiled from the reference sources;
+    else the C oracle port) over a bounded sample of the same workload, all host
+    cores. Returns (plans/sec, kind, cores, sample description)."""
+    from paper_2504_08784_b200 import abi
+    from paper_2504_08784_b200 import workload as W
+    from paper_2504_08784_b200.planner import _Handle
+    spec, F = family()
+    if os.path.exists(abi.REF_LIB):
+        lib, kind = abi.reference(), "reference"
+        cores = int(os.environ.get("SLOS_REF_THREADS", os.cpu_count() or 1))
+    else:
+        lib, kind, cores = abi.oracle(), "port", 1
+    batch = W.InstanceBatch.stress(spec.family, range(seeds_base, seeds_base + n_inst))
+    h = _Handle(lib, spec.model, spec.slo, spec.cfg)
+    hs = (C.c_void_p * batch.n)(*([h.ptr] * batch.n))
+    outs = (abi.Result * batch.n)()
+    t = time.perf_counter()
+    lib.slos_plan_batch(hs, batch.n, C.c_void_p(batch.inputs_ptr()), 0, outs, None)
+    dt = time.perf_counter() - t
+    for k in range(batch.n):
+        lib.slos_result_free(C.byref(outs[k]))
+    return batch.n / dt, kind, cores, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    ncores = int(os.environ.get("SLOS_REF_THREADS", os.cpu_count() or 1))
+    sample = max(2 * ncores, 8)  # ~0.5 s of all-core reference work per step
+    for _ in range(args.warmup):
+        cpu_reference_rate(sample)
+    rates, wall = [], 0.0
+    for k in range(args.steps):
+        r, kind, cores, dt = cpu_reference_rate(sample, seeds_base=10000 + k * sample)
+        rates.append(r)
+        wall += dt
+    value = args.steps * sample / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64+int64",
+        "data": "synthetic (reference stress generator G(240,16), acceptance_main.cpp:577-605)",
+        "config": {"workload": "C2: Mixed Summarizer+Coder, 240 running + 16 pending per instance, "
+                               "chunk 2048, desk model", "instances_per_step": sample,
+                   "parallelism": f"{cores} host threads"},
+        "cpu_baseline": {"value": value, "unit": "plans/s", "cores": cores, "kind": kind,
+                         "sample": f"{sample} C2 instances per step"},
+        "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def load_ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_08784_b200 import abi
+    from paper_2504_08784_b200 import workload as W
+    from paper_2504_08784_b200.planner import _Handle
+    from paper_2504_08784_b200.sweep import ShardSolver, gather_records, records_view, weak_seeds
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = abi.product()
+    spec, F = family()
+    per = args.instances
+    solver = ShardSolver(lib, spec, weak_seeds(rank, per))
+    stream = torch.cuda.Stream()
+    sptr = stream.cuda_stream
+    rec = torch.empty((per, C.sizeof(abi.Record)), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    solver.upload(sptr)
+    torch.cuda.synchronize()
+
+    def step():
+        solver.solve(sptr)
+        solver.records(rec.data_ptr(), sptr)
+        with torch.cuda.stream(stream):
+            allrec = gather_records(rec, world)
+        return allrec
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    dp_ms, build_ms = [], []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            evs[k][0].record(stream)
+            allrec = step()
+            evs[k][1].record(stream)
+            a, b = solver.kernel_ms()
+            dp_ms.append(a)
+            build_ms.append(b)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = sum(s.elapsed_time(e) for s, e in evs)
+    t = torch.tensor([total_ms, sum(dp_ms), sum(build_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, dp_tot, build_tot = (float(x) for x in t.tolist())
+    recs = records_view(allrec)
+    n_all = per * world
+    assert len(recs) == n_all and (recs["status"] == 0).all(), "solve produced error records"
+    value = n_all * args.steps / (total_ms / 1e3)
+
+    # correctness spot check: download the last solve of this shard
+    outs = solver.download(sptr)
+    ok = all(outs[k].status == 0 for k in range(per))
+    adm = sum(outs[k].n_admitted for k in range(per)) / per
+    solver.free_results()
+
+    # ---- e2e: the reference-facing C-ABI call with host inputs ----
+    batch = solver.batch
+    hs = (C.c_void_p * per)(*([solver.handle.ptr] * per))
+    outs2 = (abi.Result * per)()
+    for _ in range(max(2, args.warmup // 2)):
+        lib.slos_plan_batch(hs, per, C.c_void_p(batch.inputs_ptr()), 0, outs2, sptr)
+        for k in range(per):
+            lib.slos_result_free(C.byref(outs2[k]))
+    if world > 1:
+        dist.barrier()
+    e2e_wall = 0.0
+    h2d = C.c_int64()
+    d2h = C.c_int64()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        lib.slos_plan_batch(hs, per, C.c_void_p(batch.inputs_ptr()), 0, outs2, sptr)
+        e2e_wall += time.perf_counter() - t0
+        lib.slos_last_transfer_bytes(C.byref(h2d), C.byref(d2h))
+        for k in range(per):
+            lib.slos_result_free(C.byref(outs2[k]))
+    te = torch.tensor([e2e_wall], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n_all * args.steps / float(te.item())
+
+    line = None
+    if rank == 0:
+        # p50 per-plan latency: one C1 (ChatBot) instance per call, end to end
+        F1 = W.FAMILIES["C1"]
+        h1 = _Handle(lib, F1["model"], W.TWO_TIER_SLO, F1["cfg"])
+        lat = []
+        for s in range(34):
+            b1 = W.InstanceBatch.stress(F1["spec"], [50000 + s])
+            o1 = (abi.Result * 1)()
+            hh = (C.c_void_p * 1)(h1.ptr)
+            t0 = time.perf_counter()
+            lib.slos_plan_batch(hh, 1, C.c_void_p(b1.inputs_ptr()), 0, o1, sptr)
+            lat.append(time.perf_counter() - t0)
+            lib.slos_result_free(C.byref(o1[0]))
+        lat = sorted(lat[3:])
+        p50_ms = 1e3 * lat[len(lat) // 2]
+        # roofline of the dominant kernel (admission DP): algorithmic bytes per
+        # plan from the reference-defined counters:
+        #   B_smem = 80*T + 32*D + 48*S
+        T = int(recs["transitions"][:per].sum())
+        D = int(recs["dues"][:per].sum())
+        S = int(recs["slots"][:per].sum())
+        alg = 80 * T + 32 * D + 48 * S
+        ck = clk.summary()
+        f_mhz = ck.get("sm_mhz") or 1965.0
+        dp_avg_s = (dp_tot / args.steps) / 1e3
+        achieved = alg / dp_avg_s / 1e9
+        peak = 148 * 128 * f_mhz * 1e6 / 1e9
+        ncu = load_ncu_traffic()
+        traffic = None
+        if ncu and ncu.get("kernel") == "dp_kernel" and ncu.get("instances") == per:
+            traffic = ncu.get("dram_bytes_per_launch")
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            ncores = int(os.environ.get("SLOS_REF_THREADS", os.cpu_count() or 1))
+            sample = max(16 * ncores, 32)
+            r, kind, cores, dt = cpu_reference_rate(sample, seeds_base=0)
+            cpu = {"value": r, "unit": "plans/s", "cores": cores, "kind": kind,
+                   "sample": f"{sample} C2 instances (seeds 0..{sample - 1}), {dt:.1f} s wall"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp64+int64",
+            "data": "synthetic (reference stress generator G(240,16), acceptance_main.cpp:577-605)",
+            "config": {"workload": "C2: Mixed Summarizer+Coder, 240 running + 16 pending per instance, "
+                                   "chunk 2048, desk model (BASELINE configs[1])",
+                       "instances_per_gpu": per, "total_instances": n_all,
+                       "parallelism": f"{world} GPU(s), one process each, weak scaling",
+                       "l2": "flushed before every step (512 MiB write)",
+                       "p50_plan_ms": {"value": p50_ms, "workload": "C1 ChatBot: 48 running + 16 pending, "
+                                       "one instance per slos_plan_batch call, end to end"}},
+            "e2e": {"value": e2e_value, "unit": "plans/s", "h2d_bytes_per_step": int(h2d.value),
+                    "d2h_bytes_per_step": int(d2h.value)},
+            "gpu_launches": 3 * args.steps,
+            "kernel_ms_per_step": {"dp_kernel": dp_tot / args.steps, "build_kernel": build_tot / args.steps},
+            "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "dp_kernel", "alg_bytes_per_launch": alg,
+                         "note": "B_smem=80T+32D+48S per plan (reference counters, SURVEY 8d6); "
+                                 "peak=148 SM x 128 B/clk x median SM clock under load"},
+            "cpu_baseline": cpu,
+            "clocks": ck,
+            "check": {"statuses_ok": bool(ok), "mean_admitted": adm},
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

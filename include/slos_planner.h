@@ -192,6 +192,51 @@ int slos_plan_batch(slos_planner* const* planners, int32_t n, const slos_input* 
 
 void slos_result_free(slos_result* result);
 
+/* Device-resident batches: the three stages of slos_plan_batch exposed so a
+ * caller (and bench.py) can keep instances resident in HBM and re-solve them.
+ *   upload   -- host preparation + one H2D copy (instances become resident);
+ *               invalid instances get their status in outs[k] immediately
+ *   solve    -- enqueue the kernel pipeline on `stream` (asynchronous)
+ *   download -- synchronise, regrow the rare overflowed instance, compact and
+ *               copy the results back (one D2H); fills outs[k]
+ * `inputs` must stay valid until download returns. The CPU checkers implement
+ * the same calls synchronously. */
+typedef struct slos_workspace slos_workspace;
+int slos_workspace_create(slos_workspace** out);
+void slos_workspace_destroy(slos_workspace* ws);
+int slos_workspace_upload(slos_workspace* batch, slos_planner* const* planners, int32_t n,
+                      const slos_input* inputs, int32_t unit_value, slos_result* outs,
+                      void* stream);
+int slos_workspace_solve(slos_workspace* batch, void* stream);
+int slos_workspace_download(slos_workspace* batch, slos_result* outs, void* stream);
+
+/* Fixed-size per-instance result record (what a multi-GPU sweep all-gathers). */
+typedef struct slos_record {
+  int32_t status;
+  int32_t running_set_infeasible;
+  int32_t n_admitted;
+  int32_t n_declined;
+  double admitted_value;
+  int64_t n_batches;
+  int64_t n_entries;
+  double exact_until_s;
+  slos_counters counters;
+} slos_record;
+
+/* Write the n records of the last solve to `out` (n slos_record), in input order,
+ * asynchronously on `stream`. `out` is DEVICE memory for the product (a device-to-
+ * device copy that feeds an NCCL gather without a host round trip) and host
+ * memory for the CPU checkers. */
+int slos_workspace_records(slos_workspace* ws, slos_record* out, void* stream);
+
+/* Device time (ms) of the last solve's kernels: [0] admission DP, [1] plan
+ * reconstruction. CPU checkers report wall time of the whole solve in [0]. */
+int slos_workspace_kernel_ms(slos_workspace* ws, float* ms2);
+
+/* Bytes moved host->device and device->host by the calling thread's last
+ * slos_plan_batch / slos_workspace_* sequence. */
+void slos_last_transfer_bytes(int64_t* h2d, int64_t* d2h);
+
 /* ---- batch planner primitives (batch_planner.hpp:68-134, perf_model.hpp:25-61) */
 
 typedef struct slos_decode_member { /* DecodeMember batch_planner.hpp:19-25 */

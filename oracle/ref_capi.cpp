@@ -18,6 +18,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <memory>
 #include <string>
 #include <thread>
@@ -376,6 +377,92 @@ int slos_solve_spec_lengths(slos_planner* p, const int64_t* counts, int32_t n_ti
 }
 
 double slos_expected_accepted(double alpha, int32_t sl) { return expected_accepted(alpha, sl); }
+
+
+/* device-resident workspace API: synchronous CPU version (test infrastructure) */
+struct slos_workspace {
+  slos_planner* const* planners;
+  const slos_input* inputs;
+  int32_t n;
+  int32_t unit_value;
+  slos_result* res; /* results of the last solve, owned until download */
+  double solve_ms;
+};
+static void ws_clear_cpu(slos_workspace* b) {
+  if (b->res) {
+    for (int32_t k = 0; k < b->n; ++k) slos_result_free(&b->res[k]);
+    free(b->res);
+    b->res = NULL;
+  }
+}
+int slos_workspace_create(slos_workspace** out) {
+  *out = static_cast<slos_workspace*>(std::calloc(1, sizeof(slos_workspace)));
+  return *out ? SLOS_OK : SLOS_ERR_ALLOC;
+}
+void slos_workspace_destroy(slos_workspace* b) {
+  if (!b) return;
+  ws_clear_cpu(b);
+  free(b);
+}
+int slos_workspace_upload(slos_workspace* b, slos_planner* const* planners, int32_t n, const slos_input* inputs,
+                          int32_t unit_value, slos_result* outs, void* stream) {
+  (void)stream;
+  ws_clear_cpu(b);
+  for (int32_t k = 0; k < n; ++k) memset(&outs[k], 0, sizeof outs[k]);
+  b->planners = planners;
+  b->inputs = inputs;
+  b->n = n;
+  b->unit_value = unit_value;
+  return SLOS_OK;
+}
+int slos_workspace_solve(slos_workspace* b, void* stream) {
+  timespec t0, t1;
+  ws_clear_cpu(b);
+  b->res = static_cast<slos_result*>(std::calloc((size_t)(b->n > 0 ? b->n : 1), sizeof(slos_result)));
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  int r = slos_plan_batch(b->planners, b->n, b->inputs, b->unit_value, b->res, stream);
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  b->solve_ms = (double)(t1.tv_sec - t0.tv_sec) * 1e3 + (double)(t1.tv_nsec - t0.tv_nsec) * 1e-6;
+  return r;
+}
+int slos_workspace_download(slos_workspace* b, slos_result* outs, void* stream) {
+  (void)stream;
+  if (!b->res) return SLOS_ERR_INVALID_PARAMETERS;
+  memcpy(outs, b->res, sizeof(slos_result) * (size_t)b->n);
+  free(b->res);
+  b->res = NULL;
+  return SLOS_OK;
+}
+int slos_workspace_records(slos_workspace* b, slos_record* out, void* stream) {
+  (void)stream;
+  if (!b->res) return SLOS_ERR_INVALID_PARAMETERS;
+  for (int32_t k = 0; k < b->n; ++k) {
+    const slos_result* r = &b->res[k];
+    slos_record x;
+    memset(&x, 0, sizeof x);
+    x.status = r->status;
+    x.running_set_infeasible = r->running_set_infeasible;
+    x.n_admitted = r->n_admitted;
+    x.n_declined = r->n_declined;
+    x.admitted_value = r->admitted_value;
+    x.n_batches = r->n_batches;
+    x.n_entries = r->n_entries;
+    x.exact_until_s = r->exact_until_s;
+    x.counters = r->counters;
+    out[k] = x;
+  }
+  return SLOS_OK;
+}
+int slos_workspace_kernel_ms(slos_workspace* b, float* ms2) {
+  ms2[0] = (float)b->solve_ms;
+  ms2[1] = 0.0f;
+  return SLOS_OK;
+}
+void slos_last_transfer_bytes(int64_t* h2d, int64_t* d2h) {
+  *h2d = 0;
+  *d2h = 0;
+}
+
 
 const char* slos_status_slug(int s) {
   switch (s) {

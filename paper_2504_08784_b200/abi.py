@@ -149,6 +149,23 @@ class Result(C.Structure):
     ]
 
 
+class Record(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32),
+        ("running_set_infeasible", C.c_int32),
+        ("n_admitted", C.c_int32),
+        ("n_declined", C.c_int32),
+        ("admitted_value", C.c_double),
+        ("n_batches", C.c_int64),
+        ("n_entries", C.c_int64),
+        ("exact_until_s", C.c_double),
+        ("counters", Counters),
+    ]
+
+
+RECORD_DTYPE = None  # set below
+
+
 class DecodeMemberC(C.Structure):
     _fields_ = [
         ("tier", C.c_int32),
@@ -266,6 +283,18 @@ BATCH_DTYPE = np.dtype(
     }
 )
 
+RECORD_DTYPE = np.dtype(
+    {
+        "names": ["status", "infeasible", "n_admitted", "n_declined", "value", "n_batches",
+                  "n_entries", "exact_until_s", "transitions", "gap_evals", "dues", "slots",
+                  "states"],
+        "formats": [np.int32, np.int32, np.int32, np.int32, np.float64, np.int64, np.int64,
+                    np.float64, np.int64, np.int64, np.int64, np.int64, np.int64],
+        "offsets": [0, 4, 8, 12, 16, 24, 32, 40, 48, 56, 64, 72, 80],
+        "itemsize": C.sizeof(Record),
+    }
+)
+
 _LIBS: dict[str, C.CDLL] = {}
 
 
@@ -306,6 +335,23 @@ def _bind(lib: C.CDLL) -> C.CDLL:
     lib.slos_last_error.restype = C.c_char_p
     lib.slos_backend.argtypes = []
     lib.slos_backend.restype = C.c_char_p
+    lib.slos_workspace_create.argtypes = [P(C.c_void_p)]
+    lib.slos_workspace_create.restype = C.c_int
+    lib.slos_workspace_destroy.argtypes = [C.c_void_p]
+    lib.slos_workspace_destroy.restype = None
+    lib.slos_workspace_upload.argtypes = [C.c_void_p, P(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32,
+                                          P(Result), C.c_void_p]
+    lib.slos_workspace_upload.restype = C.c_int
+    lib.slos_workspace_solve.argtypes = [C.c_void_p, C.c_void_p]
+    lib.slos_workspace_solve.restype = C.c_int
+    lib.slos_workspace_download.argtypes = [C.c_void_p, P(Result), C.c_void_p]
+    lib.slos_workspace_download.restype = C.c_int
+    lib.slos_workspace_records.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.slos_workspace_records.restype = C.c_int
+    lib.slos_workspace_kernel_ms.argtypes = [C.c_void_p, P(C.c_float)]
+    lib.slos_workspace_kernel_ms.restype = C.c_int
+    lib.slos_last_transfer_bytes.argtypes = [P(C.c_int64), P(C.c_int64)]
+    lib.slos_last_transfer_bytes.restype = None
     return lib
 
 

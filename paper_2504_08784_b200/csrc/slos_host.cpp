@@ -326,6 +326,17 @@ int prep_instance(const slos_planner* P, const slos_input* in, int unit_value, P
   double max_tpot = 0.0;
   for (int l = 0; l < L; ++l) max_tpot = std::max(max_tpot, P->tpot[l]);
   pr.tail_bound = std::max({2.0 * max_tpot, in->tail_horizon_s, tb, 0.0});
+  if (pr.N == 0 && !(in->tail_horizon_s > kTimeEps)) {
+    // untrimmed decode tail (dp_scheduler.cpp:311-315): every line to completion
+    double full = 0.0;
+    for (int i = 0; i < in->n_running; ++i) {
+      const slos_running& r = in->running[i];
+      if (r.prefill_remaining > 0 || r.decode_remaining <= 0) continue;
+      const double tp = P->tpot[r.decode_tier];
+      full = std::max(full, std::max(0.0, r.next_due_s - in->now) + (double)r.decode_remaining * tp);
+    }
+    pr.tail_bound = std::max(pr.tail_bound, full + max_tpot);
+  }
   return SLOS_OK;
 }
 
@@ -351,7 +362,7 @@ Caps estimate_caps(const slos_planner* P, const slos_input* in, const Prep& pr, 
   c.surv = std::max<int64_t>(1024, 64 * (int64_t)(pr.N + 1)) * g;
   c.cand = pow2_at_least(std::max<int64_t>(512, 16 * (int64_t)(pr.N + 1)) * g);
   c.memo = pow2_at_least(std::max<int64_t>(2048, 64 * (int64_t)(pr.N + 1)) * g);
-  c.gb = (S + 8) * (grow + 1);
+  c.gb = (S + 8) << (2 * grow);
   c.go = M * c.gb;
   // plan output: gaps + tail, or the fallback (until every line completes)
   double max_tpot = 0.0;
@@ -400,16 +411,47 @@ struct Job {
 struct Layout {
   size_t planners, inst, order, dec_idx, dec_tier, dec_next, dec_backlog, dec_rem;
   size_t ch_deadline, ch_prefill, ch_tier, ch_memory, ch_value, ch_forced, ch_ref, ch_floor, ch_suffix;
-  size_t pre_idx, pre_left, run_tier;
+  size_t pre_idx, pre_left, run_tier, recdef, recmap;
   size_t in_bytes;
   size_t s_counts, s_mem, s_pb, s_value, s_nadm, s_parent, s_arena, s_level;
   size_t c_src, c_j, c_memo, c_flag, c_bucket, c_pos, c_aux, c_counts, c_mem, c_pb, c_value, c_nadm;
   size_t c_bkey, c_bval, memo, work, scr_bytes;
+  size_t memo_bytes, bkey_bytes, bval_bytes;
   size_t out, sel, ids, batches, entries, out_bytes;
 };
 
-int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, int unit_value,
-             const std::vector<Job>& jobs, slos_result* outs, std::vector<Job>& retry) {
+struct Workspace {
+  DevBuf d_in, d_scr, d_out, d_pack, d_wscr;
+  PinBuf h_in, h_small;
+  slos_planner* const* planners = nullptr;
+  const slos_input* inputs = nullptr;
+  int unit_value = 0;
+  std::vector<Job> jobs;
+  std::vector<int> valid;
+  int nv = 0;
+  Layout Ly;
+  BatchArgs A;
+  DpParams dp;
+  size_t smem = 0;
+  cudaStream_t stream = nullptr;
+  bool uploaded = false;
+  int n_total = 0;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+};
+
+thread_local int64_t g_h2d = 0, g_d2h = 0;
+
+// Host preparation + one H2D copy; the instances become device-resident.
+int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_input* inputs,
+              int unit_value, const std::vector<Job>& jobs, slos_result* outs, cudaStream_t stream) {
+  ws.planners = planners;
+  ws.inputs = inputs;
+  ws.unit_value = unit_value;
+  ws.jobs = jobs;
+  ws.stream = stream ? stream : c.stream;
+  ws.uploaded = false;
+  ws.nv = 0;
+  ws.valid.clear();
   const int n = (int)jobs.size();
   if (n == 0) return SLOS_OK;
   // ---- host preparation ----
@@ -455,7 +497,7 @@ int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, in
   }
   const int nv = (int)valid.size();
   if (nv == 0) return SLOS_OK;
-  Layout Ly;
+  Layout& Ly = ws.Ly;
   Blob bi;
   Ly.planners = bi.add<PlannerDev>(plist.size());
   Ly.inst = bi.add<InstDev>(nv);
@@ -477,6 +519,8 @@ int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, in
   Ly.pre_idx = bi.add<int32_t>(TP);
   Ly.pre_left = bi.add<int64_t>(TP);
   Ly.run_tier = bi.add<int32_t>(TR);
+  Ly.recdef = bi.add<slos_record>(n);
+  Ly.recmap = bi.add<int32_t>(nv);
   Ly.in_bytes = bi.bytes;
   Blob bs;
   Ly.s_counts = bs.add<uint64_t>(TS);
@@ -513,11 +557,11 @@ int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, in
   Ly.out_bytes = bo.bytes;
 
   cudaError_t e;
-  if ((e = c.h_in.ensure(Ly.in_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  if ((e = c.d_in.ensure(Ly.in_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  if ((e = c.d_scr.ensure(Ly.scr_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  if ((e = c.d_out.ensure(Ly.out_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  unsigned char* H = (unsigned char*)c.h_in.p;
+  if ((e = ws.h_in.ensure(Ly.in_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  if ((e = ws.d_in.ensure(Ly.in_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  if ((e = ws.d_scr.ensure(Ly.scr_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  if ((e = ws.d_out.ensure(Ly.out_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  unsigned char* H = (unsigned char*)ws.h_in.p;
   auto hp = [&](size_t off) { return H + off; };
   PlannerDev* hP = (PlannerDev*)hp(Ly.planners);
   for (size_t x = 0; x < plist.size(); ++x) hP[x] = plist[x]->dev;
@@ -641,17 +685,25 @@ int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, in
     std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
     for (int v = 0; v < nv; ++v) h_order[v] = ord[v];
   }
+  {
+    slos_record* rd = (slos_record*)hp(Ly.recdef);
+    std::memset(rd, 0, sizeof(slos_record) * (size_t)n);
+    for (int q = 0; q < n; ++q) rd[q].status = prep[q].status;
+    int32_t* rm = (int32_t*)hp(Ly.recmap);
+    for (int v = 0; v < nv; ++v) rm[v] = valid[v];
+  }
+  ws.n_total = n;
+  g_h2d += (int64_t)Ly.in_bytes;
   // ---- device pipeline ----
-  unsigned char* DI = (unsigned char*)c.d_in.p;
-  unsigned char* DS = (unsigned char*)c.d_scr.p;
-  unsigned char* DO = (unsigned char*)c.d_out.p;
-  cudaStream_t s = c.stream;
+  unsigned char* DI = (unsigned char*)ws.d_in.p;
+  unsigned char* DS = (unsigned char*)ws.d_scr.p;
+  unsigned char* DO = (unsigned char*)ws.d_out.p;
+  cudaStream_t s = ws.stream;
   cudaMemcpyAsync(DI, H, Ly.in_bytes, cudaMemcpyHostToDevice, s);
-  cudaMemsetAsync(DS + Ly.memo, 0, sizeof(MemoEnt) * TM, s);
-  cudaMemsetAsync(DS + Ly.c_bkey, 0, sizeof(uint64_t) * 2 * TCd, s);
-  cudaMemsetAsync(DS + Ly.c_bval, 0xFF, sizeof(int32_t) * 2 * TCd, s);
-  cudaMemsetAsync(DO + Ly.out, 0, sizeof(OutHdr) * nv, s);
-  BatchArgs A;
+  Ly.memo_bytes = sizeof(MemoEnt) * (size_t)TM;
+  Ly.bkey_bytes = sizeof(uint64_t) * 2 * (size_t)TCd;
+  Ly.bval_bytes = sizeof(int32_t) * 2 * (size_t)TCd;
+  BatchArgs& A = ws.A;
   std::memset(&A, 0, sizeof A);
   A.planners = (const PlannerDev*)(DI + Ly.planners);
   A.inst = (const InstDev*)(DI + Ly.inst);
@@ -704,20 +756,21 @@ int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, in
   A.batches = (slos_batch*)(DO + Ly.batches);
   A.entries = (slos_entry*)(DO + Ly.entries);
 
-  DpParams dp;
+  DpParams& dp = ws.dp;
   dp.a = A;
   dp.Lmax = Lmax;
   dp.Sc = (int)std::min<double>(S_need, 1 << 20);
   const size_t stride = dp_warp_scr_stride(dp.Sc, Lmax);
   dp.wscr_stride = stride;
   const size_t kSmemBudget = 100 * 1024;
-  size_t smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, true);
+  size_t& smem = ws.smem;
+  smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, true);
   if (smem <= kSmemBudget) {
     dp.wscr_global = nullptr;
   } else {
-    if ((e = c.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
+    if ((e = ws.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-    dp.wscr_global = (unsigned char*)c.d_wscr.p;
+    dp.wscr_global = (unsigned char*)ws.d_wscr.p;
     smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, false);
   }
   dp.dec_smem_max = 0;
@@ -725,16 +778,58 @@ int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, in
     const size_t with_dec = dp_smem_bytes(maxN, maxDec, dp.Sc, Lmax, dp.wscr_global == nullptr);
     if (with_dec <= kSmemBudget) { dp.dec_smem_max = maxDec; smem = with_dec; }
   }
+  ws.valid = valid;
+  ws.nv = nv;
+  ws.uploaded = true;
+  return SLOS_OK;
+}
+
+// Enqueue the kernel pipeline on the device-resident batch (no host sync).
+int ws_solve(Workspace& ws, cudaStream_t stream) {
+  if (!ws.uploaded || ws.nv == 0) return SLOS_OK;
+  const cudaStream_t s = stream ? stream : ws.stream;
+  const int nv = ws.nv;
+  DpParams& dp = ws.dp;
+  const size_t smem = ws.smem;
+  unsigned char* DS = (unsigned char*)ws.d_scr.p;
+  unsigned char* DO = (unsigned char*)ws.d_out.p;
+  const Layout& Ly = ws.Ly;
+  // scratch init is part of every solve (memo tables, bucket hashes, headers)
+  cudaMemsetAsync(DS + Ly.memo, 0, Ly.memo_bytes, s);
+  cudaMemsetAsync(DS + Ly.c_bkey, 0, Ly.bkey_bytes, s);
+  cudaMemsetAsync(DS + Ly.c_bval, 0xFF, Ly.bval_bytes, s);
+  cudaMemsetAsync(DO + Ly.out, 0, sizeof(OutHdr) * nv, s);
+  cudaError_t e;
+  for (int k = 0; k < 3; ++k)
+    if (!ws.ev[k]) cudaEventCreate(&ws.ev[k]);
+  cudaEventRecord(ws.ev[0], s);
   if ((e = launch_dp(dp, nv, smem, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  cudaEventRecord(ws.ev[1], s);
   BuildParams bp;
-  bp.a = A;
+  bp.a = ws.A;
   if ((e = launch_build(bp, nv, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  cudaEventRecord(ws.ev[2], s);
+  return SLOS_OK;
+}
+
+// Headers back, capacity regrowth list, compaction and one D2H of the results.
+int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry) {
+  if (!ws.uploaded || ws.nv == 0) return SLOS_OK;
+  const int nv = ws.nv;
+  const std::vector<int>& valid = ws.valid;
+  const std::vector<Job>& jobs = ws.jobs;
+  const Layout& Ly = ws.Ly;
+  const BatchArgs& A = ws.A;
+  const cudaStream_t s = ws.stream;
+  unsigned char* DO = (unsigned char*)ws.d_out.p;
+  cudaError_t e;
   // ---- headers back, capacity check ----
-  if ((e = c.h_small.ensure(sizeof(OutHdr) * nv)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  OutHdr* hO = (OutHdr*)c.h_small.p;
+  if ((e = ws.h_small.ensure(sizeof(OutHdr) * nv)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  OutHdr* hO = (OutHdr*)ws.h_small.p;
   cudaMemcpyAsync(hO, DO + Ly.out, sizeof(OutHdr) * nv, cudaMemcpyDeviceToHost, s);
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   std::vector<OutHdr> hdr(hO, hO + nv);
+  g_d2h += (int64_t)(sizeof(OutHdr) * (size_t)nv);
   // packed offsets
   std::vector<int64_t> boff(nv, 0), eoff(nv, 0), ioff(nv, 0);
   size_t packed = 0;
@@ -761,14 +856,14 @@ int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, in
   ResultArena* ra = nullptr;
   if (!good.empty()) {
     const size_t offs_bytes = sizeof(int64_t) * 3 * (size_t)nv;
-    if ((e = c.d_pack.ensure(packed + offs_bytes + 256)) != cudaSuccess)
+    if ((e = ws.d_pack.ensure(packed + offs_bytes + 256)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-    if ((e = c.h_small.ensure(offs_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-    int64_t* ho = (int64_t*)c.h_small.p;
+    if ((e = ws.h_small.ensure(offs_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    int64_t* ho = (int64_t*)ws.h_small.p;
     std::memcpy(ho, boff.data(), sizeof(int64_t) * nv);
     std::memcpy(ho + nv, eoff.data(), sizeof(int64_t) * nv);
     std::memcpy(ho + 2 * nv, ioff.data(), sizeof(int64_t) * nv);
-    unsigned char* DP_ = (unsigned char*)c.d_pack.p;
+    unsigned char* DP_ = (unsigned char*)ws.d_pack.p;
     const size_t offs_at = (packed + 255) & ~(size_t)255;
     cudaMemcpyAsync(DP_ + offs_at, ho, offs_bytes, cudaMemcpyHostToDevice, s);
     CompactParams cpp;
@@ -785,6 +880,8 @@ int run_jobs(Ctx& c, slos_planner* const* planners, const slos_input* inputs, in
     ra = arena_get(c, packed + 64);
     if (!ra) return set_err(SLOS_ERR_ALLOC, "result arena");
     cudaMemcpyAsync(ra->p, DP_, packed, cudaMemcpyDeviceToHost, s);
+    g_d2h += (int64_t)packed;
+    g_h2d += (int64_t)offs_bytes;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   }
   for (int v = 0; v < nv; ++v) {
@@ -896,23 +993,33 @@ int slos_planner_create(const slos_perf_term* terms, int32_t n_terms, const doub
 
 void slos_planner_destroy(slos_planner* p) { delete p; }
 
-int slos_plan_batch(slos_planner* const* planners, int32_t n, const slos_input* inputs,
-                    int32_t unit_value, slos_result* outs, void* stream) {
-  (void)stream;
-  for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
-  Ctx& c = ctx();
-  std::lock_guard<std::mutex> g(c.mu);
-  const int st = ensure_device(c);
-  if (st != SLOS_OK) {
-    set_err(st, c.why);
-    for (int k = 0; k < n; ++k) outs[k].status = st;
-    return st;
-  }
+}  // extern "C"
+
+struct slos_workspace {
+  Workspace ws;
+  std::vector<Job> pending_retry;
+  bool has_inputs = false;
+  int n = 0;
+};
+
+namespace {
+Workspace& default_ws() {
+  static Workspace* w = new Workspace();
+  return *w;
+}
+
+// full pipeline with capacity regrowth; caller holds ctx().mu
+int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, const slos_input* inputs,
+             int32_t unit_value, slos_result* outs, cudaStream_t stream) {
   std::vector<Job> jobs(n), retry;
   for (int k = 0; k < n; ++k) jobs[k] = {k, 0};
+  g_h2d = 0;
+  g_d2h = 0;
   for (int round = 0; round < 8 && !jobs.empty(); ++round) {
     retry.clear();
-    const int r = run_jobs(c, planners, inputs, unit_value, jobs, outs, retry);
+    int r = ws_upload(c, ws, planners, inputs, unit_value, jobs, outs, stream);
+    if (r == SLOS_OK) r = ws_solve(ws, stream);
+    if (r == SLOS_OK) r = ws_collect(c, ws, outs, retry);
     if (r != SLOS_OK) {
       for (const Job& j : jobs) outs[j.k].status = r;
       return r;
@@ -924,6 +1031,115 @@ int slos_plan_batch(slos_planner* const* planners, int32_t n, const slos_input* 
     outs[j.k].status = SLOS_ERR_CAPACITY;
   }
   return SLOS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int slos_plan_batch(slos_planner* const* planners, int32_t n, const slos_input* inputs,
+                    int32_t unit_value, slos_result* outs, void* stream) {
+  for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  const int st = ensure_device(c);
+  if (st != SLOS_OK) {
+    set_err(st, c.why);
+    for (int k = 0; k < n; ++k) outs[k].status = st;
+    return st;
+  }
+  return plan_all(c, default_ws(), planners, n, inputs, unit_value, outs, (cudaStream_t)stream);
+}
+
+int slos_workspace_create(slos_workspace** out) {
+  *out = nullptr;
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  const int st = ensure_device(c);
+  if (st != SLOS_OK) return set_err(st, c.why);
+  *out = new slos_workspace();
+  return SLOS_OK;
+}
+
+void slos_workspace_destroy(slos_workspace* b) {
+  if (!b) return;
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  cudaDeviceSynchronize();
+  for (DevBuf* d : {&b->ws.d_in, &b->ws.d_scr, &b->ws.d_out, &b->ws.d_pack, &b->ws.d_wscr})
+    if (d->p) cudaFree(d->p);
+  for (PinBuf* h : {&b->ws.h_in, &b->ws.h_small})
+    if (h->p) cudaFreeHost(h->p);
+  delete b;
+}
+
+int slos_workspace_upload(slos_workspace* b, slos_planner* const* planners, int32_t n, const slos_input* inputs,
+                      int32_t unit_value, slos_result* outs, void* stream) {
+  for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  std::vector<Job> jobs(n);
+  for (int k = 0; k < n; ++k) jobs[k] = {k, 0};
+  b->n = n;
+  b->has_inputs = true;
+  g_h2d = 0;
+  g_d2h = 0;
+  return ws_upload(c, b->ws, planners, inputs, unit_value, jobs, outs, (cudaStream_t)stream);
+}
+
+int slos_workspace_solve(slos_workspace* b, void* stream) {
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  return ws_solve(b->ws, (cudaStream_t)stream);
+}
+
+int slos_workspace_download(slos_workspace* b, slos_result* outs, void* stream) {
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  std::vector<Job> retry;
+  int r = ws_collect(c, b->ws, outs, retry);
+  if (r != SLOS_OK || retry.empty()) return r;
+  // regrow the overflowed instances (rare) through the full pipeline
+  std::vector<Job> jobs = retry;
+  for (int round = 0; round < 8 && !jobs.empty(); ++round) {
+    std::vector<Job> again;
+    r = ws_upload(c, b->ws, b->ws.planners, b->ws.inputs, b->ws.unit_value, jobs, outs, (cudaStream_t)stream);
+    if (r == SLOS_OK) r = ws_solve(b->ws, (cudaStream_t)stream);
+    if (r == SLOS_OK) r = ws_collect(c, b->ws, outs, again);
+    if (r != SLOS_OK) return r;
+    jobs.swap(again);
+  }
+  for (const Job& j : jobs) outs[j.k].status = SLOS_ERR_CAPACITY;
+  b->has_inputs = false;
+  return SLOS_OK;
+}
+
+int slos_workspace_records(slos_workspace* b, slos_record* out, void* stream) {
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  Workspace& ws = b->ws;
+  if (!ws.uploaded) return set_err(SLOS_ERR_INVALID_PARAMETERS, "nothing uploaded");
+  const cudaStream_t s = stream ? (cudaStream_t)stream : ws.stream;
+  unsigned char* DI = (unsigned char*)ws.d_in.p;
+  cudaError_t e = cudaMemcpyAsync(out, DI + ws.Ly.recdef, sizeof(slos_record) * (size_t)ws.n_total,
+                                  cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess)
+    e = launch_records(ws.A.out, (const int32_t*)(DI + ws.Ly.recmap), ws.nv, out, s);
+  return e == cudaSuccess ? SLOS_OK : set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+}
+
+int slos_workspace_kernel_ms(slos_workspace* b, float* ms2) {
+  Workspace& ws = b->ws;
+  ms2[0] = ms2[1] = 0.0f;
+  if (!ws.ev[2]) return SLOS_OK;
+  cudaEventSynchronize(ws.ev[2]);
+  cudaEventElapsedTime(&ms2[0], ws.ev[0], ws.ev[1]);
+  cudaEventElapsedTime(&ms2[1], ws.ev[1], ws.ev[2]);
+  return SLOS_OK;
+}
+
+void slos_last_transfer_bytes(int64_t* h2d, int64_t* d2h) {
+  *h2d = g_h2d;
+  *d2h = g_d2h;
 }
 
 int slos_plan(slos_planner* p, const slos_input* in, int32_t unit_value, slos_result* out) {

@@ -94,4 +94,31 @@ cudaError_t launch_spec(const PlannerDev* P, const int64_t* counts, void* out, c
 
 size_t spec_sol_bytes() { return sizeof(SpecSol); }
 
+__global__ void records_kernel(const OutHdr* out, const int32_t* map, int nv, slos_record* rec) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const OutHdr& h = out[v];
+  slos_record r;
+  r.status = h.status;
+  r.running_set_infeasible = h.infeasible;
+  r.n_admitted = h.n_admitted;
+  r.n_declined = h.n_declined;
+  r.admitted_value = h.value;
+  r.n_batches = h.n_batches;
+  r.n_entries = h.n_entries;
+  r.exact_until_s = h.exact_until;
+  r.counters.transitions = h.ctr[0];
+  r.counters.gap_evals = h.ctr[1];
+  r.counters.dues = h.ctr[2];
+  r.counters.slots = h.ctr[3];
+  r.counters.states = h.ctr[4];
+  rec[map[v]] = r;
+}
+
+cudaError_t launch_records(const OutHdr* out, const int32_t* map, int nv, slos_record* rec, cudaStream_t s) {
+  if (nv <= 0) return cudaSuccess;
+  records_kernel<<<(nv + 127) / 128, 128, 0, s>>>(out, map, nv, rec);
+  return cudaGetLastError();
+}
+
 }  // namespace slos
