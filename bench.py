@@ -193,6 +193,7 @@ def run_ours(args):
     rec = torch.empty((per, C.sizeof(abi.Record)), dtype=torch.uint8, device="cuda")
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     solver.upload(sptr)
+    solver.converge(rec, sptr)
     torch.cuda.synchronize()
 
     def step():

@@ -359,9 +359,10 @@ Caps estimate_caps(const slos_planner* P, const slos_input* in, const Prep& pr, 
   const int64_t S = std::max<int64_t>({S_gap, S_tail, 16});
   const int64_t M = pr.n_dec + pr.N + 1;
   const int64_t g = (int64_t)1 << (2 * grow);
-  c.surv = std::max<int64_t>(1024, 64 * (int64_t)(pr.N + 1)) * g;
-  c.cand = pow2_at_least(std::max<int64_t>(512, 16 * (int64_t)(pr.N + 1)) * g);
-  c.memo = pow2_at_least(std::max<int64_t>(2048, 64 * (int64_t)(pr.N + 1)) * g);
+  const int64_t N1 = pr.N + 1;
+  c.surv = std::max<int64_t>(4096, 16 * N1 * N1) * g;
+  c.cand = pow2_at_least(std::max<int64_t>(1024, 4 * N1 * N1) * g);
+  c.memo = pow2_at_least(std::max<int64_t>(4096, 8 * N1 * N1) * g);
   c.gb = (S + 8) << (2 * grow);
   c.go = M * c.gb;
   // plan output: gaps + tail, or the fallback (until every line completes)
@@ -997,7 +998,7 @@ void slos_planner_destroy(slos_planner* p) { delete p; }
 
 struct slos_workspace {
   Workspace ws;
-  std::vector<Job> pending_retry;
+  std::vector<int> grow;  // per instance: capacity growth that made it fit
   bool has_inputs = false;
   int n = 0;
 };
@@ -1077,8 +1078,9 @@ int slos_workspace_upload(slos_workspace* b, slos_planner* const* planners, int3
   for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
   Ctx& c = ctx();
   std::lock_guard<std::mutex> g(c.mu);
+  if ((int)b->grow.size() != n || b->ws.inputs != inputs) b->grow.assign(n, 0);
   std::vector<Job> jobs(n);
-  for (int k = 0; k < n; ++k) jobs[k] = {k, 0};
+  for (int k = 0; k < n; ++k) jobs[k] = {k, b->grow[k]};
   b->n = n;
   b->has_inputs = true;
   g_h2d = 0;
@@ -1098,9 +1100,11 @@ int slos_workspace_download(slos_workspace* b, slos_result* outs, void* stream) 
   std::vector<Job> retry;
   int r = ws_collect(c, b->ws, outs, retry);
   if (r != SLOS_OK || retry.empty()) return r;
-  // regrow the overflowed instances (rare) through the full pipeline
+  // Regrow the overflowed instances (rare), remember their capacities, then
+  // re-upload the whole batch so the resident workspace fits from now on.
   std::vector<Job> jobs = retry;
   for (int round = 0; round < 8 && !jobs.empty(); ++round) {
+    for (const Job& j : jobs) b->grow[j.k] = j.grow;
     std::vector<Job> again;
     r = ws_upload(c, b->ws, b->ws.planners, b->ws.inputs, b->ws.unit_value, jobs, outs, (cudaStream_t)stream);
     if (r == SLOS_OK) r = ws_solve(b->ws, (cudaStream_t)stream);
@@ -1109,8 +1113,11 @@ int slos_workspace_download(slos_workspace* b, slos_result* outs, void* stream) 
     jobs.swap(again);
   }
   for (const Job& j : jobs) outs[j.k].status = SLOS_ERR_CAPACITY;
-  b->has_inputs = false;
-  return SLOS_OK;
+  std::vector<Job> all(b->n);
+  for (int k = 0; k < b->n; ++k) all[k] = {k, b->grow[k]};
+  std::vector<slos_result> scratch(b->n);
+  return ws_upload(c, b->ws, b->ws.planners, b->ws.inputs, b->ws.unit_value, all, scratch.data(),
+                   (cudaStream_t)stream);
 }
 
 int slos_workspace_records(slos_workspace* b, slos_record* out, void* stream) {

@@ -14,7 +14,7 @@ sharding and gather logic is covered by world_size-2 gloo tests on CPU.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -40,7 +40,7 @@ class ShardSpec:
     family: StressSpec
     model: list
     cfg: PlannerConfig
-    slo: SloConfig = TWO_TIER_SLO
+    slo: SloConfig = field(default_factory=lambda: TWO_TIER_SLO)
 
 
 class ShardSolver:
@@ -75,6 +75,20 @@ class ShardSolver:
         st = self.lib.slos_workspace_records(self.ws, C.c_void_p(out_ptr), stream)
         if st != abi.SLOS_OK:
             raise RuntimeError(self.lib.slos_last_error().decode())
+
+    def converge(self, rec_tensor, stream=None, rounds: int = 4) -> None:
+        """Solve once; if an instance overflowed its scratch estimate, let download
+        regrow it (the workspace remembers) so every later solve fits."""
+        import torch
+        for _ in range(rounds):
+            self.solve(stream)
+            self.records(rec_tensor.data_ptr(), stream)
+            torch.cuda.synchronize()
+            st = records_view(rec_tensor)["status"]
+            if not (st == abi.SLOS_ERR_CAPACITY).any():
+                return
+            self.download(stream)
+            self.free_results()
 
     def kernel_ms(self):
         ms = (C.c_float * 2)()
