@@ -35,6 +35,8 @@ struct DpParams {
   int dec_smem_max;    // stage decoders in smem when n_dec <= this
   unsigned char* wscr_global;  // per-CTA-slot warp scratch when not in smem (nullptr = smem)
   size_t wscr_stride;  // bytes per warp in wscr_global
+  int Gmax;            // anchor groups per evaluation wave (shared variants in smem)
+  size_t gstride;      // bytes per group variant
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -97,14 +99,18 @@ __device__ inline int memo_find_insert(MemoEnt* T, int64_t cap, uint64_t k0, uin
 }
 
 // Evaluate one memo key (counts c) of a group: tile_gap(gap, census, dh).prefill_budget.
-__device__ inline EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D, GapGroup& g,
-                                           Variant& v, const WarpScr& w, const int64_t* c,
-                                           double min_slot) {
+// `gv`/`ga` is the group's shared exact-census variant (built by the block); a
+// count vector whose tightest tier differs builds a private variant in `w`.
+__device__ inline EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D, const GapGroup& g,
+                                           const Variant& gv, const GroupVar& ga, int Sc,
+                                           const WarpScr& w, const int64_t* c, double min_slot,
+                                           int* spill_out) {
   EvalOut o;
   o.status = 0; o.has = false; o.budget = 0; o.dues = 0; o.slots = 0;
   const int L = P.L;
   unsigned cmask = 0;
   for (int l = 0; l < L; ++l) if (c[l] > 0) cmask |= 1u << l;
+  *spill_out = gv.valid ? gv.spill : 0;
   // ---------------- tile_gap_ar (budget) ----------------
   bool ar_has = false;
   int64_t ar_budget = 0;
@@ -113,53 +119,59 @@ __device__ inline EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D
   } else {
     const unsigned present = g.exact_mask | cmask;
     if (!present) {
-      if (g.po_state == 0) {
+      int st = 0;
+      int64_t b = 0;
+      if (lane_id() == 0) b = prefill_only_budget(P, g.gap, min_slot, &st);
+      st = __shfl_sync(0xffffffffu, st, 0);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (st) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return o; }
+      ar_has = true;
+      ar_budget = b;
+    } else {
+      const double t0 = P.tpot[__ffs(present) - 1];
+      Variant vp;
+      const Variant* v;
+      const double* ends;
+      const int64_t* cap;
+      const int32_t* nx;
+      const int32_t* hc;
+      int scap;
+      if (gv.valid && gv.t0 == t0) {
+        v = &gv; ends = ga.ends; cap = ga.cap; nx = ga.nx; hc = ga.hc; scap = Sc;
+        if (gv.S > Sc) { o.status = SLOS_ERR_CAPACITY; return o; }  // histogram was not built
+      } else {
+        warp_build_variant(P, D, g, t0, min_slot, w, vp);
+        v = &vp; ends = w.ends; cap = w.cap; nx = w.nx; hc = w.hc; scap = w.Sc;
+        *spill_out = vp.spill;
+      }
+      int64_t Dtot = v->Dx;
+      for (int l = 0; l < L; ++l) Dtot += c[l] * (int64_t)v->q[l];
+      o.dues += Dtot;
+      if (Dtot == 0) {
         int st = 0;
         int64_t b = 0;
         if (lane_id() == 0) b = prefill_only_budget(P, g.gap, min_slot, &st);
         st = __shfl_sync(0xffffffffu, st, 0);
         b = __shfl_sync(0xffffffffu, b, 0);
-        g.po_state = st ? 2 : 1;
-        g.po_budget = b;
-      }
-      if (g.po_state == 2) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return o; }
-      ar_has = true;
-      ar_budget = g.po_budget;
-    } else {
-      const double t0 = P.tpot[__ffs(present) - 1];
-      if (!v.valid || v.t0 != t0) warp_build_variant(P, D, g, t0, min_slot, w, v);
-      int64_t Dtot = v.Dx;
-      for (int l = 0; l < L; ++l) Dtot += c[l] * (int64_t)v.q[l];
-      o.dues += Dtot;
-      if (Dtot == 0) {
-        if (g.po_state == 0) {
-          int st = 0;
-          int64_t b = 0;
-          if (lane_id() == 0) b = prefill_only_budget(P, g.gap, min_slot, &st);
-          st = __shfl_sync(0xffffffffu, st, 0);
-          b = __shfl_sync(0xffffffffu, b, 0);
-          g.po_state = st ? 2 : 1;
-          g.po_budget = b;
-        }
-        if (g.po_state == 2) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return o; }
+        if (st) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return o; }
         ar_has = true;
-        ar_budget = g.po_budget;
+        ar_budget = b;
       } else if (min_slot > t0 + kTimeEps) {
         ar_has = false;
       } else {
-        o.slots += v.S;
-        if (v.S == 0) {
+        o.slots += v->S;
+        if (v->S == 0) {
           ar_has = false;
-        } else if (v.S > w.Sc) {
+        } else if (v->S > scap) {
           o.status = SLOS_ERR_CAPACITY;
           return o;
-        } else if (v.cap_err) {
+        } else if (v->cap_err) {
           o.status = SLOS_ERR_INFEASIBLE_BUDGET;
           return o;
-        } else if (v.exact_fail || (v.cfail & cmask)) {
+        } else if (v->exact_fail || (v->cfail & cmask)) {
           ar_has = false;
         } else {
-          ar_has = warp_place_budget(P, v, w.ends, w.cap, w.nx, w.hc, w.tmp, c, &ar_budget) != 0;
+          ar_has = warp_place_budget(P, *v, ends, cap, nx, hc, w.tmp, c, &ar_budget) != 0;
         }
       }
     }
@@ -169,7 +181,7 @@ __device__ inline EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D
   // ---------------- tile_gap speculative branch (batch_planner.cpp:318-405) -----
   if (!P.speculative) return o;
   if (g.n_exact == 0 && cmask == 0) return o;  // census.empty()
-  const bool spill = v.valid ? v.spill : false;
+  const bool spill = *spill_out != 0;
   if (g.has_backlog) return o;
   if (g.dh > g.gap + kTimeEps && spill) return o;
   int64_t merged[kMaxTiers];
@@ -265,7 +277,7 @@ __device__ inline EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D
   return o;
 }
 
-__global__ void __launch_bounds__(kDpThreads) dp_kernel(DpParams prm) {
+__global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;
@@ -276,7 +288,8 @@ __global__ void __launch_bounds__(kDpThreads) dp_kernel(DpParams prm) {
   __shared__ int32_t s_joff[SLOS_MAX_CHAIN + 2];
   __shared__ int64_t s_wsum[kDpWarps + 1];
   __shared__ unsigned long long s_ctr[5];
-  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_next_grp, s_best;
+  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_next_grp, s_best, s_ng;
+  __shared__ int32_t s_glist[SLOS_MAX_CHAIN + 2];
   __shared__ int64_t s_next_free, s_arena_next;
 
   const BatchArgs& A = prm.a;
@@ -349,6 +362,12 @@ __global__ void __launch_bounds__(kDpThreads) dp_kernel(DpParams prm) {
     wbase = p + (size_t)warp_id() * prm.wscr_stride;
   }
   const WarpScr W = warp_scr_carve(wbase, prm.Sc, prm.Lmax);
+  if (!prm.wscr_global) p += (size_t)kDpWarps * prm.wscr_stride;
+  p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+  GroupHdr* ghdr = (GroupHdr*)p;
+  p += sizeof(GroupHdr) * (size_t)prm.Gmax;
+  p = (unsigned char*)(((uintptr_t)p + 127) & ~(uintptr_t)127);
+  unsigned char* gvbase = p;
 
   // ---- scratch slices ----
   uint64_t* Sc_ = A.s_counts + I.off_surv;
@@ -459,17 +478,21 @@ __global__ void __launch_bounds__(kDpThreads) dp_kernel(DpParams prm) {
       G[pos] = slot;
     }
     __syncthreads();
-    {
-      const int lane = lane_id();
-      unsigned long long wd = 0, ws = 0;
-      for (;;) {
-        int grp = 0;
-        if (lane == 0) grp = atomicAdd(&s_next_grp, 1);
-        grp = __shfl_sync(0xffffffffu, grp, 0);
-        if (grp >= nlev || s_err) break;
-        const int cnt = s_jcnt[grp];
-        if (cnt == 0) continue;
-        const int j = jlo + grp;
+    if (tid == 0) {  // anchors with at least one new key, ascending
+      int ng = 0;
+      for (int k = 0; k < nlev; ++k) if (s_jcnt[k] > 0) s_glist[ng++] = k;
+      s_ng = ng;
+    }
+    __syncthreads();
+    const int ng = s_ng;
+    const int nch = (D.n + 31) / 32;
+    for (int w0 = 0; w0 < ng && !s_err; w0 += prm.Gmax) {
+      const int gw = min(prm.Gmax, ng - w0);
+      // E1: group setup, one warp per anchor group
+      for (int gi = warp_id(); gi < gw; gi += kDpWarps) {
+        const int k = s_glist[w0 + gi];
+        const int j = jlo + k;
+        GroupHdr& H = ghdr[gi];
         GapGroup g;
         g.a = (j < 0) ? I.now : ch_dl[j];
         const double raw = dmax(0.0, t_i - g.a);
@@ -480,36 +503,79 @@ __global__ void __launch_bounds__(kDpThreads) dp_kernel(DpParams prm) {
         if (g.exact) { g.gap = len; g.dh = raw + pull; }
         else { g.gap = quantize_gap(len); g.dh = 0.0; }
         g.horizon = dmax(g.gap, g.dh);
-        warp_group_setup(P, D, g);
         Variant v;
-        v.valid = false;
-        for (int q = 0; q < cnt; ++q) {
-          MemoEnt* e = &Memo[G[s_joff[grp] + q]];
+        const GroupVar ga = group_var_carve(gvbase + (size_t)gi * prm.gstride, prm.Sc, L);
+        warp_group_init(P, D, g, v, ga, prm.Sc, min_slot);
+        if (lane_id() == 0) { H.g = g; H.v = v; }
+      }
+      __syncthreads();
+      // E2: member-chunk histogram tasks (group, 32 members)
+      for (int t = warp_id(); t < gw * nch; t += kDpWarps) {
+        const int gi = t / nch;
+        GroupHdr& H = ghdr[gi];
+        if (!H.v.valid || H.v.S > prm.Sc) continue;
+        const GroupVar ga = group_var_carve(gvbase + (size_t)gi * prm.gstride, prm.Sc, L);
+        const int k = (t % nch) * 32 + lane_id();
+        int64_t late = 0, dues = 0;
+        int fail = 0, spill = 0;
+        if (k < D.n) {
+          const Member m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], H.g.now, H.g.a, H.g.pull);
+          if (m.valid && m.rem > 0)
+            member_dues(P, m, H.g, ga.ends, H.v.S, true, H.v.inc != 0, ga.nx, late, dues, fail, spill);
+        }
+        late = warp_sum(late);
+        dues = warp_sum(dues);
+        fail = warp_or(fail);
+        spill = warp_or(spill);
+        if (lane_id() == 0) {
+          if (late) atomicAdd((unsigned long long*)&H.v.Lx, (unsigned long long)late);
+          if (late + dues) atomicAdd((unsigned long long*)&H.v.Dx, (unsigned long long)(late + dues));
+          if (fail) atomicOr(&H.v.exact_fail, 1);
+          if (spill) atomicOr(&H.v.spill, 1);
+        }
+      }
+      __syncthreads();
+      // E3: one warp per memo key of this wave
+      {
+        const int kfirst = s_glist[w0], klast = s_glist[w0 + gw - 1];
+        const int q0 = s_joff[kfirst], q1 = s_joff[klast] + s_jcnt[klast];
+        unsigned long long wd = 0, wsl = 0;
+        for (int q = q0 + warp_id(); q < q1; q += kDpWarps) {
+          if (s_err) break;
+          int lo = 0, hi = gw - 1;  // group of key q: last gi with s_joff[glist[w0+gi]] <= q
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (s_joff[s_glist[w0 + mid]] <= q) lo = mid; else hi = mid - 1;
+          }
+          const GroupHdr& H = ghdr[lo];
+          const GroupVar ga = group_var_carve(gvbase + (size_t)lo * prm.gstride, prm.Sc, L);
+          MemoEnt* e = &Memo[G[q]];
           const uint64_t cw = e->k2;
           int64_t cv[kMaxTiers];
           for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
-          const EvalOut r = warp_eval_counts(P, D, g, v, W, cv, min_slot);
+          int spill = 0;
+          const EvalOut r = warp_eval_counts(P, D, H.g, H.v, ga, prm.Sc, W, cv, min_slot, &spill);
           wd += (unsigned long long)r.dues;
-          ws += (unsigned long long)r.slots;
+          wsl += (unsigned long long)r.slots;
           if (r.status) {
-            if (lane == 0) {
+            if (lane_id() == 0) {
               atomicCAS(&s_err, 0, r.status);
               if (r.status == SLOS_ERR_CAPACITY) out->need_work = 2 * prm.Sc;
             }
             break;
           }
-          if (lane == 0) {
+          if (lane_id() == 0) {
             e->has = r.has ? 1 : 0;
             e->val = r.budget;
           }
         }
+        if (lane_id() == 0) {
+          atomicAdd(&s_ctr[2], wd);
+          atomicAdd(&s_ctr[3], wsl);
+        }
       }
-      if (lane == 0) {
-        atomicAdd(&s_ctr[2], wd);
-        atomicAdd(&s_ctr[3], ws);
-      }
+      __syncthreads();
     }
-    __syncthreads();
     if (s_err) break;
     for (int q = tid; q < n_new; q += kDpThreads) Memo[X0[q]].state = 3;
     // ---- 4: candidate states ----

@@ -96,12 +96,81 @@ struct Variant {
   int64_t Lx;       // exact late dues
   int64_t Dx;       // exact dues materialised
   int q[kMaxTiers]; // canonical due times per tier
-  bool exact_fail;  // an exact non-late due with jit < 0
+  int exact_fail;   // an exact non-late due with jit < 0
   unsigned cfail;   // tiers whose canonical dues have jit < 0
-  bool cap_err;     // plan_time2bs threw on some slot
-  bool spill;       // spec: an exact due past gap (within due_horizon)
-  bool valid;
+  int cap_err;      // plan_time2bs threw on some slot
+  int spill;        // spec: an exact due past gap (within due_horizon)
+  int valid;
+  int inc;          // slot ends strictly increasing -> jit may be walked
 };
+
+// A group's shared variant arrays (shared memory).
+struct GroupVar {
+  double* ends;
+  int64_t* cap;
+  int32_t* nx;
+  int32_t* hc;
+};
+
+struct GroupHdr {
+  GapGroup g;
+  Variant v;
+};
+
+__host__ __device__ __forceinline__ size_t group_var_stride(int Sc, int L) {
+  return (((size_t)Sc * (8 + 8 + 4 + 4 * (size_t)L)) + 127) & ~(size_t)127;
+}
+
+__device__ __forceinline__ GroupVar group_var_carve(unsigned char* base, int Sc, int L) {
+  GroupVar g;
+  g.ends = (double*)base;
+  g.cap = (int64_t*)(base + (size_t)Sc * 8);
+  g.nx = (int32_t*)(base + (size_t)Sc * 16);
+  g.hc = (int32_t*)(base + (size_t)Sc * 20);
+  (void)L;
+  return g;
+}
+
+// Exact-member dues of one member into a slot histogram (shared by the warp
+// variant builder and the block-wide member-chunk tasks). jit is walked forward
+// from the previous due (due times increase along a line) when the slot ends
+// are strictly increasing, which gives exactly the reference's binary-search
+// result; otherwise every due binary-searches like the reference.
+__device__ __forceinline__ void member_dues(const PlannerDev& P, const Member& m, const GapGroup& g,
+                                            const double* ends, int S, bool fits, bool inc,
+                                            int32_t* nx, int64_t& late, int64_t& dues, int& fail,
+                                            int& spill) {
+  int64_t issued = m.backlog > 0 ? imin(m.backlog, m.rem) : 0;
+  late += issued;
+  const double tpot = P.tpot[m.tier];
+  int jit = -1;
+  bool first = true;
+  for (double d = dmax(m.phase, 0.0); time_le(d, g.horizon) && issued < m.rem; d += tpot, ++issued) {
+    if (!time_le(d, g.gap)) spill = 1;
+    if (d <= kTimeEps) {
+      ++late;
+    } else {
+      ++dues;
+      if (fits) {
+        if (!inc || first) {
+          jit = jit_search(ends, S, d);
+          first = false;
+        } else {
+          while (jit + 1 < S && time_le(ends[jit + 1], d)) ++jit;
+        }
+        if (jit < 0) fail = 1; else atomicAdd(&nx[jit], 1);
+      }
+    }
+  }
+  if (m.backlog < 0 && g.dh > g.gap + kTimeEps) {
+    // tile_gap's spill scan starts from min(backlog, remaining) (batch_planner.cpp:329):
+    // with a negative backlog it runs past the autoregressive loop's last due.
+    int64_t is2 = imin(m.backlog, m.rem);
+    for (double d = dmax(m.phase, 0.0); time_le(d, g.dh) && is2 < m.rem; d += tpot, ++is2)
+      if (!time_le(d, g.gap)) spill = 1;
+  }
+}
+
 
 struct EvalOut {
   int status;     // 0 ok, else SLOS_ERR_*
@@ -204,7 +273,7 @@ __device__ inline void warp_build_variant(const PlannerDev& P, const DecView& D,
   v.t0 = t0;
   v.t0_first = warp_t0_first(P, D, g, t0, min_slot);
   v.S = warp_slot_ends(w.ends, w.Sc, v.t0_first, t0, g.gap, min_slot);
-  v.valid = true;
+  v.valid = 1;
   const int S = v.S;
   const bool fits = S <= w.Sc;
   int cap_err = 0;
@@ -218,35 +287,25 @@ __device__ inline void warp_build_variant(const PlannerDev& P, const DecView& D,
     }
     for (int x = lane; x < S * P.L; x += 32) w.hc[x] = 0;  // layout hc[l*S + s]
   }
-  v.cap_err = warp_or(cap_err) != 0;
+  v.cap_err = warp_or(cap_err);
   __syncwarp();
+  int inc = 1;
+  if (fits && lane_id() == 0)
+    for (int x = 1; x < S; ++x) if (!(w.ends[x - 1] < w.ends[x])) inc = 0;
+  v.inc = __shfl_sync(0xffffffffu, inc, 0);
   int64_t late = 0, dues = 0;
   int fail = 0, spill = 0;
   if (g.exact) {
     for (int k = lane; k < D.n; k += 32) {
       const Member m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], g.now, g.a, g.pull);
       if (!m.valid || m.rem <= 0) continue;
-      int64_t issued = m.backlog > 0 ? imin(m.backlog, m.rem) : 0;
-      late += issued;
-      const double tpot = P.tpot[m.tier];
-      for (double d = dmax(m.phase, 0.0); time_le(d, g.horizon) && issued < m.rem; d += tpot, ++issued) {
-        if (!time_le(d, g.gap)) spill = 1;
-        if (d <= kTimeEps) {
-          ++late;
-        } else {
-          ++dues;
-          if (fits) {
-            const int jit = jit_search(w.ends, S, d);
-            if (jit < 0) fail = 1; else atomicAdd(&w.nx[jit], 1);
-          }
-        }
-      }
+      member_dues(P, m, g, w.ends, S, fits, v.inc != 0, w.nx, late, dues, fail, spill);
     }
   }
   v.Lx = warp_sum(late);
   v.Dx = warp_sum(dues) + v.Lx;
-  v.exact_fail = warp_or(fail) != 0;
-  v.spill = warp_or(spill) != 0;
+  v.exact_fail = warp_or(fail);
+  v.spill = warp_or(spill);
   // canonical dues per tier (batch_planner.cpp:214-220): lane l owns tier l
   int q = 0, cf = 0;
   if (lane < P.L) {
@@ -264,6 +323,65 @@ __device__ inline void warp_build_variant(const PlannerDev& P, const DecView& D,
   __syncwarp();
 }
 
+// Group setup (E1 of a DP level): group facts + the shared variant's slot grid,
+// capacities and canonical histogram for the exact census' tightest tier. The
+// member-due histogram (nx, Lx, Dx, flags) is filled afterwards by block-wide
+// member-chunk tasks (E2), see dp_kernel.
+__device__ inline void warp_group_init(const PlannerDev& P, const DecView& D, GapGroup& g,
+                                       Variant& v, const GroupVar& ga, int Sc, double min_slot) {
+  const int lane = lane_id();
+  warp_group_setup(P, D, g);
+  v.valid = 0;
+  v.S = 0;
+  v.Lx = 0;
+  v.Dx = 0;
+  v.exact_fail = 0;
+  v.spill = 0;
+  v.cap_err = 0;
+  v.cfail = 0;
+  v.inc = 0;
+  for (int l = 0; l < kMaxTiers; ++l) v.q[l] = 0;
+  if (g.gap <= kTimeEps || !g.exact_mask) return;
+  const double t0 = P.tpot[__ffs(g.exact_mask) - 1];
+  v.t0 = t0;
+  v.t0_first = warp_t0_first(P, D, g, t0, min_slot);
+  v.S = warp_slot_ends(ga.ends, Sc, v.t0_first, t0, g.gap, min_slot);
+  v.valid = 1;
+  const int S = v.S;
+  {
+    int q = 0;
+    if (lane < P.L)
+      for (double d = P.tpot[lane]; time_le(d, g.gap); d += P.tpot[lane]) ++q;
+    for (int l = 0; l < P.L; ++l) v.q[l] = __shfl_sync(0xffffffffu, q, l);
+  }
+  if (S > Sc) return;  // surfaces as SLOS_ERR_CAPACITY when a key reaches the slots
+  int cap_err = 0;
+  for (int s = lane; s < S; s += 32) {
+    const double dur = ga.ends[s] - (s == 0 ? 0.0 : ga.ends[s - 1]);
+    const int64_t c = plan_time2bs(P, dur, 0);
+    if (c < 0) cap_err = 1;
+    ga.cap[s] = imin(c, P.max_batch);
+    ga.nx[s] = 0;
+  }
+  for (int x = lane; x < S * P.L; x += 32) ga.hc[x] = 0;
+  v.cap_err = warp_or(cap_err);
+  int inc = 1;
+  if (lane == 0)
+    for (int x = 1; x < S; ++x) if (!(ga.ends[x - 1] < ga.ends[x])) inc = 0;
+  v.inc = __shfl_sync(0xffffffffu, inc, 0);
+  __syncwarp();
+  int cf = 0;
+  if (lane < P.L) {
+    const double tpot = P.tpot[lane];
+    for (double d = tpot; time_le(d, g.gap); d += tpot) {
+      const int jit = jit_search(ga.ends, S, d);
+      if (jit < 0) cf = 1; else ga.hc[lane * S + jit] += 1;
+    }
+  }
+  v.cfail = __ballot_sync(0xffffffffu, cf != 0);
+  __syncwarp();
+}
+
 // Canonical-only variant (no exact members) for the speculative remainder
 // tile_gap_ar(gap - used, rest) (batch_planner.cpp:390-395).
 __device__ inline void warp_build_canon_variant(const PlannerDev& P, double gap, double t0,
@@ -273,7 +391,7 @@ __device__ inline void warp_build_canon_variant(const PlannerDev& P, double gap,
   v.t0 = t0;
   v.t0_first = t0;
   v.S = warp_slot_ends(ends, Sc, t0, t0, gap, min_slot);
-  v.valid = true;
+  v.valid = 1;
   const int S = v.S;
   const bool fits = S <= Sc;
   int cap_err = 0;
@@ -286,11 +404,12 @@ __device__ inline void warp_build_canon_variant(const PlannerDev& P, double gap,
     }
     for (int x = lane; x < S * P.L; x += 32) hc[x] = 0;
   }
-  v.cap_err = warp_or(cap_err) != 0;
+  v.cap_err = warp_or(cap_err);
   v.Lx = 0;
   v.Dx = 0;
-  v.exact_fail = false;
-  v.spill = false;
+  v.exact_fail = 0;
+  v.spill = 0;
+  v.inc = 0;
   __syncwarp();
   int q = 0, cf = 0;
   if (lane < P.L) {

@@ -34,6 +34,8 @@ struct DpParams {
   int dec_smem_max;
   unsigned char* wscr_global;
   size_t wscr_stride;
+  int Gmax;
+  size_t gstride;
 };
 struct BuildParams {
   BatchArgs a;
@@ -763,20 +765,23 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   dp.Sc = (int)std::min<double>(S_need, 1 << 20);
   const size_t stride = dp_warp_scr_stride(dp.Sc, Lmax);
   dp.wscr_stride = stride;
-  const size_t kSmemBudget = 100 * 1024;
+  const size_t kSmemBudget = 72 * 1024;  // 3 CTAs of 256 threads per SM
+  dp.gstride = dp_group_stride(dp.Sc, Lmax);
+  dp.Gmax = std::max(1, std::min(maxN + 1, 32));
   size_t& smem = ws.smem;
-  smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, true);
-  if (smem <= kSmemBudget) {
-    dp.wscr_global = nullptr;
-  } else {
+  dp.wscr_global = nullptr;
+  while (dp.Gmax > 4 && dp_smem_bytes(maxN, 0, dp.Sc, Lmax, true, dp.Gmax) > kSmemBudget) dp.Gmax /= 2;
+  smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, true, dp.Gmax);
+  if (smem > kSmemBudget) {
     if ((e = ws.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     dp.wscr_global = (unsigned char*)ws.d_wscr.p;
-    smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, false);
+    dp.Gmax = 1;
+    smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, false, dp.Gmax);
   }
   dp.dec_smem_max = 0;
   {
-    const size_t with_dec = dp_smem_bytes(maxN, maxDec, dp.Sc, Lmax, dp.wscr_global == nullptr);
+    const size_t with_dec = dp_smem_bytes(maxN, maxDec, dp.Sc, Lmax, dp.wscr_global == nullptr, dp.Gmax);
     if (with_dec <= kSmemBudget) { dp.dec_smem_max = maxDec; smem = with_dec; }
   }
   ws.valid = valid;

@@ -30,13 +30,16 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactParams p) {
   for (int x = threadIdx.x; x < o.n_declined; x += blockDim.x) di[o.n_admitted + x] = ids[I.n_pending + x];
 }
 
-size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, bool wscr_in_smem) {
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, bool wscr_in_smem, int Gmax) {
   const size_t N = (size_t)max_N;
   size_t b = 8 * (N + 1) * 4 + 8 * (N + 2) + 4 * (N + 2) * 3 + 64;
   b += (size_t)max_dec_staged * 28 + 64;
   if (wscr_in_smem) b += (size_t)kDpWarps * dp_warp_scr_stride(Sc, L);
+  b += 16 + sizeof(GroupHdr) * (size_t)Gmax + 128 + group_var_stride(Sc, L) * (size_t)Gmax;
   return b;
 }
+
+size_t dp_group_stride(int Sc, int L) { return group_var_stride(Sc, L); }
 
 size_t dp_warp_scr_stride(int Sc, int L) {
   const size_t s = (size_t)Sc * (8 + 8 + 4 + 4 * L + 8 + 8 + 8 + 4 * L) + (size_t)(Sc + 2) * 8 + 64;

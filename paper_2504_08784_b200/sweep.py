@@ -118,7 +118,12 @@ def gather_records(local, world: int, group=None):
     if world == 1:
         return local
     out = torch.empty((world * local.shape[0], local.shape[1]), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(out, local, group=group)
+    if local.is_cuda:
+        dist.all_gather_into_tensor(out, local, group=group)
+    else:  # gloo (CPU tests)
+        parts = list(out.chunk(world, dim=0))
+        dist.all_gather(parts, local, group=group)
+        out = torch.cat(parts, dim=0)
     return out
 
 
