@@ -26,6 +26,18 @@
 namespace slos {
 
 constexpr int kDpThreads = 256;
+constexpr int kNumPhases = 10;
+
+// Optional per-phase cycle accounting (DpParams.phase_cycles != nullptr): thread 0
+// reads clock64() at block-synchronous phase boundaries.
+#define SLOS_PHASE(k)                                                          \
+  do {                                                                         \
+    if (prm.phase_cycles && threadIdx.x == 0) {                                \
+      const long long now_ = clock64();                                        \
+      atomicAdd(&prm.phase_cycles[(k)], (unsigned long long)(now_ - ph_t0_));  \
+      ph_t0_ = now_;                                                           \
+    }                                                                          \
+  } while (0)
 constexpr int kDpWarps = kDpThreads / 32;
 
 struct DpParams {
@@ -37,6 +49,7 @@ struct DpParams {
   size_t wscr_stride;  // bytes per warp in wscr_global
   int Gmax;            // anchor groups per evaluation wave (shared variants in smem)
   size_t gstride;      // bytes per group variant
+  unsigned long long* phase_cycles;  // kNumPhases counters, or nullptr
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -407,6 +420,8 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
   }
   __syncthreads();
 
+  long long ph_t0_ = clock64();
+  SLOS_PHASE(0);  // 0: instance load / setup
   for (int i = 0; i < N && !s_err; ++i) {
     const int jlo = ch_fl[i];
     const int nlev = i - jlo;  // levels jlo+1 .. i
@@ -456,6 +471,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
       break;
     }
     const int n_new = s_n_new;
+    SLOS_PHASE(1);  // 1: candidate enumeration + memo find-or-insert
     // ---- 3: group new keys by anchor j and evaluate ----
     for (int k = tid; k <= nlev; k += kDpThreads) s_jcnt[k] = 0;
     __syncthreads();
@@ -486,6 +502,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
     __syncthreads();
     const int ng = s_ng;
     const int nch = (D.n + 31) / 32;
+    SLOS_PHASE(2);  // 2: key grouping
     for (int w0 = 0; w0 < ng && !s_err; w0 += prm.Gmax) {
       const int gw = min(prm.Gmax, ng - w0);
       // E1: group setup, one warp per anchor group
@@ -509,6 +526,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
         if (lane_id() == 0) { H.g = g; H.v = v; }
       }
       __syncthreads();
+      SLOS_PHASE(3);  // 3: E1 group setup
       // E2: member-chunk histogram tasks (group, 32 members)
       for (int t = warp_id(); t < gw * nch; t += kDpWarps) {
         const int gi = t / nch;
@@ -535,6 +553,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
         }
       }
       __syncthreads();
+      SLOS_PHASE(4);  // 4: E2 member histograms
       // E3: one warp per memo key of this wave
       {
         const int kfirst = s_glist[w0], klast = s_glist[w0 + gw - 1];
@@ -576,6 +595,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
       }
       __syncthreads();
     }
+    SLOS_PHASE(5);  // 5: E3 placements
     if (s_err) break;
     for (int q = tid; q < n_new; q += kDpThreads) Memo[X0[q]].state = 3;
     // ---- 4: candidate states ----
@@ -610,6 +630,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
     }
     __syncthreads();
     if (s_err) break;
+    SLOS_PHASE(6);  // 6: candidate states
     // ---- 5: Pareto buckets ----
     for (int c = tid; c < T; c += kDpThreads) {
       int b = -1;
@@ -715,6 +736,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
       Bval[Caux[b]] = -1;
     }
     __syncthreads();
+    SLOS_PHASE(7);  // 7: Pareto buckets
     // ---- 6: arena ids and survivors ----
     {
       int64_t carry_acc = 0, carry_sv = 0;
@@ -752,6 +774,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
       }
     }
     __syncthreads();
+    SLOS_PHASE(8);  // 8: arena ids + survivors
   }
   __syncthreads();
   if (s_err) {
@@ -874,6 +897,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
     }
     out->status = 0;
   }
+  SLOS_PHASE(9);  // 9: terminal selection + backtrack
 }
 
 }  // namespace slos

@@ -36,6 +36,7 @@ struct DpParams {
   size_t wscr_stride;
   int Gmax;
   size_t gstride;
+  unsigned long long* phase_cycles;
 };
 struct BuildParams {
   BatchArgs a;
@@ -779,6 +780,15 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     dp.Gmax = 1;
     smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, false, dp.Gmax);
   }
+  dp.phase_cycles = nullptr;
+  if (std::getenv("SLOS_PHASE_TIMING")) {
+    static unsigned long long* dev_pc = nullptr;
+    if (!dev_pc) {
+      cudaMalloc(&dev_pc, 16 * sizeof(unsigned long long));
+      cudaMemset(dev_pc, 0, 16 * sizeof(unsigned long long));
+    }
+    dp.phase_cycles = dev_pc;
+  }
   dp.dec_smem_max = 0;
   {
     const size_t with_dec = dp_smem_bytes(maxN, maxDec, dp.Sc, Lmax, dp.wscr_global == nullptr, dp.Gmax);
@@ -836,6 +846,17 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   std::vector<OutHdr> hdr(hO, hO + nv);
   g_d2h += (int64_t)(sizeof(OutHdr) * (size_t)nv);
+  if (ws.dp.phase_cycles) {
+    unsigned long long pc[16];
+    cudaMemcpy(pc, ws.dp.phase_cycles, sizeof pc, cudaMemcpyDeviceToHost);
+    unsigned long long tot = 0;
+    for (int k = 0; k < 10; ++k) tot += pc[k];
+    static const char* names[10] = {"setup", "memo", "group", "E1", "E2", "E3", "states", "buckets",
+                                    "survivors", "terminal"};
+    std::fprintf(stderr, "[slos phases] total %.3e cycles:", (double)tot);
+    for (int k = 0; k < 10; ++k) std::fprintf(stderr, " %s %.1f%%", names[k], 100.0 * (double)pc[k] / (double)(tot ? tot : 1));
+    std::fprintf(stderr, "\n");
+  }
   // packed offsets
   std::vector<int64_t> boff(nv, 0), eoff(nv, 0), ioff(nv, 0);
   size_t packed = 0;
