@@ -50,6 +50,8 @@ struct DpParams {
   int Gmax;            // anchor groups per evaluation wave (shared variants in smem)
   size_t gstride;      // bytes per group variant
   unsigned long long* phase_cycles;  // kNumPhases counters, or nullptr
+  int Tsm;             // candidates per level kept in shared memory
+  size_t overlay_bytes;  // group-variant / candidate-state overlay (bytes)
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -368,19 +370,39 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
     D.rem = A.dec_rem + I.off_dec;
     D.tier = A.dec_tier + I.off_dec;
   }
-  unsigned char* wbase;
-  if (prm.wscr_global) {
-    wbase = prm.wscr_global + ((size_t)blockIdx.x * kDpWarps + warp_id()) * prm.wscr_stride;
-  } else {
-    wbase = p + (size_t)warp_id() * prm.wscr_stride;
-  }
-  const WarpScr W = warp_scr_carve(wbase, prm.Sc, prm.Lmax);
-  if (!prm.wscr_global) p += (size_t)kDpWarps * prm.wscr_stride;
+  // per-warp scratch for the rare private-variant / speculative paths (global);
+  // the placement temporaries live in shared memory
+  unsigned char* wbase = prm.wscr_global + ((size_t)blockIdx.x * kDpWarps + warp_id()) * prm.wscr_stride;
+  WarpScr W = warp_scr_carve(wbase, prm.Sc, prm.Lmax);
+  W.tmp = (int64_t*)p + (size_t)warp_id() * prm.Sc;
+  p += sizeof(int64_t) * (size_t)prm.Sc * kDpWarps;
   p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
   GroupHdr* ghdr = (GroupHdr*)p;
   p += sizeof(GroupHdr) * (size_t)prm.Gmax;
   p = (unsigned char*)(((uintptr_t)p + 127) & ~(uintptr_t)127);
+  // the group-variant area doubles as the level's candidate-state area (phases 4-6)
   unsigned char* gvbase = p;
+  unsigned char* ovl = p;
+  p += prm.overlay_bytes;
+  p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+  const int Tsm = prm.Tsm;
+  int32_t* k_src = (int32_t*)p; p += 4 * (size_t)Tsm;   // kept through phase 4
+  int32_t* k_j = (int32_t*)p; p += 4 * (size_t)Tsm;
+  int32_t* k_me = (int32_t*)p; p += 4 * (size_t)Tsm;
+  int32_t* k_new = (int32_t*)p; p += 4 * (size_t)Tsm;
+  int32_t* k_grp = (int32_t*)p; p += 4 * (size_t)Tsm;
+  // overlay layout (phases 4-6): 8-byte arrays first
+  uint64_t* o_cn = (uint64_t*)ovl;
+  int64_t* o_mm = (int64_t*)(ovl + 8 * (size_t)Tsm);
+  int64_t* o_pb = (int64_t*)(ovl + 16 * (size_t)Tsm);
+  double* o_vl = (double*)(ovl + 24 * (size_t)Tsm);
+  uint64_t* o_bkey = (uint64_t*)(ovl + 32 * (size_t)Tsm);           // 2*Tsm
+  int32_t* o_na = (int32_t*)(ovl + 48 * (size_t)Tsm);
+  int32_t* o_fl = (int32_t*)(ovl + 52 * (size_t)Tsm);
+  int32_t* o_bk = (int32_t*)(ovl + 56 * (size_t)Tsm);
+  int32_t* o_aux = (int32_t*)(ovl + 60 * (size_t)Tsm);
+  int32_t* o_lst = (int32_t*)(ovl + 64 * (size_t)Tsm);
+  int32_t* o_bval = (int32_t*)(ovl + 68 * (size_t)Tsm);              // 2*Tsm
 
   // ---- scratch slices ----
   uint64_t* Sc_ = A.s_counts + I.off_surv;
@@ -391,25 +413,8 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
   int32_t* Spar = A.s_parent + I.off_surv;
   int32_t* Sar = A.s_arena + I.off_surv;
   int32_t* Sit = A.s_level + I.off_surv;
-  int32_t* Csrc = A.c_src + I.off_cand;
-  int32_t* Cj = A.c_j + I.off_cand;
-  int32_t* Cme = A.c_memo + I.off_cand;
-  int32_t* Cfl = A.c_flag + I.off_cand;
-  int32_t* Cbk = A.c_bucket + I.off_cand;
-  int32_t* Cps = A.c_pos + I.off_cand;
-  int32_t* Caux = A.c_aux + I.off_cand;
-  uint64_t* Ccn = A.c_counts + I.off_cand;
-  int64_t* Cmm = A.c_mem + I.off_cand;
-  int64_t* Cpb = A.c_pb + I.off_cand;
-  double* Cvl = A.c_value + I.off_cand;
-  int32_t* Cna = A.c_nadm + I.off_cand;
-  uint64_t* Bkey = A.c_bkey + 2 * I.off_cand;
-  int32_t* Bval = A.c_bval + 2 * I.off_cand;
   MemoEnt* Memo = A.memo + I.off_memo;
   const int64_t capC = I.cap_cand;
-  const int64_t capB = 2 * I.cap_cand;
-  // generic int scratch: reuse bucket value space halves
-  int32_t* X0 = Cps;  // new list / bucket lists
 
   if (tid == 0) {
     Sc_[0] = 0; Sm_[0] = 0; Sp_[0] = 0; Sv_[0] = 0.0; Sn_[0] = 0; Spar[0] = -1; Sar[0] = 0; Sit[0] = -1;
@@ -431,12 +436,30 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
       s_pre[nlev] = acc;
       s_n_new = 0;
       s_nb = 0;
-      s_next_grp = 0;
-      if (acc > capC) { s_err = SLOS_ERR_CAPACITY; out->need_cand = acc; }
+      if (acc > Tsm && acc > capC) { s_err = SLOS_ERR_CAPACITY; out->need_cand = acc; }
     }
     __syncthreads();
     if (s_err) break;
     const int T = s_pre[nlev];
+    // level arrays: shared memory when the level fits, else the HBM slice
+    const bool sm = T <= Tsm;
+    int32_t* Csrc = sm ? k_src : A.c_src + I.off_cand;
+    int32_t* Cj = sm ? k_j : A.c_j + I.off_cand;
+    int32_t* Cme = sm ? k_me : A.c_memo + I.off_cand;
+    int32_t* X0 = sm ? k_new : A.c_pos + I.off_cand;
+    int32_t* G = sm ? k_grp : A.c_aux + I.off_cand;
+    uint64_t* Ccn = sm ? o_cn : A.c_counts + I.off_cand;
+    int64_t* Cmm = sm ? o_mm : A.c_mem + I.off_cand;
+    int64_t* Cpb = sm ? o_pb : A.c_pb + I.off_cand;
+    double* Cvl = sm ? o_vl : A.c_value + I.off_cand;
+    int32_t* Cna = sm ? o_na : A.c_nadm + I.off_cand;
+    int32_t* Cfl = sm ? o_fl : A.c_flag + I.off_cand;
+    int32_t* Cbk = sm ? o_bk : A.c_bucket + I.off_cand;
+    int32_t* Caux = sm ? o_aux : A.c_aux + I.off_cand;
+    int32_t* Blst = sm ? o_lst : A.c_pos + I.off_cand;
+    uint64_t* Bkey = sm ? o_bkey : A.c_bkey + 2 * I.off_cand;
+    int32_t* Bval = sm ? o_bval : A.c_bval + 2 * I.off_cand;
+    const int64_t capB = sm ? 2 * (int64_t)Tsm : 2 * capC;
     if (tid == 0) s_ctr[0] += (unsigned long long)T;
     const double t_i = ch_dl[i];
     // ---- 1+2: candidates and memo keys ----
@@ -486,7 +509,6 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
       s_ctr[1] += (unsigned long long)n_new;
     }
     __syncthreads();
-    int32_t* G = Cbk;  // grouped key slots
     for (int q = tid; q < n_new; q += kDpThreads) {
       const int slot = X0[q];
       const int k = Cj[Memo[slot].first] - jlo;
@@ -527,7 +549,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
       }
       __syncthreads();
       SLOS_PHASE(3);  // 3: E1 group setup
-      // E2: member-chunk histogram tasks (group, 32 members)
+      // E2: member-chunk histogram tasks (group, 32 members), lanes in lockstep
       for (int t = warp_id(); t < gw * nch; t += kDpWarps) {
         const int gi = t / nch;
         GroupHdr& H = ghdr[gi];
@@ -536,11 +558,10 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
         const int k = (t % nch) * 32 + lane_id();
         int64_t late = 0, dues = 0;
         int fail = 0, spill = 0;
-        if (k < D.n) {
-          const Member m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], H.g.now, H.g.a, H.g.pull);
-          if (m.valid && m.rem > 0)
-            member_dues(P, m, H.g, ga.ends, H.v.S, true, H.v.inc != 0, ga.nx, late, dues, fail, spill);
-        }
+        Member m;
+        m.valid = false;
+        if (k < D.n) m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], H.g.now, H.g.a, H.g.pull);
+        member_dues_warp(P, m, H.g, ga.ends, H.v.S, H.v.inc != 0, ga.nx, late, dues, fail, spill);
         late = warp_sum(late);
         dues = warp_sum(dues);
         fail = warp_or(fail);
@@ -571,6 +592,7 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
           MemoEnt* e = &Memo[G[q]];
           const uint64_t cw = e->k2;
           int64_t cv[kMaxTiers];
+#pragma unroll
           for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
           int spill = 0;
           const EvalOut r = warp_eval_counts(P, D, H.g, H.v, ga, prm.Sc, W, cv, min_slot, &spill);
@@ -627,6 +649,9 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
         }
       }
       Cfl[c] = flag;
+    }
+    if (sm) {  // fresh level-local bucket table
+      for (int x = tid; x < capB; x += kDpThreads) { Bkey[x] = 0ull; Bval[x] = -1; }
     }
     __syncthreads();
     if (s_err) break;
@@ -694,46 +719,65 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
             cntB[b] = basepos + __popc(peers);
           }
           basepos = __shfl_sync(0xffffffffu, basepos, leader);
-          if (b >= 0) X0[offB[b] + basepos + rank] = c;
+          if (b >= 0) Blst[offB[b] + basepos + rank] = c;
         }
         __syncthreads();
       }
     }
-    // one thread per bucket: try_insert replay (dp_scheduler.cpp:445-465)
-    for (int b = tid; b < NB; b += kDpThreads) {
-      int32_t* lst = X0 + offB[b];
+    // one warp per bucket: try_insert replay (dp_scheduler.cpp:445-465) in candidate
+    // order; the frontier scan of each step is lane-parallel (ballots).
+    for (int b = warp_id(); b < NB; b += kDpWarps) {
+      int32_t* lst = Blst + offB[b];
       const int n = cntB[b];
+      const int lane = lane_id();
       int f = 0;  // frontier lst[0..f)
       for (int q = 0; q < n; ++q) {
         const int c = lst[q];
         const double sv = Cvl[c];
-        const int64_t sm = Cmm[c], sp = Cpb[c];
+        const int64_t smm = Cmm[c], spb = Cpb[c];
         const int sn = Cna[c];
         bool reject = false;
-        for (int r = 0; r < f; ++r) {
-          const int e = lst[r];
-          if (Cvl[e] >= sv - kValueEps && Cmm[e] <= sm && Cpb[e] >= sp) {
-            const bool equal = fabs(Cvl[e] - sv) <= kValueEps && Cmm[e] == sm && Cpb[e] == sp;
-            if (!equal || Cna[e] >= sn) { reject = true; break; }
+        for (int r0 = 0; r0 < f && !reject; r0 += 32) {
+          bool rj = false;
+          if (r0 + lane < f) {
+            const int e = lst[r0 + lane];
+            if (Cvl[e] >= sv - kValueEps && Cmm[e] <= smm && Cpb[e] >= spb) {
+              const bool equal = fabs(Cvl[e] - sv) <= kValueEps && Cmm[e] == smm && Cpb[e] == spb;
+              rj = !equal || Cna[e] >= sn;
+            }
           }
+          reject = __any_sync(0xffffffffu, rj);
         }
         if (reject) continue;
         int wq = 0;
-        for (int r = 0; r < f; ++r) {
-          const int e = lst[r];
-          if (sv >= Cvl[e] - kValueEps && sm <= Cmm[e] && sp >= Cpb[e]) Cfl[e] |= 4;  // pruned
-          else lst[wq++] = e;
+        for (int r0 = 0; r0 < f; r0 += 32) {
+          int e = -1;
+          bool keep = false;
+          if (r0 + lane < f) {
+            e = lst[r0 + lane];
+            if (sv >= Cvl[e] - kValueEps && smm <= Cmm[e] && spb >= Cpb[e]) Cfl[e] |= 4;  // pruned
+            else keep = true;
+          }
+          const unsigned km = __ballot_sync(0xffffffffu, keep);
+          __syncwarp();
+          if (keep) lst[wq + __popc(km & ((1u << lane) - 1))] = e;
+          wq += __popc(km);
+          __syncwarp();
         }
-        lst[wq++] = c;
-        f = wq;
-        Cfl[c] |= 2;  // accepted
+        if (lane == 0) {
+          lst[wq] = c;
+          Cfl[c] |= 2;  // accepted
+        }
+        f = wq + 1;
+        __syncwarp();
       }
     }
     __syncthreads();
-    // reset the bucket hash slots claimed by this level (table returns to empty)
-    for (int b = tid; b < NB; b += kDpThreads) {
-      Bkey[Caux[b]] = 0ull;
-      Bval[Caux[b]] = -1;
+    if (!sm) {  // reset the HBM bucket hash slots claimed by this level
+      for (int b = tid; b < NB; b += kDpThreads) {
+        Bkey[Caux[b]] = 0ull;
+        Bval[Caux[b]] = -1;
+      }
     }
     __syncthreads();
     SLOS_PHASE(7);  // 7: Pareto buckets

@@ -172,6 +172,92 @@ __device__ __forceinline__ void member_dues(const PlannerDev& P, const Member& m
 }
 
 
+// E2 form of member_dues: the 32 lanes (one member each) walk their lines in
+// lockstep, one due per lane per round, so the histogram updates of lanes that
+// land in the same slot (the k-th due of every same-tier line usually does)
+// aggregate into one shared-memory atomic via __match_any_sync.
+__device__ inline void member_dues_warp(const PlannerDev& P, const Member& m, const GapGroup& g,
+                                        const double* ends, int S, bool inc, int32_t* nx,
+                                        int64_t& late, int64_t& dues, int& fail, int& spill) {
+  bool act = m.valid && m.rem > 0;
+  int64_t issued = 0;
+  double d = 0.0, tpot = 0.0;
+  int jit = -1;
+  bool first = true;
+  if (act) {
+    issued = m.backlog > 0 ? imin(m.backlog, m.rem) : 0;
+    late += issued;
+    tpot = P.tpot[m.tier];
+    d = dmax(m.phase, 0.0);
+  }
+  for (;;) {
+    act = act && time_le(d, g.horizon) && issued < m.rem;
+    if (!__any_sync(0xffffffffu, act)) break;
+    int key = -1;
+    if (act) {
+      if (!time_le(d, g.gap)) spill = 1;
+      if (d <= kTimeEps) {
+        ++late;
+      } else {
+        ++dues;
+        if (!inc || first) {
+          jit = jit_search(ends, S, d);
+          first = false;
+        } else {
+          while (jit + 1 < S && time_le(ends[jit + 1], d)) ++jit;
+        }
+        if (jit < 0) fail = 1; else key = jit;
+      }
+      d += tpot;
+      ++issued;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (key >= 0 && lane_id() == __ffs(peers) - 1) atomicAdd(&nx[key], __popc(peers));
+  }
+  if (m.valid && m.rem > 0 && m.backlog < 0 && g.dh > g.gap + kTimeEps) {
+    int64_t is2 = imin(m.backlog, m.rem);  // see member_dues
+    for (double e = dmax(m.phase, 0.0); time_le(e, g.dh) && is2 < m.rem; e += tpot, ++is2)
+      if (!time_le(e, g.gap)) spill = 1;
+  }
+}
+
+// Slot capacities cap[s] = min(plan_time2bs(dur_s), max_batch) (batch_planner.cpp:250-255).
+// time2bs is monotone in its budget, so when the interior durations (which differ
+// only by ulps of the repeated-addition grid) map to the same capacity at their
+// min and max, every interior slot shares it: 4 binary searches instead of S.
+// Returns 1 if some slot's time2bs throws (infeasible-budget).
+__device__ inline int warp_slot_caps(const PlannerDev& P, const double* ends, int S, int64_t* cap) {
+  const int lane = lane_id();
+  double lo = INFINITY, hi = -INFINITY;
+  for (int s = 1 + lane; s < S - 1; s += 32) {
+    const double dur = ends[s] - ends[s - 1];
+    lo = dmin(lo, dur);
+    hi = dmax(hi, dur);
+  }
+  lo = warp_min(lo);
+  for (int o = 16; o; o >>= 1) hi = dmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  int64_t shared_cap = -2;
+  if (S > 2) {
+    const int64_t a = lane == 0 ? plan_time2bs(P, lo, 0) : 0;
+    const int64_t b = lane == 1 ? plan_time2bs(P, hi, 0) : 0;
+    const int64_t ca = __shfl_sync(0xffffffffu, a, 0), cb = __shfl_sync(0xffffffffu, b, 1);
+    if (ca == cb && ca >= 0) shared_cap = imin(ca, P.max_batch);
+  }
+  int err = 0;
+  for (int s = lane; s < S; s += 32) {
+    if (s > 0 && s < S - 1 && shared_cap >= 0) {
+      cap[s] = shared_cap;
+      continue;
+    }
+    const double dur = ends[s] - (s == 0 ? 0.0 : ends[s - 1]);
+    const int64_t c = plan_time2bs(P, dur, 0);
+    if (c < 0) err = 1;
+    cap[s] = imin(c, P.max_batch);
+  }
+  __syncwarp();
+  return warp_or(err);
+}
+
 struct EvalOut {
   int status;     // 0 ok, else SLOS_ERR_*
   bool has;       // optional<int64_t>
@@ -278,16 +364,11 @@ __device__ inline void warp_build_variant(const PlannerDev& P, const DecView& D,
   const bool fits = S <= w.Sc;
   int cap_err = 0;
   if (fits) {
-    for (int s = lane; s < S; s += 32) {
-      const double dur = w.ends[s] - (s == 0 ? 0.0 : w.ends[s - 1]);
-      const int64_t c = plan_time2bs(P, dur, 0);
-      if (c < 0) cap_err = 1;
-      w.cap[s] = imin(c, P.max_batch);
-      w.nx[s] = 0;
-    }
+    for (int s = lane; s < S; s += 32) w.nx[s] = 0;
     for (int x = lane; x < S * P.L; x += 32) w.hc[x] = 0;  // layout hc[l*S + s]
+    cap_err = warp_slot_caps(P, w.ends, S, w.cap);
   }
-  v.cap_err = warp_or(cap_err);
+  v.cap_err = cap_err;
   __syncwarp();
   int inc = 1;
   if (fits && lane_id() == 0)
@@ -355,16 +436,9 @@ __device__ inline void warp_group_init(const PlannerDev& P, const DecView& D, Ga
     for (int l = 0; l < P.L; ++l) v.q[l] = __shfl_sync(0xffffffffu, q, l);
   }
   if (S > Sc) return;  // surfaces as SLOS_ERR_CAPACITY when a key reaches the slots
-  int cap_err = 0;
-  for (int s = lane; s < S; s += 32) {
-    const double dur = ga.ends[s] - (s == 0 ? 0.0 : ga.ends[s - 1]);
-    const int64_t c = plan_time2bs(P, dur, 0);
-    if (c < 0) cap_err = 1;
-    ga.cap[s] = imin(c, P.max_batch);
-    ga.nx[s] = 0;
-  }
+  for (int s = lane; s < S; s += 32) ga.nx[s] = 0;
   for (int x = lane; x < S * P.L; x += 32) ga.hc[x] = 0;
-  v.cap_err = warp_or(cap_err);
+  v.cap_err = warp_slot_caps(P, ga.ends, S, ga.cap);
   int inc = 1;
   if (lane == 0)
     for (int x = 1; x < S; ++x) if (!(ga.ends[x - 1] < ga.ends[x])) inc = 0;
@@ -396,15 +470,10 @@ __device__ inline void warp_build_canon_variant(const PlannerDev& P, double gap,
   const bool fits = S <= Sc;
   int cap_err = 0;
   if (fits) {
-    for (int s = lane; s < S; s += 32) {
-      const double dur = ends[s] - (s == 0 ? 0.0 : ends[s - 1]);
-      const int64_t c = plan_time2bs(P, dur, 0);
-      if (c < 0) cap_err = 1;
-      cap[s] = imin(c, P.max_batch);
-    }
     for (int x = lane; x < S * P.L; x += 32) hc[x] = 0;
+    cap_err = warp_slot_caps(P, ends, S, cap);
   }
-  v.cap_err = warp_or(cap_err);
+  v.cap_err = cap_err;
   v.Lx = 0;
   v.Dx = 0;
   v.exact_fail = 0;

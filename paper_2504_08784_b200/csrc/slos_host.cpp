@@ -37,6 +37,8 @@ struct DpParams {
   int Gmax;
   size_t gstride;
   unsigned long long* phase_cycles;
+  int Tsm;
+  size_t overlay_bytes;
 };
 struct BuildParams {
   BatchArgs a;
@@ -766,20 +768,22 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   dp.Sc = (int)std::min<double>(S_need, 1 << 20);
   const size_t stride = dp_warp_scr_stride(dp.Sc, Lmax);
   dp.wscr_stride = stride;
-  const size_t kSmemBudget = 72 * 1024;  // 3 CTAs of 256 threads per SM
+  // 3 CTAs of 256 threads per SM (the register limit at 80 regs/thread)
+  const size_t kSmemBudget = 74 * 1024;
   dp.gstride = dp_group_stride(dp.Sc, Lmax);
-  dp.Gmax = std::max(1, std::min(maxN + 1, 32));
+  if ((e = ws.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
+    return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  dp.wscr_global = (unsigned char*)ws.d_wscr.p;
   size_t& smem = ws.smem;
-  dp.wscr_global = nullptr;
-  while (dp.Gmax > 4 && dp_smem_bytes(maxN, 0, dp.Sc, Lmax, true, dp.Gmax) > kSmemBudget) dp.Gmax /= 2;
-  smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, true, dp.Gmax);
-  if (smem > kSmemBudget) {
-    if ((e = ws.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
-      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-    dp.wscr_global = (unsigned char*)ws.d_wscr.p;
-    dp.Gmax = 1;
-    smem = dp_smem_bytes(maxN, 0, dp.Sc, Lmax, false, dp.Gmax);
+  dp.Gmax = std::max(1, std::min(maxN + 1, 32));
+  dp.Tsm = 512;
+  auto fit = [&](int dec) { return dp_smem_bytes(maxN, dec, dp.Sc, Lmax, dp.Gmax, dp.Tsm, &dp.overlay_bytes); };
+  while (fit(0) > kSmemBudget && (dp.Gmax > 2 || dp.Tsm > 64)) {
+    if (dp.Tsm > 256) dp.Tsm -= 64;
+    else if (dp.Gmax > 2) dp.Gmax /= 2;
+    else dp.Tsm /= 2;
   }
+  smem = fit(0);
   dp.phase_cycles = nullptr;
   if (std::getenv("SLOS_PHASE_TIMING")) {
     static unsigned long long* dev_pc = nullptr;
@@ -790,10 +794,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     dp.phase_cycles = dev_pc;
   }
   dp.dec_smem_max = 0;
-  {
-    const size_t with_dec = dp_smem_bytes(maxN, maxDec, dp.Sc, Lmax, dp.wscr_global == nullptr, dp.Gmax);
-    if (with_dec <= kSmemBudget) { dp.dec_smem_max = maxDec; smem = with_dec; }
-  }
+  if (fit(maxDec) <= kSmemBudget) dp.dec_smem_max = maxDec;
+  smem = fit(dp.dec_smem_max);
   ws.valid = valid;
   ws.nv = nv;
   ws.uploaded = true;

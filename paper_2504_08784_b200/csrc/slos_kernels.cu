@@ -3,6 +3,8 @@
 // (-fmad=false is part of the bit-exactness contract, see slos_common.cuh).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "slos_build.cuh"
 #include "slos_dp.cuh"
 #include "slos_launch.h"
@@ -30,13 +32,18 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactParams p) {
   for (int x = threadIdx.x; x < o.n_declined; x += blockDim.x) di[o.n_admitted + x] = ids[I.n_pending + x];
 }
 
-size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, bool wscr_in_smem, int Gmax) {
+// dynamic shared memory of dp_kernel (must mirror the carve-up in dp_kernel)
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Gmax, int Tsm, size_t* overlay) {
   const size_t N = (size_t)max_N;
-  size_t b = 8 * (N + 1) * 4 + 8 * (N + 2) + 4 * (N + 2) * 3 + 64;
-  b += (size_t)max_dec_staged * 28 + 64;
-  if (wscr_in_smem) b += (size_t)kDpWarps * dp_warp_scr_stride(Sc, L);
-  b += 16 + sizeof(GroupHdr) * (size_t)Gmax + 128 + group_var_stride(Sc, L) * (size_t)Gmax;
-  return b;
+  size_t b = 8 * (N + 1) * 4 + 8 * (N + 2) + 4 * (N + 2) * 3 + 16;   // chain
+  b += (size_t)max_dec_staged * 28 + 16;                              // decoders
+  b += 8 * (size_t)Sc * kDpWarps + 16;                                // placement temporaries
+  b += sizeof(GroupHdr) * (size_t)Gmax + 128;                         // group headers
+  const size_t ov = std::max(group_var_stride(Sc, L) * (size_t)Gmax, (size_t)76 * (size_t)Tsm);
+  *overlay = ov;
+  b += ov + 16;
+  b += (size_t)20 * (size_t)Tsm;                                      // kept candidate arrays
+  return b + 64;
 }
 
 size_t dp_group_stride(int Sc, int L) { return group_var_stride(Sc, L); }

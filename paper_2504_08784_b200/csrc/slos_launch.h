@@ -24,7 +24,7 @@ struct CompactParams {
   unsigned char* dst;
 };
 
-size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, bool wscr_in_smem, int Gmax);
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Gmax, int Tsm, size_t* overlay);
 size_t dp_group_stride(int Sc, int L);
 size_t dp_warp_scr_stride(int Sc, int L);
 cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
