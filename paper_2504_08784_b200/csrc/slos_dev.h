@@ -73,6 +73,7 @@ struct InstDev {
   int64_t off_run;                       // running tiers (R_total ints)
   int64_t cap_gb;                        // gap batches per tile_gap call
   int64_t cap_go;                        // owner pairs per tile_gap call
+  int64_t off_anchor; int64_t anchor_stride;  // per-anchor caches (bytes), N+1 anchors
 };
 
 // Per-instance result header written by the kernels.
@@ -157,6 +158,7 @@ struct BatchArgs {
   slos_batch* batches;
   slos_entry* entries;
   unsigned char* work;
+  unsigned char* anchors;
   OutHdr* out;
 };
 

@@ -292,6 +292,120 @@ __device__ inline EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D
   return o;
 }
 
+
+// Build the anchor cache of anchor j (gap start a) for this instance: block-wide.
+// gmax: the longest gap any later chain item can open from this anchor.
+__device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D, const AnchorView& av,
+                                          double a, double now, double pull, double gmax, int Sc,
+                                          const double* ctime, const int* ccnt, double min_slot,
+                                          int64_t* s_red) {
+  const int tid = threadIdx.x;
+  const int lane = lane_id(), w = warp_id();
+  __shared__ unsigned s_mask;
+  __shared__ int s_nex, s_hb, s_abl;
+  __shared__ unsigned long long s_pt[kMaxTiers];
+  __shared__ double s_minph[kDpWarps];
+  if (tid == 0) {
+    s_mask = 0; s_nex = 0; s_hb = 0; s_abl = 0;
+    for (int l = 0; l < kMaxTiers; ++l) s_pt[l] = 0;
+  }
+  __syncthreads();
+  double minph = INFINITY;
+  unsigned mask = 0;
+  int nex = 0, hb = 0, abl = 0;
+  for (int k = tid; k < D.n; k += kDpThreads) {
+    const Member m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], now, a, pull);
+    av.ph[k] = m.valid ? m.phase : 0.0;
+    av.bl[k] = m.valid ? m.backlog : 0;
+    av.rm[k] = m.valid ? m.rem : 0;
+    if (!m.valid) continue;
+    ++nex;
+    atomicAdd(&s_pt[m.tier], 1ull);
+    if (m.backlog > 0) hb = 1;
+    if (m.rem > 0) {
+      mask |= 1u << m.tier;
+      if (m.backlog > 0) abl = 1;
+      minph = dmin(minph, m.phase);
+    }
+  }
+  mask = __reduce_or_sync(0xffffffffu, mask);
+  nex = __reduce_add_sync(0xffffffffu, (unsigned)nex);
+  hb = warp_or(hb);
+  abl = warp_or(abl);
+  minph = warp_min(minph);
+  if (lane == 0) {
+    atomicOr(&s_mask, mask);
+    atomicAdd(&s_nex, nex);
+    if (hb) atomicOr(&s_hb, 1);
+    if (abl) atomicOr(&s_abl, 1);
+    s_minph[w] = minph;
+  }
+  __syncthreads();
+  AnchorFacts* F = av.f;
+  if (tid == 0) {
+    F->a = a;
+    F->exact_mask = s_mask;
+    F->n_exact = s_nex;
+    F->has_backlog = s_hb;
+    F->any_bl = s_abl;
+    double mp = s_minph[0];
+    for (int x = 1; x < kDpWarps; ++x) mp = dmin(mp, s_minph[x]);
+    F->min_phase = mp;
+    for (int l = 0; l < kMaxTiers; ++l) F->per_tier[l] = (int64_t)s_pt[l];
+    F->t0 = s_mask ? P.tpot[__ffs(s_mask) - 1] : 0.0;
+    F->Kg = 0;
+    F->grid_ok = 0;
+    F->cap_uniform_err = 0;
+  }
+  __syncthreads();
+  const unsigned emask = F->exact_mask;
+  if (!emask) return;
+  const double t0 = F->t0;
+  // t0_first (batch_planner.cpp:234-239): ordered scan, warp 0
+  if (w == 0) {
+    double cur = t0;
+    for (int base = 0; base < D.n; base += 32) {
+      const int k = base + lane;
+      const bool ok = k < D.n && av.rm[k] > 0 && av.ph[k] > kTimeEps;
+      const double ph = ok ? av.ph[k] : 0.0;
+      unsigned above = 0xffffffffu;
+      for (;;) {
+        const unsigned q = __ballot_sync(0xffffffffu, ok && ph < cur - kTimeEps) & above;
+        if (!q) break;
+        const int f = __ffs(q) - 1;
+        cur = dmax(__shfl_sync(0xffffffffu, ph, f), min_slot);
+        above = (f == 31) ? 0u : (0xffffffffu << (f + 1));
+      }
+    }
+    if (lane == 0) {
+      F->t0_first = cur;
+      // grid e_k = t0_first + k*t0 by repeated addition (:241) up to the longest gap
+      int K = 0, ok = 1;
+      double prev = -INFINITY;
+      for (double e = cur; time_le(e, gmax) && K < Sc; e += t0) {
+        if (!(prev < e)) ok = 0;
+        av.ge[K++] = e;
+        prev = e;
+      }
+      F->Kg = K;
+      F->grid_ok = ok;
+    }
+  }
+  __syncthreads();
+  const int Kg = F->Kg;
+  // grid slot capacities (duration e_k - e_{k-1}); -1 where time2bs throws
+  for (int s = tid; s < Kg; s += kDpThreads) {
+    const double dur = av.ge[s] - (s == 0 ? 0.0 : av.ge[s - 1]);
+    const int64_t c = plan_time2bs(P, dur, 0);
+    av.gcap[s] = c < 0 ? -1 : imin(c, P.max_batch);
+  }
+  // canonical due times -> grid jit
+  for (int l = 0; l < P.L; ++l)
+    for (int k = tid; k < ccnt[l]; k += kDpThreads) av.ccell[l * Sc + k] = jit_search(av.ge, Kg, ctime[l * Sc + k]);
+  __syncthreads();
+  (void)s_red;
+}
+
 __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ PlannerDev sP;
@@ -370,6 +484,27 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
     D.rem = A.dec_rem + I.off_dec;
     D.tier = A.dec_tier + I.off_dec;
   }
+  // instance-wide canonical due times per tier (batch_planner.cpp:216)
+  double* ctime = (double*)p;
+  p += sizeof(double) * (size_t)prm.Lmax * prm.Sc;
+  __shared__ int ccnt[kMaxTiers];
+  __shared__ double s_maxdl, s_minA;
+  __syncthreads();
+  if (tid == 0) {
+    double mx = I.now, mn = I.now;
+    for (int k = 0; k < N; ++k) { mx = dmax(mx, ch_dl[k]); mn = dmin(mn, ch_dl[k]); }
+    s_maxdl = mx;
+    s_minA = mn;
+  }
+  __syncthreads();
+  if (tid < L) {
+    const double gall = quantize_gap(dmax(0.0, s_maxdl - s_minA));
+    const double tp = P.tpot[tid];
+    int k = 0;
+    for (double d = tp; time_le(d, gall) && k < prm.Sc; d += tp) ctime[tid * prm.Sc + k++] = d;
+    ccnt[tid] = k;
+  }
+  unsigned char* anc_base = A.anchors + I.off_anchor;
   // per-warp scratch for the rare private-variant / speculative paths (global);
   // the placement temporaries live in shared memory
   unsigned char* wbase = prm.wscr_global + ((size_t)blockIdx.x * kDpWarps + warp_id()) * prm.wscr_stride;
@@ -462,6 +597,13 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
     const int64_t capB = sm ? 2 * (int64_t)Tsm : 2 * capC;
     if (tid == 0) s_ctr[0] += (unsigned long long)T;
     const double t_i = ch_dl[i];
+    {  // the anchor that becomes available at this level: j = i - 1
+      const int j = i - 1;
+      const double a = (j < 0) ? I.now : ch_dl[j];
+      const AnchorView av = anchor_view(anc_base + (size_t)(j + 1) * I.anchor_stride, D.n, prm.Sc, L);
+      block_build_anchor(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), prm.Sc, ctime,
+                         ccnt, min_slot, s_wsum);
+    }
     // ---- 1+2: candidates and memo keys ----
     for (int c = tid; c < T; c += kDpThreads) {
       int lo = 0, hi = nlev - 1;
@@ -544,8 +686,9 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
         g.horizon = dmax(g.gap, g.dh);
         Variant v;
         const GroupVar ga = group_var_carve(gvbase + (size_t)gi * prm.gstride, prm.Sc, L);
-        warp_group_init(P, D, g, v, ga, prm.Sc, min_slot);
-        if (lane_id() == 0) { H.g = g; H.v = v; }
+        const AnchorView av = anchor_view(anc_base + (size_t)(j + 1) * I.anchor_stride, D.n, prm.Sc, L);
+        warp_group_from_anchor(P, av, g, v, ga, prm.Sc, min_slot, ctime, ccnt);
+        if (lane_id() == 0) { H.g = g; H.v = v; H.j = j; }
       }
       __syncthreads();
       SLOS_PHASE(3);  // 3: E1 group setup
@@ -560,7 +703,14 @@ __global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
         int fail = 0, spill = 0;
         Member m;
         m.valid = false;
-        if (k < D.n) m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], H.g.now, H.g.a, H.g.pull);
+        if (k < D.n) {
+          const AnchorView av = anchor_view(anc_base + (size_t)(H.j + 1) * I.anchor_stride, D.n, prm.Sc, L);
+          m.rem = av.rm[k];
+          m.valid = m.rem > 0;
+          m.phase = av.ph[k];
+          m.backlog = av.bl[k];
+          m.tier = D.tier[k];
+        }
         member_dues_warp(P, m, H.g, ga.ends, H.v.S, H.v.inc != 0, ga.nx, late, dues, fail, spill);
         late = warp_sum(late);
         dues = warp_sum(dues);

@@ -115,6 +115,7 @@ struct GroupVar {
 struct GroupHdr {
   GapGroup g;
   Variant v;
+  int j;
 };
 
 __host__ __device__ __forceinline__ size_t group_var_stride(int Sc, int L) {
@@ -256,6 +257,168 @@ __device__ inline int warp_slot_caps(const PlannerDev& P, const double* ends, in
   }
   __syncwarp();
   return warp_or(err);
+}
+
+// ---- per-anchor cache ----------------------------------------------------------
+// Everything about a gap that depends only on its start a = t_j (the anchor) and
+// not on the chain item i that ends it: the exact census members_at(a), the census
+// facts, t0_first for the exact census' tightest tier, the slot grid
+// e_k = t0_first + k*t0 (repeated addition, batch_planner.cpp:241) up to the
+// longest gap this anchor can see, its per-slot capacities, and the grid slot of
+// every canonical due time. Built once per anchor (one new anchor per DP level);
+// every (level, anchor) group then derives its variant with lane-parallel copies.
+struct AnchorFacts {
+  double a;
+  double t0;
+  double t0_first;
+  double min_phase;      // over members with remaining > 0
+  int64_t per_tier[kMaxTiers];
+  unsigned exact_mask;
+  int n_exact;
+  int has_backlog;       // any member backlog > 0 (tile_gap :321-322)
+  int any_bl;            // any member with remaining > 0 and backlog > 0 (:160)
+  int Kg;                // grid points stored (may exceed Sc -> overflow)
+  int grid_ok;           // grid strictly increasing and complete
+  int cap_uniform_err;
+  int pad;
+};
+
+struct AnchorView {
+  AnchorFacts* f;
+  double* ph;
+  int64_t* bl;
+  int64_t* rm;
+  double* ge;
+  int64_t* gcap;   // -1: plan_time2bs throws for that grid slot
+  int32_t* ccell;  // [L][Sc] grid jit of canonical time k of tier l
+};
+
+__host__ __device__ __forceinline__ size_t anchor_stride_bytes(int R, int Sc, int L) {
+  size_t b = 256 + (size_t)R * 24 + (size_t)Sc * 16 + (size_t)L * Sc * 4;
+  return (b + 127) & ~(size_t)127;
+}
+
+__device__ __forceinline__ AnchorView anchor_view(unsigned char* base, int R, int Sc, int L) {
+  AnchorView v;
+  v.f = (AnchorFacts*)base;
+  unsigned char* p = base + 256;
+  v.ph = (double*)p; p += (size_t)R * 8;
+  v.bl = (int64_t*)p; p += (size_t)R * 8;
+  v.rm = (int64_t*)p; p += (size_t)R * 8;
+  v.ge = (double*)p; p += (size_t)Sc * 8;
+  v.gcap = (int64_t*)p; p += (size_t)Sc * 8;
+  v.ccell = (int32_t*)p;
+  (void)L;
+  return v;
+}
+
+// Derive a (level, anchor) group's variant from the anchor cache (warp).
+// `ctime/ccnt` is the instance's canonical due-time list per tier.
+__device__ inline void warp_group_from_anchor(const PlannerDev& P, const AnchorView& av, GapGroup& g,
+                                              Variant& v, const GroupVar& ga, int Sc, double min_slot,
+                                              const double* ctime, const int* ccnt) {
+  const int lane = lane_id();
+  const AnchorFacts& F = *av.f;
+  g.exact_mask = F.exact_mask;
+  for (int l = 0; l < kMaxTiers; ++l) g.exact_per_tier[l] = F.per_tier[l];
+  g.n_exact = F.n_exact;
+  g.has_backlog = F.has_backlog != 0;
+  g.min_phase = F.min_phase;
+  g.any_due = F.any_bl || (g.horizon > kTimeEps && time_le(F.min_phase, g.horizon));
+  g.po_state = 0;
+  g.po_budget = 0;
+  v.valid = 0;
+  v.S = 0;
+  v.Lx = 0;
+  v.Dx = 0;
+  v.exact_fail = 0;
+  v.spill = 0;
+  v.cap_err = 0;
+  v.cfail = 0;
+  v.inc = 0;
+  for (int l = 0; l < kMaxTiers; ++l) v.q[l] = 0;
+  if (g.gap <= kTimeEps || !F.exact_mask) return;
+  v.t0 = F.t0;
+  v.t0_first = F.t0_first;
+  // canonical due counts (batch_planner.cpp:216): prefix of the canonical list
+  {
+    int q = 0;
+    if (lane < P.L) {
+      int lo = 0, hi = ccnt[lane];
+      while (lo < hi) {
+        const int mid = (lo + hi) / 2;
+        if (time_le(ctime[lane * Sc + mid], g.gap)) lo = mid + 1; else hi = mid;
+      }
+      q = lo;
+    }
+    for (int l = 0; l < P.L; ++l) v.q[l] = __shfl_sync(0xffffffffu, q, l);
+  }
+  if (!F.grid_ok) {  // degenerate grid: slow path per key
+    v.valid = 0;
+    v.inc = -1;
+    return;
+  }
+  // prefix of the grid inside the gap (:241): first k with !time_le(e_k, gap)
+  int Sp;
+  {
+    int lo = 0, hi = F.Kg;
+    while (lo < hi) {
+      const int mid = (lo + hi) / 2;
+      if (time_le(av.ge[mid], g.gap)) lo = mid + 1; else hi = mid;
+    }
+    Sp = lo;
+  }
+  int app;
+  if (Sp == 0) app = time_le(min_slot, g.gap) ? 1 : 0;
+  else app = (g.gap - av.ge[Sp - 1] >= min_slot - kTimeEps) ? 1 : 0;
+  const int S = Sp + app;
+  v.S = S;
+  v.valid = 1;
+  if (Sp >= F.Kg && F.Kg >= Sc) { v.S = Sc + 1; return; }  // grid truncated: capacity
+  for (int l = 0; l < P.L; ++l)
+    if (v.q[l] >= ccnt[l] && ccnt[l] >= Sc) { v.S = Sc + 1; return; }  // canonical list truncated
+  if (S > Sc) return;
+  int err = 0;
+  for (int s = lane; s < S; s += 32) {
+    if (s < Sp) {
+      ga.ends[s] = av.ge[s];
+      const int64_t c = av.gcap[s];
+      if (c < 0) err = 1;
+      ga.cap[s] = c;
+    } else {
+      ga.ends[s] = g.gap;
+      const int64_t c = plan_time2bs(P, g.gap - (Sp == 0 ? 0.0 : av.ge[Sp - 1]), 0);
+      if (c < 0) err = 1;
+      ga.cap[s] = imin(c, P.max_batch);
+    }
+    ga.nx[s] = 0;
+  }
+  for (int x = lane; x < S * P.L; x += 32) ga.hc[x] = 0;
+  v.cap_err = warp_or(err);
+  // strictly increasing ends (the appended end may not exceed the grid when min_slot ~ 0)
+  const int inc = app == 0 || Sp == 0 || av.ge[Sp - 1] < g.gap;
+  v.inc = inc;
+  __syncwarp();
+  // canonical dues -> slots: grid jit clipped to the prefix, or the appended slot
+  int cf = 0;
+  for (int l = 0; l < P.L; ++l) {
+    const int ql = v.q[l];
+    for (int k = lane; k < ql; k += 32) {
+      const double d = ctime[l * Sc + k];
+      int jit;
+      if (inc) {
+        jit = av.ccell[l * Sc + k];
+        if (jit > Sp - 1) jit = Sp - 1;
+        if (app && time_le(g.gap, d)) jit = Sp;
+      } else {
+        jit = jit_search(ga.ends, S, d);
+      }
+      if (jit < 0) cf |= 1 << l;
+      else atomicAdd(&ga.hc[l * S + jit], 1);
+    }
+  }
+  v.cfail = __reduce_or_sync(0xffffffffu, (unsigned)cf);
+  __syncwarp();
 }
 
 struct EvalOut {
@@ -523,6 +686,27 @@ __device__ inline int warp_place_budget(const PlannerDev& P, const Variant& v, c
   const int lane = lane_id();
   const int S = v.S;
   const int L = P.L;
+  if (v.Lx == 0) {
+    // fast path: no late dues and every jit group fits its own slot -> latest-fit
+    // places each group in its jit slot and free_s = cap_s - n_s.
+    bool ok = true;
+    int64_t b = 0;
+    for (int base = 0; base < S; base += 32) {
+      const int s = base + lane;
+      if (s < S) {
+        int64_t n = nx ? nx[s] : 0;
+        for (int l = 0; l < L; ++l)
+          if (c[l] > 0) n += c[l] * (int64_t)hc[l * S + s];
+        const int64_t f = cap[s] - n;
+        if (f < 0) ok = false;
+        b += imin(f, P.max_chunk);
+      }
+    }
+    if (__all_sync(0xffffffffu, ok)) {
+      *budget = warp_sum(b);
+      return 1;
+    }
+  }
   // forward pass: free capacity after late dues, F - D prefix
   int64_t carry_cap = 0, carry_F = 0, carry_D = 0, min_diff = INT64_MAX;
   for (int base = 0; base < S; base += 32) {

@@ -421,7 +421,7 @@ struct Layout {
   size_t in_bytes;
   size_t s_counts, s_mem, s_pb, s_value, s_nadm, s_parent, s_arena, s_level;
   size_t c_src, c_j, c_memo, c_flag, c_bucket, c_pos, c_aux, c_counts, c_mem, c_pb, c_value, c_nadm;
-  size_t c_bkey, c_bval, memo, work, scr_bytes;
+  size_t c_bkey, c_bval, memo, work, anchors, scr_bytes;
   size_t memo_bytes, bkey_bytes, bval_bytes;
   size_t out, sel, ids, batches, entries, out_bytes;
 };
@@ -503,6 +503,13 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   }
   const int nv = (int)valid.size();
   if (nv == 0) return SLOS_OK;
+  const int Sc = (int)std::min<double>(S_need, 1 << 20);
+  int64_t TA = 0;
+  std::vector<int64_t> astride(n, 0);
+  for (int q : valid) {
+    astride[q] = (int64_t)dp_anchor_stride(prep[q].n_dec, Sc, Lmax);
+    TA += astride[q] * (prep[q].N + 1);
+  }
   Layout& Ly = ws.Ly;
   Blob bi;
   Ly.planners = bi.add<PlannerDev>(plist.size());
@@ -553,6 +560,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.c_bval = bs.add<int32_t>(2 * TCd);
   Ly.memo = bs.add<MemoEnt>(TM);
   Ly.work = bs.add<unsigned char>(TW);
+  Ly.anchors = bs.add<unsigned char>(TA);
   Ly.scr_bytes = bs.bytes;
   Blob bo;
   Ly.out = bo.add<OutHdr>(nv);
@@ -589,7 +597,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   int32_t* h_pre_idx = (int32_t*)hp(Ly.pre_idx);
   int64_t* h_pre_left = (int64_t*)hp(Ly.pre_left);
   int32_t* h_run_tier = (int32_t*)hp(Ly.run_tier);
-  int64_t oD = 0, oC = 0, oP = 0, oR = 0, oS = 0, oCd = 0, oM = 0, oW = 0, oSel = 0, oIds = 0, oB = 0, oE = 0;
+  int64_t oD = 0, oC = 0, oP = 0, oR = 0, oS = 0, oCd = 0, oM = 0, oW = 0, oSel = 0, oIds = 0, oB = 0, oE = 0, oA = 0;
   std::vector<double> cost(nv);
   for (int v = 0; v < nv; ++v) {
     const int q = valid[v];
@@ -626,6 +634,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     I.off_work = oW; I.cap_work = cp.work;
     I.cap_gb = cp.gb;
     I.cap_go = cp.go;
+    I.off_anchor = oA;
+    I.anchor_stride = astride[q];
     for (int i = 0; i < in->n_running; ++i) {
       const slos_running& r = in->running[i];
       h_run_tier[oR + i] = r.decode_tier;
@@ -683,6 +693,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     oIds += 2 * (int64_t)in->n_pending + 1;
     oB += cp.batch;
     oE += cp.entry;
+    oA += astride[q] * (pr.N + 1);
   }
   int32_t* h_order = (int32_t*)hp(Ly.order);
   {
@@ -756,6 +767,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   A.c_bval = (int32_t*)(DS + Ly.c_bval);
   A.memo = (MemoEnt*)(DS + Ly.memo);
   A.work = DS + Ly.work;
+  A.anchors = DS + Ly.anchors;
   A.out = (OutHdr*)(DO + Ly.out);
   A.sel = (int32_t*)(DO + Ly.sel);
   A.ids = (int32_t*)(DO + Ly.ids);
@@ -765,7 +777,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   DpParams& dp = ws.dp;
   dp.a = A;
   dp.Lmax = Lmax;
-  dp.Sc = (int)std::min<double>(S_need, 1 << 20);
+  dp.Sc = Sc;
   const size_t stride = dp_warp_scr_stride(dp.Sc, Lmax);
   dp.wscr_stride = stride;
   // 3 CTAs of 256 threads per SM (the register limit at 80 regs/thread)

@@ -43,7 +43,11 @@ size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Gmax, int
   *overlay = ov;
   b += ov + 16;
   b += (size_t)20 * (size_t)Tsm;                                      // kept candidate arrays
+  b += sizeof(double) * (size_t)L * (size_t)Sc + 16;                  // canonical due times
   return b + 64;
+}
+
+size_t dp_anchor_stride(int R, int Sc, int L) { return anchor_stride_bytes(R, Sc, L);
 }
 
 size_t dp_group_stride(int Sc, int L) { return group_var_stride(Sc, L); }
