@@ -17,7 +17,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PKG = os.path.dirname(os.path.abspath(__file__))
 
-PRODUCT_LIB = os.path.join(PKG, "libslos_b200.so")
+PRODUCT_LIB = os.environ.get("SLOS_PRODUCT_LIB", os.path.join(PKG, "libslos_b200.so"))
 WORKLOAD_LIB = os.path.join(PKG, "libslos_workload.so")
 ORACLE_LIB = os.path.join(ROOT, "oracle", "liboracle_slos.so")
 REF_LIB = os.path.join(ROOT, "oracle", "_ref", "libslos_ref.so")

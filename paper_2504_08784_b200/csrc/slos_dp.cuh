@@ -406,7 +406,10 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
   (void)s_red;
 }
 
-__global__ void __launch_bounds__(kDpThreads, 3) dp_kernel(DpParams prm) {
+#ifndef SLOS_DP_MIN_BLOCKS
+#define SLOS_DP_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpParams prm) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;
