@@ -29,12 +29,13 @@ struct BuildShared {
 };
 
 // members_at(running, now, at, pull) compacted in decoder (= owner) order.
+template <class G>
 __device__ inline int build_members_at(const BatchArgs& A, BuildShared& sh, double at, double pull,
                                        const MemBuf& E) {
   const InstDev& I = sh.I;
   int64_t carry = 0;
-  for (int base = 0; base < I.n_dec; base += kBT) {
-    const int k = base + threadIdx.x;
+  for (int base = 0; base < I.n_dec; base += G::kSize) {
+    const int k = base + G::rank();
     Member m;
     m.valid = false;
     if (k < I.n_dec) {
@@ -42,7 +43,7 @@ __device__ inline int build_members_at(const BatchArgs& A, BuildShared& sh, doub
       m = member_at(sh.P, A.dec_next[o], A.dec_backlog[o], A.dec_rem[o], A.dec_tier[o], I.now, at, pull);
     }
     int64_t tot;
-    const int64_t ex = blk_excl(sh.bs, m.valid ? 1 : 0, &tot);
+    const int64_t ex = G::excl(sh.bs, m.valid ? 1 : 0, &tot);
     if (m.valid) {
       const int64_t d = carry + ex;
       E.ph[d] = m.phase;
@@ -90,8 +91,9 @@ __device__ __forceinline__ int owner_tier(const BatchArgs& A, const BuildShared&
 // Emit one tiled gap (offset `a`): decode entries per owner, then EDF prefill
 // fill (fill_prefill, dp_scheduler.cpp:220-232). track=true updates
 // decode_assigned of chain owners (the gap loop, :287; not the tail, :341-344).
+template <class G>
 __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bool track) {
-  const int tid = threadIdx.x;
+  const int tid = G::rank();
   const InstDev& I = sh.I;
   GapPlanBuf& o = sh.o;
   slos_batch* OB = A.batches + I.off_batch;
@@ -101,7 +103,7 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
     const bool spec_batch = gb.spec_step > 0 && o.n_spec > 0;
     const int64_t e0 = sh.n_entry;
     // decode entries (parallel copy)
-    for (int q = tid; q < gb.n_owner; q += kBT) {
+    for (int q = tid; q < gb.n_owner; q += G::kSize) {
       const int64_t owner = o.own[2 * (gb.first_owner + q)];
       const int64_t t = o.own[2 * (gb.first_owner + q) + 1];
       const int64_t at = e0 + q;
@@ -115,7 +117,7 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
       }
       if (track && owner >= I.R_total) atomicAdd(&sh.m_asg[owner - I.R_total], (unsigned long long)t);
     }
-    __syncthreads();
+    G::sync();
     if (tid == 0) {
       int64_t ne = e0 + gb.n_owner;
       const double end_abs = a + gb.end_s;
@@ -153,14 +155,15 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
       sh.n_batch++;
       sh.n_entry = ne;
     }
-    __syncthreads();
+    G::sync();
   }
   return 0;
 }
 
 // edf_fallback dp_scheduler.cpp:96-188 (block-parallel over decoders/prefills).
+template <class G>
 __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena ar, OutHdr* out) {
-  const int tid = threadIdx.x;
+  const int tid = G::rank();
   const InstDev& I = sh.I;
   const PlannerDev& P = sh.P;
   const int nd = I.n_dec, np = I.n_pre;
@@ -170,30 +173,30 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
   int64_t* pleft = (int64_t*)ar.take(sizeof(int64_t) * (np + 1));
   if (ar.used > ar.cap) {
     if (tid == 0) { sh.err = SLOS_ERR_CAPACITY; out->need_work = 2 * ar.used; }
-    __syncthreads();
+    G::sync();
     return;
   }
   double tmin = INFINITY;
-  for (int k = tid; k < nd; k += kBT) {
+  for (int k = tid; k < nd; k += G::kSize) {
     const int64_t o = I.off_dec + k;
     dnext[k] = A.dec_next[o];
     dleft[k] = A.dec_rem[o];
     dbl[k] = imin(A.dec_backlog[o], A.dec_rem[o]);
     tmin = dmin(tmin, P.tpot[A.dec_tier[o]]);
   }
-  for (int k = tid; k < np; k += kBT) pleft[k] = A.pre_left[I.off_pre + k];
-  const double t0 = nd > 0 ? blk_min(sh.bs, tmin) : 0.0;
+  for (int k = tid; k < np; k += G::kSize) pleft[k] = A.pre_left[I.off_pre + k];
+  const double t0 = nd > 0 ? G::min(sh.bs, tmin) : 0.0;
   slos_batch* OB = A.batches + I.off_batch;
   slos_entry* OE = A.entries + I.off_entry;
   const int64_t chunk_cap = P.max_chunk;
   if (tid == 0) { sh.n_batch = 0; sh.n_entry = 0; }
-  __syncthreads();
+  G::sync();
   double t = I.now;
   for (int guard = 0; guard < 100000; ++guard) {
     int any_d = 0, any_p = 0;
-    for (int k = tid; k < nd; k += kBT) if (dleft[k] > 0) any_d = 1;
-    for (int k = tid; k < np; k += kBT) if (pleft[k] > 0) any_p = 1;
-    const int fl = blk_or(sh.bs, any_d | (any_p << 1));
+    for (int k = tid; k < nd; k += G::kSize) if (dleft[k] > 0) any_d = 1;
+    for (int k = tid; k < np; k += G::kSize) if (pleft[k] > 0) any_p = 1;
+    const int fl = G::or_(sh.bs, any_d | (any_p << 1));
     const bool decodes = fl & 1, prefills = (fl >> 1) & 1;
     if (!prefills && !decodes) break;
     const int64_t e0 = sh.n_entry;
@@ -207,7 +210,7 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
     if (decodes) {
       const double slot_end = t + t0;
       int64_t carry = 0;
-      for (int base = 0; base < nd; base += kBT) {
+      for (int base = 0; base < nd; base += G::kSize) {
         const int k = base + tid;
         int64_t due = 0;
         bool emit = false;
@@ -222,7 +225,7 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
           if (due > 0) { dleft[k] -= due; emit = true; }
         }
         int64_t tot;
-        const int64_t ex = blk_excl(sh.bs, emit ? 1 : 0, &tot);
+        const int64_t ex = G::excl(sh.bs, emit ? 1 : 0, &tot);
         if (emit) {
           const int64_t at = ne + carry + ex;
           if (at < I.cap_entry) {
@@ -238,11 +241,11 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
         dtok += emit ? due : 0;
       }
       ne += carry;
-      dtok = blk_sum64(sh.bs, dtok);
+      dtok = G::sum64(sh.bs, dtok);
       cap = plan_time2bs(P, t0, 0);
       if (cap < 0) {
         if (tid == 0) sh.err = SLOS_ERR_INFEASIBLE_BUDGET;
-        __syncthreads();
+        G::sync();
         return;
       }
       free = imax(0, imin(cap - dtok, chunk_cap));
@@ -251,14 +254,14 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
     }
     // EDF prefill: take_k = min(left_k, max(0, free - sum_{k'<k} left_k'))
     int64_t carry = 0, spent = 0;
-    for (int base = 0; base < np; base += kBT) {
+    for (int base = 0; base < np; base += G::kSize) {
       const int k = base + tid;
       const int64_t lk = (k < np && pleft[k] > 0) ? pleft[k] : 0;
       int64_t tot;
-      const int64_t before = carry + blk_excl(sh.bs, lk, &tot);
+      const int64_t before = carry + G::excl(sh.bs, lk, &tot);
       const int64_t take = imin(lk, imax(0, free - before));
       int64_t t2;
-      const int64_t ex = blk_excl(sh.bs, take > 0 ? 1 : 0, &t2);
+      const int64_t ex = G::excl(sh.bs, take > 0 ? 1 : 0, &t2);
       if (take > 0) {
         pleft[k] -= take;
         const int64_t at = ne + ex;
@@ -275,7 +278,7 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
       spent += take;
       carry += tot;
     }
-    spent = blk_sum64(sh.bs, spent);
+    spent = G::sum64(sh.bs, spent);
     if (decodes) {
       const int64_t total = dtok + spent;
       const double dur = dmax(t0, total > 0 ? plan_predict(P, total, 0) : 0.0);
@@ -294,17 +297,15 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
       sh.n_entry = ne;
     }
     t = b.end_s;
-    __syncthreads();
+    G::sync();
   }
   if (tid == 0) out->exact_until = t;
-  __syncthreads();
+  G::sync();
 }
 
-__global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
-  __shared__ BuildShared sh;
-  const BatchArgs& A = prm.a;
-  const int tid = threadIdx.x;
-  const int inst = A.order[blockIdx.x];
+template <class G>
+__device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int inst) {
+  const int tid = G::rank();
   OutHdr* out = &A.out[inst];
   if (out->status != 0) return;
   if (tid == 0) {
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
     sh.edf = 0;
     sh.fill_late = 0;
   }
-  __syncthreads();
+  G::sync();
   const InstDev& I = sh.I;
   const PlannerDev& P = sh.P;
   const double pull = plan_predict(P, 1, 0);
@@ -362,12 +363,12 @@ __global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
       }
       sh.nb = nb;
     }
-    __syncthreads();
+    G::sync();
     for (int k = 0; k + 1 < sh.nb && !fallback; ++k) {  // :262-293
       const double a = sh.bounds[k];
       const double raw = sh.bounds[k + 1] - a;
       const double len = quantize_gap(raw);
-      int m = build_members_at(A, sh, a, pull, E);
+      int m = build_members_at<G>(A, sh, a, pull, E);
       if (tid == 0) {
         int mm = m;
         for (int mi = 0; mi < sh.nsel; ++mi)
@@ -375,11 +376,11 @@ __global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
             chain_member(A, sh, mi, a, raw + pull, pull, E, mm++);
         sh.m1 = mm;
       }
-      __syncthreads();
+      G::sync();
       MemBuf EE = E;
       EE.M = sh.m1;
       Arena ar2 = ar;
-      block_tile_gap(P, sh.bs, len, raw + pull, zero, EE, true, ar2, sh.o, sh.tmp);
+      block_tile_gap<G>(P, sh.bs, len, raw + pull, zero, EE, true, ar2, sh.o, sh.tmp);
       if (sh.o.status) {
         if (tid == 0) { out->status = sh.o.status; out->need_work = sh.o.need_work; }
         return;
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
         return;
       }
       if (!sh.o.feasible) { fallback = true; break; }
-      emit_gap(A, sh, a, true);
+      emit_gap<G>(A, sh, a, true);
     }
     if (!fallback) {
       if (tid == 0) {  // :294-300
@@ -397,22 +398,22 @@ __global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
         for (int k = 0; k < sh.nsel; ++k) if (sh.m_left[k] > 0) shortfall = 1;
         sh.err = shortfall;
       }
-      __syncthreads();
+      G::sync();
       if (sh.err) fallback = true;
-      __syncthreads();
+      G::sync();
       if (tid == 0) sh.err = 0;
     }
     if (!fallback) {  // decode tail :302-349
       const double t_last = sh.bounds[sh.nb - 1];
-      const int m = build_members_at(A, sh, t_last, pull, E);
+      const int m = build_members_at<G>(A, sh, t_last, pull, E);
       double tl = 0.0, capv = 0.0;
-      for (int q = tid; q < m; q += kBT) {
+      for (int q = tid; q < m; q += G::kSize) {
         const double tpot = P.tpot[E.tr[q]];
         tl = dmax(tl, E.ph[q] + (double)E.rm[q] * tpot);
         if (E.rm[q] > 0) capv = dmax(capv, E.ph[q] + tpot);
       }
-      double tail_len = blk_max(sh.bs, tl);
-      const double capm = blk_max(sh.bs, capv);
+      double tail_len = G::max(sh.bs, tl);
+      const double capm = G::max(sh.bs, capv);
       if (sh.nsel > 0 || I.tail_horizon > kTimeEps) {
         double max_tpot = 0.0;
         for (int l = 0; l < P.L; ++l) max_tpot = dmax(max_tpot, P.tpot[l]);
@@ -425,13 +426,13 @@ __global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
         for (int mi = 0; mi < sh.nsel; ++mi) chain_member(A, sh, mi, t_last, tail_len, pull, E, mm++);
         sh.m1 = mm;
       }
-      __syncthreads();
+      G::sync();
       const double tlen = quantize_gap(tail_len);
       if (tlen > kTimeEps && sh.m1 > 0) {
         MemBuf EE = E;
         EE.M = sh.m1;
         Arena ar2 = ar;
-        block_tile_gap(P, sh.bs, tlen, tail_len, zero, EE, true, ar2, sh.o, sh.tmp);
+        block_tile_gap<G>(P, sh.bs, tlen, tail_len, zero, EE, true, ar2, sh.o, sh.tmp);
         if (sh.o.status) {
           if (tid == 0) { out->status = sh.o.status; out->need_work = sh.o.need_work; }
           return;
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
           return;
         }
         if (!sh.o.feasible) fallback = true;
-        else emit_gap(A, sh, t_last, false);
+        else emit_gap<G>(A, sh, t_last, false);
       }
     }
     if (!fallback && tid == 0) {
@@ -459,14 +460,14 @@ __global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
       for (int q = 0; q < I.n_pending; ++q) dec[q] = q;
       out->n_declined = I.n_pending;
     }
-    __syncthreads();
-    edf_fallback(A, sh, ar, out);
+    G::sync();
+    edf_fallback<G>(A, sh, ar, out);
     if (sh.err) {
       if (tid == 0) out->status = sh.err;
       return;
     }
   }
-  __syncthreads();
+  G::sync();
   if (tid == 0) {
     out->n_batches = sh.n_batch;
     out->n_entries = sh.n_entry;
@@ -476,6 +477,16 @@ __global__ void __launch_bounds__(kBT) build_kernel(BuildParams prm) {
       out->need_entry = 2 * sh.n_entry;
     }
   }
+}
+
+constexpr int kBuildWarps = 4;  // instances per CTA (one warp each)
+
+__global__ void __launch_bounds__(32 * kBuildWarps) build_kernel(BuildParams prm) {
+  __shared__ BuildShared shs[kBuildWarps];
+  const BatchArgs& A = prm.a;
+  const int idx = blockIdx.x * kBuildWarps + warp_id();
+  if (idx >= A.n_inst) return;  // whole warp; the engine never uses CTA barriers here
+  build_instance<WarpGrp>(A, shs[warp_id()], A.order[idx]);
 }
 
 // ---- standalone gap queries (slos_tile_gap_batch) ----------------------------
@@ -524,13 +535,13 @@ __global__ void __launch_bounds__(kBT) gap_kernel(GapParams prm) {
   bool sorted = true;
   for (int m = 1; m < E.M; ++m) if (E.ow[m] <= E.ow[m - 1]) { sorted = false; break; }
   if (q.mode == SLOS_GAP_TILE_AR) {
-    block_tile_gap_ar(P, bs, q.gap_s, q.horizon, c, E, sorted, ar, o);
+    block_tile_gap_ar<BlockGrp>(P, bs, q.gap_s, q.horizon, c, E, sorted, ar, o);
   } else if (q.mode == SLOS_GAP_TILE) {
-    block_tile_gap(P, bs, q.gap_s, q.horizon, c, E, sorted, ar, o, tmp);
+    block_tile_gap<BlockGrp>(P, bs, q.gap_s, q.horizon, c, E, sorted, ar, o, tmp);
   } else {  // prefill_budget: quantised gap, canonical census, due_horizon 0
     MemBuf none = E;
     none.M = 0;
-    block_tile_gap(P, bs, quantize_gap(q.gap_s), 0.0, c, none, true, ar, o, tmp);
+    block_tile_gap<BlockGrp>(P, bs, quantize_gap(q.gap_s), 0.0, c, none, true, ar, o, tmp);
   }
   if (tid == 0) {
     GapOutDev r;

@@ -55,7 +55,7 @@ struct GapPlanBuf {  // output of one tile_gap call
   int64_t need_b, need_own, need_work;
 };
 
-struct BlockShared {  // static shared scratch for the block engine
+struct BlockShared {  // shared scratch of one cooperating group (a CTA or a warp)
   int64_t r64[kBW + 2];
   double rd[kBW + 2];
   int32_t r32[kBW + 2];
@@ -64,63 +64,96 @@ struct BlockShared {  // static shared scratch for the block engine
   int flag2;
   int64_t v64a, v64b;
   double vd;
+  SpecSol sp;
 };
 
-__device__ __forceinline__ int64_t blk_sum64(BlockShared& sh, int64_t v) {
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane_id() == 0) sh.r64[warp_id()] = v;
-  __syncthreads();
-  int64_t t = 0;
-  for (int w = 0; w < kBW; ++w) t += sh.r64[w];
-  __syncthreads();
-  return t;
-}
-__device__ __forceinline__ int blk_or(BlockShared& sh, int v) {
-  v = __reduce_or_sync(0xffffffffu, (unsigned)v);
-  __syncthreads();
-  if (lane_id() == 0) sh.r32[warp_id()] = v;
-  __syncthreads();
-  int t = 0;
-  for (int w = 0; w < kBW; ++w) t |= sh.r32[w];
-  __syncthreads();
-  return t;
-}
-__device__ __forceinline__ double blk_max(BlockShared& sh, double v) {
-  for (int o = 16; o; o >>= 1) { const double y = __shfl_xor_sync(0xffffffffu, v, o); v = dmax(v, y); }
-  __syncthreads();
-  if (lane_id() == 0) sh.rd[warp_id()] = v;
-  __syncthreads();
-  double t = sh.rd[0];
-  for (int w = 1; w < kBW; ++w) t = dmax(t, sh.rd[w]);
-  __syncthreads();
-  return t;
-}
-__device__ __forceinline__ double blk_min(BlockShared& sh, double v) {
-  for (int o = 16; o; o >>= 1) { const double y = __shfl_xor_sync(0xffffffffu, v, o); v = dmin(v, y); }
-  __syncthreads();
-  if (lane_id() == 0) sh.rd[warp_id()] = v;
-  __syncthreads();
-  double t = sh.rd[0];
-  for (int w = 1; w < kBW; ++w) t = dmin(t, sh.rd[w]);
-  __syncthreads();
-  return t;
-}
-// exclusive scan over the block (one value per thread); *tot = block total
-__device__ __forceinline__ int64_t blk_excl(BlockShared& sh, int64_t v, int64_t* tot) {
-  const int64_t inc = warp_incl_scan(v);
-  __syncthreads();
-  if (lane_id() == 31) sh.r64[warp_id()] = inc;
-  __syncthreads();
-  int64_t base = 0, t = 0;
-  for (int w = 0; w < kBW; ++w) {
-    if (w < warp_id()) base += sh.r64[w];
-    t += sh.r64[w];
+// Cooperative-group policies: the same engine runs on a whole CTA (BlockGrp,
+// standalone gap queries) or on one warp (WarpGrp, plan reconstruction: one
+// instance per warp, no CTA barriers).
+struct BlockGrp {
+  static constexpr int kSize = kBT;
+  __device__ static int rank() { return threadIdx.x; }
+  __device__ static void sync() { __syncthreads(); }
+  __device__ static bool leader_warp() { return warp_id() == 0; }
+  __device__ static int64_t sum64(BlockShared& sh, int64_t v) {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane_id() == 0) sh.r64[warp_id()] = v;
+    __syncthreads();
+    int64_t t = 0;
+    for (int w = 0; w < kBW; ++w) t += sh.r64[w];
+    __syncthreads();
+    return t;
   }
-  __syncthreads();
-  *tot = t;
-  return base + inc - v;
-}
+  __device__ static int or_(BlockShared& sh, int v) {
+    v = __reduce_or_sync(0xffffffffu, (unsigned)v);
+    __syncthreads();
+    if (lane_id() == 0) sh.r32[warp_id()] = v;
+    __syncthreads();
+    int t = 0;
+    for (int w = 0; w < kBW; ++w) t |= sh.r32[w];
+    __syncthreads();
+    return t;
+  }
+  __device__ static double max(BlockShared& sh, double v) {
+    for (int o = 16; o; o >>= 1) { const double y = __shfl_xor_sync(0xffffffffu, v, o); v = dmax(v, y); }
+    __syncthreads();
+    if (lane_id() == 0) sh.rd[warp_id()] = v;
+    __syncthreads();
+    double t = sh.rd[0];
+    for (int w = 1; w < kBW; ++w) t = dmax(t, sh.rd[w]);
+    __syncthreads();
+    return t;
+  }
+  __device__ static double min(BlockShared& sh, double v) {
+    for (int o = 16; o; o >>= 1) { const double y = __shfl_xor_sync(0xffffffffu, v, o); v = dmin(v, y); }
+    __syncthreads();
+    if (lane_id() == 0) sh.rd[warp_id()] = v;
+    __syncthreads();
+    double t = sh.rd[0];
+    for (int w = 1; w < kBW; ++w) t = dmin(t, sh.rd[w]);
+    __syncthreads();
+    return t;
+  }
+  // exclusive scan (one value per thread); *tot = group total
+  __device__ static int64_t excl(BlockShared& sh, int64_t v, int64_t* tot) {
+    const int64_t inc = warp_incl_scan(v);
+    __syncthreads();
+    if (lane_id() == 31) sh.r64[warp_id()] = inc;
+    __syncthreads();
+    int64_t base = 0, t = 0;
+    for (int w = 0; w < kBW; ++w) {
+      if (w < warp_id()) base += sh.r64[w];
+      t += sh.r64[w];
+    }
+    __syncthreads();
+    *tot = t;
+    return base + inc - v;
+  }
+};
+
+struct WarpGrp {
+  static constexpr int kSize = 32;
+  __device__ static int rank() { return lane_id(); }
+  __device__ static void sync() { __syncwarp(); }
+  __device__ static bool leader_warp() { return true; }
+  __device__ static int64_t sum64(BlockShared&, int64_t v) { return warp_sum(v); }
+  __device__ static int or_(BlockShared&, int v) { return (int)__reduce_or_sync(0xffffffffu, (unsigned)v); }
+  __device__ static double max(BlockShared&, double v) {
+    for (int o = 16; o; o >>= 1) { const double y = __shfl_xor_sync(0xffffffffu, v, o); v = dmax(v, y); }
+    return v;
+  }
+  __device__ static double min(BlockShared&, double v) {
+    for (int o = 16; o; o >>= 1) { const double y = __shfl_xor_sync(0xffffffffu, v, o); v = dmin(v, y); }
+    return v;
+  }
+  __device__ static int64_t excl(BlockShared&, int64_t v, int64_t* tot) {
+    const int64_t inc = warp_incl_scan(v);
+    *tot = __shfl_sync(0xffffffffu, inc, 31);
+    __syncwarp();
+    return inc - v;
+  }
+};
 
 // Work-area bump allocator (global memory, per CTA).
 struct Arena {
@@ -151,10 +184,11 @@ __device__ __forceinline__ bool mrec_less(const MRec& a, const MRec& b) {
 }
 
 // block bitonic sort over n records (n padded to pow2 with +inf sentinels)
+template <class G>
 __device__ inline void blk_sort_mrec(MRec* r, int n_pow2) {
   for (int k = 2; k <= n_pow2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n_pow2; i += kBT) {
+      for (int i = G::rank(); i < n_pow2; i += G::kSize) {
         const int ixj = i ^ j;
         if (ixj > i) {
           const bool up = (i & k) == 0;
@@ -163,7 +197,7 @@ __device__ inline void blk_sort_mrec(MRec* r, int n_pow2) {
           if (sw) { r[i] = b; r[ixj] = a; }
         }
       }
-      __syncthreads();
+      G::sync();
     }
   }
 }
@@ -200,36 +234,37 @@ __device__ inline int gap_prefill_only(const PlannerDev& P, double gap, double m
 // tile_gap_ar with full output. Block-wide; all threads must call. Returns in o
 // (feasible/status). `E` holds the exact members; counts c[L] the canonical ones.
 // owners_sorted: member owners strictly ascending (true for build_plan censuses).
+template <class G>
 __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, double gap,
                                          double dh, const int64_t* c, const MemBuf& E,
                                          bool owners_sorted, Arena ar, GapPlanBuf& o) {
-  const int tid = threadIdx.x;
+  const int tid = G::rank();
   const int L = P.L;
   const int M = E.M;
   if (tid == 0) { o.n_b = 0; o.n_own = 0; o.budget = 0; o.feasible = 0; o.status = 0; o.n_spec = 0; }
-  __syncthreads();
+  G::sync();
   const double horizon = dmax(gap, dh);
   if (gap <= kTimeEps) {  // :156-164
     int any = 0;
-    for (int m = tid; m < M; m += kBT) {
+    for (int m = tid; m < M; m += G::kSize) {
       if (E.rm[m] <= 0) continue;
       if (E.bl[m] > 0) any = 1;
       if (horizon > kTimeEps && time_le(E.ph[m], horizon)) any = 1;
     }
-    any = blk_or(sh, any);
+    any = G::or_(sh, any);
     if (tid == 0) o.feasible = any ? 0 : 1;
-    __syncthreads();
+    G::sync();
     return;
   }
   const double min_slot = plan_predict(P, 1, 0);
   unsigned cmask = 0;
   for (int l = 0; l < L; ++l) if (c[l] > 0) cmask |= 1u << l;
   int em = 0;
-  for (int m = tid; m < M; m += kBT) if (E.rm[m] > 0) em |= 1 << E.tr[m];
-  const unsigned present = (unsigned)blk_or(sh, em) | cmask;
+  for (int m = tid; m < M; m += G::kSize) if (E.rm[m] > 0) em |= 1 << E.tr[m];
+  const unsigned present = (unsigned)G::or_(sh, em) | cmask;
   if (!present) {
     if (tid == 0) { o.status = gap_prefill_only(P, gap, min_slot, o); o.feasible = o.status == 0; }
-    __syncthreads();
+    G::sync();
     return;
   }
   // per-member due counts (late l_m, non-late), spill not needed here
@@ -237,11 +272,11 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
   int64_t* lpre = (int64_t*)ar.take(sizeof(int64_t) * (M + 1));
   if (ar.used > ar.cap) {
     if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
-    __syncthreads();
+    G::sync();
     return;
   }
   int64_t nd = 0;
-  for (int m = tid; m < M; m += kBT) {
+  for (int m = tid; m < M; m += G::kSize) {
     int64_t late = 0, nl = 0;
     const int64_t rem = E.rm[m];
     if (rem > 0) {
@@ -262,16 +297,16 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
     q[l] = n;
     nd += (tid == 0) ? c[l] * (int64_t)n : 0;
   }
-  const int64_t D = blk_sum64(sh, nd);
+  const int64_t D = G::sum64(sh, nd);
   if (D == 0) {  // :223
     if (tid == 0) { o.status = gap_prefill_only(P, gap, min_slot, o); o.feasible = o.status == 0; }
-    __syncthreads();
+    G::sync();
     return;
   }
   const double t0 = P.tpot[__ffs(present) - 1];
   if (min_slot > t0 + kTimeEps) return;  // :231 (feasible = 0)
   // t0_first (:234-239): ordered scan by warp 0
-  if (warp_id() == 0) {
+  if (G::leader_warp()) {
     double cur = t0;
     for (int base = 0; base < M; base += 32) {
       const int m = base + lane_id();
@@ -288,7 +323,7 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
     }
     if (lane_id() == 0) sh.vd = cur;
   }
-  __syncthreads();
+  G::sync();
   const double t0_first = sh.vd;
   // slot ends (thread 0): count first, then fill
   if (tid == 0) {
@@ -299,7 +334,7 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
     else if (gap - last >= min_slot - kTimeEps) ++S;
     sh.S = S;
   }
-  __syncthreads();
+  G::sync();
   const int S = sh.S;
   if (S == 0) return;  // :248
   double* ends = (double*)ar.take(sizeof(double) * S);
@@ -313,7 +348,7 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
   int64_t* ptier = (int64_t*)ar.take(sizeof(int64_t) * (int64_t)S * L);
   if (ar.used > ar.cap) {
     if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
-    __syncthreads();
+    G::sync();
     return;
   }
   if (tid == 0) {
@@ -323,26 +358,26 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
     if (s == 0) { if (time_le(min_slot, gap)) ends[s++] = gap; }
     else if (gap - last >= min_slot - kTimeEps) ends[s++] = gap;
   }
-  __syncthreads();
+  G::sync();
   int cerr = 0;
-  for (int s = tid; s < S; s += kBT) {  // :250-255
+  for (int s = tid; s < S; s += G::kSize) {  // :250-255
     const double dur = ends[s] - (s == 0 ? 0.0 : ends[s - 1]);
     const int64_t cc = plan_time2bs(P, dur, 0);
     if (cc < 0) cerr = 1;
     cap[s] = imin(cc, P.max_batch);
     ng[s] = 0;
   }
-  for (int64_t x = tid; x < (int64_t)S * (M + 1); x += kBT) tok[x] = 0;
-  for (int64_t x = tid; x < (int64_t)S * L; x += kBT) ptier[x] = 0;
-  cerr = blk_or(sh, cerr);
+  for (int64_t x = tid; x < (int64_t)S * (M + 1); x += G::kSize) tok[x] = 0;
+  for (int64_t x = tid; x < (int64_t)S * L; x += G::kSize) ptier[x] = 0;
+  cerr = G::or_(sh, cerr);
   if (cerr) {
     if (tid == 0) o.status = SLOS_ERR_INFEASIBLE_BUDGET;
-    __syncthreads();
+    G::sync();
     return;
   }
   // jit histogram of non-late dues (exact + canonical)
   int fail = 0;
-  for (int m = tid; m < M; m += kBT) {
+  for (int m = tid; m < M; m += G::kSize) {
     const int64_t rem = E.rm[m];
     if (rem <= 0) continue;
     int64_t issued = E.bl[m] > 0 ? imin(E.bl[m], rem) : 0;
@@ -362,16 +397,16 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
   // late prefix over members (insertion order)
   {
     int64_t carry = 0;
-    for (int base = 0; base < M; base += kBT) {
+    for (int base = 0; base < M; base += G::kSize) {
       const int m = base + tid;
       int64_t tot;
-      const int64_t ex = blk_excl(sh, m < M ? lcount[m] : 0, &tot);
+      const int64_t ex = G::excl(sh, m < M ? lcount[m] : 0, &tot);
       if (m < M) lpre[m] = carry + ex;
       carry += tot;
     }
     if (tid == 0) sh.v64a = carry;
   }
-  fail = blk_or(sh, fail);
+  fail = G::or_(sh, fail);
   if (fail) return;  // a non-late due precedes every slot end
   // latest-fit stack over groups (thread 0)
   if (tid == 0) {
@@ -407,10 +442,10 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
     }
     sh.flag = ok;
   }
-  __syncthreads();
+  G::sync();
   if (!sh.flag) return;
   // late tokens: member m's late dues occupy [lpre, lpre + l) of the cumulative cap
-  for (int m = tid; m < M; m += kBT) {
+  for (int m = tid; m < M; m += G::kSize) {
     int64_t a = lpre[m], n = lcount[m];
     int64_t before = 0;
     for (int s = 0; s < S && n > 0; ++s) {
@@ -427,7 +462,7 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
   }
   // non-late tokens: single-segment groups direct; multi-segment groups gathered
   int64_t nmulti = 0;
-  for (int m = tid; m < M; m += kBT) {
+  for (int m = tid; m < M; m += G::kSize) {
     const int64_t rem = E.rm[m];
     if (rem <= 0) continue;
     int64_t issued = E.bl[m] > 0 ? imin(E.bl[m], rem) : 0;
@@ -446,19 +481,19 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
       else ++nmulti;
     }
   }
-  nmulti = blk_sum64(sh, nmulti);
+  nmulti = G::sum64(sh, nmulti);
   if (nmulti > 0) {
     int np2 = 1;
     while (np2 < nmulti) np2 <<= 1;
     MRec* rec = (MRec*)ar.take(sizeof(MRec) * np2);
     if (ar.used > ar.cap) {
       if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
-      __syncthreads();
+      G::sync();
       return;
     }
     if (tid == 0) sh.v64b = 0;
-    __syncthreads();
-    for (int m = tid; m < M; m += kBT) {
+    G::sync();
+    for (int m = tid; m < M; m += G::kSize) {
       const int64_t rem = E.rm[m];
       if (rem <= 0) continue;
       int64_t issued = E.bl[m] > 0 ? imin(E.bl[m], rem) : 0;
@@ -486,14 +521,14 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
         rec[at] = r;
       }
     }
-    __syncthreads();
-    for (int64_t x = nmulti + tid; x < np2; x += kBT) {
+    G::sync();
+    for (int64_t x = nmulti + tid; x < np2; x += G::kSize) {
       MRec r;
       r.time = INFINITY; r.key = ~0ull; r.grp = 0x7fffffff; r.who = 0; r.w = 0;
       rec[x] = r;
     }
-    __syncthreads();
-    blk_sort_mrec(rec, np2);
+    G::sync();
+    blk_sort_mrec<G>(rec, np2);
     if (tid == 0) {  // deal sorted dues along each group's segments
       int64_t x = 0;
       while (x < nmulti) {
@@ -515,7 +550,7 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
       }
     }
   }
-  __syncthreads();
+  G::sync();
   // emission: batches slot by slot; owners in member order (ascending owner)
   if (tid == 0) { o.n_b = S; }
   int64_t budget = 0;
@@ -523,18 +558,18 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
     int32_t* row = tok + (int64_t)s * (M + 1);
     const int base_own = o.n_own;
     int64_t carry = 0;
-    for (int base = 0; base < M; base += kBT) {
+    for (int base = 0; base < M; base += G::kSize) {
       const int m = base + tid;
       const int has = (m < M && row[m] > 0) ? 1 : 0;
       int64_t tot;
-      const int64_t ex = blk_excl(sh, has, &tot);
+      const int64_t ex = G::excl(sh, has, &tot);
       if (has) {
         const int64_t at = base_own + carry + ex;
         if (at < o.cap_own) { o.own[2 * at] = E.ow[m]; o.own[2 * at + 1] = row[m]; }
       }
       carry += tot;
     }
-    __syncthreads();
+    G::sync();
     if (tid == 0) {
       int n_here = (int)carry;
       if (!owners_sorted && base_own + n_here <= o.cap_own) {  // std::map order + merge
@@ -567,21 +602,22 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
       budget += imin(fr[s], P.max_chunk);
       o.n_own = base_own + n_here;
     }
-    __syncthreads();
+    G::sync();
   }
   if (tid == 0) { o.budget = budget; o.feasible = 1; }
-  __syncthreads();
+  G::sync();
 }
 
 // tile_gap (batch_planner.cpp:315-406) with full output. `Ebuf` must hold the
 // exact members; `merged_all` are census.merged_counts (exact members of every
 // remaining, plus canonical).
+template <class G>
 __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, double gap, double dh,
                                       const int64_t* c, const MemBuf& E, bool owners_sorted,
                                       Arena ar, GapPlanBuf& o, GapPlanBuf& tmp) {
-  const int tid = threadIdx.x;
+  const int tid = G::rank();
   const int L = P.L;
-  block_tile_gap_ar(P, sh, gap, dh, c, E, owners_sorted, ar, o);
+  block_tile_gap_ar<G>(P, sh, gap, dh, c, E, owners_sorted, ar, o);
   if (o.status) return;
   if (!P.speculative) return;
   unsigned cmask = 0;
@@ -592,7 +628,7 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
   int64_t per[kMaxTiers];
   for (int l = 0; l < kMaxTiers; ++l) per[l] = 0;
   double minph = INFINITY;
-  for (int m = tid; m < E.M; m += kBT) {
+  for (int m = tid; m < E.M; m += G::kSize) {
     per[E.tr[m]] += 1;
     if (E.bl[m] > 0) bad = 1;
     const int64_t rem = E.rm[m];
@@ -604,15 +640,14 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
         if (!time_le(d, gap)) { bad = 1; break; }
     }
   }
-  bad = blk_or(sh, bad);
+  bad = G::or_(sh, bad);
   int64_t merged[kMaxTiers];
-  for (int l = 0; l < L; ++l) merged[l] = c[l] + blk_sum64(sh, per[l]);
-  minph = blk_min(sh, minph);
+  for (int l = 0; l < L; ++l) merged[l] = c[l] + G::sum64(sh, per[l]);
+  minph = G::min(sh, minph);
   if (bad) return;
-  __shared__ SpecSol s_sp;
-  if (tid == 0) s_sp = solve_spec(P, merged);
-  __syncthreads();
-  const SpecSol sp = s_sp;
+  if (tid == 0) sh.sp = solve_spec(P, merged);
+  G::sync();
+  const SpecSol sp = sh.sp;
   if (!sp.ok) return;
   if (minph < sp.bt - kTimeEps) return;  // (:341-346) over members with remaining > 0
   const int full = (int)floor(gap / sp.bt + kTimeEps);
@@ -625,12 +660,12 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
     int64_t* kh = (int64_t*)ar.take(sizeof(int64_t) * (full + 2));
     if (ar.used > ar.cap) {
       if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
-      __syncthreads();
+      G::sync();
       return;
     }
-    for (int k = tid; k <= full + 1; k += kBT) kh[k] = 0;
-    __syncthreads();
-    for (int m = tid; m < E.M; m += kBT) {
+    for (int k = tid; k <= full + 1; k += G::kSize) kh[k] = 0;
+    G::sync();
+    for (int m = tid; m < E.M; m += G::kSize) {
       const int64_t rem = E.rm[m];
       if (rem <= 0) continue;
       const int64_t sl = sp.lengths[E.tr[m]];
@@ -641,7 +676,7 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
         atomicAdd((unsigned long long*)&kh[q + 1], (unsigned long long)(-r));
       }
     }
-    __syncthreads();
+    G::sync();
     if (tid == 0) {
       int64_t e = 0;
       for (int k = 0; k < full; ++k) {
@@ -650,7 +685,7 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
       }
       sh.v64a = spec_budget;
     }
-    __syncthreads();
+    G::sync();
     spec_budget = sh.v64a;
   }
   const double used = full * sp.bt;
@@ -661,8 +696,8 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
   if (gap - used > kTimeEps) {
     MemBuf none = E;
     none.M = 0;
-    block_tile_gap_ar(P, sh, gap - used, 0.0, merged, none, true, ar, tmp);
-    if (tmp.status) { if (tid == 0) { o.status = tmp.status; o.need_work = tmp.need_work; } __syncthreads(); return; }
+    block_tile_gap_ar<G>(P, sh, gap - used, 0.0, merged, none, true, ar, tmp);
+    if (tmp.status) { if (tid == 0) { o.status = tmp.status; o.need_work = tmp.need_work; } G::sync(); return; }
     if (!tmp.feasible) return;  // keep ar
     spec_budget += tmp.budget;
     has_tail = true;
@@ -677,12 +712,12 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
     o.n_spec = L;
     for (int l = 0; l < kMaxTiers; ++l) o.spec[l] = l < L ? sp.lengths[l] : 0;
   }
-  __syncthreads();
+  G::sync();
   // per batch k: owners in census order with n = min(left, sl) > 0
   for (int k = 0; k < full; ++k) {
     const int base_own = o.n_own;
     int64_t carry = 0, dec_ex = 0, step = 0;
-    for (int base = 0; base < E.M; base += kBT) {
+    for (int base = 0; base < E.M; base += G::kSize) {
       const int m = base + tid;
       int64_t n = 0, sl = 0;
       if (m < E.M) {
@@ -692,7 +727,7 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
       }
       const int has = n > 0;
       int64_t tot;
-      const int64_t ex = blk_excl(sh, has, &tot);
+      const int64_t ex = G::excl(sh, has, &tot);
       if (has) {
         const int64_t at = base_own + carry + ex;
         if (at < o.cap_own) { o.own[2 * at] = E.ow[m]; o.own[2 * at + 1] = n; }
@@ -701,14 +736,14 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
       }
       carry += tot;
     }
-    dec_ex = blk_sum64(sh, dec_ex);
+    dec_ex = G::sum64(sh, dec_ex);
     for (int o2 = 16; o2; o2 >>= 1) step = imax(step, __shfl_xor_sync(0xffffffffu, step, o2));
-    __syncthreads();
-    if (lane_id() == 0) sh.r64[warp_id()] = step;
-    __syncthreads();
+    G::sync();
+    if (lane_id() == 0) sh.r64[G::kSize == 32 ? 0 : warp_id()] = step;
+    G::sync();
     if (tid == 0) {
       int64_t st = 0;
-      for (int w = 0; w < kBW; ++w) st = imax(st, sh.r64[w]);
+      for (int w = 0; w < (G::kSize + 31) / 32; ++w) st = imax(st, sh.r64[w]);
       int64_t decode = 0;
       GapBatchOut b;
       b.start_s = k * sp.bt;
@@ -729,7 +764,7 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
       o.n_b++;
       o.n_own = base_own + (int32_t)carry;
     }
-    __syncthreads();
+    G::sync();
   }
   if (has_tail && tid == 0) {
     for (int k = 0; k < tmp.n_b; ++k) {
@@ -742,7 +777,7 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
       o.n_b++;
     }
   }
-  __syncthreads();
+  G::sync();
 }
 
 }  // namespace slos
