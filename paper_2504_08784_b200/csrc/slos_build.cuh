@@ -92,37 +92,26 @@ __device__ __forceinline__ int owner_tier(const BatchArgs& A, const BuildShared&
 // fill (fill_prefill, dp_scheduler.cpp:220-232). track=true updates
 // decode_assigned of chain owners (the gap loop, :287; not the tail, :341-344).
 template <class G>
-__device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bool track) {
+__device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bool track, Arena ar) {
   const int tid = G::rank();
   const InstDev& I = sh.I;
   GapPlanBuf& o = sh.o;
   slos_batch* OB = A.batches + I.off_batch;
   slos_entry* OE = A.entries + I.off_entry;
-  for (int k = 0; k < o.n_b; ++k) {
-    const GapBatchOut& gb = o.b[k];
-    const bool spec_batch = gb.spec_step > 0 && o.n_spec > 0;
-    const int64_t e0 = sh.n_entry;
-    // decode entries (parallel copy)
-    for (int q = tid; q < gb.n_owner; q += G::kSize) {
-      const int64_t owner = o.own[2 * (gb.first_owner + q)];
-      const int64_t t = o.own[2 * (gb.first_owner + q) + 1];
-      const int64_t at = e0 + q;
-      if (at < I.cap_entry) {
-        slos_entry e;
-        e.req = owner_ref(A, sh, owner);
-        e.spec_len = spec_batch ? o.spec[owner_tier(A, sh, owner)] : 0;
-        e.prefill_tokens = 0;
-        e.decode_tokens = t;
-        OE[at] = e;
-      }
-      if (track && owner >= I.R_total) atomicAdd(&sh.m_asg[owner - I.R_total], (unsigned long long)t);
-    }
-    G::sync();
-    if (tid == 0) {
-      int64_t ne = e0 + gb.n_owner;
+  int64_t* bpos = (int64_t*)ar.take(sizeof(int64_t) * (o.n_b + 1));
+  // (1) one thread: EDF prefill fill (fill_prefill, dp_scheduler.cpp:220-232) and
+  //     the batch records; each batch's decode entries are reserved ahead of its
+  //     prefill entries.
+  if (tid == 0) {
+    int64_t ne = sh.n_entry;
+    for (int k = 0; k < o.n_b; ++k) {
+      const GapBatchOut& gb = o.b[k];
+      const int64_t e0 = ne;
+      bpos[k] = e0;
+      ne += gb.n_owner;
       const double end_abs = a + gb.end_s;
       int64_t budget = gb.prefill_budget;
-      while (budget > 0) {  // fill_prefill
+      while (budget > 0) {
         while (sh.edf < sh.nsel && sh.m_left[sh.edf] == 0) ++sh.edf;
         if (sh.edf == sh.nsel) break;
         const int mi = sh.edf;
@@ -142,21 +131,43 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
         ++ne;
       }
       if (sh.n_batch < I.cap_batch) {
-        slos_batch b;
-        b.start_s = a + gb.start_s;
-        b.end_s = a + gb.end_s;
-        b.capacity_tokens = gb.capacity;
-        b.spec_step = gb.spec_step;
-        b.prefill_budget_left = budget;
-        b.first_entry = e0;
-        b.n_entries = ne - e0;
-        OB[sh.n_batch] = b;
+        slos_batch bt;
+        bt.start_s = a + gb.start_s;
+        bt.end_s = a + gb.end_s;
+        bt.capacity_tokens = gb.capacity;
+        bt.spec_step = gb.spec_step;
+        bt.prefill_budget_left = budget;
+        bt.first_entry = e0;
+        bt.n_entries = ne - e0;
+        OB[sh.n_batch] = bt;
       }
       sh.n_batch++;
-      sh.n_entry = ne;
     }
-    G::sync();
+    sh.n_entry = ne;
   }
+  G::sync();
+  // (2) decode entries, one warp per batch, lanes over owners
+  const int nw = G::kSize / 32, wr = tid / 32, lane = lane_id();
+  for (int k = wr; k < o.n_b; k += nw) {
+    const GapBatchOut& gb = o.b[k];
+    const bool spec_batch = gb.spec_step > 0 && o.n_spec > 0;
+    const int64_t e0 = bpos[k];
+    for (int q = lane; q < gb.n_owner; q += 32) {
+      const int64_t owner = o.own[2 * (gb.first_owner + q)];
+      const int64_t t = o.own[2 * (gb.first_owner + q) + 1];
+      const int64_t at = e0 + q;
+      if (at < I.cap_entry) {
+        slos_entry e;
+        e.req = owner_ref(A, sh, owner);
+        e.spec_len = spec_batch ? o.spec[owner_tier(A, sh, owner)] : 0;
+        e.prefill_tokens = 0;
+        e.decode_tokens = t;
+        OE[at] = e;
+      }
+      if (track && owner >= I.R_total) atomicAdd(&sh.m_asg[owner - I.R_total], (unsigned long long)t);
+    }
+  }
+  G::sync();
   return 0;
 }
 
@@ -390,7 +401,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
         return;
       }
       if (!sh.o.feasible) { fallback = true; break; }
-      emit_gap<G>(A, sh, a, true);
+      emit_gap<G>(A, sh, a, true, ar);
     }
     if (!fallback) {
       if (tid == 0) {  // :294-300
@@ -442,7 +453,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
           return;
         }
         if (!sh.o.feasible) fallback = true;
-        else emit_gap<G>(A, sh, t_last, false);
+        else emit_gap<G>(A, sh, t_last, false, ar);
       }
     }
     if (!fallback && tid == 0) {
@@ -479,14 +490,31 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
   }
 }
 
-constexpr int kBuildWarps = 4;  // instances per CTA (one warp each)
+// Plan reconstruction granularity (SLOS_BUILD_MODE): 0 = one warp per instance,
+// 4 instances per CTA; 1 = one 128-thread CTA per instance; 2 = 256 threads.
+#ifndef SLOS_BUILD_MODE
+#define SLOS_BUILD_MODE 1
+#endif
+#if SLOS_BUILD_MODE == 0
+constexpr int kBuildWarps = 4;
+constexpr int kBuildThreads = 32 * kBuildWarps;
+constexpr int kBuildPerCta = kBuildWarps;
+#else
+constexpr int kBuildThreads = SLOS_BUILD_MODE == 1 ? 128 : 256;
+constexpr int kBuildPerCta = 1;
+#endif
 
-__global__ void __launch_bounds__(32 * kBuildWarps) build_kernel(BuildParams prm) {
-  __shared__ BuildShared shs[kBuildWarps];
+__global__ void __launch_bounds__(kBuildThreads) build_kernel(BuildParams prm) {
   const BatchArgs& A = prm.a;
+#if SLOS_BUILD_MODE == 0
+  __shared__ BuildShared shs[kBuildWarps];
   const int idx = blockIdx.x * kBuildWarps + warp_id();
   if (idx >= A.n_inst) return;  // whole warp; the engine never uses CTA barriers here
   build_instance<WarpGrp>(A, shs[warp_id()], A.order[idx]);
+#else
+  __shared__ BuildShared sh;
+  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.order[blockIdx.x]);
+#endif
 }
 
 // ---- standalone gap queries (slos_tile_gap_batch) ----------------------------

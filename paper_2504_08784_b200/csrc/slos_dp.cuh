@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   __shared__ int32_t s_joff[SLOS_MAX_CHAIN + 2];
   __shared__ int64_t s_wsum[kDpWarps + 1];
   __shared__ unsigned long long s_ctr[5];
-  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_next_grp, s_best, s_ng;
+  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_ng;
   __shared__ int32_t s_glist[SLOS_MAX_CHAIN + 2];
   __shared__ int64_t s_next_free, s_arena_next;
 

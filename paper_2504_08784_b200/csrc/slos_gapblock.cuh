@@ -70,8 +70,10 @@ struct BlockShared {  // shared scratch of one cooperating group (a CTA or a war
 // Cooperative-group policies: the same engine runs on a whole CTA (BlockGrp,
 // standalone gap queries) or on one warp (WarpGrp, plan reconstruction: one
 // instance per warp, no CTA barriers).
-struct BlockGrp {
-  static constexpr int kSize = kBT;
+template <int NT>
+struct BlockGrpT {
+  static constexpr int kSize = NT;
+  static constexpr int kW = NT / 32;
   __device__ static int rank() { return threadIdx.x; }
   __device__ static void sync() { __syncthreads(); }
   __device__ static bool leader_warp() { return warp_id() == 0; }
@@ -81,7 +83,7 @@ struct BlockGrp {
     if (lane_id() == 0) sh.r64[warp_id()] = v;
     __syncthreads();
     int64_t t = 0;
-    for (int w = 0; w < kBW; ++w) t += sh.r64[w];
+    for (int w = 0; w < kW; ++w) t += sh.r64[w];
     __syncthreads();
     return t;
   }
@@ -91,7 +93,7 @@ struct BlockGrp {
     if (lane_id() == 0) sh.r32[warp_id()] = v;
     __syncthreads();
     int t = 0;
-    for (int w = 0; w < kBW; ++w) t |= sh.r32[w];
+    for (int w = 0; w < kW; ++w) t |= sh.r32[w];
     __syncthreads();
     return t;
   }
@@ -101,7 +103,7 @@ struct BlockGrp {
     if (lane_id() == 0) sh.rd[warp_id()] = v;
     __syncthreads();
     double t = sh.rd[0];
-    for (int w = 1; w < kBW; ++w) t = dmax(t, sh.rd[w]);
+    for (int w = 1; w < kW; ++w) t = dmax(t, sh.rd[w]);
     __syncthreads();
     return t;
   }
@@ -111,7 +113,7 @@ struct BlockGrp {
     if (lane_id() == 0) sh.rd[warp_id()] = v;
     __syncthreads();
     double t = sh.rd[0];
-    for (int w = 1; w < kBW; ++w) t = dmin(t, sh.rd[w]);
+    for (int w = 1; w < kW; ++w) t = dmin(t, sh.rd[w]);
     __syncthreads();
     return t;
   }
@@ -122,7 +124,7 @@ struct BlockGrp {
     if (lane_id() == 31) sh.r64[warp_id()] = inc;
     __syncthreads();
     int64_t base = 0, t = 0;
-    for (int w = 0; w < kBW; ++w) {
+    for (int w = 0; w < kW; ++w) {
       if (w < warp_id()) base += sh.r64[w];
       t += sh.r64[w];
     }
@@ -131,6 +133,8 @@ struct BlockGrp {
     return base + inc - v;
   }
 };
+
+using BlockGrp = BlockGrpT<kBT>;
 
 struct WarpGrp {
   static constexpr int kSize = 32;
@@ -554,6 +558,72 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
   // emission: batches slot by slot; owners in member order (ascending owner)
   if (tid == 0) { o.n_b = S; }
   int64_t budget = 0;
+  if (owners_sorted) {
+    // constant number of barriers: per-slot nonzero counts -> offsets -> scatter
+    int32_t* scnt = (int32_t*)ar.take(sizeof(int32_t) * (S + 1));
+    int32_t* soff = (int32_t*)ar.take(sizeof(int32_t) * (S + 1));
+    if (ar.used > ar.cap) {
+      if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
+      G::sync();
+      return;
+    }
+    const int nw = G::kSize / 32, wr = tid / 32, lane = lane_id();
+    for (int s = wr; s < S; s += nw) {
+      const int32_t* row = tok + (int64_t)s * (M + 1);
+      int cnt = 0;
+      for (int base = 0; base < M; base += 32) {
+        const int m = base + lane;
+        cnt += __popc(__ballot_sync(0xffffffffu, m < M && row[m] > 0));
+      }
+      if (lane == 0) scnt[s] = cnt;
+    }
+    G::sync();
+    if (wr == 0) {
+      int carry = 0;
+      for (int base = 0; base < S; base += 32) {
+        const int s = base + lane;
+        const int x = s < S ? scnt[s] : 0;
+        const int inc = warp_incl_scan(x);
+        if (s < S) soff[s] = carry + inc - x;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (lane == 0) soff[S] = carry;
+    }
+    G::sync();
+    const int base_own = o.n_own;
+    for (int s = wr; s < S; s += nw) {
+      const int32_t* row = tok + (int64_t)s * (M + 1);
+      int carry = 0;
+      for (int base = 0; base < M; base += 32) {
+        const int m = base + lane;
+        const bool has = m < M && row[m] > 0;
+        const unsigned msk = __ballot_sync(0xffffffffu, has);
+        if (has) {
+          const int64_t at = base_own + soff[s] + carry + __popc(msk & ((1u << lane) - 1));
+          if (at < o.cap_own) { o.own[2 * at] = E.ow[m]; o.own[2 * at + 1] = row[m]; }
+        }
+        carry += __popc(msk);
+      }
+      if (lane == 0 && s < o.cap_b) {
+        GapBatchOut& bt = o.b[s];
+        bt.start_s = s == 0 ? 0.0 : ends[s - 1];
+        bt.end_s = ends[s];
+        bt.capacity = cap[s];
+        bt.spec_step = 0;
+        bt.decode_tokens = cap[s] - fr[s];
+        bt.prefill_budget = imin(fr[s], P.max_chunk);
+        for (int l = 0; l < kMaxTiers; ++l) bt.per_tier[l] = l < L ? ptier[(int64_t)s * L + l] : 0;
+        bt.first_owner = base_own + soff[s];
+        bt.n_owner = scnt[s];
+      }
+    }
+    for (int s = tid; s < S; s += G::kSize) budget += imin(fr[s], P.max_chunk);
+    budget = G::sum64(sh, budget);
+    G::sync();
+    if (tid == 0) { o.n_own = base_own + soff[S]; o.budget = budget; o.feasible = 1; }
+    G::sync();
+    return;
+  }
   for (int s = 0; s < S; ++s) {
     int32_t* row = tok + (int64_t)s * (M + 1);
     const int base_own = o.n_own;
@@ -572,32 +642,32 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
     G::sync();
     if (tid == 0) {
       int n_here = (int)carry;
-      if (!owners_sorted && base_own + n_here <= o.cap_own) {  // std::map order + merge
+      if (base_own + n_here <= o.cap_own) {  // std::map order + merge (owners may repeat)
         int64_t* pr = o.own + 2 * base_own;
-        for (int a = 1; a < n_here; ++a) {
-          const int64_t ko = pr[2 * a], kt = pr[2 * a + 1];
-          int b = a - 1;
-          while (b >= 0 && pr[2 * b] > ko) { pr[2 * (b + 1)] = pr[2 * b]; pr[2 * (b + 1) + 1] = pr[2 * b + 1]; --b; }
-          pr[2 * (b + 1)] = ko; pr[2 * (b + 1) + 1] = kt;
+        for (int a2 = 1; a2 < n_here; ++a2) {
+          const int64_t ko = pr[2 * a2], kt = pr[2 * a2 + 1];
+          int b2 = a2 - 1;
+          while (b2 >= 0 && pr[2 * b2] > ko) { pr[2 * (b2 + 1)] = pr[2 * b2]; pr[2 * (b2 + 1) + 1] = pr[2 * b2 + 1]; --b2; }
+          pr[2 * (b2 + 1)] = ko; pr[2 * (b2 + 1) + 1] = kt;
         }
         int w = 0;
-        for (int a = 0; a < n_here; ++a) {
-          if (w > 0 && pr[2 * (w - 1)] == pr[2 * a]) pr[2 * (w - 1) + 1] += pr[2 * a + 1];
-          else { pr[2 * w] = pr[2 * a]; pr[2 * w + 1] = pr[2 * a + 1]; ++w; }
+        for (int a2 = 0; a2 < n_here; ++a2) {
+          if (w > 0 && pr[2 * (w - 1)] == pr[2 * a2]) pr[2 * (w - 1) + 1] += pr[2 * a2 + 1];
+          else { pr[2 * w] = pr[2 * a2]; pr[2 * w + 1] = pr[2 * a2 + 1]; ++w; }
         }
         n_here = w;
       }
       if (s < o.cap_b) {
-        GapBatchOut& b = o.b[s];
-        b.start_s = s == 0 ? 0.0 : ends[s - 1];
-        b.end_s = ends[s];
-        b.capacity = cap[s];
-        b.spec_step = 0;
-        b.decode_tokens = cap[s] - fr[s];
-        b.prefill_budget = imin(fr[s], P.max_chunk);
-        for (int l = 0; l < kMaxTiers; ++l) b.per_tier[l] = l < L ? ptier[(int64_t)s * L + l] : 0;
-        b.first_owner = base_own;
-        b.n_owner = n_here;
+        GapBatchOut& bt = o.b[s];
+        bt.start_s = s == 0 ? 0.0 : ends[s - 1];
+        bt.end_s = ends[s];
+        bt.capacity = cap[s];
+        bt.spec_step = 0;
+        bt.decode_tokens = cap[s] - fr[s];
+        bt.prefill_budget = imin(fr[s], P.max_chunk);
+        for (int l = 0; l < kMaxTiers; ++l) bt.per_tier[l] = l < L ? ptier[(int64_t)s * L + l] : 0;
+        bt.first_owner = base_own;
+        bt.n_owner = n_here;
       }
       budget += imin(fr[s], P.max_chunk);
       o.n_own = base_own + n_here;

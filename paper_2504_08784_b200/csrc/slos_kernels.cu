@@ -67,7 +67,7 @@ cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s
 
 cudaError_t launch_build(const BuildParams& prm, int grid, cudaStream_t s) {
   if (grid <= 0) return cudaSuccess;
-  build_kernel<<<(grid + kBuildWarps - 1) / kBuildWarps, 32 * kBuildWarps, 0, s>>>(prm);
+  build_kernel<<<(grid + kBuildPerCta - 1) / kBuildPerCta, kBuildThreads, 0, s>>>(prm);
   return cudaGetLastError();
 }
 
