@@ -12,6 +12,7 @@ namespace slos {
 
 struct BuildParams {
   BatchArgs a;
+  size_t smem_bytes;  // dynamic shared memory per CTA (per-gap working set)
 };
 
 struct BuildShared {
@@ -182,8 +183,8 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
   int64_t* dbl = (int64_t*)ar.take(sizeof(int64_t) * (nd + 1));
   int64_t* dleft = (int64_t*)ar.take(sizeof(int64_t) * (nd + 1));
   int64_t* pleft = (int64_t*)ar.take(sizeof(int64_t) * (np + 1));
-  if (ar.used > ar.cap) {
-    if (tid == 0) { sh.err = SLOS_ERR_CAPACITY; out->need_work = 2 * ar.used; }
+  if (ar.over()) {
+    if (tid == 0) { sh.err = SLOS_ERR_CAPACITY; out->need_work = ar.need(); }
     G::sync();
     return;
   }
@@ -315,7 +316,8 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
 }
 
 template <class G>
-__device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int inst) {
+__device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int inst,
+                                      unsigned char* smem_buf, int64_t smem_cap) {
   const int tid = G::rank();
   OutHdr* out = &A.out[inst];
   if (out->status != 0) return;
@@ -332,10 +334,25 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
   const InstDev& I = sh.I;
   const PlannerDev& P = sh.P;
   const double pull = plan_predict(P, 1, 0);
+  // global work area: plan outputs of a gap; the per-gap working set goes to
+  // shared memory first (smem_buf), overflowing into the rest of the work area
+  Arena ga;
+  ga.base = A.work + I.off_work;
+  ga.cap = I.cap_work;
+  ga.used = 0;
+  ga.base2 = nullptr;
+  ga.cap2 = 0;
+  ga.used2 = 0;
+  GapBatchOut* gb = (GapBatchOut*)ga.take(sizeof(GapBatchOut) * I.cap_gb);
+  int64_t* go = (int64_t*)ga.take(sizeof(int64_t) * 2 * I.cap_go);
+  GapBatchOut* tb = (GapBatchOut*)ga.take(sizeof(GapBatchOut) * I.cap_gb);
   Arena ar;
-  ar.base = A.work + I.off_work;
-  ar.cap = I.cap_work;
+  ar.base = smem_buf;
+  ar.cap = smem_cap;
   ar.used = 0;
+  ar.base2 = ga.base + ((ga.used + 255) & ~(int64_t)255);
+  ar.cap2 = ga.cap - ((ga.used + 255) & ~(int64_t)255);
+  ar.used2 = 0;
   const int Mmax = I.n_dec + I.N + 1;
   MemBuf E;
   E.ph = (double*)ar.take(sizeof(double) * Mmax);
@@ -343,11 +360,8 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
   E.rm = (int64_t*)ar.take(sizeof(int64_t) * Mmax);
   E.tr = (int32_t*)ar.take(sizeof(int32_t) * Mmax);
   E.ow = (int32_t*)ar.take(sizeof(int32_t) * Mmax);
-  GapBatchOut* gb = (GapBatchOut*)ar.take(sizeof(GapBatchOut) * I.cap_gb);
-  int64_t* go = (int64_t*)ar.take(sizeof(int64_t) * 2 * I.cap_go);
-  GapBatchOut* tb = (GapBatchOut*)ar.take(sizeof(GapBatchOut) * I.cap_gb);
-  if (ar.used > ar.cap) {
-    if (tid == 0) { out->status = SLOS_ERR_CAPACITY; out->need_work = 2 * ar.used; }
+  if (ga.over() || ar.over()) {
+    if (tid == 0) { out->status = SLOS_ERR_CAPACITY; out->need_work = ar.need(); }
     return;
   }
   if (tid == 0) {
@@ -504,16 +518,22 @@ constexpr int kBuildThreads = SLOS_BUILD_MODE == 1 ? 128 : 256;
 constexpr int kBuildPerCta = 1;
 #endif
 
-__global__ void __launch_bounds__(kBuildThreads) build_kernel(BuildParams prm) {
+#ifndef SLOS_BUILD_MIN_BLOCKS
+#define SLOS_BUILD_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_kernel(BuildParams prm) {
   const BatchArgs& A = prm.a;
 #if SLOS_BUILD_MODE == 0
   __shared__ BuildShared shs[kBuildWarps];
+  extern __shared__ __align__(16) unsigned char bsm[];
   const int idx = blockIdx.x * kBuildWarps + warp_id();
   if (idx >= A.n_inst) return;  // whole warp; the engine never uses CTA barriers here
-  build_instance<WarpGrp>(A, shs[warp_id()], A.order[idx]);
+  const int64_t per = (int64_t)(prm.smem_bytes / kBuildWarps) & ~(int64_t)255;
+  build_instance<WarpGrp>(A, shs[warp_id()], A.order[idx], bsm + per * warp_id(), per);
 #else
   __shared__ BuildShared sh;
-  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.order[blockIdx.x]);
+  extern __shared__ __align__(16) unsigned char bsm[];
+  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.order[blockIdx.x], bsm, (int64_t)prm.smem_bytes);
 #endif
 }
 

@@ -159,16 +159,28 @@ struct WarpGrp {
   }
 };
 
-// Work-area bump allocator (global memory, per CTA).
+// Two-level bump allocator: a primary region (shared memory when the caller has
+// one) and a secondary global-memory work area for whatever does not fit. Every
+// thread of a group performs the same takes, so all agree on the placement.
 struct Arena {
-  unsigned char* base;
+  unsigned char* base;   // primary
   int64_t cap;
   int64_t used;
+  unsigned char* base2;  // secondary (global), may be null
+  int64_t cap2;
+  int64_t used2;
   __device__ void* take(int64_t bytes) {
     const int64_t o = (used + 15) & ~(int64_t)15;
-    used = o + bytes;
-    return base + o;
+    if (o + bytes <= cap || !base2) {
+      used = o + bytes;
+      return base + o;
+    }
+    const int64_t o2 = (used2 + 15) & ~(int64_t)15;
+    used2 = o2 + bytes;
+    return base2 + o2;
   }
+  __device__ bool over() const { return used > cap || (base2 && used2 > cap2); }
+  __device__ int64_t need() const { return 2 * ((base2 ? used2 : used) + 1024); }
 };
 
 // Multi-segment group due record, ordered by (time, insertion key).
@@ -274,8 +286,8 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
   // per-member due counts (late l_m, non-late), spill not needed here
   int64_t* lcount = (int64_t*)ar.take(sizeof(int64_t) * (M + 1));
   int64_t* lpre = (int64_t*)ar.take(sizeof(int64_t) * (M + 1));
-  if (ar.used > ar.cap) {
-    if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
+  if (ar.over()) {
+    if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.need(); }
     G::sync();
     return;
   }
@@ -350,8 +362,8 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
   int64_t* samt = (int64_t*)ar.take(sizeof(int64_t) * (2 * S + 2));
   int32_t* tok = (int32_t*)ar.take(sizeof(int32_t) * (int64_t)S * (M + 1));
   int64_t* ptier = (int64_t*)ar.take(sizeof(int64_t) * (int64_t)S * L);
-  if (ar.used > ar.cap) {
-    if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
+  if (ar.over()) {
+    if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.need(); }
     G::sync();
     return;
   }
@@ -490,8 +502,8 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
     int np2 = 1;
     while (np2 < nmulti) np2 <<= 1;
     MRec* rec = (MRec*)ar.take(sizeof(MRec) * np2);
-    if (ar.used > ar.cap) {
-      if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
+    if (ar.over()) {
+      if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.need(); }
       G::sync();
       return;
     }
@@ -562,8 +574,8 @@ __device__ inline void block_tile_gap_ar(const PlannerDev& P, BlockShared& sh, d
     // constant number of barriers: per-slot nonzero counts -> offsets -> scatter
     int32_t* scnt = (int32_t*)ar.take(sizeof(int32_t) * (S + 1));
     int32_t* soff = (int32_t*)ar.take(sizeof(int32_t) * (S + 1));
-    if (ar.used > ar.cap) {
-      if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
+    if (ar.over()) {
+      if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.need(); }
       G::sync();
       return;
     }
@@ -728,8 +740,8 @@ __device__ inline void block_tile_gap(const PlannerDev& P, BlockShared& sh, doub
     int64_t canon = 0;
     for (int l = 0; l < L; ++l) canon += c[l] * (int64_t)sp.lengths[l];
     int64_t* kh = (int64_t*)ar.take(sizeof(int64_t) * (full + 2));
-    if (ar.used > ar.cap) {
-      if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.used * 2; }
+    if (ar.over()) {
+      if (tid == 0) { o.status = SLOS_ERR_CAPACITY; o.need_work = ar.need(); }
       G::sync();
       return;
     }

@@ -42,6 +42,7 @@ struct DpParams {
 };
 struct BuildParams {
   BatchArgs a;
+  size_t smem_bytes;
 };
 struct GapBatchOut {
   double start_s, end_s;
@@ -837,6 +838,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   cudaEventRecord(ws.ev[1], s);
   BuildParams bp;
   bp.a = ws.A;
+  bp.smem_bytes = 44 * 1024;
   if ((e = launch_build(bp, nv, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   cudaEventRecord(ws.ev[2], s);
   return SLOS_OK;

@@ -67,7 +67,10 @@ cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s
 
 cudaError_t launch_build(const BuildParams& prm, int grid, cudaStream_t s) {
   if (grid <= 0) return cudaSuccess;
-  build_kernel<<<(grid + kBuildPerCta - 1) / kBuildPerCta, kBuildThreads, 0, s>>>(prm);
+  cudaError_t e = cudaFuncSetAttribute(build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)prm.smem_bytes);
+  if (e != cudaSuccess) return e;
+  build_kernel<<<(grid + kBuildPerCta - 1) / kBuildPerCta, kBuildThreads, prm.smem_bytes, s>>>(prm);
   return cudaGetLastError();
 }
 
