@@ -13,7 +13,17 @@ namespace slos {
 struct BuildParams {
   BatchArgs a;
   size_t smem_bytes;  // dynamic shared memory per CTA (per-gap working set)
+  unsigned long long* phase_cycles;  // 8 counters or nullptr (SLOS_PHASE_TIMING)
 };
+
+#define SLOS_BPHASE(k)                                                         \
+  do {                                                                         \
+    if (phase_cycles && G::rank() == 0) {                                      \
+      const long long now_ = clock64();                                        \
+      atomicAdd(&phase_cycles[(k)], (unsigned long long)(now_ - bph_t0_));     \
+      bph_t0_ = now_;                                                          \
+    }                                                                          \
+  } while (0)
 
 struct BuildShared {
   BlockShared bs;
@@ -317,7 +327,9 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
 
 template <class G>
 __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int inst,
-                                      unsigned char* smem_buf, int64_t smem_cap) {
+                                      unsigned char* smem_buf, int64_t smem_cap,
+                                      unsigned long long* phase_cycles) {
+  long long bph_t0_ = clock64();
   const int tid = G::rank();
   OutHdr* out = &A.out[inst];
   if (out->status != 0) return;
@@ -393,6 +405,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
       const double a = sh.bounds[k];
       const double raw = sh.bounds[k + 1] - a;
       const double len = quantize_gap(raw);
+      SLOS_BPHASE(0);  // 0: setup / previous gap bookkeeping
       int m = build_members_at<G>(A, sh, a, pull, E);
       if (tid == 0) {
         int mm = m;
@@ -402,10 +415,12 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
         sh.m1 = mm;
       }
       G::sync();
+      SLOS_BPHASE(1);  // 1: census (members_at + chain lines)
       MemBuf EE = E;
       EE.M = sh.m1;
       Arena ar2 = ar;
       block_tile_gap<G>(P, sh.bs, len, raw + pull, zero, EE, true, ar2, sh.o, sh.tmp);
+      SLOS_BPHASE(2);  // 2: tile_gap
       if (sh.o.status) {
         if (tid == 0) { out->status = sh.o.status; out->need_work = sh.o.need_work; }
         return;
@@ -416,6 +431,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
       }
       if (!sh.o.feasible) { fallback = true; break; }
       emit_gap<G>(A, sh, a, true, ar);
+      SLOS_BPHASE(3);  // 3: emission
     }
     if (!fallback) {
       if (tid == 0) {  // :294-300
@@ -470,6 +486,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
         else emit_gap<G>(A, sh, t_last, false, ar);
       }
     }
+    SLOS_BPHASE(4);  // 4: decode tail
     if (!fallback && tid == 0) {
       const slos_batch* OB = A.batches + I.off_batch;
       out->exact_until = sh.n_batch == 0 ? I.now
@@ -487,6 +504,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
     }
     G::sync();
     edf_fallback<G>(A, sh, ar, out);
+    SLOS_BPHASE(5);  // 5: fallback
     if (sh.err) {
       if (tid == 0) out->status = sh.err;
       return;
@@ -529,11 +547,11 @@ __global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_ke
   const int idx = blockIdx.x * kBuildWarps + warp_id();
   if (idx >= A.n_inst) return;  // whole warp; the engine never uses CTA barriers here
   const int64_t per = (int64_t)(prm.smem_bytes / kBuildWarps) & ~(int64_t)255;
-  build_instance<WarpGrp>(A, shs[warp_id()], A.order[idx], bsm + per * warp_id(), per);
+  build_instance<WarpGrp>(A, shs[warp_id()], A.order[idx], bsm + per * warp_id(), per, prm.phase_cycles);
 #else
   __shared__ BuildShared sh;
   extern __shared__ __align__(16) unsigned char bsm[];
-  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.order[blockIdx.x], bsm, (int64_t)prm.smem_bytes);
+  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.order[blockIdx.x], bsm, (int64_t)prm.smem_bytes, prm.phase_cycles);
 #endif
 }
 
@@ -564,6 +582,9 @@ __global__ void __launch_bounds__(kBT) gap_kernel(GapParams prm) {
   ar.base = prm.work + q.off_work;
   ar.cap = q.cap_work;
   ar.used = 0;
+  ar.base2 = nullptr;
+  ar.cap2 = 0;
+  ar.used2 = 0;
   MemBuf E;
   E.ph = const_cast<double*>(prm.ph) + q.off_exact;
   E.bl = const_cast<int64_t*>(prm.bl) + q.off_exact;

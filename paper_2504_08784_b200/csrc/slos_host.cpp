@@ -43,6 +43,7 @@ struct DpParams {
 struct BuildParams {
   BatchArgs a;
   size_t smem_bytes;
+  unsigned long long* phase_cycles;
 };
 struct GapBatchOut {
   double start_s, end_s;
@@ -839,6 +840,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   BuildParams bp;
   bp.a = ws.A;
   bp.smem_bytes = 44 * 1024;
+  bp.phase_cycles = dp.phase_cycles ? dp.phase_cycles + 10 : nullptr;
   if ((e = launch_build(bp, nv, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   cudaEventRecord(ws.ev[2], s);
   return SLOS_OK;
@@ -871,6 +873,12 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
                                     "survivors", "terminal"};
     std::fprintf(stderr, "[slos phases] total %.3e cycles:", (double)tot);
     for (int k = 0; k < 10; ++k) std::fprintf(stderr, " %s %.1f%%", names[k], 100.0 * (double)pc[k] / (double)(tot ? tot : 1));
+    std::fprintf(stderr, "\n");
+    unsigned long long bt = 0;
+    for (int k = 10; k < 16; ++k) bt += pc[k];
+    static const char* bn[6] = {"setup", "census", "tile_gap", "emit", "tail", "fallback"};
+    std::fprintf(stderr, "[slos build phases] total %.3e cycles:", (double)bt);
+    for (int k = 0; k < 6; ++k) std::fprintf(stderr, " %s %.1f%%", bn[k], 100.0 * (double)pc[10 + k] / (double)(bt ? bt : 1));
     std::fprintf(stderr, "\n");
   }
   // packed offsets
