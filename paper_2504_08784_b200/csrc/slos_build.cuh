@@ -214,6 +214,7 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
   if (tid == 0) { sh.n_batch = 0; sh.n_entry = 0; }
   G::sync();
   double t = I.now;
+  int64_t cap_t0 = -2;
   for (int guard = 0; guard < 100000; ++guard) {
     int any_d = 0, any_p = 0;
     for (int k = tid; k < nd; k += G::kSize) if (dleft[k] > 0) any_d = 1;
@@ -264,7 +265,8 @@ __device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena a
       }
       ne += carry;
       dtok = G::sum64(sh.bs, dtok);
-      cap = plan_time2bs(P, t0, 0);
+      if (cap_t0 == -2) cap_t0 = plan_time2bs(P, t0, 0);  // loop-invariant (t0 is fixed)
+      cap = cap_t0;
       if (cap < 0) {
         if (tid == 0) sh.err = SLOS_ERR_INFEASIBLE_BUDGET;
         G::sync();
@@ -330,6 +332,18 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
                                       unsigned char* smem_buf, int64_t smem_cap,
                                       unsigned long long* phase_cycles) {
   long long bph_t0_ = clock64();
+  const long long bph_start_ = bph_t0_;
+  struct EndTimer {
+    unsigned long long* pc;
+    long long t0;
+    __device__ ~EndTimer() {
+      if (pc && G::rank() == 0) {
+        const unsigned long long d = (unsigned long long)(clock64() - t0);
+        atomicMax(&pc[6], d);
+        atomicAdd(&pc[7], 1ull);
+      }
+    }
+  } end_timer_{phase_cycles, bph_start_};
   const int tid = G::rank();
   OutHdr* out = &A.out[inst];
   if (out->status != 0) return;
@@ -503,7 +517,12 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
       out->n_declined = I.n_pending;
     }
     G::sync();
-    edf_fallback<G>(A, sh, ar, out);
+    if (G::kSize > 32) {  // a sequential batch loop: one warp, shuffle scans, no CTA barriers
+      if (warp_id() == 0) edf_fallback<WarpGrp>(A, sh, ar, out);
+      G::sync();
+    } else {
+      edf_fallback<G>(A, sh, ar, out);
+    }
     SLOS_BPHASE(5);  // 5: fallback
     if (sh.err) {
       if (tid == 0) out->status = sh.err;

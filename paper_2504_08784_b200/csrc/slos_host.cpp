@@ -802,8 +802,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   if (std::getenv("SLOS_PHASE_TIMING")) {
     static unsigned long long* dev_pc = nullptr;
     if (!dev_pc) {
-      cudaMalloc(&dev_pc, 16 * sizeof(unsigned long long));
-      cudaMemset(dev_pc, 0, 16 * sizeof(unsigned long long));
+      cudaMalloc(&dev_pc, 32 * sizeof(unsigned long long));
+      cudaMemset(dev_pc, 0, 32 * sizeof(unsigned long long));
     }
     dp.phase_cycles = dev_pc;
   }
@@ -865,7 +865,7 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
   std::vector<OutHdr> hdr(hO, hO + nv);
   g_d2h += (int64_t)(sizeof(OutHdr) * (size_t)nv);
   if (ws.dp.phase_cycles) {
-    unsigned long long pc[16];
+    unsigned long long pc[32];
     cudaMemcpy(pc, ws.dp.phase_cycles, sizeof pc, cudaMemcpyDeviceToHost);
     unsigned long long tot = 0;
     for (int k = 0; k < 10; ++k) tot += pc[k];
@@ -879,7 +879,7 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
     static const char* bn[6] = {"setup", "census", "tile_gap", "emit", "tail", "fallback"};
     std::fprintf(stderr, "[slos build phases] total %.3e cycles:", (double)bt);
     for (int k = 0; k < 6; ++k) std::fprintf(stderr, " %s %.1f%%", bn[k], 100.0 * (double)pc[10 + k] / (double)(bt ? bt : 1));
-    std::fprintf(stderr, "\n");
+    std::fprintf(stderr, " | max instance %.3e cycles over %llu instances\n", (double)pc[16], pc[17]);
   }
   // packed offsets
   std::vector<int64_t> boff(nv, 0), eoff(nv, 0), ioff(nv, 0);
