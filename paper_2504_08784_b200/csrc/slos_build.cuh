@@ -182,149 +182,176 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
   return 0;
 }
 
-// edf_fallback dp_scheduler.cpp:96-188 (block-parallel over decoders/prefills).
-template <class G>
-__device__ inline void edf_fallback(const BatchArgs& A, BuildShared& sh, Arena ar, OutHdr* out) {
-  const int tid = G::rank();
+// edf_fallback dp_scheduler.cpp:96-188, on ONE warp: the batch loop is inherently
+// sequential (hundreds of batches until every line completes), so it runs without
+// CTA barriers. Lane l owns a contiguous range of decoders (and of prefills), so
+// entry order (decoder order, then EDF prefill order) is lane-major and one warp
+// scan per batch places every entry.
+__device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Arena ar, OutHdr* out) {
+  const int lane = lane_id();
   const InstDev& I = sh.I;
   const PlannerDev& P = sh.P;
   const int nd = I.n_dec, np = I.n_pre;
   double* dnext = (double*)ar.take(sizeof(double) * (nd + 1));
+  double* dtp = (double*)ar.take(sizeof(double) * (nd + 1));
   int64_t* dbl = (int64_t*)ar.take(sizeof(int64_t) * (nd + 1));
   int64_t* dleft = (int64_t*)ar.take(sizeof(int64_t) * (nd + 1));
+  int64_t* ddue = (int64_t*)ar.take(sizeof(int64_t) * (nd + 1));
+  int32_t* didx = (int32_t*)ar.take(sizeof(int32_t) * (nd + 1));
   int64_t* pleft = (int64_t*)ar.take(sizeof(int64_t) * (np + 1));
+  int32_t* pidx = (int32_t*)ar.take(sizeof(int32_t) * (np + 1));
   if (ar.over()) {
-    if (tid == 0) { sh.err = SLOS_ERR_CAPACITY; out->need_work = ar.need(); }
-    G::sync();
+    if (lane == 0) { sh.err = SLOS_ERR_CAPACITY; out->need_work = ar.need(); }
+    __syncwarp();
     return;
   }
+  const int dper = (nd + 31) / 32, d0 = min(nd, lane * dper), d1 = min(nd, d0 + dper);
+  const int pper = (np + 31) / 32, p0 = min(np, lane * pper), p1 = min(np, p0 + pper);
   double tmin = INFINITY;
-  for (int k = tid; k < nd; k += G::kSize) {
+  int act = 0;
+  for (int k = d0; k < d1; ++k) {
     const int64_t o = I.off_dec + k;
     dnext[k] = A.dec_next[o];
     dleft[k] = A.dec_rem[o];
     dbl[k] = imin(A.dec_backlog[o], A.dec_rem[o]);
-    tmin = dmin(tmin, P.tpot[A.dec_tier[o]]);
+    dtp[k] = P.tpot[A.dec_tier[o]];
+    didx[k] = A.dec_idx[o];
+    tmin = dmin(tmin, dtp[k]);
+    if (dleft[k] > 0) act = 1;
   }
-  for (int k = tid; k < np; k += G::kSize) pleft[k] = A.pre_left[I.off_pre + k];
-  const double t0 = nd > 0 ? G::min(sh.bs, tmin) : 0.0;
+  int64_t lsum = 0;  // prefill tokens still pending in this lane's range
+  for (int k = p0; k < p1; ++k) {
+    pleft[k] = A.pre_left[I.off_pre + k];
+    pidx[k] = A.pre_idx[I.off_pre + k];
+    if (pleft[k] > 0) lsum += pleft[k];
+  }
+  __syncwarp();
+  const double t0 = nd > 0 ? warp_min(tmin) : 0.0;  // :125-126
   slos_batch* OB = A.batches + I.off_batch;
   slos_entry* OE = A.entries + I.off_entry;
   const int64_t chunk_cap = P.max_chunk;
-  if (tid == 0) { sh.n_batch = 0; sh.n_entry = 0; }
-  G::sync();
+  int64_t nb = 0, ne = 0, cap_t0 = -2;
   double t = I.now;
-  int64_t cap_t0 = -2;
+  bool decodes = __any_sync(0xffffffffu, act);
+  bool prefills = __any_sync(0xffffffffu, lsum > 0);
   for (int guard = 0; guard < 100000; ++guard) {
-    int any_d = 0, any_p = 0;
-    for (int k = tid; k < nd; k += G::kSize) if (dleft[k] > 0) any_d = 1;
-    for (int k = tid; k < np; k += G::kSize) if (pleft[k] > 0) any_p = 1;
-    const int fl = G::or_(sh.bs, any_d | (any_p << 1));
-    const bool decodes = fl & 1, prefills = (fl >> 1) & 1;
     if (!prefills && !decodes) break;
-    const int64_t e0 = sh.n_entry;
-    int64_t ne = e0;
-    slos_batch b;
-    b.start_s = t;
-    b.spec_step = 0;
-    b.first_entry = e0;
-    int64_t free = 0;
-    int64_t dtok = 0, cap = 0;
-    if (decodes) {
+    const bool dec_branch = decodes;
+    const int64_t e0 = ne;
+    int64_t free, dtok = 0, cap = 0;
+    if (dec_branch) {
       const double slot_end = t + t0;
-      int64_t carry = 0;
-      for (int base = 0; base < nd; base += G::kSize) {
-        const int k = base + tid;
+      int cnt = 0, still = 0;
+      int64_t tok = 0;
+      for (int k = d0; k < d1; ++k) {
         int64_t due = 0;
-        bool emit = false;
-        if (k < nd && dleft[k] > 0) {
+        if (dleft[k] > 0) {
           due = imin(dbl[k], dleft[k]);
           dbl[k] -= due;
-          const double tpot = P.tpot[A.dec_tier[I.off_dec + k]];
           while (dleft[k] - due > 0 && time_le(dnext[k], slot_end)) {
             ++due;
-            dnext[k] += tpot;
+            dnext[k] += dtp[k];
           }
-          if (due > 0) { dleft[k] -= due; emit = true; }
-        }
-        int64_t tot;
-        const int64_t ex = G::excl(sh.bs, emit ? 1 : 0, &tot);
-        if (emit) {
-          const int64_t at = ne + carry + ex;
-          if (at < I.cap_entry) {
-            slos_entry e;
-            e.req = A.dec_idx[I.off_dec + k];
-            e.spec_len = 0;
-            e.prefill_tokens = 0;
-            e.decode_tokens = due;
-            OE[at] = e;
+          if (due > 0) {
+            dleft[k] -= due;
+            ++cnt;
+            tok += due;
           }
         }
-        carry += tot;
-        dtok += emit ? due : 0;
+        ddue[k] = due;
+        if (dleft[k] > 0) still = 1;
       }
-      ne += carry;
-      dtok = G::sum64(sh.bs, dtok);
-      if (cap_t0 == -2) cap_t0 = plan_time2bs(P, t0, 0);  // loop-invariant (t0 is fixed)
+      const int inc = warp_incl_scan(cnt);
+      int64_t pos = e0 + inc - cnt;
+      for (int k = d0; k < d1; ++k) {
+        if (ddue[k] <= 0) continue;
+        if (pos < I.cap_entry) {
+          slos_entry e;
+          e.req = didx[k];
+          e.spec_len = 0;
+          e.prefill_tokens = 0;
+          e.decode_tokens = ddue[k];
+          OE[pos] = e;
+        }
+        ++pos;
+      }
+      ne += __shfl_sync(0xffffffffu, inc, 31);
+      dtok = warp_sum(tok);
+      decodes = __any_sync(0xffffffffu, still);
+      if (cap_t0 == -2) cap_t0 = plan_time2bs(P, t0, 0);  // loop-invariant: t0 is fixed
       cap = cap_t0;
       if (cap < 0) {
-        if (tid == 0) sh.err = SLOS_ERR_INFEASIBLE_BUDGET;
-        G::sync();
+        if (lane == 0) sh.err = SLOS_ERR_INFEASIBLE_BUDGET;
+        __syncwarp();
         return;
       }
       free = imax(0, imin(cap - dtok, chunk_cap));
     } else {
       free = chunk_cap;
     }
-    // EDF prefill: take_k = min(left_k, max(0, free - sum_{k'<k} left_k'))
-    int64_t carry = 0, spent = 0;
-    for (int base = 0; base < np; base += G::kSize) {
-      const int k = base + tid;
-      const int64_t lk = (k < np && pleft[k] > 0) ? pleft[k] : 0;
-      int64_t tot;
-      const int64_t before = carry + G::excl(sh.bs, lk, &tot);
-      const int64_t take = imin(lk, imax(0, free - before));
-      int64_t t2;
-      const int64_t ex = G::excl(sh.bs, take > 0 ? 1 : 0, &t2);
-      if (take > 0) {
+    // EDF prefill in order: take_k = min(left_k, max(0, free - sum_{k'<k} left_k'))
+    int64_t spent = 0;
+    if (prefills) {
+      const int64_t before = warp_incl_scan(lsum) - lsum;
+      int cnt = 0;
+      int64_t run = before, mine = 0;
+      for (int k = p0; k < p1; ++k) {
+        const int64_t lk = pleft[k] > 0 ? pleft[k] : 0;
+        const int64_t take = imin(lk, imax(0, free - run));
+        run += lk;
+        if (take > 0) ++cnt;
+        mine += take;
+      }
+      const int inc = warp_incl_scan(cnt);
+      int64_t pos = ne + inc - cnt;
+      run = before;
+      for (int k = p0; k < p1; ++k) {
+        const int64_t lk = pleft[k] > 0 ? pleft[k] : 0;
+        const int64_t take = imin(lk, imax(0, free - run));
+        run += lk;
+        if (take <= 0) continue;
         pleft[k] -= take;
-        const int64_t at = ne + ex;
-        if (at < I.cap_entry) {
+        if (pos < I.cap_entry) {
           slos_entry e;
-          e.req = A.pre_idx[I.off_pre + k];
+          e.req = pidx[k];
           e.spec_len = 0;
           e.prefill_tokens = take;
           e.decode_tokens = 0;
-          OE[at] = e;
+          OE[pos] = e;
         }
+        ++pos;
       }
-      ne += t2;
-      spent += take;
-      carry += tot;
+      ne += __shfl_sync(0xffffffffu, inc, 31);
+      spent = warp_sum(mine);
+      lsum -= mine;
+      prefills = __any_sync(0xffffffffu, lsum > 0);
     }
-    spent = G::sum64(sh.bs, spent);
-    if (decodes) {
+    slos_batch b;
+    b.start_s = t;
+    b.spec_step = 0;
+    b.first_entry = e0;
+    b.n_entries = ne - e0;
+    if (dec_branch) {  // :138-169
       const int64_t total = dtok + spent;
       const double dur = dmax(t0, total > 0 ? plan_predict(P, total, 0) : 0.0);
       b.end_s = t + dur;
       b.capacity_tokens = imax(cap, total);
       b.prefill_budget_left = imax(0, free - spent);
-    } else {
+    } else {  // :170-182
       b.end_s = t + plan_predict(P, spent, 0);
       b.capacity_tokens = spent;
       b.prefill_budget_left = 0;
     }
-    b.n_entries = ne - e0;
-    if (tid == 0) {
-      if (sh.n_batch < I.cap_batch) OB[sh.n_batch] = b;
-      sh.n_batch++;
-      sh.n_entry = ne;
-    }
+    if (lane == 0 && nb < I.cap_batch) OB[nb] = b;
+    ++nb;
     t = b.end_s;
-    G::sync();
   }
-  if (tid == 0) out->exact_until = t;
-  G::sync();
+  if (lane == 0) {
+    sh.n_batch = nb;
+    sh.n_entry = ne;
+    out->exact_until = t;
+  }
+  __syncwarp();
 }
 
 template <class G>
@@ -336,14 +363,16 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
   struct EndTimer {
     unsigned long long* pc;
     long long t0;
+    OutHdr* o;
     __device__ ~EndTimer() {
       if (pc && G::rank() == 0) {
         const unsigned long long d = (unsigned long long)(clock64() - t0);
         atomicMax(&pc[6], d);
         atomicAdd(&pc[7], 1ull);
+        o->dbg_cycles = (int64_t)d;
       }
     }
-  } end_timer_{phase_cycles, bph_start_};
+  } end_timer_{phase_cycles, bph_start_, &A.out[inst]};
   const int tid = G::rank();
   OutHdr* out = &A.out[inst];
   if (out->status != 0) return;
@@ -517,12 +546,8 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
       out->n_declined = I.n_pending;
     }
     G::sync();
-    if (G::kSize > 32) {  // a sequential batch loop: one warp, shuffle scans, no CTA barriers
-      if (warp_id() == 0) edf_fallback<WarpGrp>(A, sh, ar, out);
-      G::sync();
-    } else {
-      edf_fallback<G>(A, sh, ar, out);
-    }
+    if (warp_id() == 0 || G::kSize == 32) warp_edf_fallback(A, sh, ar, out);
+    G::sync();
     SLOS_BPHASE(5);  // 5: fallback
     if (sh.err) {
       if (tid == 0) out->status = sh.err;

@@ -880,6 +880,15 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
     std::fprintf(stderr, "[slos build phases] total %.3e cycles:", (double)bt);
     for (int k = 0; k < 6; ++k) std::fprintf(stderr, " %s %.1f%%", bn[k], 100.0 * (double)pc[10 + k] / (double)(bt ? bt : 1));
     std::fprintf(stderr, " | max instance %.3e cycles over %llu instances\n", (double)pc[16], pc[17]);
+    std::vector<int> idx(nv);
+    for (int v = 0; v < nv; ++v) idx[v] = v;
+    std::sort(idx.begin(), idx.end(), [&](int x, int y) { return hdr[x].dbg_cycles > hdr[y].dbg_cycles; });
+    for (int r = 0; r < std::min(nv, 6); ++r) {
+      const OutHdr& h = hdr[idx[r]];
+      std::fprintf(stderr, "  slow build #%d: job %d cycles %.3e batches %lld entries %lld infeasible %d admitted %d T %lld\n", r,
+                   jobs[valid[idx[r]]].k, (double)h.dbg_cycles, (long long)h.n_batches, (long long)h.n_entries,
+                   h.infeasible, h.n_admitted, (long long)h.ctr[0]);
+    }
   }
   // packed offsets
   std::vector<int64_t> boff(nv, 0), eoff(nv, 0), ioff(nv, 0);
