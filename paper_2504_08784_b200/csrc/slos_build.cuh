@@ -591,11 +591,11 @@ __global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_ke
   const int idx = blockIdx.x * kBuildWarps + warp_id();
   if (idx >= A.n_inst) return;  // whole warp; the engine never uses CTA barriers here
   const int64_t per = (int64_t)(prm.smem_bytes / kBuildWarps) & ~(int64_t)255;
-  build_instance<WarpGrp>(A, shs[warp_id()], A.order[idx], bsm + per * warp_id(), per, prm.phase_cycles);
+  build_instance<WarpGrp>(A, shs[warp_id()], A.bq[2 + idx], bsm + per * warp_id(), per, prm.phase_cycles);
 #else
   __shared__ BuildShared sh;
   extern __shared__ __align__(16) unsigned char bsm[];
-  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.order[blockIdx.x], bsm, (int64_t)prm.smem_bytes, prm.phase_cycles);
+  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.bq[2 + blockIdx.x], bsm, (int64_t)prm.smem_bytes, prm.phase_cycles);
 #endif
 }
 

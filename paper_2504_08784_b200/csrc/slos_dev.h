@@ -160,6 +160,7 @@ struct BatchArgs {
   slos_entry* entries;
   unsigned char* work;
   unsigned char* anchors;
+  int32_t* bq;       // build queue: fallback instances first (n_inst + 2 ints; [0],[1] = counters)
   OutHdr* out;
 };
 

@@ -975,7 +975,10 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   }
   __syncthreads();
   if (s_err) {
-    if (tid == 0) out->status = s_err;
+    if (tid == 0) {
+      out->status = s_err;
+      A.bq[2 + A.n_inst - 1 - atomicAdd(&A.bq[1], 1)] = inst;
+    }
     return;
   }
   // ---- terminal selection (dp_scheduler.cpp:504-522) ----
@@ -1093,6 +1096,10 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       out->value = value;
     }
     out->status = 0;
+    // plan-reconstruction queue: instances that fall back (a long sequential batch
+    // loop) are queued from the front, the rest from the back
+    if (best < 0) A.bq[2 + atomicAdd(&A.bq[0], 1)] = inst;
+    else A.bq[2 + A.n_inst - 1 - atomicAdd(&A.bq[1], 1)] = inst;
   }
   SLOS_PHASE(9);  // 9: terminal selection + backtrack
 }

@@ -423,7 +423,7 @@ struct Layout {
   size_t in_bytes;
   size_t s_counts, s_mem, s_pb, s_value, s_nadm, s_parent, s_arena, s_level;
   size_t c_src, c_j, c_memo, c_flag, c_bucket, c_pos, c_aux, c_counts, c_mem, c_pb, c_value, c_nadm;
-  size_t c_bkey, c_bval, memo, work, anchors, scr_bytes;
+  size_t c_bkey, c_bval, memo, bq, work, anchors, scr_bytes;
   size_t memo_bytes, bkey_bytes, bval_bytes;
   size_t out, sel, ids, batches, entries, out_bytes;
 };
@@ -561,6 +561,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.c_bkey = bs.add<uint64_t>(2 * TCd);
   Ly.c_bval = bs.add<int32_t>(2 * TCd);
   Ly.memo = bs.add<MemoEnt>(TM);
+  Ly.bq = bs.add<int32_t>(nv + 2);
   Ly.work = bs.add<unsigned char>(TW);
   Ly.anchors = bs.add<unsigned char>(TA);
   Ly.scr_bytes = bs.bytes;
@@ -770,6 +771,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   A.memo = (MemoEnt*)(DS + Ly.memo);
   A.work = DS + Ly.work;
   A.anchors = DS + Ly.anchors;
+  A.bq = (int32_t*)(DS + Ly.bq);
   A.out = (OutHdr*)(DO + Ly.out);
   A.sel = (int32_t*)(DO + Ly.sel);
   A.ids = (int32_t*)(DO + Ly.ids);
@@ -831,6 +833,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   cudaMemsetAsync(DS + Ly.c_bkey, 0, Ly.bkey_bytes, s);
   cudaMemsetAsync(DS + Ly.c_bval, 0xFF, Ly.bval_bytes, s);
   cudaMemsetAsync(DO + Ly.out, 0, sizeof(OutHdr) * nv, s);
+  cudaMemsetAsync(DS + Ly.bq, 0, 2 * sizeof(int32_t), s);
   cudaError_t e;
   for (int k = 0; k < 3; ++k)
     if (!ws.ev[k]) cudaEventCreate(&ws.ev[k]);
