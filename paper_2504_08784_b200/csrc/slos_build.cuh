@@ -182,13 +182,15 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
   return 0;
 }
 
-// edf_fallback dp_scheduler.cpp:96-188, on ONE warp: the batch loop is inherently
-// sequential (hundreds of batches until every line completes), so it runs without
-// CTA barriers. Lane l owns a contiguous range of decoders (and of prefills), so
-// entry order (decoder order, then EDF prefill order) is lane-major and one warp
-// scan per batch places every entry.
-__device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Arena ar, OutHdr* out) {
-  const int lane = lane_id();
+// edf_fallback dp_scheduler.cpp:96-188. The batch loop is inherently sequential
+// (hundreds of batches until every line completes); inside a batch every thread of
+// the group owns a contiguous range of decoders (and of prefills), so entry order
+// (decoder order, then EDF prefill order) is rank-major and one group scan per batch
+// places every entry.
+template <class G>
+__device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, Arena ar, OutHdr* out) {
+  const int lane = G::rank();
+  constexpr int NT = G::kSize;
   const InstDev& I = sh.I;
   const PlannerDev& P = sh.P;
   const int nd = I.n_dec, np = I.n_pre;
@@ -202,11 +204,11 @@ __device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Ar
   int32_t* pidx = (int32_t*)ar.take(sizeof(int32_t) * (np + 1));
   if (ar.over()) {
     if (lane == 0) { sh.err = SLOS_ERR_CAPACITY; out->need_work = ar.need(); }
-    __syncwarp();
+    G::sync();
     return;
   }
-  const int dper = (nd + 31) / 32, d0 = min(nd, lane * dper), d1 = min(nd, d0 + dper);
-  const int pper = (np + 31) / 32, p0 = min(np, lane * pper), p1 = min(np, p0 + pper);
+  const int dper = (nd + NT - 1) / NT, d0 = min(nd, lane * dper), d1 = min(nd, d0 + dper);
+  const int pper = (np + NT - 1) / NT, p0 = min(np, lane * pper), p1 = min(np, p0 + pper);
   double tmin = INFINITY;
   int act = 0;
   for (int k = d0; k < d1; ++k) {
@@ -225,15 +227,15 @@ __device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Ar
     pidx[k] = A.pre_idx[I.off_pre + k];
     if (pleft[k] > 0) lsum += pleft[k];
   }
-  __syncwarp();
-  const double t0 = nd > 0 ? warp_min(tmin) : 0.0;  // :125-126
+  G::sync();
+  const double t0 = nd > 0 ? G::min(sh.bs, tmin) : 0.0;  // :125-126
   slos_batch* OB = A.batches + I.off_batch;
   slos_entry* OE = A.entries + I.off_entry;
   const int64_t chunk_cap = P.max_chunk;
   int64_t nb = 0, ne = 0, cap_t0 = -2;
   double t = I.now;
-  bool decodes = __any_sync(0xffffffffu, act);
-  bool prefills = __any_sync(0xffffffffu, lsum > 0);
+  bool decodes = G::or_(sh.bs, act) != 0;
+  bool prefills = G::or_(sh.bs, lsum > 0 ? 1 : 0) != 0;
   for (int guard = 0; guard < 100000; ++guard) {
     if (!prefills && !decodes) break;
     const bool dec_branch = decodes;
@@ -261,8 +263,10 @@ __device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Ar
         ddue[k] = due;
         if (dleft[k] > 0) still = 1;
       }
-      const int inc = warp_incl_scan(cnt);
-      int64_t pos = e0 + inc - cnt;
+      // one scan: entry counts in the low 32 bits, "still decoding" in the high bits
+      int64_t tot;
+      const int64_t ex = G::excl(sh.bs, (int64_t)cnt | ((int64_t)still << 32), &tot);
+      int64_t pos = e0 + (ex & 0xffffffffLL);
       for (int k = d0; k < d1; ++k) {
         if (ddue[k] <= 0) continue;
         if (pos < I.cap_entry) {
@@ -275,14 +279,14 @@ __device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Ar
         }
         ++pos;
       }
-      ne += __shfl_sync(0xffffffffu, inc, 31);
-      dtok = warp_sum(tok);
-      decodes = __any_sync(0xffffffffu, still);
+      ne += tot & 0xffffffffLL;
+      dtok = G::sum64(sh.bs, tok);
+      decodes = (tot >> 32) != 0;
       if (cap_t0 == -2) cap_t0 = plan_time2bs(P, t0, 0);  // loop-invariant: t0 is fixed
       cap = cap_t0;
       if (cap < 0) {
         if (lane == 0) sh.err = SLOS_ERR_INFEASIBLE_BUDGET;
-        __syncwarp();
+        G::sync();
         return;
       }
       free = imax(0, imin(cap - dtok, chunk_cap));
@@ -292,7 +296,8 @@ __device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Ar
     // EDF prefill in order: take_k = min(left_k, max(0, free - sum_{k'<k} left_k'))
     int64_t spent = 0;
     if (prefills) {
-      const int64_t before = warp_incl_scan(lsum) - lsum;
+      int64_t tot0;
+      const int64_t before = G::excl(sh.bs, lsum, &tot0);
       int cnt = 0;
       int64_t run = before, mine = 0;
       for (int k = p0; k < p1; ++k) {
@@ -302,8 +307,9 @@ __device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Ar
         if (take > 0) ++cnt;
         mine += take;
       }
-      const int inc = warp_incl_scan(cnt);
-      int64_t pos = ne + inc - cnt;
+      int64_t totc;
+      const int64_t exc = G::excl(sh.bs, cnt, &totc);
+      int64_t pos = ne + exc;
       run = before;
       for (int k = p0; k < p1; ++k) {
         const int64_t lk = pleft[k] > 0 ? pleft[k] : 0;
@@ -321,10 +327,10 @@ __device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Ar
         }
         ++pos;
       }
-      ne += __shfl_sync(0xffffffffu, inc, 31);
-      spent = warp_sum(mine);
+      ne += totc;
+      spent = G::sum64(sh.bs, mine);
       lsum -= mine;
-      prefills = __any_sync(0xffffffffu, lsum > 0);
+      prefills = G::or_(sh.bs, lsum > 0 ? 1 : 0) != 0;
     }
     slos_batch b;
     b.start_s = t;
@@ -351,7 +357,7 @@ __device__ inline void warp_edf_fallback(const BatchArgs& A, BuildShared& sh, Ar
     sh.n_entry = ne;
     out->exact_until = t;
   }
-  __syncwarp();
+  G::sync();
 }
 
 template <class G>
@@ -546,8 +552,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
       out->n_declined = I.n_pending;
     }
     G::sync();
-    if (warp_id() == 0 || G::kSize == 32) warp_edf_fallback(A, sh, ar, out);
-    G::sync();
+    group_edf_fallback<G>(A, sh, ar, out);
     SLOS_BPHASE(5);  // 5: fallback
     if (sh.err) {
       if (tid == 0) out->status = sh.err;
