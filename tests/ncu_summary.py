@@ -1,0 +1,116 @@
+"""Distil ncu captures (gpurun_out/*.ncu-rep + launches.csv) into profiles/.
+
+  python tests/ncu_summary.py <tag>     -> profiles/<tag>_ncu_summary.{json,md}
+                                           and profiles/ncu_summary.json (read by bench.py)
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+METRICS = [
+    "gpu__time_duration.sum",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "lts__t_bytes.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum",
+    "launch__registers_per_thread",
+    "launch__occupancy_limit_registers",
+    "launch__occupancy_limit_shared_mem",
+    "launch__grid_size",
+    "launch__block_size",
+    "sm__cycles_elapsed.avg.per_second",
+    "smsp__average_warp_latency_issue_stalled_barrier",
+]
+
+
+def raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d = {}
+    for i, n in enumerate(hdr):
+        if n in METRICS:
+            d[n] = {"value": vals[i], "unit": units[i]}
+    return d
+
+
+def to_bytes(m):
+    v = float(m["value"].replace(",", ""))
+    u = m["unit"].lower()
+    return v * {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(u, 1)
+
+
+def launches(path):
+    rows = []
+    with open(path) as f:
+        lines = [l for l in f if l.startswith('"')]
+    rd = csv.reader(io.StringIO("".join(lines)))
+    hdr = next(rd)
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    for r in rd:
+        v = float(r[vi].replace(",", ""))
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
+        rows.append((r[ki].split("(")[0], v * scale))
+    return rows
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "latest"
+    summ = {"tag": tag, "kernels": {}}
+    for name, rep in (("dp_kernel", "prof_dp.ncu-rep"), ("build_kernel", "prof_build.ncu-rep")):
+        p = os.path.join(OUT, rep)
+        if os.path.exists(p):
+            m = raw(p)
+            summ["kernels"][name] = {k: v["value"] + " " + v["unit"] for k, v in m.items()}
+            if "dram__bytes_read.sum" in m:
+                summ["kernels"][name]["dram_bytes_per_launch"] = to_bytes(m["dram__bytes_read.sum"]) + \
+                    to_bytes(m["dram__bytes_write.sum"])
+    lp = os.path.join(OUT, "launches.csv")
+    if os.path.exists(lp):
+        rows = launches(lp)
+        agg = {}
+        for k, us in rows:
+            a = agg.setdefault(k, [0, 0.0])
+            a[0] += 1
+            a[1] += us
+        tot = sum(a[1] for a in agg.values())
+        summ["launch_list"] = {k: {"launches": a[0], "total_us": round(a[1], 1),
+                                   "share": round(a[1] / tot, 4)} for k, a in agg.items()}
+    os.makedirs(PROF, exist_ok=True)
+    with open(os.path.join(PROF, f"{tag}_ncu_summary.json"), "w") as f:
+        json.dump(summ, f, indent=1)
+    dp = summ["kernels"].get("dp_kernel", {})
+    with open(os.path.join(PROF, "ncu_summary.json"), "w") as f:
+        json.dump({"kernel": "dp_kernel", "instances": 1024,
+                   "dram_bytes_per_launch": dp.get("dram_bytes_per_launch"), "source": f"{tag}_ncu_summary.json"},
+                  f, indent=1)
+    lines = [f"# ncu summary ({tag})", ""]
+    for k, d in summ["kernels"].items():
+        lines.append(f"## {k}")
+        for m in METRICS + ["dram_bytes_per_launch"]:
+            if m in d:
+                lines.append(f"- `{m}`: {d[m]}")
+        lines.append("")
+    if "launch_list" in summ:
+        lines.append("## launch list (ncu --metrics gpu__time_duration.sum, cold, serialised)")
+        for k, a in sorted(summ["launch_list"].items(), key=lambda kv: -kv[1]["total_us"]):
+            lines.append(f"- {k}: {a['launches']} launches, {a['total_us']} us total, share {a['share']:.1%}")
+    with open(os.path.join(PROF, f"{tag}_ncu_summary.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
