@@ -26,7 +26,7 @@
 namespace slos {
 
 constexpr int kDpThreads = 256;
-constexpr int kNumPhases = 10;
+constexpr int kNumPhases = 12;
 
 // Optional per-phase cycle accounting (DpParams.phase_cycles != nullptr): thread 0
 // reads clock64() at block-synchronous phase boundaries.
@@ -406,6 +406,211 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
   (void)s_red;
 }
 
+// Anchor due pass (replaces the per-group member walks of E2): every exact member's
+// due line from anchor a is walked ONCE, up to the longest due horizon of any group
+// (j, i) this anchor opens, exactly as member_dues_warp walks it (same repeated
+// additions, the same jit on the strictly increasing anchor grid). Dues land in a
+// per-grid-cell histogram; a group's slots below Sp_i-1 are exactly those cells.
+// Only the dues in a group's TAIL cells (>= Sp_i-1, up to its horizon) depend on i
+// (slot Sp_i-1 vs the appended slot, inclusion, spill), so each due also visits the
+// few groups whose tail covers its cell and accumulates their GroupTail.
+// Runs only when the anchor grid is usable (grid_ok) and no member has a negative
+// backlog (tile_gap's second spill scan); otherwise the groups fall back to E2.
+__device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, const AnchorView& av,
+                                         int j, int N, const double* ch_dl, const int32_t* ch_fl,
+                                         double a, double pull, double min_slot, int Sc,
+                                         unsigned char* scr, size_t scr_bytes) {
+  const int tid = threadIdx.x;
+  AnchorFacts* F = av.f;
+  __shared__ int s_ok, s_nl;
+  __shared__ unsigned long long s_lx;
+  __shared__ double s_hmax;
+  const int Kg = F->Kg;
+  const int nG = N - j - 1;  // chain items i = j+1 .. N-1 (group index i-j-1)
+  // scratch carve (overlay area, free at this point of the level)
+  unsigned char* p = scr;
+  double* sge = (double*)p; p += 8 * (size_t)Kg;
+  double* g_gap = (double*)p; p += 8 * (size_t)nG;
+  double* g_hor = (double*)p; p += 8 * (size_t)nG;
+  int32_t* g_Sp = (int32_t*)p; p += 4 * (size_t)nG;
+  int32_t* g_lo = (int32_t*)p; p += 4 * (size_t)nG;
+  int32_t* g_hi = (int32_t*)p; p += 4 * (size_t)nG;
+  int32_t* g_acc = (int32_t*)p; p += 4 * 5 * (size_t)nG;  // tA, tB, td, fail, spill
+  int32_t* sHc = (int32_t*)p; p += 4 * (size_t)(Kg + 1);
+  int32_t* l_off = (int32_t*)p; p += 4 * (size_t)(Kg + 2);
+  const size_t used = (size_t)(p - scr);
+  const int lcap = used < scr_bytes ? (int)((scr_bytes - used) / 4) : 0;
+  int32_t* l_item = (int32_t*)p;
+  if (tid == 0) {
+    s_ok = (F->grid_ok && F->exact_mask && Kg > 0 && nG > 0 && used <= scr_bytes) ? 1 : 0;
+    s_lx = 0;
+    s_nl = 0;
+    s_hmax = 0.0;
+  }
+  __syncthreads();
+  if (!s_ok) {
+    if (tid == 0) F->dues_ok = 0;
+    return;
+  }
+  for (int k = tid; k < Kg; k += kDpThreads) sge[k] = av.ge[k];
+  for (int k = tid; k <= Kg; k += kDpThreads) sHc[k] = 0;
+  for (int k = tid; k < 5 * nG; k += kDpThreads) g_acc[k] = 0;
+  int neg = 0;
+  for (int k = tid; k < D.n; k += kDpThreads)
+    if (av.rm[k] > 0 && av.bl[k] < 0) neg = 1;
+  __syncthreads();
+  // per group: gap, horizon, Sp, tail cell range [lo, hi] (cells -1 .. Kg-1)
+  double hloc = 0.0;
+  for (int gi = tid; gi < nG; gi += kDpThreads) {
+    const int i = j + 1 + gi;
+    if (ch_fl[i] > j) {  // (j, i) is never a DP transition
+      g_lo[gi] = 1; g_hi[gi] = 0; g_Sp[gi] = 0; g_gap[gi] = 0.0; g_hor[gi] = 0.0;
+      continue;
+    }
+    const double raw = dmax(0.0, ch_dl[i] - a);
+    const double gap = quantize_gap(raw);
+    const double hor = dmax(gap, raw + pull);
+    int lo = 0, hi = Kg;
+    while (lo < hi) {
+      const int mid = (lo + hi) / 2;
+      if (time_le(sge[mid], gap)) lo = mid + 1; else hi = mid;
+    }
+    const int Sp = lo;
+    // last cell whose start can be <= a due within the horizon (superset; every tail
+    // due is tested exactly below)
+    int c_hi = -1;
+    {
+      int l2 = 0, h2 = Kg;
+      const double lim = hor + 3e-9;
+      while (l2 < h2) {
+        const int mid = (l2 + h2) / 2;
+        if (sge[mid] <= lim) l2 = mid + 1; else h2 = mid;
+      }
+      c_hi = l2 - 1;
+    }
+    g_gap[gi] = gap;
+    g_hor[gi] = hor;
+    g_Sp[gi] = Sp;
+    g_lo[gi] = Sp - 1;
+    g_hi[gi] = c_hi < Sp - 1 ? Sp - 1 : c_hi;
+    hloc = dmax(hloc, hor);
+  }
+  for (int o = 16; o; o >>= 1) hloc = dmax(hloc, __shfl_xor_sync(0xffffffffu, hloc, o));
+  neg = warp_or(neg);
+  if (lane_id() == 0) {
+    if (neg) atomicExch(&s_ok, 0);
+    // non-negative doubles order like their bit patterns
+    atomicMax((unsigned long long*)&s_hmax, (unsigned long long)__double_as_longlong(hloc));
+  }
+  __syncthreads();
+  if (!s_ok) {
+    if (tid == 0) F->dues_ok = 0;
+    return;
+  }
+  // per-cell group lists (cell y = c+1): counts, exclusive offsets, items
+  for (int y = tid; y <= Kg; y += kDpThreads) {
+    int n = 0;
+    for (int gi = 0; gi < nG; ++gi) n += (g_lo[gi] <= y - 1 && y - 1 <= g_hi[gi]) ? 1 : 0;
+    l_off[y + 1] = n;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    l_off[0] = 0;
+    int acc = 0;
+    for (int y = 0; y <= Kg; ++y) { const int n = l_off[y + 1]; l_off[y + 1] = acc + n; acc += n; }
+    s_nl = acc;
+    if (acc > lcap) s_ok = 0;
+  }
+  __syncthreads();
+  if (!s_ok) {
+    if (tid == 0) F->dues_ok = 0;
+    return;
+  }
+  for (int y = tid; y <= Kg; y += kDpThreads) {
+    int pos = l_off[y];
+    for (int gi = 0; gi < nG; ++gi)
+      if (g_lo[gi] <= y - 1 && y - 1 <= g_hi[gi]) l_item[pos++] = gi;
+  }
+  __syncthreads();
+  const double hmax = s_hmax;
+  // the walk: lanes over members in lockstep (one due per lane per round)
+  unsigned long long lx = 0;
+  for (int base = 0; base < D.n; base += kDpThreads) {
+    const int k = base + tid;
+    int64_t rem = 0, issued = 0;
+    double d = 0.0, tpot = 0.0;
+    bool act = false;
+    if (k < D.n) {
+      rem = av.rm[k];
+      act = rem > 0;
+      if (act) {
+        const int64_t bl = av.bl[k];
+        issued = bl > 0 ? imin(bl, rem) : 0;
+        lx += (unsigned long long)issued;
+        tpot = P.tpot[D.tier[k]];
+        d = dmax(av.ph[k], 0.0);
+      }
+    }
+    int cell = -2;  // grid cell of the previous due (-1: before e_0); -2: none yet
+    for (;;) {
+      act = act && time_le(d, hmax) && issued < rem;
+      if (!__any_sync(0xffffffffu, act)) break;
+      int y = -1;
+      if (act) {
+        if (d <= kTimeEps) {
+          ++lx;
+        } else {
+          if (cell == -2) cell = jit_search(sge, Kg, d);
+          else while (cell + 1 < Kg && time_le(sge[cell + 1], d)) ++cell;
+          y = cell + 1;
+          for (int q = l_off[y]; q < l_off[y + 1]; ++q) {
+            const int gi = l_item[q];
+            if (!time_le(d, g_hor[gi])) continue;
+            const double gap = g_gap[gi];
+            const int Sp = g_Sp[gi];
+            int32_t* acc = g_acc + 5 * gi;
+            atomicAdd(&acc[2], 1);
+            if (!time_le(d, gap)) acc[4] = 1;
+            // slot: Sp-1 (Sp >= 1), or the appended slot when time_le(gap, d)
+            bool app;
+            if (Sp == 0) app = time_le(min_slot, gap);
+            else app = (gap - sge[Sp - 1] >= min_slot - kTimeEps);
+            if (app && time_le(gap, d)) atomicAdd(&acc[1], 1);
+            else if (Sp >= 1) atomicAdd(&acc[0], 1);
+            else acc[3] = 1;
+          }
+        }
+        d += tpot;
+        ++issued;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, y);
+      if (y >= 0 && lane_id() == __ffs(peers) - 1) atomicAdd(&sHc[y], __popc(peers));
+    }
+  }
+  lx = warp_sum(lx);
+  if (lane_id() == 0 && lx) atomicAdd(&s_lx, lx);
+  __syncthreads();
+  // publish: cumulative histogram, per-group tails, facts
+  if (tid == 0) {
+    int acc = 0;
+    av.hcum[0] = 0;
+    for (int y = 0; y <= Kg; ++y) { acc += sHc[y]; av.hcum[y + 1] = acc; }
+    F->Lx = (int64_t)s_lx;
+    F->dues_ok = 1;
+  }
+  for (int gi = tid; gi < nG; gi += kDpThreads) {
+    GroupTail t;
+    t.tA = g_acc[5 * gi + 0];
+    t.tB = g_acc[5 * gi + 1];
+    t.td = g_acc[5 * gi + 2];
+    t.fail = (int16_t)(g_acc[5 * gi + 3] ? 1 : 0);
+    t.spill = (int16_t)(g_acc[5 * gi + 4] ? 1 : 0);
+    av.gt[j + 1 + gi] = t;
+  }
+  __syncthreads();
+  (void)Sc;
+}
+
 #ifndef SLOS_DP_MIN_BLOCKS
 #define SLOS_DP_MIN_BLOCKS 3
 #endif
@@ -420,7 +625,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   __shared__ int32_t s_joff[SLOS_MAX_CHAIN + 2];
   __shared__ int64_t s_wsum[kDpWarps + 1];
   __shared__ unsigned long long s_ctr[5];
-  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_ng;
+  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_ng, s_e2, s_nw;
   __shared__ int32_t s_glist[SLOS_MAX_CHAIN + 2];
   __shared__ int64_t s_next_free, s_arena_next;
 
@@ -606,6 +811,9 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       const AnchorView av = anchor_view(anc_base + (size_t)(j + 1) * I.anchor_stride, D.n, prm.Sc, L);
       block_build_anchor(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), prm.Sc, ctime,
                          ccnt, min_slot, s_wsum);
+      SLOS_PHASE(1);  // 1: anchor cache (members, grid, capacities)
+      block_anchor_dues(P, D, av, j, N, ch_dl, ch_fl, a, pull, min_slot, prm.Sc, ovl, prm.overlay_bytes);
+      SLOS_PHASE(2);  // 2: anchor due pass
     }
     // ---- 1+2: candidates and memo keys ----
     for (int c = tid; c < T; c += kDpThreads) {
@@ -639,7 +847,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       break;
     }
     const int n_new = s_n_new;
-    SLOS_PHASE(1);  // 1: candidate enumeration + memo find-or-insert
+    SLOS_PHASE(3);  // 3: candidate enumeration + memo find-or-insert
     // ---- 3: group new keys by anchor j and evaluate ----
     for (int k = tid; k <= nlev; k += kDpThreads) s_jcnt[k] = 0;
     __syncthreads();
@@ -662,6 +870,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     }
     __syncthreads();
     if (tid == 0) {  // anchors with at least one new key, ascending
+      s_e2 = 0;
       int ng = 0;
       for (int k = 0; k < nlev; ++k) if (s_jcnt[k] > 0) s_glist[ng++] = k;
       s_ng = ng;
@@ -669,9 +878,10 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     __syncthreads();
     const int ng = s_ng;
     const int nch = (D.n + 31) / 32;
-    SLOS_PHASE(2);  // 2: key grouping
+    SLOS_PHASE(4);  // 4: key grouping
     for (int w0 = 0; w0 < ng && !s_err; w0 += prm.Gmax) {
       const int gw = min(prm.Gmax, ng - w0);
+      if (tid == 0) s_nw = 0;  // read only after the E1 barrier below
       // E1: group setup, one warp per anchor group
       for (int gi = warp_id(); gi < gw; gi += kDpWarps) {
         const int k = s_glist[w0 + gi];
@@ -690,16 +900,21 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         Variant v;
         const GroupVar ga = group_var_carve(gvbase + (size_t)gi * prm.gstride, prm.Sc, L);
         const AnchorView av = anchor_view(anc_base + (size_t)(j + 1) * I.anchor_stride, D.n, prm.Sc, L);
-        warp_group_from_anchor(P, av, g, v, ga, prm.Sc, min_slot, ctime, ccnt);
-        if (lane_id() == 0) { H.g = g; H.v = v; H.j = j; }
+        warp_group_from_anchor(P, av, g, v, ga, prm.Sc, min_slot, ctime, ccnt, i);
+        if (lane_id() == 0) {
+          H.g = g; H.v = v; H.j = j;
+          if (v.valid && v.S <= prm.Sc && !v.dues_done) s_e2 = 1;
+        }
       }
       __syncthreads();
-      SLOS_PHASE(3);  // 3: E1 group setup
-      // E2: member-chunk histogram tasks (group, 32 members), lanes in lockstep
+      SLOS_PHASE(5);  // 5: E1 group setup
+      // E2 (fallback when the anchor due pass did not run): member-chunk histogram
+      // tasks (group, 32 members), lanes in lockstep
+      if (s_e2) {
       for (int t = warp_id(); t < gw * nch; t += kDpWarps) {
         const int gi = t / nch;
         GroupHdr& H = ghdr[gi];
-        if (!H.v.valid || H.v.S > prm.Sc) continue;
+        if (!H.v.valid || H.v.S > prm.Sc || H.v.dues_done) continue;
         const GroupVar ga = group_var_carve(gvbase + (size_t)gi * prm.gstride, prm.Sc, L);
         const int k = (t % nch) * 32 + lane_id();
         int64_t late = 0, dues = 0;
@@ -727,15 +942,58 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         }
       }
       __syncthreads();
-      SLOS_PHASE(4);  // 4: E2 member histograms
-      // E3: one warp per memo key of this wave
+      }
+      SLOS_PHASE(6);  // 6: E2 member histograms
+      // E3a: lanes over the memo keys of this wave (thread_eval_counts); keys that
+      // need a private variant or the speculative branch are queued for E3b
       {
         const int kfirst = s_glist[w0], klast = s_glist[w0 + gw - 1];
         const int q0 = s_joff[kfirst], q1 = s_joff[klast] + s_jcnt[klast];
-        unsigned long long wd = 0, wsl = 0;
-        for (int q = q0 + warp_id(); q < q1; q += kDpWarps) {
-          if (s_err) break;
+        unsigned long long td = 0, tsl = 0;
+        for (int q = q0 + tid; q < q1; q += kDpThreads) {
           int lo = 0, hi = gw - 1;  // group of key q: last gi with s_joff[glist[w0+gi]] <= q
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (s_joff[s_glist[w0 + mid]] <= q) lo = mid; else hi = mid - 1;
+          }
+          const GroupHdr& H = ghdr[lo];
+          const GroupVar ga = group_var_carve(gvbase + (size_t)lo * prm.gstride, prm.Sc, L);
+          MemoEnt* e = &Memo[G[q]];
+          const uint64_t cw = e->k2;
+          int64_t cv[kMaxTiers];
+#pragma unroll
+          for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
+          EvalOut r;
+          if (thread_eval_counts(P, H.g, H.v, ga, prm.Sc, cv, min_slot, r)) {
+            Cj[atomicAdd(&s_nw, 1)] = q;
+            continue;
+          }
+          td += (unsigned long long)r.dues;
+          tsl += (unsigned long long)r.slots;
+          if (r.status) {
+            atomicCAS(&s_err, 0, r.status);
+            if (r.status == SLOS_ERR_CAPACITY) out->need_work = 2 * prm.Sc;
+            continue;
+          }
+          e->has = r.has ? 1 : 0;
+          e->val = r.budget;
+        }
+        td = warp_sum(td);
+        tsl = warp_sum(tsl);
+        if (lane_id() == 0 && (td | tsl)) {
+          atomicAdd(&s_ctr[2], td);
+          atomicAdd(&s_ctr[3], tsl);
+        }
+      }
+      __syncthreads();
+      // E3b: one warp per queued key
+      {
+        const int nw = s_nw;
+        unsigned long long wd = 0, wsl = 0;
+        for (int x = warp_id(); x < nw; x += kDpWarps) {
+          if (s_err) break;
+          const int q = Cj[x];
+          int lo = 0, hi = gw - 1;
           while (lo < hi) {
             const int mid = (lo + hi + 1) / 2;
             if (s_joff[s_glist[w0 + mid]] <= q) lo = mid; else hi = mid - 1;
@@ -763,14 +1021,15 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
             e->val = r.budget;
           }
         }
-        if (lane_id() == 0) {
+        if (lane_id() == 0 && (wd | wsl)) {
           atomicAdd(&s_ctr[2], wd);
           atomicAdd(&s_ctr[3], wsl);
         }
+        if (tid == 0) s_e2 = 0;  // next wave (read by E2 before the barriers above)
       }
       __syncthreads();
     }
-    SLOS_PHASE(5);  // 5: E3 placements
+    SLOS_PHASE(7);  // 7: E3 placements
     if (s_err) break;
     for (int q = tid; q < n_new; q += kDpThreads) Memo[X0[q]].state = 3;
     // ---- 4: candidate states ----
@@ -808,7 +1067,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     }
     __syncthreads();
     if (s_err) break;
-    SLOS_PHASE(6);  // 6: candidate states
+    SLOS_PHASE(8);  // 8: candidate states
     // ---- 5: Pareto buckets ----
     for (int c = tid; c < T; c += kDpThreads) {
       int b = -1;
@@ -933,7 +1192,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       }
     }
     __syncthreads();
-    SLOS_PHASE(7);  // 7: Pareto buckets
+    SLOS_PHASE(9);  // 9: Pareto buckets
     // ---- 6: arena ids and survivors ----
     {
       int64_t carry_acc = 0, carry_sv = 0;
@@ -971,7 +1230,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       }
     }
     __syncthreads();
-    SLOS_PHASE(8);  // 8: arena ids + survivors
+    SLOS_PHASE(10);  // 10: arena ids + survivors
   }
   __syncthreads();
   if (s_err) {
@@ -1101,7 +1360,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     if (best < 0) A.bq[2 + atomicAdd(&A.bq[0], 1)] = inst;
     else A.bq[2 + A.n_inst - 1 - atomicAdd(&A.bq[1], 1)] = inst;
   }
-  SLOS_PHASE(9);  // 9: terminal selection + backtrack
+  SLOS_PHASE(11);  // 11: terminal selection + backtrack
 }
 
 }  // namespace slos

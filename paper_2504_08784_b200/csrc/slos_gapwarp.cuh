@@ -102,6 +102,7 @@ struct Variant {
   int spill;        // spec: an exact due past gap (within due_horizon)
   int valid;
   int inc;          // slot ends strictly increasing -> jit may be walked
+  int dues_done;    // exact dues filled from the anchor due pass (no E2 task)
 };
 
 // A group's shared variant arrays (shared memory).
@@ -280,7 +281,19 @@ struct AnchorFacts {
   int Kg;                // grid points stored (may exceed Sc -> overflow)
   int grid_ok;           // grid strictly increasing and complete
   int cap_uniform_err;
-  int pad;
+  int dues_ok;           // the anchor due pass below ran: groups skip E2
+  int64_t Lx;            // exact late dues (backlog issued + dues at d <= eps)
+};
+
+// Per (anchor j, chain item i) result of the anchor due pass: the exact dues of the
+// group's tail cells (grid cells >= Sp-1 up to the group's due horizon), which are
+// the only ones whose slot or inclusion depends on i.
+struct GroupTail {
+  int32_t tA;     // dues placed in slot Sp-1
+  int32_t tB;     // dues placed in the appended slot Sp
+  int32_t td;     // non-late dues counted in the tail
+  int16_t fail;   // a tail due with jit < 0 (only when Sp == 0)
+  int16_t spill;  // a tail due past the gap (within the horizon)
 };
 
 struct AnchorView {
@@ -291,10 +304,14 @@ struct AnchorView {
   double* ge;
   int64_t* gcap;   // -1: plan_time2bs throws for that grid slot
   int32_t* ccell;  // [L][Sc] grid jit of canonical time k of tier l
+  int32_t* hcum;   // [Sc+2] cumulative exact due count over grid cells -1, 0, 1, ...
+  GroupTail* gt;   // [N+1] per chain item i
 };
 
-__host__ __device__ __forceinline__ size_t anchor_stride_bytes(int R, int Sc, int L) {
-  size_t b = 256 + (size_t)R * 24 + (size_t)Sc * 16 + (size_t)L * Sc * 4;
+__host__ __device__ __forceinline__ size_t anchor_stride_bytes(int R, int Sc, int L, int N) {
+  size_t b = 256 + (size_t)R * 24 + (size_t)Sc * 16 + (size_t)L * Sc * 4 + (size_t)(Sc + 2) * 4;
+  b = (b + 15) & ~(size_t)15;
+  b += (size_t)(N + 1) * sizeof(GroupTail);
   return (b + 127) & ~(size_t)127;
 }
 
@@ -307,8 +324,10 @@ __device__ __forceinline__ AnchorView anchor_view(unsigned char* base, int R, in
   v.rm = (int64_t*)p; p += (size_t)R * 8;
   v.ge = (double*)p; p += (size_t)Sc * 8;
   v.gcap = (int64_t*)p; p += (size_t)Sc * 8;
-  v.ccell = (int32_t*)p;
-  (void)L;
+  v.ccell = (int32_t*)p; p += (size_t)L * Sc * 4;
+  v.hcum = (int32_t*)p; p += (size_t)(Sc + 2) * 4;
+  p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+  v.gt = (GroupTail*)p;
   return v;
 }
 
@@ -316,7 +335,7 @@ __device__ __forceinline__ AnchorView anchor_view(unsigned char* base, int R, in
 // `ctime/ccnt` is the instance's canonical due-time list per tier.
 __device__ inline void warp_group_from_anchor(const PlannerDev& P, const AnchorView& av, GapGroup& g,
                                               Variant& v, const GroupVar& ga, int Sc, double min_slot,
-                                              const double* ctime, const int* ccnt) {
+                                              const double* ctime, const int* ccnt, int item) {
   const int lane = lane_id();
   const AnchorFacts& F = *av.f;
   g.exact_mask = F.exact_mask;
@@ -336,6 +355,7 @@ __device__ inline void warp_group_from_anchor(const PlannerDev& P, const AnchorV
   v.cap_err = 0;
   v.cfail = 0;
   v.inc = 0;
+  v.dues_done = 0;
   for (int l = 0; l < kMaxTiers; ++l) v.q[l] = 0;
   if (g.gap <= kTimeEps || !F.exact_mask) return;
   v.t0 = F.t0;
@@ -398,6 +418,25 @@ __device__ inline void warp_group_from_anchor(const PlannerDev& P, const AnchorV
   // strictly increasing ends (the appended end may not exceed the grid when min_slot ~ 0)
   const int inc = app == 0 || Sp == 0 || av.ge[Sp - 1] < g.gap;
   v.inc = inc;
+  if (F.dues_ok && inc) {
+    // exact dues from the anchor due pass: grid cells below Sp-1 keep their counts,
+    // the group's tail (slots Sp-1 and Sp) comes from its GroupTail
+    const GroupTail t = av.gt[item];
+    __syncwarp();
+    for (int s = lane; s < S; s += 32) {
+      int32_t n;
+      if (s < Sp - 1) n = av.hcum[s + 2] - av.hcum[s + 1];
+      else if (s == Sp - 1) n = t.tA;
+      else n = t.tB;
+      ga.nx[s] = n;
+    }
+    const int64_t pre = av.hcum[Sp];  // grid cells -1 .. Sp-2
+    v.Lx = F.Lx;
+    v.Dx = F.Lx + pre + t.td;
+    v.exact_fail = Sp >= 1 ? (av.hcum[1] > 0 ? 1 : 0) : (t.fail ? 1 : 0);
+    v.spill = t.spill ? 1 : 0;
+    v.dues_done = 1;
+  }
   __syncwarp();
   // canonical dues -> slots: grid jit clipped to the prefix, or the appended slot
   int cf = 0;
@@ -764,6 +803,106 @@ __device__ inline int warp_place_budget(const PlannerDev& P, const Variant& v, c
   *budget = warp_sum(b);
   __syncwarp();
   return 1;
+}
+
+}  // namespace slos
+
+namespace slos {
+
+// One-thread form of warp_place_budget (same arithmetic, same result): a forward
+// pass for the totals and min_u (F(u) - D(u)), then a backward pass that rebuilds
+// F and D from the totals, keeps the suffix minimum G(u) and sums
+// min(G(s) - G(s-1), max_chunk). No per-slot storage, so 32 count vectors of a
+// DP level are placed per warp at once (lanes over memo keys).
+__device__ inline int thread_place_budget(const PlannerDev& P, const Variant& v, const int64_t* cap,
+                                          const int32_t* nx, const int32_t* hc, const int64_t* c,
+                                          int64_t* budget) {
+  const int S = v.S;
+  const int L = P.L;
+  auto dues_at = [&](int s) -> int64_t {
+    int64_t n = nx ? nx[s] : 0;
+    for (int l = 0; l < L; ++l)
+      if (c[l] > 0) n += c[l] * (int64_t)hc[l * S + s];
+    return n;
+  };
+  if (v.Lx == 0) {
+    bool ok = true;
+    int64_t b = 0;
+    for (int s = 0; s < S; ++s) {
+      const int64_t f = cap[s] - dues_at(s);
+      if (f < 0) { ok = false; break; }
+      b += imin(f, P.max_chunk);
+    }
+    if (ok) { *budget = b; return 1; }
+  }
+  int64_t capT = 0, F = 0, Dn = 0, min_diff = INT64_MAX;
+  for (int s = 0; s < S; ++s) {
+    const int64_t capv = cap[s];
+    int64_t used = v.Lx - capT;
+    used = used < 0 ? 0 : (used > capv ? capv : used);
+    capT += capv;
+    F += capv - used;
+    Dn += dues_at(s);
+    min_diff = imin(min_diff, F - Dn);
+  }
+  if (v.Lx > capT) return 0;
+  if (min_diff < 0) return 0;
+  int64_t cap_after = 0, G_next = INT64_MAX, b = 0;
+  for (int u = S - 1; u >= 0; --u) {
+    const int64_t capv = cap[u];
+    const int64_t before = capT - cap_after - capv;
+    int64_t used = v.Lx - before;
+    used = used < 0 ? 0 : (used > capv ? capv : used);
+    const int64_t Gu = imin(F - Dn, G_next);
+    if (u + 1 < S) b += imin(G_next - Gu, P.max_chunk);
+    G_next = Gu;
+    F -= capv - used;
+    Dn -= dues_at(u);
+    cap_after += capv;
+  }
+  b += imin(G_next, P.max_chunk);
+  *budget = b;
+  return 1;
+}
+
+// One-thread form of warp_eval_counts for the autoregressive budget when the
+// group's shared variant applies (the common case). Returns 1 when the key needs
+// the warp path instead (speculative planner, or a tightest tier that differs from
+// the group variant's and so needs a private variant).
+__device__ inline int thread_eval_counts(const PlannerDev& P, const GapGroup& g, const Variant& gv,
+                                         const GroupVar& ga, int Sc, const int64_t* c, double min_slot,
+                                         EvalOut& o) {
+  o.status = 0; o.has = false; o.budget = 0; o.dues = 0; o.slots = 0;
+  if (P.speculative) return 1;
+  const int L = P.L;
+  unsigned cmask = 0;
+  for (int l = 0; l < L; ++l) if (c[l] > 0) cmask |= 1u << l;
+  if (g.gap <= kTimeEps) { o.has = !g.any_due; return 0; }
+  const unsigned present = g.exact_mask | cmask;
+  auto prefill_only = [&]() {
+    int st = 0;
+    const int64_t b = prefill_only_budget(P, g.gap, min_slot, &st);
+    if (st) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return; }
+    o.has = true;
+    o.budget = b;
+  };
+  if (!present) { prefill_only(); return 0; }
+  const double t0 = P.tpot[__ffs(present) - 1];
+  if (!(gv.valid && gv.t0 == t0)) return 1;
+  if (gv.S > Sc) { o.status = SLOS_ERR_CAPACITY; return 0; }
+  int64_t Dtot = gv.Dx;
+  for (int l = 0; l < L; ++l) Dtot += c[l] * (int64_t)gv.q[l];
+  o.dues = Dtot;
+  if (Dtot == 0) { prefill_only(); return 0; }
+  if (min_slot > t0 + kTimeEps) return 0;
+  o.slots = gv.S;
+  if (gv.S == 0) return 0;
+  if (gv.cap_err) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return 0; }
+  if (gv.exact_fail || (gv.cfail & cmask)) return 0;
+  int64_t b = 0;
+  o.has = thread_place_budget(P, gv, ga.cap, ga.nx, ga.hc, c, &b) != 0;
+  o.budget = o.has ? b : 0;
+  return 0;
 }
 
 }  // namespace slos

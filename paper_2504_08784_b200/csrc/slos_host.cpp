@@ -509,7 +509,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   int64_t TA = 0;
   std::vector<int64_t> astride(n, 0);
   for (int q : valid) {
-    astride[q] = (int64_t)dp_anchor_stride(prep[q].n_dec, Sc, Lmax);
+    astride[q] = (int64_t)dp_anchor_stride(prep[q].n_dec, Sc, Lmax, prep[q].N);
     TA += astride[q] * (prep[q].N + 1);
   }
   Layout& Ly = ws.Ly;
@@ -843,7 +843,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   BuildParams bp;
   bp.a = ws.A;
   bp.smem_bytes = 44 * 1024;
-  bp.phase_cycles = dp.phase_cycles ? dp.phase_cycles + 10 : nullptr;
+  bp.phase_cycles = dp.phase_cycles ? dp.phase_cycles + 16 : nullptr;
   if ((e = launch_build(bp, nv, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   cudaEventRecord(ws.ev[2], s);
   return SLOS_OK;
@@ -871,18 +871,18 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
     unsigned long long pc[32];
     cudaMemcpy(pc, ws.dp.phase_cycles, sizeof pc, cudaMemcpyDeviceToHost);
     unsigned long long tot = 0;
-    for (int k = 0; k < 10; ++k) tot += pc[k];
-    static const char* names[10] = {"setup", "memo", "group", "E1", "E2", "E3", "states", "buckets",
-                                    "survivors", "terminal"};
+    for (int k = 0; k < 12; ++k) tot += pc[k];
+    static const char* names[12] = {"setup", "anchor", "anchor_dues", "memo", "group", "E1", "E2", "E3",
+                                    "states", "buckets", "survivors", "terminal"};
     std::fprintf(stderr, "[slos phases] total %.3e cycles:", (double)tot);
-    for (int k = 0; k < 10; ++k) std::fprintf(stderr, " %s %.1f%%", names[k], 100.0 * (double)pc[k] / (double)(tot ? tot : 1));
+    for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %s %.1f%%", names[k], 100.0 * (double)pc[k] / (double)(tot ? tot : 1));
     std::fprintf(stderr, "\n");
     unsigned long long bt = 0;
-    for (int k = 10; k < 16; ++k) bt += pc[k];
+    for (int k = 16; k < 22; ++k) bt += pc[k];
     static const char* bn[6] = {"setup", "census", "tile_gap", "emit", "tail", "fallback"};
     std::fprintf(stderr, "[slos build phases] total %.3e cycles:", (double)bt);
-    for (int k = 0; k < 6; ++k) std::fprintf(stderr, " %s %.1f%%", bn[k], 100.0 * (double)pc[10 + k] / (double)(bt ? bt : 1));
-    std::fprintf(stderr, " | max instance %.3e cycles over %llu instances\n", (double)pc[16], pc[17]);
+    for (int k = 0; k < 6; ++k) std::fprintf(stderr, " %s %.1f%%", bn[k], 100.0 * (double)pc[16 + k] / (double)(bt ? bt : 1));
+    std::fprintf(stderr, " | max instance %.3e cycles over %llu instances\n", (double)pc[22], pc[23]);
     std::vector<int> idx(nv);
     for (int v = 0; v < nv; ++v) idx[v] = v;
     std::sort(idx.begin(), idx.end(), [&](int x, int y) { return hdr[x].dbg_cycles > hdr[y].dbg_cycles; });

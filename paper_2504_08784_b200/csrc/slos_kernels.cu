@@ -47,7 +47,7 @@ size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Gmax, int
   return b + 64;
 }
 
-size_t dp_anchor_stride(int R, int Sc, int L) { return anchor_stride_bytes(R, Sc, L);
+size_t dp_anchor_stride(int R, int Sc, int L, int N) { return anchor_stride_bytes(R, Sc, L, N);
 }
 
 size_t dp_group_stride(int Sc, int L) { return group_var_stride(Sc, L); }

@@ -26,7 +26,7 @@ struct CompactParams {
 
 size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Gmax, int Tsm, size_t* overlay);
 size_t dp_group_stride(int Sc, int L);
-size_t dp_anchor_stride(int R, int Sc, int L);
+size_t dp_anchor_stride(int R, int Sc, int L, int N);
 size_t dp_warp_scr_stride(int Sc, int L);
 cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_build(const BuildParams& prm, int grid, cudaStream_t s);

@@ -6,7 +6,8 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["SLOS_PHASE_TIMING"] = "1"
+if os.environ.get("SLOS_NO_PHASES") is None:
+    os.environ["SLOS_PHASE_TIMING"] = "1"
 import torch  # noqa: E402
 
 from paper_2504_08784_b200 import abi  # noqa: E402
@@ -20,7 +21,7 @@ s = ShardSolver(abi.product(), ShardSpec(F["spec"], F["model"], F["cfg"]), range
 rec = torch.empty((n, C.sizeof(abi.Record)), dtype=torch.uint8, device="cuda")
 s.upload()
 s.converge(rec)
-for _ in range(3):
+for _ in range(int(os.environ.get("SLOS_SOLVES", "3"))):
     s.solve()
     torch.cuda.synchronize()
     print(fam, n, "kernel ms", s.kernel_ms(), flush=True)
