@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   __shared__ int32_t s_joff[SLOS_MAX_CHAIN + 2];
   __shared__ int64_t s_wsum[kDpWarps + 1];
   __shared__ unsigned long long s_ctr[5];
-  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_ng, s_e2, s_nw;
+  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_ng, s_e2, s_nw, s_bovf;
   __shared__ int32_t s_glist[SLOS_MAX_CHAIN + 2];
   __shared__ int64_t s_next_free, s_arena_next;
 
@@ -1096,92 +1096,249 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     }
     __syncthreads();
     const int NB = s_nb;
-    int32_t* cntB = Cj;   // anchors are no longer needed this level
-    int32_t* offB = Cme;  // memo slots are no longer needed after step 4
-    for (int b = tid; b < NB; b += kDpThreads) cntB[b] = 0;
-    __syncthreads();
-    for (int c = tid; c < T; c += kDpThreads)
-      if (Cbk[c] >= 0) atomicAdd(&cntB[Cbk[c]], 1);
-    __syncthreads();
-    {
-      int64_t carry = 0;
-      for (int base = 0; base < NB; base += kDpThreads) {
-        const int b = base + tid;
-        const int64_t x = b < NB ? cntB[b] : 0;
-        int64_t tot;
-        const int64_t ex = block_excl_scan(x, s_wsum, &tot);
-        if (b < NB) { offB[b] = (int32_t)(carry + ex); cntB[b] = 0; }
-        carry += tot;
+    SLOS_PHASE(12);  // 12 (sub of buckets): bucket hashing
+    // try_insert replay (dp_scheduler.cpp:445-465). Fast path: one warp per bucket
+    // finds its candidates in creation order by ballots over the level and keeps
+    // the bucket's Pareto frontier in registers (lane r, slot k holds frontier
+    // entry 32k+r; up to kFront entries); dominance tests are warp votes. The
+    // frontier is a set: rejection is an any-vote and pruning a per-entry test, so
+    // its order never matters. Big levels or frontiers take the list path below.
+    // Integral values make the eps tests exact, so dominance is transitive and the
+    // sequential replay has a closed form: c is accepted iff no EARLIER candidate of
+    // its bucket rejects it, and an accepted c is pruned iff a LATER accepted
+    // candidate of its bucket weakly dominates it: decided pairwise, one thread per
+    // candidate over its bucket's list.
+    const bool pairwise = I.values_integral != 0;
+    bool fastB = !pairwise && NB <= 64;
+    if (pairwise) {
+      // unordered bucket lists (counting sort without stability: "earlier" is the
+      // candidate index itself)
+      int32_t* cntB = Cj;   // anchors are no longer needed this level
+      int32_t* offB = Cme;  // memo slots are no longer needed after step 4
+      for (int b = tid; b < NB; b += kDpThreads) cntB[b] = 0;
+      __syncthreads();
+      for (int c = tid; c < T; c += kDpThreads)
+        if (Cbk[c] >= 0) atomicAdd(&cntB[Cbk[c]], 1);
+      __syncthreads();
+      {
+        int64_t carry = 0;
+        for (int base = 0; base < NB; base += kDpThreads) {
+          const int b = base + tid;
+          const int64_t x = b < NB ? cntB[b] : 0;
+          int64_t tot;
+          const int64_t ex = block_excl_scan(x, s_wsum, &tot);
+          if (b < NB) { offB[b] = (int32_t)(carry + ex); cntB[b] = 0; }
+          carry += tot;
+        }
+      }
+      __syncthreads();
+      for (int c = tid; c < T; c += kDpThreads) {
+        const int b = Cbk[c];
+        if (b >= 0) Blst[offB[b] + atomicAdd(&cntB[b], 1)] = c;
+      }
+      __syncthreads();
+      for (int c = tid; c < T; c += kDpThreads) {
+        const int b = Cbk[c];
+        if (b < 0) continue;
+        const double xv = Cvl[c];
+        const int64_t xm = Cmm[c], xp = Cpb[c];
+        const int xn = Cna[c];
+        const int32_t* lst = Blst + offB[b];
+        const int n = cntB[b];
+        bool acc = true;
+        for (int q = 0; q < n; ++q) {
+          const int y = lst[q];
+          if (y >= c) continue;
+          const double yv = Cvl[y];
+          const int64_t ym = Cmm[y], yp = Cpb[y];
+          if (yv >= xv && ym <= xm && yp >= xp) {
+            const bool equal = yv == xv && ym == xm && yp == xp;
+            if (!equal || Cna[y] >= xn) { acc = false; break; }
+          }
+        }
+        if (acc) Cfl[c] |= 2;
+      }
+      __syncthreads();
+      for (int c = tid; c < T; c += kDpThreads) {
+        if (!(Cfl[c] & 2)) continue;
+        const int b = Cbk[c];
+        const double xv = Cvl[c];
+        const int64_t xm = Cmm[c], xp = Cpb[c];
+        const int32_t* lst = Blst + offB[b];
+        const int n = cntB[b];
+        for (int q = 0; q < n; ++q) {
+          const int y = lst[q];
+          if (y <= c || !(Cfl[y] & 2)) continue;
+          if (Cvl[y] >= xv && Cmm[y] <= xm && Cpb[y] >= xp) { Cfl[c] |= 4; break; }
+        }
       }
     }
-    __syncthreads();
-    // stable multi-split: chunk by chunk, warp by warp, candidate order preserved
-    for (int base = 0; base < T; base += kDpThreads) {
-      const int c = base + tid;
-      const int b = c < T ? Cbk[c] : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, b);
+    if (fastB) {
+      if (tid == 0) s_bovf = 0;
+      __syncthreads();
+      constexpr int kFront = 4;
       const int lane = lane_id();
-      const int rank = __popc(peers & ((1u << lane) - 1));
-      const int leader = __ffs(peers) - 1;
-      for (int w = 0; w < kDpWarps; ++w) {
-        if (warp_id() == w) {
-          int basepos = 0;
-          if (b >= 0 && lane == leader) {
-            basepos = cntB[b];
-            cntB[b] = basepos + __popc(peers);
+      for (int b = warp_id(); b < NB; b += kDpWarps) {
+        double fv[kFront];
+        int64_t fm[kFront], fp[kFront];
+        int fn[kFront], fc[kFront];
+        unsigned A[kFront];
+#pragma unroll
+        for (int k = 0; k < kFront; ++k) { A[k] = 0u; fv[k] = 0.0; fm[k] = 0; fp[k] = 0; fn[k] = 0; fc[k] = 0; }
+        bool ovf = false;
+        for (int base = 0; base < T && !ovf; base += 32) {
+          const int c = base + lane;
+          const bool in = c < T && Cbk[c] == b;
+          unsigned mm = __ballot_sync(0xffffffffu, in);
+          if (!mm) continue;
+          double xv = 0.0;
+          int64_t xm = 0, xp = 0;
+          int xn = 0;
+          if (in) { xv = Cvl[c]; xm = Cmm[c]; xp = Cpb[c]; xn = Cna[c]; }
+          while (mm) {
+            const int src = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const double sv = __shfl_sync(0xffffffffu, xv, src);
+            const int64_t smm = __shfl_sync(0xffffffffu, xm, src);
+            const int64_t spb = __shfl_sync(0xffffffffu, xp, src);
+            const int sn = __shfl_sync(0xffffffffu, xn, src);
+            bool rj = false;
+#pragma unroll
+            for (int k = 0; k < kFront; ++k) {
+              if ((A[k] >> lane) & 1u) {
+                if (fv[k] >= sv - kValueEps && fm[k] <= smm && fp[k] >= spb) {
+                  const bool equal = fabs(fv[k] - sv) <= kValueEps && fm[k] == smm && fp[k] == spb;
+                  if (!equal || fn[k] >= sn) rj = true;
+                }
+              }
+            }
+            if (__any_sync(0xffffffffu, rj)) continue;
+#pragma unroll
+            for (int k = 0; k < kFront; ++k) {
+              bool pr = false;
+              if ((A[k] >> lane) & 1u) {
+                if (sv >= fv[k] - kValueEps && smm <= fm[k] && spb >= fp[k]) {
+                  pr = true;
+                  Cfl[fc[k]] |= 4;  // pruned (this lane accepted it earlier)
+                }
+              }
+              A[k] &= ~__ballot_sync(0xffffffffu, pr);
+            }
+            int ks = -1;
+#pragma unroll
+            for (int k = kFront - 1; k >= 0; --k) if (A[k] != 0xffffffffu) ks = k;
+            if (ks < 0) { ovf = true; break; }
+            const int slot = __ffs(~A[ks]) - 1;
+#pragma unroll
+            for (int k = 0; k < kFront; ++k) {
+              if (k == ks) {
+                if (lane == slot) {
+                  fv[k] = sv; fm[k] = smm; fp[k] = spb; fn[k] = sn; fc[k] = base + src;
+                  Cfl[base + src] |= 2;  // accepted
+                }
+                A[k] |= 1u << slot;
+              }
+            }
           }
-          basepos = __shfl_sync(0xffffffffu, basepos, leader);
-          if (b >= 0) Blst[offB[b] + basepos + rank] = c;
         }
+        if (ovf && lane == 0) s_bovf = 1;
+      }
+      __syncthreads();
+      if (s_bovf) {  // some frontier outgrew the registers: redo the level on the list path
+        for (int c = tid; c < T; c += kDpThreads) Cfl[c] &= 1;
+        fastB = false;
         __syncthreads();
       }
     }
-    // one warp per bucket: try_insert replay (dp_scheduler.cpp:445-465) in candidate
-    // order; the frontier scan of each step is lane-parallel (ballots).
-    for (int b = warp_id(); b < NB; b += kDpWarps) {
-      int32_t* lst = Blst + offB[b];
-      const int n = cntB[b];
-      const int lane = lane_id();
-      int f = 0;  // frontier lst[0..f)
-      for (int q = 0; q < n; ++q) {
-        const int c = lst[q];
-        const double sv = Cvl[c];
-        const int64_t smm = Cmm[c], spb = Cpb[c];
-        const int sn = Cna[c];
-        bool reject = false;
-        for (int r0 = 0; r0 < f && !reject; r0 += 32) {
-          bool rj = false;
-          if (r0 + lane < f) {
-            const int e = lst[r0 + lane];
-            if (Cvl[e] >= sv - kValueEps && Cmm[e] <= smm && Cpb[e] >= spb) {
-              const bool equal = fabs(Cvl[e] - sv) <= kValueEps && Cmm[e] == smm && Cpb[e] == spb;
-              rj = !equal || Cna[e] >= sn;
+    SLOS_PHASE(13);  // 13 (sub): fast try_insert
+    if (!fastB && !pairwise) {
+      int32_t* cntB = Cj;   // anchors are no longer needed this level
+      int32_t* offB = Cme;  // memo slots are no longer needed after step 4
+      for (int b = tid; b < NB; b += kDpThreads) cntB[b] = 0;
+      __syncthreads();
+      for (int c = tid; c < T; c += kDpThreads)
+        if (Cbk[c] >= 0) atomicAdd(&cntB[Cbk[c]], 1);
+      __syncthreads();
+      {
+        int64_t carry = 0;
+        for (int base = 0; base < NB; base += kDpThreads) {
+          const int b = base + tid;
+          const int64_t x = b < NB ? cntB[b] : 0;
+          int64_t tot;
+          const int64_t ex = block_excl_scan(x, s_wsum, &tot);
+          if (b < NB) { offB[b] = (int32_t)(carry + ex); cntB[b] = 0; }
+          carry += tot;
+        }
+      }
+      __syncthreads();
+      // stable multi-split: chunk by chunk, warp by warp, candidate order preserved
+      for (int base = 0; base < T; base += kDpThreads) {
+        const int c = base + tid;
+        const int b = c < T ? Cbk[c] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int lane = lane_id();
+        const int rank = __popc(peers & ((1u << lane) - 1));
+        const int leader = __ffs(peers) - 1;
+        for (int w = 0; w < kDpWarps; ++w) {
+          if (warp_id() == w) {
+            int basepos = 0;
+            if (b >= 0 && lane == leader) {
+              basepos = cntB[b];
+              cntB[b] = basepos + __popc(peers);
             }
+            basepos = __shfl_sync(0xffffffffu, basepos, leader);
+            if (b >= 0) Blst[offB[b] + basepos + rank] = c;
           }
-          reject = __any_sync(0xffffffffu, rj);
+          __syncthreads();
         }
-        if (reject) continue;
-        int wq = 0;
-        for (int r0 = 0; r0 < f; r0 += 32) {
-          int e = -1;
-          bool keep = false;
-          if (r0 + lane < f) {
-            e = lst[r0 + lane];
-            if (sv >= Cvl[e] - kValueEps && smm <= Cmm[e] && spb >= Cpb[e]) Cfl[e] |= 4;  // pruned
-            else keep = true;
+      }
+      // one warp per bucket: try_insert replay (dp_scheduler.cpp:445-465) in candidate
+      // order; the frontier scan of each step is lane-parallel (ballots).
+      for (int b = warp_id(); b < NB; b += kDpWarps) {
+        int32_t* lst = Blst + offB[b];
+        const int n = cntB[b];
+        const int lane = lane_id();
+        int f = 0;  // frontier lst[0..f)
+        for (int q = 0; q < n; ++q) {
+          const int c = lst[q];
+          const double sv = Cvl[c];
+          const int64_t smm = Cmm[c], spb = Cpb[c];
+          const int sn = Cna[c];
+          bool reject = false;
+          for (int r0 = 0; r0 < f && !reject; r0 += 32) {
+            bool rj = false;
+            if (r0 + lane < f) {
+              const int e = lst[r0 + lane];
+              if (Cvl[e] >= sv - kValueEps && Cmm[e] <= smm && Cpb[e] >= spb) {
+                const bool equal = fabs(Cvl[e] - sv) <= kValueEps && Cmm[e] == smm && Cpb[e] == spb;
+                rj = !equal || Cna[e] >= sn;
+              }
+            }
+            reject = __any_sync(0xffffffffu, rj);
           }
-          const unsigned km = __ballot_sync(0xffffffffu, keep);
-          __syncwarp();
-          if (keep) lst[wq + __popc(km & ((1u << lane) - 1))] = e;
-          wq += __popc(km);
+          if (reject) continue;
+          int wq = 0;
+          for (int r0 = 0; r0 < f; r0 += 32) {
+            int e = -1;
+            bool keep = false;
+            if (r0 + lane < f) {
+              e = lst[r0 + lane];
+              if (sv >= Cvl[e] - kValueEps && smm <= Cmm[e] && spb >= Cpb[e]) Cfl[e] |= 4;  // pruned
+              else keep = true;
+            }
+            const unsigned km = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();
+            if (keep) lst[wq + __popc(km & ((1u << lane) - 1))] = e;
+            wq += __popc(km);
+            __syncwarp();
+          }
+          if (lane == 0) {
+            lst[wq] = c;
+            Cfl[c] |= 2;  // accepted
+          }
+          f = wq + 1;
           __syncwarp();
         }
-        if (lane == 0) {
-          lst[wq] = c;
-          Cfl[c] |= 2;  // accepted
-        }
-        f = wq + 1;
-        __syncwarp();
       }
     }
     __syncthreads();

@@ -871,12 +871,13 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
     unsigned long long pc[32];
     cudaMemcpy(pc, ws.dp.phase_cycles, sizeof pc, cudaMemcpyDeviceToHost);
     unsigned long long tot = 0;
-    for (int k = 0; k < 12; ++k) tot += pc[k];
+    for (int k = 0; k < 14; ++k) tot += pc[k];
     static const char* names[12] = {"setup", "anchor", "anchor_dues", "memo", "group", "E1", "E2", "E3",
                                     "states", "buckets", "survivors", "terminal"};
     std::fprintf(stderr, "[slos phases] total %.3e cycles:", (double)tot);
     for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %s %.1f%%", names[k], 100.0 * (double)pc[k] / (double)(tot ? tot : 1));
-    std::fprintf(stderr, "\n");
+    std::fprintf(stderr, " | buckets sub: hash %.1f%% fast %.1f%% \n", 100.0 * (double)pc[12] / (double)(tot ? tot : 1),
+                 100.0 * (double)pc[13] / (double)(tot ? tot : 1));
     unsigned long long bt = 0;
     for (int k = 16; k < 22; ++k) bt += pc[k];
     static const char* bn[6] = {"setup", "census", "tile_gap", "emit", "tail", "fallback"};
