@@ -453,6 +453,12 @@ int slos_workspace_records(slos_workspace* b, slos_record* out, void* stream) {
   }
   return SLOS_OK;
 }
+int slos_workspace_stage_ms(slos_workspace* b, float* ms, int32_t n) {
+  (void)b;
+  for (int k = 0; k < n; ++k) ms[k] = 0.0f;
+  return SLOS_OK;
+}
+
 int slos_workspace_kernel_ms(slos_workspace* b, float* ms2) {
   ms2[0] = (float)b->solve_ms;
   ms2[1] = 0.0f;

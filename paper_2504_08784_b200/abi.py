@@ -350,6 +350,8 @@ def _bind(lib: C.CDLL) -> C.CDLL:
     lib.slos_workspace_records.restype = C.c_int
     lib.slos_workspace_kernel_ms.argtypes = [C.c_void_p, P(C.c_float)]
     lib.slos_workspace_kernel_ms.restype = C.c_int
+    lib.slos_workspace_stage_ms.argtypes = [C.c_void_p, P(C.c_float), C.c_int32]
+    lib.slos_workspace_stage_ms.restype = C.c_int
     lib.slos_last_transfer_bytes.argtypes = [P(C.c_int64), P(C.c_int64)]
     lib.slos_last_transfer_bytes.restype = None
     return lib

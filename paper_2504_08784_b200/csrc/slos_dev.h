@@ -109,6 +109,8 @@ struct BatchArgs {
   const InstDev* inst;
   const int32_t* order;  // launch order of instances (cost-descending)
   int32_t n_inst;
+  const int32_t* atask;  // anchor tasks (instance, anchor j) pairs, j = -1 .. N-2
+  int32_t n_atask;
   // decoders
   const int32_t* dec_idx;
   const int32_t* dec_tier;
@@ -193,6 +195,22 @@ struct GapOutDev {
   int64_t n_batches;
   int64_t n_owner_pairs;
   int64_t need_batch, need_owner, need_work;
+};
+
+// dp_kernel / anchor_kernel launch parameters (host and device share this layout).
+struct DpParams {
+  BatchArgs a;
+  int Sc;              // per-warp slot capacity
+  int Lmax;            // max tiers over planners
+  int dec_smem_max;    // stage decoders in smem when n_dec <= this
+  unsigned char* wscr_global;  // per-CTA-slot warp scratch when not in smem (nullptr = smem)
+  size_t wscr_stride;  // bytes per warp in wscr_global
+  int Gmax;            // anchor groups per evaluation wave (shared variants in smem)
+  size_t gstride;      // bytes per group variant
+  unsigned long long* phase_cycles;  // kNumPhases counters, or nullptr
+  int Tsm;             // candidates per level kept in shared memory
+  size_t overlay_bytes;  // group-variant / candidate-state overlay (bytes)
+  size_t anchor_scr_bytes;  // anchor_kernel: due-pass scratch (bytes)
 };
 
 }  // namespace slos

@@ -40,19 +40,6 @@ constexpr int kNumPhases = 12;
   } while (0)
 constexpr int kDpWarps = kDpThreads / 32;
 
-struct DpParams {
-  BatchArgs a;
-  int Sc;              // per-warp slot capacity
-  int Lmax;            // max tiers over planners
-  int dec_smem_max;    // stage decoders in smem when n_dec <= this
-  unsigned char* wscr_global;  // per-CTA-slot warp scratch when not in smem (nullptr = smem)
-  size_t wscr_stride;  // bytes per warp in wscr_global
-  int Gmax;            // anchor groups per evaluation wave (shared variants in smem)
-  size_t gstride;      // bytes per group variant
-  unsigned long long* phase_cycles;  // kNumPhases counters, or nullptr
-  int Tsm;             // candidates per level kept in shared memory
-  size_t overlay_bytes;  // group-variant / candidate-state overlay (bytes)
-};
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x ^= x >> 33; x *= 0xff51afd7ed558ccdULL; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ULL; x ^= x >> 33;
@@ -611,6 +598,66 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
   (void)Sc;
 }
 
+// Anchor caches (prologue of the admission DP). Everything about a gap that depends
+// only on its start a = t_j -- the exact census members_at(a), the slot grid and its
+// capacities, the canonical due cells and the exact-due histogram with every later
+// group's tail (block_anchor_dues) -- is independent of the DP's states, so all
+// anchors of all instances are built up front, one CTA per (instance, anchor),
+// instead of on the DP's level-sequential critical path.
+__global__ void __launch_bounds__(kDpThreads) anchor_kernel(DpParams prm) {
+  extern __shared__ __align__(16) unsigned char asm_[];
+  __shared__ PlannerDev sP;
+  __shared__ InstDev sI;
+  __shared__ int ccnt[kMaxTiers];
+  __shared__ double s_maxdl, s_minA;
+  __shared__ int64_t s_wsum[kDpWarps + 1];
+  const BatchArgs& A = prm.a;
+  const int tid = threadIdx.x;
+  const int v = A.atask[2 * blockIdx.x], j = A.atask[2 * blockIdx.x + 1];
+  if (tid == 0) {
+    sI = A.inst[v];
+    sP = A.planners[sI.planner];
+  }
+  __syncthreads();
+  const PlannerDev& P = sP;
+  const InstDev& I = sI;
+  const int N = I.N;
+  const int L = P.L;
+  const int Sc = prm.Sc;
+  const double* ch_dl = A.ch_deadline + I.off_chain;
+  const int32_t* ch_fl = A.ch_floor + I.off_chain;
+  DecView D;
+  D.n = I.have_running_decode ? I.n_dec : 0;
+  D.next = A.dec_next + I.off_dec;
+  D.backlog = A.dec_backlog + I.off_dec;
+  D.rem = A.dec_rem + I.off_dec;
+  D.tier = A.dec_tier + I.off_dec;
+  double* ctime = (double*)asm_;
+  unsigned char* scr = asm_ + sizeof(double) * (size_t)prm.Lmax * Sc;
+  if (tid == 0) {
+    double mx = I.now, mn = I.now;
+    for (int k = 0; k < N; ++k) { mx = dmax(mx, ch_dl[k]); mn = dmin(mn, ch_dl[k]); }
+    s_maxdl = mx;
+    s_minA = mn;
+  }
+  __syncthreads();
+  if (tid < L) {  // instance-wide canonical due times per tier (batch_planner.cpp:216)
+    const double gall = quantize_gap(dmax(0.0, s_maxdl - s_minA));
+    const double tp = P.tpot[tid];
+    int k = 0;
+    for (double d = tp; time_le(d, gall) && k < Sc; d += tp) ctime[tid * Sc + k++] = d;
+    ccnt[tid] = k;
+  }
+  __syncthreads();
+  const double min_slot = plan_predict(P, 1, 0);  // BatchPlanner::min_slot_s
+  const double pull = min_slot;
+  const double a = (j < 0) ? I.now : ch_dl[j];
+  const AnchorView av = anchor_view(A.anchors + I.off_anchor + (size_t)(j + 1) * I.anchor_stride, D.n, Sc, L);
+  block_build_anchor(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), Sc, ctime, ccnt,
+                     min_slot, s_wsum);
+  block_anchor_dues(P, D, av, j, N, ch_dl, ch_fl, a, pull, min_slot, Sc, scr, prm.anchor_scr_bytes);
+}
+
 #ifndef SLOS_DP_MIN_BLOCKS
 #define SLOS_DP_MIN_BLOCKS 3
 #endif
@@ -805,16 +852,6 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     const int64_t capB = sm ? 2 * (int64_t)Tsm : 2 * capC;
     if (tid == 0) s_ctr[0] += (unsigned long long)T;
     const double t_i = ch_dl[i];
-    {  // the anchor that becomes available at this level: j = i - 1
-      const int j = i - 1;
-      const double a = (j < 0) ? I.now : ch_dl[j];
-      const AnchorView av = anchor_view(anc_base + (size_t)(j + 1) * I.anchor_stride, D.n, prm.Sc, L);
-      block_build_anchor(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), prm.Sc, ctime,
-                         ccnt, min_slot, s_wsum);
-      SLOS_PHASE(1);  // 1: anchor cache (members, grid, capacities)
-      block_anchor_dues(P, D, av, j, N, ch_dl, ch_fl, a, pull, min_slot, prm.Sc, ovl, prm.overlay_bytes);
-      SLOS_PHASE(2);  // 2: anchor due pass
-    }
     // ---- 1+2: candidates and memo keys ----
     for (int c = tid; c < T; c += kDpThreads) {
       int lo = 0, hi = nlev - 1;

@@ -27,19 +27,6 @@
 #include "../../include/slos_planner.h"
 
 namespace slos {
-struct DpParams {
-  BatchArgs a;
-  int Sc;
-  int Lmax;
-  int dec_smem_max;
-  unsigned char* wscr_global;
-  size_t wscr_stride;
-  int Gmax;
-  size_t gstride;
-  unsigned long long* phase_cycles;
-  int Tsm;
-  size_t overlay_bytes;
-};
 struct BuildParams {
   BatchArgs a;
   size_t smem_bytes;
@@ -423,7 +410,8 @@ struct Layout {
   size_t in_bytes;
   size_t s_counts, s_mem, s_pb, s_value, s_nadm, s_parent, s_arena, s_level;
   size_t c_src, c_j, c_memo, c_flag, c_bucket, c_pos, c_aux, c_counts, c_mem, c_pb, c_value, c_nadm;
-  size_t c_bkey, c_bval, memo, bq, work, anchors, scr_bytes;
+  size_t c_bkey, c_bval, memo, bq, work, anchors, scr_bytes, atask;
+  int64_t n_atask;
   size_t memo_bytes, bkey_bytes, bval_bytes;
   size_t out, sel, ids, batches, entries, out_bytes;
 };
@@ -441,10 +429,11 @@ struct Workspace {
   BatchArgs A;
   DpParams dp;
   size_t smem = 0;
+  size_t anchor_smem = 0;
   cudaStream_t stream = nullptr;
   bool uploaded = false;
   int n_total = 0;
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 thread_local int64_t g_h2d = 0, g_d2h = 0;
@@ -517,6 +506,9 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.planners = bi.add<PlannerDev>(plist.size());
   Ly.inst = bi.add<InstDev>(nv);
   Ly.order = bi.add<int32_t>(nv);
+  int64_t TT = 0;
+  for (int q : valid) TT += prep[q].N;
+  Ly.atask = bi.add<int32_t>(2 * TT);
   Ly.dec_idx = bi.add<int32_t>(TD);
   Ly.dec_tier = bi.add<int32_t>(TD);
   Ly.dec_next = bi.add<double>(TD);
@@ -698,6 +690,13 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     oE += cp.entry;
     oA += astride[q] * (pr.N + 1);
   }
+  {  // anchor tasks: (instance, anchor j), j = -1 .. N-2
+    int32_t* t = (int32_t*)hp(Ly.atask);
+    int64_t x = 0;
+    for (int v = 0; v < nv; ++v)
+      for (int j = -1; j < prep[valid[v]].N - 1; ++j) { t[2 * x] = v; t[2 * x + 1] = j; ++x; }
+    Ly.n_atask = x;
+  }
   int32_t* h_order = (int32_t*)hp(Ly.order);
   {
     std::vector<int> ord(nv);
@@ -728,6 +727,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   A.planners = (const PlannerDev*)(DI + Ly.planners);
   A.inst = (const InstDev*)(DI + Ly.inst);
   A.order = (const int32_t*)(DI + Ly.order);
+  A.atask = (const int32_t*)(DI + Ly.atask);
+  A.n_atask = (int32_t)Ly.n_atask;
   A.n_inst = nv;
   A.dec_idx = (const int32_t*)(DI + Ly.dec_idx);
   A.dec_tier = (const int32_t*)(DI + Ly.dec_tier);
@@ -812,6 +813,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   dp.dec_smem_max = 0;
   if (fit(maxDec) <= kSmemBudget) dp.dec_smem_max = maxDec;
   smem = fit(dp.dec_smem_max);
+  ws.anchor_smem = anchor_smem_bytes(maxN, dp.Sc, Lmax, &dp.anchor_scr_bytes);
   ws.valid = valid;
   ws.nv = nv;
   ws.uploaded = true;
@@ -835,9 +837,12 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   cudaMemsetAsync(DO + Ly.out, 0, sizeof(OutHdr) * nv, s);
   cudaMemsetAsync(DS + Ly.bq, 0, 2 * sizeof(int32_t), s);
   cudaError_t e;
-  for (int k = 0; k < 3; ++k)
+  for (int k = 0; k < 4; ++k)
     if (!ws.ev[k]) cudaEventCreate(&ws.ev[k]);
   cudaEventRecord(ws.ev[0], s);
+  if ((e = launch_anchor(dp, ws.A.n_atask, ws.anchor_smem, s)) != cudaSuccess)
+    return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  cudaEventRecord(ws.ev[3], s);
   if ((e = launch_dp(dp, nv, smem, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   cudaEventRecord(ws.ev[1], s);
   BuildParams bp;
@@ -1204,6 +1209,19 @@ int slos_workspace_kernel_ms(slos_workspace* b, float* ms2) {
   cudaEventSynchronize(ws.ev[2]);
   cudaEventElapsedTime(&ms2[0], ws.ev[0], ws.ev[1]);
   cudaEventElapsedTime(&ms2[1], ws.ev[1], ws.ev[2]);
+  return SLOS_OK;
+}
+
+int slos_workspace_stage_ms(slos_workspace* b, float* ms, int32_t n) {
+  Workspace& ws = b->ws;
+  float t[3] = {0.0f, 0.0f, 0.0f};
+  if (ws.ev[2]) {
+    cudaEventSynchronize(ws.ev[2]);
+    cudaEventElapsedTime(&t[0], ws.ev[0], ws.ev[3]);
+    cudaEventElapsedTime(&t[1], ws.ev[3], ws.ev[1]);
+    cudaEventElapsedTime(&t[2], ws.ev[1], ws.ev[2]);
+  }
+  for (int k = 0; k < n && k < 3; ++k) ms[k] = t[k];
   return SLOS_OK;
 }
 

@@ -57,6 +57,23 @@ size_t dp_warp_scr_stride(int Sc, int L) {
   return (s + 127) & ~(size_t)127;
 }
 
+size_t anchor_smem_bytes(int max_N, int Sc, int L, size_t* scr) {
+  const size_t N = (size_t)max_N, S = (size_t)Sc;
+  // due pass: grid copy, per-group gap/horizon/Sp/lo/hi/accumulators, cell histogram,
+  // list offsets and a list area of 8 entries per group plus one per cell
+  const size_t b = 8 * S + N * (8 + 8 + 4 * 3 + 4 * 5) + 4 * (S + 1) + 4 * (S + 2) + 4 * (8 * N + S) + 64;
+  *scr = b;
+  return sizeof(double) * (size_t)L * S + b;
+}
+
+cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(anchor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  anchor_kernel<<<grid, kDpThreads, smem, s>>>(prm);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s) {
   if (grid <= 0) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(dp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

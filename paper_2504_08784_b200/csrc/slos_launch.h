@@ -29,6 +29,8 @@ size_t dp_group_stride(int Sc, int L);
 size_t dp_anchor_stride(int R, int Sc, int L, int N);
 size_t dp_warp_scr_stride(int Sc, int L);
 cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
+size_t anchor_smem_bytes(int max_N, int Sc, int L, size_t* scr);
+cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_build(const BuildParams& prm, int grid, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& prm, int grid, cudaStream_t s);
 cudaError_t launch_gap(const GapParams& prm, int grid, cudaStream_t s);

@@ -95,6 +95,12 @@ class ShardSolver:
         self.lib.slos_workspace_kernel_ms(self.ws, ms)
         return float(ms[0]), float(ms[1])
 
+    def stage_ms(self):
+        """[anchor_kernel, dp_kernel, build_kernel] device ms of the last solve."""
+        ms = (C.c_float * 3)()
+        self.lib.slos_workspace_stage_ms(self.ws, ms, 3)
+        return [float(x) for x in ms]
+
     def download(self, stream=None):
         st = self.lib.slos_workspace_download(self.ws, self._outs, stream)
         if st != abi.SLOS_OK:

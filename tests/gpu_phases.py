@@ -24,6 +24,6 @@ s.converge(rec)
 for _ in range(int(os.environ.get("SLOS_SOLVES", "3"))):
     s.solve()
     torch.cuda.synchronize()
-    print(fam, n, "kernel ms", s.kernel_ms(), flush=True)
+    print(fam, n, "stage ms [anchor, dp, build]", s.stage_ms(), flush=True)
 s.download()
 s.free_results()
