@@ -17,6 +17,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <cuda_runtime.h>
 
 #include "../../include/slos_planner.h"
 
@@ -74,6 +75,8 @@ struct InstDev {
   int64_t cap_gb;                        // gap batches per tile_gap call
   int64_t cap_go;                        // owner pairs per tile_gap call
   int64_t off_anchor; int64_t anchor_stride;  // per-anchor caches (bytes), N+1 anchors
+  int64_t off_pair;    // into pair_shared: N(N+1)/2 flags, triangular (anchor j+1, item i)
+  int64_t off_group;   // into groups (bytes): one GroupHdr + variant arrays per pair
 };
 
 // Per-instance result header written by the kernels.
@@ -162,6 +165,11 @@ struct BatchArgs {
   slos_entry* entries;
   unsigned char* work;
   unsigned char* anchors;
+  const uint8_t* pair_shared;  // 1: the pair's memo key (a_us, raw_us) recurs in another pair
+  unsigned char* groups;       // per-pair gap group records (anchor_kernel -> dp_kernel)
+  int32_t* s_sb;               // survivor: dense id of its Pareto bucket within its level
+  uint64_t* s_bcnt;            // per level, per surviving bucket: its count vector
+  int64_t* k_val;              // per level: fresh-pair key results (budget, or -1 = nullopt)
   int32_t* bq;       // build queue: fallback instances first (n_inst + 2 ints; [0],[1] = counters)
   OutHdr* out;
 };
@@ -205,12 +213,17 @@ struct DpParams {
   int dec_smem_max;    // stage decoders in smem when n_dec <= this
   unsigned char* wscr_global;  // per-CTA-slot warp scratch when not in smem (nullptr = smem)
   size_t wscr_stride;  // bytes per warp in wscr_global
-  int Gmax;            // anchor groups per evaluation wave (shared variants in smem)
-  size_t gstride;      // bytes per group variant
   unsigned long long* phase_cycles;  // kNumPhases counters, or nullptr
   int Tsm;             // candidates per level kept in shared memory
   size_t overlay_bytes;  // group-variant / candidate-state overlay (bytes)
   size_t anchor_scr_bytes;  // anchor_kernel: due-pass scratch (bytes)
+  size_t grec_stride;       // bytes per pair group record
+  size_t grec_hdr;          // header bytes before the variant arrays
 };
+
+// Triangular index of the pair (anchor a = j+1, chain item i), 0 <= a <= i < N.
+__host__ __device__ __forceinline__ int64_t pair_index(int N, int a, int i) {
+  return (int64_t)a * N - (int64_t)a * (a - 1) / 2 + (i - a);
+}
 
 }  // namespace slos

@@ -656,6 +656,55 @@ __global__ void __launch_bounds__(kDpThreads) anchor_kernel(DpParams prm) {
   block_build_anchor(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), Sc, ctime, ccnt,
                      min_slot, s_wsum);
   block_anchor_dues(P, D, av, j, N, ch_dl, ch_fl, a, pull, min_slot, Sc, scr, prm.anchor_scr_bytes);
+  // the gap group of every pair (j, i) this anchor opens (the DP's E1/E2, moved off
+  // its critical path): one warp per pair, record written to HBM
+  const int nG = N - j - 1;
+  for (int gi = warp_id(); gi < nG; gi += kDpWarps) {
+    const int i = j + 1 + gi;
+    if (ch_fl[i] > j) continue;  // never a DP transition
+    unsigned char* rec = A.groups + I.off_group + (size_t)pair_index(N, j + 1, i) * prm.grec_stride;
+    GroupHdr* H = (GroupHdr*)rec;
+    const GroupVar ga = group_var_carve(rec + prm.grec_hdr, Sc, L);
+    GapGroup g;
+    g.a = a;
+    const double raw = dmax(0.0, ch_dl[i] - g.a);
+    const double len = quantize_gap(raw);
+    g.now = I.now;
+    g.pull = pull;
+    g.exact = I.have_running_decode != 0;
+    if (g.exact) { g.gap = len; g.dh = raw + pull; }
+    else { g.gap = quantize_gap(len); g.dh = 0.0; }
+    g.horizon = dmax(g.gap, g.dh);
+    Variant v;
+    warp_group_from_anchor(P, av, g, v, ga, Sc, min_slot, ctime, ccnt, i);
+    if (v.valid && v.S <= Sc && !v.dues_done) {
+      // no anchor due pass: walk the members for this group (lanes in lockstep)
+      int64_t late = 0, dues = 0;
+      int fail = 0, spill = 0;
+      for (int base = 0; base < D.n; base += 32) {
+        const int k = base + lane_id();
+        Member m;
+        m.valid = false;
+        if (k < D.n) {
+          m.rem = av.rm[k];
+          m.valid = m.rem > 0;
+          m.phase = av.ph[k];
+          m.backlog = av.bl[k];
+          m.tier = D.tier[k];
+        }
+        member_dues_warp(P, m, g, ga.ends, v.S, v.inc != 0, ga.nx, late, dues, fail, spill);
+      }
+      late = warp_sum(late);
+      dues = warp_sum(dues);
+      v.Lx = late;
+      v.Dx = late + dues;
+      v.exact_fail = warp_or(fail);
+      v.spill = warp_or(spill);
+      v.dues_done = 1;
+    }
+    __syncwarp();
+    if (lane_id() == 0) { H->g = g; H->v = v; H->j = j; }
+  }
 }
 
 #ifndef SLOS_DP_MIN_BLOCKS
@@ -667,14 +716,15 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   __shared__ InstDev sI;
   __shared__ int64_t lvl_off[SLOS_MAX_CHAIN + 2];
   __shared__ int32_t lvl_cnt[SLOS_MAX_CHAIN + 2];
-  __shared__ int32_t s_pre[SLOS_MAX_CHAIN + 2];
-  __shared__ int32_t s_jcnt[SLOS_MAX_CHAIN + 2];
-  __shared__ int32_t s_joff[SLOS_MAX_CHAIN + 2];
+  __shared__ int32_t lvl_boff[SLOS_MAX_CHAIN + 2];  // per level: first surviving-bucket slot
+  __shared__ int32_t lvl_nsb[SLOS_MAX_CHAIN + 2];   // per level: surviving buckets
+  __shared__ int32_t s_pre[SLOS_MAX_CHAIN + 2];     // candidate prefix over source levels
+  __shared__ int32_t s_kpre[SLOS_MAX_CHAIN + 2];    // fresh-key prefix over source levels
+  __shared__ uint8_t s_sh[SLOS_MAX_CHAIN + 2];      // source level's pair is memo-shared
   __shared__ int64_t s_wsum[kDpWarps + 1];
   __shared__ unsigned long long s_ctr[5];
-  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_ng, s_e2, s_nw, s_bovf;
-  __shared__ int32_t s_glist[SLOS_MAX_CHAIN + 2];
-  __shared__ int64_t s_next_free, s_arena_next;
+  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_nw, s_bovf, s_anysh;
+  __shared__ int64_t s_next_free, s_arena_next, s_bnext;
 
   const BatchArgs& A = prm.a;
   const int tid = threadIdx.x;
@@ -718,6 +768,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     ch_fl[k] = A.ch_floor[o];
   }
   for (int k = tid; k <= N; k += kDpThreads) ch_sf[k] = A.ch_suffix[I.off_chain + k];
+  // decoders: only the private-variant / speculative warp path reads them
   DecView D;
   D.n = I.have_running_decode ? I.n_dec : 0;
   if (I.n_dec <= prm.dec_smem_max) {
@@ -739,49 +790,24 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     D.rem = A.dec_rem + I.off_dec;
     D.tier = A.dec_tier + I.off_dec;
   }
-  // instance-wide canonical due times per tier (batch_planner.cpp:216)
-  double* ctime = (double*)p;
-  p += sizeof(double) * (size_t)prm.Lmax * prm.Sc;
-  __shared__ int ccnt[kMaxTiers];
-  __shared__ double s_maxdl, s_minA;
-  __syncthreads();
-  if (tid == 0) {
-    double mx = I.now, mn = I.now;
-    for (int k = 0; k < N; ++k) { mx = dmax(mx, ch_dl[k]); mn = dmin(mn, ch_dl[k]); }
-    s_maxdl = mx;
-    s_minA = mn;
-  }
-  __syncthreads();
-  if (tid < L) {
-    const double gall = quantize_gap(dmax(0.0, s_maxdl - s_minA));
-    const double tp = P.tpot[tid];
-    int k = 0;
-    for (double d = tp; time_le(d, gall) && k < prm.Sc; d += tp) ctime[tid * prm.Sc + k++] = d;
-    ccnt[tid] = k;
-  }
-  unsigned char* anc_base = A.anchors + I.off_anchor;
   // per-warp scratch for the rare private-variant / speculative paths (global);
   // the placement temporaries live in shared memory
   unsigned char* wbase = prm.wscr_global + ((size_t)blockIdx.x * kDpWarps + warp_id()) * prm.wscr_stride;
   WarpScr W = warp_scr_carve(wbase, prm.Sc, prm.Lmax);
   W.tmp = (int64_t*)p + (size_t)warp_id() * prm.Sc;
   p += sizeof(int64_t) * (size_t)prm.Sc * kDpWarps;
-  p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-  GroupHdr* ghdr = (GroupHdr*)p;
-  p += sizeof(GroupHdr) * (size_t)prm.Gmax;
   p = (unsigned char*)(((uintptr_t)p + 127) & ~(uintptr_t)127);
-  // the group-variant area doubles as the level's candidate-state area (phases 4-6)
-  unsigned char* gvbase = p;
-  unsigned char* ovl = p;
+  unsigned char* ovl = p;  // the level's candidate states
   p += prm.overlay_bytes;
   p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
   const int Tsm = prm.Tsm;
-  int32_t* k_src = (int32_t*)p; p += 4 * (size_t)Tsm;   // kept through phase 4
+  int32_t* k_src = (int32_t*)p; p += 4 * (size_t)Tsm;
   int32_t* k_j = (int32_t*)p; p += 4 * (size_t)Tsm;
   int32_t* k_me = (int32_t*)p; p += 4 * (size_t)Tsm;
   int32_t* k_new = (int32_t*)p; p += 4 * (size_t)Tsm;
   int32_t* k_grp = (int32_t*)p; p += 4 * (size_t)Tsm;
-  // overlay layout (phases 4-6): 8-byte arrays first
+  (void)k_grp;
+  // overlay layout: 8-byte arrays first
   uint64_t* o_cn = (uint64_t*)ovl;
   int64_t* o_mm = (int64_t*)(ovl + 8 * (size_t)Tsm);
   int64_t* o_pb = (int64_t*)(ovl + 16 * (size_t)Tsm);
@@ -803,15 +829,24 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   int32_t* Spar = A.s_parent + I.off_surv;
   int32_t* Sar = A.s_arena + I.off_surv;
   int32_t* Sit = A.s_level + I.off_surv;
+  int32_t* Ssb = A.s_sb + I.off_surv;
+  uint64_t* Bc = A.s_bcnt + I.off_surv;
+  int64_t* Kv = A.k_val + I.off_cand;
   MemoEnt* Memo = A.memo + I.off_memo;
+  const uint8_t* PS = A.pair_shared + I.off_pair;
+  unsigned char* GR = A.groups + I.off_group;
   const int64_t capC = I.cap_cand;
 
   if (tid == 0) {
     Sc_[0] = 0; Sm_[0] = 0; Sp_[0] = 0; Sv_[0] = 0.0; Sn_[0] = 0; Spar[0] = -1; Sar[0] = 0; Sit[0] = -1;
+    Ssb[0] = 0; Bc[0] = 0;
     lvl_off[0] = 0;
     lvl_cnt[0] = 1;
+    lvl_boff[0] = 0;
+    lvl_nsb[0] = 1;
     s_next_free = 1;
     s_arena_next = 1;
+    s_bnext = 1;
   }
   __syncthreads();
 
@@ -819,25 +854,38 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   SLOS_PHASE(0);  // 0: instance load / setup
   for (int i = 0; i < N && !s_err; ++i) {
     const int jlo = ch_fl[i];
-    const int nlev = i - jlo;  // levels jlo+1 .. i
+    const int nlev = i - jlo;  // source levels jlo+1 .. i (anchor j = level - 1)
     if (tid == 0) {
-      int acc = 0;
-      for (int k = 0; k < nlev; ++k) { s_pre[k] = acc; acc += lvl_cnt[jlo + 1 + k]; }
+      int acc = 0, kacc = 0, anysh = 0;
+      for (int k = 0; k < nlev; ++k) {
+        const int lv = jlo + 1 + k;
+        s_pre[k] = acc;
+        acc += lvl_cnt[lv];
+        const uint8_t sh = PS[pair_index(N, lv, i)];
+        s_sh[k] = sh;
+        s_kpre[k] = kacc;
+        if (sh) anysh = 1;
+        else kacc += lvl_nsb[lv];
+      }
       s_pre[nlev] = acc;
+      s_kpre[nlev] = kacc;
+      s_anysh = anysh;
       s_n_new = 0;
       s_nb = 0;
+      s_nw = 0;
       if (acc > Tsm && acc > capC) { s_err = SLOS_ERR_CAPACITY; out->need_cand = acc; }
+      else if (kacc > capC) { s_err = SLOS_ERR_CAPACITY; out->need_cand = kacc; }
     }
     __syncthreads();
     if (s_err) break;
     const int T = s_pre[nlev];
+    const int KF = s_kpre[nlev];
     // level arrays: shared memory when the level fits, else the HBM slice
     const bool sm = T <= Tsm;
     int32_t* Csrc = sm ? k_src : A.c_src + I.off_cand;
     int32_t* Cj = sm ? k_j : A.c_j + I.off_cand;
     int32_t* Cme = sm ? k_me : A.c_memo + I.off_cand;
     int32_t* X0 = sm ? k_new : A.c_pos + I.off_cand;
-    int32_t* G = sm ? k_grp : A.c_aux + I.off_cand;
     uint64_t* Ccn = sm ? o_cn : A.c_counts + I.off_cand;
     int64_t* Cmm = sm ? o_mm : A.c_mem + I.off_cand;
     int64_t* Cpb = sm ? o_pb : A.c_pb + I.off_cand;
@@ -852,18 +900,26 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     const int64_t capB = sm ? 2 * (int64_t)Tsm : 2 * capC;
     if (tid == 0) s_ctr[0] += (unsigned long long)T;
     const double t_i = ch_dl[i];
-    // ---- 1+2: candidates and memo keys ----
-    for (int c = tid; c < T; c += kDpThreads) {
+    // source level index of candidate c: last k with s_pre[k] <= c
+    auto level_of = [&](int c) {
       int lo = 0, hi = nlev - 1;
-      while (lo < hi) {  // last k with s_pre[k] <= c
+      while (lo < hi) {
         const int mid = (lo + hi + 1) / 2;
         if (s_pre[mid] <= c) lo = mid; else hi = mid - 1;
       }
-      const int lv = jlo + 1 + lo;
-      const int src = (int)(lvl_off[lv] + (c - s_pre[lo]));
-      const int j = lv - 1;
+      return lo;
+    };
+    // ---- 1: memo keys. A pair whose key (a_us, raw_us) is unique to it (host
+    // flag) has one key per surviving source bucket: key s_kpre[k] + bucket id,
+    // no table. Shared pairs use the instance's hash memo, whose first-inserted
+    // candidate decides under µs key collisions (dp_scheduler.cpp:423-435). ----
+    for (int c = tid; c < T; c += kDpThreads) {
+      const int k = level_of(c);
+      const int lv = jlo + 1 + k;
+      const int src = (int)(lvl_off[lv] + (c - s_pre[k]));
       Csrc[c] = src;
-      Cj[c] = j;
+      if (!s_sh[k]) continue;
+      const int j = lv - 1;
       const double a = (j < 0) ? I.now : ch_dl[j];
       const double raw = dmax(0.0, t_i - a);
       uint64_t k0, k1;
@@ -884,185 +940,100 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       break;
     }
     const int n_new = s_n_new;
-    SLOS_PHASE(3);  // 3: candidate enumeration + memo find-or-insert
-    // ---- 3: group new keys by anchor j and evaluate ----
-    for (int k = tid; k <= nlev; k += kDpThreads) s_jcnt[k] = 0;
-    __syncthreads();
-    for (int q = tid; q < n_new; q += kDpThreads) {
-      const int c = Memo[X0[q]].first;
-      atomicAdd(&s_jcnt[Cj[c] - jlo], 1);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int acc = 0;
-      for (int k = 0; k < nlev; ++k) { s_joff[k] = acc; acc += s_jcnt[k]; s_jcnt[k] = 0; }
-      s_ctr[1] += (unsigned long long)n_new;
-    }
-    __syncthreads();
-    for (int q = tid; q < n_new; q += kDpThreads) {
-      const int slot = X0[q];
-      const int k = Cj[Memo[slot].first] - jlo;
-      const int pos = s_joff[k] + atomicAdd(&s_jcnt[k], 1);
-      G[pos] = slot;
-    }
-    __syncthreads();
-    if (tid == 0) {  // anchors with at least one new key, ascending
-      s_e2 = 0;
-      int ng = 0;
-      for (int k = 0; k < nlev; ++k) if (s_jcnt[k] > 0) s_glist[ng++] = k;
-      s_ng = ng;
-    }
-    __syncthreads();
-    const int ng = s_ng;
-    const int nch = (D.n + 31) / 32;
-    SLOS_PHASE(4);  // 4: key grouping
-    for (int w0 = 0; w0 < ng && !s_err; w0 += prm.Gmax) {
-      const int gw = min(prm.Gmax, ng - w0);
-      if (tid == 0) s_nw = 0;  // read only after the E1 barrier below
-      // E1: group setup, one warp per anchor group
-      for (int gi = warp_id(); gi < gw; gi += kDpWarps) {
-        const int k = s_glist[w0 + gi];
-        const int j = jlo + k;
-        GroupHdr& H = ghdr[gi];
-        GapGroup g;
-        g.a = (j < 0) ? I.now : ch_dl[j];
-        const double raw = dmax(0.0, t_i - g.a);
-        const double len = quantize_gap(raw);
-        g.now = I.now;
-        g.pull = pull;
-        g.exact = I.have_running_decode != 0;
-        if (g.exact) { g.gap = len; g.dh = raw + pull; }
-        else { g.gap = quantize_gap(len); g.dh = 0.0; }
-        g.horizon = dmax(g.gap, g.dh);
-        Variant v;
-        const GroupVar ga = group_var_carve(gvbase + (size_t)gi * prm.gstride, prm.Sc, L);
-        const AnchorView av = anchor_view(anc_base + (size_t)(j + 1) * I.anchor_stride, D.n, prm.Sc, L);
-        warp_group_from_anchor(P, av, g, v, ga, prm.Sc, min_slot, ctime, ccnt, i);
-        if (lane_id() == 0) {
-          H.g = g; H.v = v; H.j = j;
-          if (v.valid && v.S <= prm.Sc && !v.dues_done) s_e2 = 1;
+    const int nkeys = KF + n_new;
+    if (tid == 0) s_ctr[1] += (unsigned long long)nkeys;
+    SLOS_PHASE(3);  // 3: candidate enumeration + memo keys
+    // key q -> (anchor j, counts, result slot)
+    auto key_of = [&](int q, int& j, uint64_t& cw, MemoEnt*& e) {
+      if (q < KF) {
+        int lo = 0, hi = nlev - 1;  // last k with s_kpre[k] <= q
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) / 2;
+          if (s_kpre[mid] <= q) lo = mid; else hi = mid - 1;
         }
+        const int lv = jlo + 1 + lo;
+        j = lv - 1;
+        cw = Bc[lvl_boff[lv] + (q - s_kpre[lo])];
+        e = nullptr;
+      } else {
+        e = &Memo[X0[q - KF]];
+        cw = e->k2;
+        j = jlo + level_of(e->first);
       }
-      __syncthreads();
-      SLOS_PHASE(5);  // 5: E1 group setup
-      // E2 (fallback when the anchor due pass did not run): member-chunk histogram
-      // tasks (group, 32 members), lanes in lockstep
-      if (s_e2) {
-      for (int t = warp_id(); t < gw * nch; t += kDpWarps) {
-        const int gi = t / nch;
-        GroupHdr& H = ghdr[gi];
-        if (!H.v.valid || H.v.S > prm.Sc || H.v.dues_done) continue;
-        const GroupVar ga = group_var_carve(gvbase + (size_t)gi * prm.gstride, prm.Sc, L);
-        const int k = (t % nch) * 32 + lane_id();
-        int64_t late = 0, dues = 0;
-        int fail = 0, spill = 0;
-        Member m;
-        m.valid = false;
-        if (k < D.n) {
-          const AnchorView av = anchor_view(anc_base + (size_t)(H.j + 1) * I.anchor_stride, D.n, prm.Sc, L);
-          m.rem = av.rm[k];
-          m.valid = m.rem > 0;
-          m.phase = av.ph[k];
-          m.backlog = av.bl[k];
-          m.tier = D.tier[k];
-        }
-        member_dues_warp(P, m, H.g, ga.ends, H.v.S, H.v.inc != 0, ga.nx, late, dues, fail, spill);
-        late = warp_sum(late);
-        dues = warp_sum(dues);
-        fail = warp_or(fail);
-        spill = warp_or(spill);
-        if (lane_id() == 0) {
-          if (late) atomicAdd((unsigned long long*)&H.v.Lx, (unsigned long long)late);
-          if (late + dues) atomicAdd((unsigned long long*)&H.v.Dx, (unsigned long long)(late + dues));
-          if (fail) atomicOr(&H.v.exact_fail, 1);
-          if (spill) atomicOr(&H.v.spill, 1);
-        }
-      }
-      __syncthreads();
-      }
-      SLOS_PHASE(6);  // 6: E2 member histograms
-      // E3a: lanes over the memo keys of this wave (thread_eval_counts); keys that
-      // need a private variant or the speculative branch are queued for E3b
-      {
-        const int kfirst = s_glist[w0], klast = s_glist[w0 + gw - 1];
-        const int q0 = s_joff[kfirst], q1 = s_joff[klast] + s_jcnt[klast];
-        unsigned long long td = 0, tsl = 0;
-        for (int q = q0 + tid; q < q1; q += kDpThreads) {
-          int lo = 0, hi = gw - 1;  // group of key q: last gi with s_joff[glist[w0+gi]] <= q
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) / 2;
-            if (s_joff[s_glist[w0 + mid]] <= q) lo = mid; else hi = mid - 1;
-          }
-          const GroupHdr& H = ghdr[lo];
-          const GroupVar ga = group_var_carve(gvbase + (size_t)lo * prm.gstride, prm.Sc, L);
-          MemoEnt* e = &Memo[G[q]];
-          const uint64_t cw = e->k2;
-          int64_t cv[kMaxTiers];
+    };
+    // ---- 2: E3a, lanes over keys (thread_eval_counts on the pair's group record);
+    // keys that need a private variant or the speculative branch go to E3b ----
+    {
+      unsigned long long td = 0, tsl = 0;
+      for (int q = tid; q < nkeys; q += kDpThreads) {
+        int j;
+        uint64_t cw;
+        MemoEnt* e;
+        key_of(q, j, cw, e);
+        const unsigned char* rec = GR + (size_t)pair_index(N, j + 1, i) * prm.grec_stride;
+        const GroupHdr& H = *(const GroupHdr*)rec;
+        const GroupVar ga = group_var_carve((unsigned char*)rec + prm.grec_hdr, prm.Sc, L);
+        int64_t cv[kMaxTiers];
 #pragma unroll
-          for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
-          EvalOut r;
-          if (thread_eval_counts(P, H.g, H.v, ga, prm.Sc, cv, min_slot, r)) {
-            Cj[atomicAdd(&s_nw, 1)] = q;
-            continue;
-          }
-          td += (unsigned long long)r.dues;
-          tsl += (unsigned long long)r.slots;
-          if (r.status) {
+        for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
+        EvalOut r;
+        if (thread_eval_counts(P, H.g, H.v, ga, prm.Sc, cv, min_slot, r)) {
+          Cj[atomicAdd(&s_nw, 1)] = q;
+          continue;
+        }
+        td += (unsigned long long)r.dues;
+        tsl += (unsigned long long)r.slots;
+        if (r.status) {
+          atomicCAS(&s_err, 0, r.status);
+          if (r.status == SLOS_ERR_CAPACITY) out->need_work = 2 * prm.Sc;
+          continue;
+        }
+        if (e) { e->has = r.has ? 1 : 0; e->val = r.budget; }
+        else Kv[q] = r.has ? r.budget : -1;
+      }
+      td = warp_sum(td);
+      tsl = warp_sum(tsl);
+      if (lane_id() == 0 && (td | tsl)) {
+        atomicAdd(&s_ctr[2], td);
+        atomicAdd(&s_ctr[3], tsl);
+      }
+    }
+    __syncthreads();
+    if (s_nw) {  // ---- E3b: one warp per queued key ----
+      const int nw = s_nw;
+      unsigned long long wd = 0, wsl = 0;
+      for (int x = warp_id(); x < nw; x += kDpWarps) {
+        if (s_err) break;
+        const int q = Cj[x];
+        int j;
+        uint64_t cw;
+        MemoEnt* e;
+        key_of(q, j, cw, e);
+        const unsigned char* rec = GR + (size_t)pair_index(N, j + 1, i) * prm.grec_stride;
+        const GroupHdr& H = *(const GroupHdr*)rec;
+        const GroupVar ga = group_var_carve((unsigned char*)rec + prm.grec_hdr, prm.Sc, L);
+        int64_t cv[kMaxTiers];
+#pragma unroll
+        for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
+        int spill = 0;
+        const EvalOut r = warp_eval_counts(P, D, H.g, H.v, ga, prm.Sc, W, cv, min_slot, &spill);
+        wd += (unsigned long long)r.dues;
+        wsl += (unsigned long long)r.slots;
+        if (r.status) {
+          if (lane_id() == 0) {
             atomicCAS(&s_err, 0, r.status);
             if (r.status == SLOS_ERR_CAPACITY) out->need_work = 2 * prm.Sc;
-            continue;
           }
-          e->has = r.has ? 1 : 0;
-          e->val = r.budget;
+          break;
         }
-        td = warp_sum(td);
-        tsl = warp_sum(tsl);
-        if (lane_id() == 0 && (td | tsl)) {
-          atomicAdd(&s_ctr[2], td);
-          atomicAdd(&s_ctr[3], tsl);
+        if (lane_id() == 0) {
+          if (e) { e->has = r.has ? 1 : 0; e->val = r.budget; }
+          else Kv[q] = r.has ? r.budget : -1;
         }
       }
-      __syncthreads();
-      // E3b: one warp per queued key
-      {
-        const int nw = s_nw;
-        unsigned long long wd = 0, wsl = 0;
-        for (int x = warp_id(); x < nw; x += kDpWarps) {
-          if (s_err) break;
-          const int q = Cj[x];
-          int lo = 0, hi = gw - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) / 2;
-            if (s_joff[s_glist[w0 + mid]] <= q) lo = mid; else hi = mid - 1;
-          }
-          const GroupHdr& H = ghdr[lo];
-          const GroupVar ga = group_var_carve(gvbase + (size_t)lo * prm.gstride, prm.Sc, L);
-          MemoEnt* e = &Memo[G[q]];
-          const uint64_t cw = e->k2;
-          int64_t cv[kMaxTiers];
-#pragma unroll
-          for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
-          int spill = 0;
-          const EvalOut r = warp_eval_counts(P, D, H.g, H.v, ga, prm.Sc, W, cv, min_slot, &spill);
-          wd += (unsigned long long)r.dues;
-          wsl += (unsigned long long)r.slots;
-          if (r.status) {
-            if (lane_id() == 0) {
-              atomicCAS(&s_err, 0, r.status);
-              if (r.status == SLOS_ERR_CAPACITY) out->need_work = 2 * prm.Sc;
-            }
-            break;
-          }
-          if (lane_id() == 0) {
-            e->has = r.has ? 1 : 0;
-            e->val = r.budget;
-          }
-        }
-        if (lane_id() == 0 && (wd | wsl)) {
-          atomicAdd(&s_ctr[2], wd);
-          atomicAdd(&s_ctr[3], wsl);
-        }
-        if (tid == 0) s_e2 = 0;  // next wave (read by E2 before the barriers above)
+      if (lane_id() == 0 && (wd | wsl)) {
+        atomicAdd(&s_ctr[2], wd);
+        atomicAdd(&s_ctr[3], wsl);
       }
       __syncthreads();
     }
@@ -1073,11 +1044,21 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     const int tier_i = ch_tr[i];
     const bool forced = ch_fc[i] != 0;
     for (int c = tid; c < T; c += kDpThreads) {
-      const MemoEnt* e = &Memo[Cme[c]];
-      int flag = 0;
       const int src = Csrc[c];
-      if (e->has) {
-        const int64_t avail = Sp_[src] + e->val;
+      const int k = level_of(c);
+      bool has;
+      int64_t val;
+      if (s_sh[k]) {
+        const MemoEnt* e = &Memo[Cme[c]];
+        has = e->has != 0;
+        val = e->val;
+      } else {
+        val = Kv[s_kpre[k] + Ssb[src]];
+        has = val >= 0;
+      }
+      int flag = 0;
+      if (has) {
+        const int64_t avail = Sp_[src] + val;
         if (avail >= ch_pf[i]) {
           const uint64_t nc = pack_add(Sc_[src], tier_i);
           if (pack_get(nc, tier_i) > 250) atomicCAS(&s_err, 0, SLOS_ERR_INTERNAL_INCONSISTENCY);
@@ -1387,8 +1368,28 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     }
     __syncthreads();
     SLOS_PHASE(9);  // 9: Pareto buckets
-    // ---- 6: arena ids and survivors ----
+    // ---- 6: arena ids, survivors and their surviving-bucket ids ----
     {
+      int32_t* hsb = Cj;   // per bucket: has a survivor -> dense id
+      int32_t* sbid = Cme;
+      for (int b = tid; b < NB; b += kDpThreads) hsb[b] = 0;
+      __syncthreads();
+      for (int c = tid; c < T; c += kDpThreads) {
+        const int fl = Cfl[c];
+        if ((fl & 2) && !(fl & 4)) hsb[Cbk[c]] = 1;
+      }
+      __syncthreads();
+      int64_t nsb = 0;
+      for (int base = 0; base < NB; base += kDpThreads) {
+        const int b = base + tid;
+        const int64_t x = b < NB ? hsb[b] : 0;
+        int64_t tot;
+        const int64_t ex = block_excl_scan(x, s_wsum, &tot);
+        if (b < NB) sbid[b] = (int32_t)(nsb + ex);
+        nsb += tot;
+      }
+      __syncthreads();
+      const int64_t bbase = s_bnext;
       int64_t carry_acc = 0, carry_sv = 0;
       const int64_t base_free = s_next_free;
       for (int base = 0; base < T; base += kDpThreads) {
@@ -1402,6 +1403,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         if (sv) {
           const int64_t dst = base_free + carry_sv + r_sv;
           if (dst < I.cap_surv) {
+            const int sb = sbid[Cbk[c]];
             Sc_[dst] = Ccn[c];
             Sm_[dst] = Cmm[c];
             Sp_[dst] = Cpb[c];
@@ -1410,6 +1412,8 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
             Spar[dst] = Csrc[c];
             Sar[dst] = (int32_t)(s_arena_next + carry_acc + r_acc);
             Sit[dst] = i;
+            Ssb[dst] = sb;
+            Bc[bbase + sb] = Ccn[c];  // every survivor of the bucket writes the same counts
           }
         }
         carry_acc += tot_acc;
@@ -1418,6 +1422,9 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       if (tid == 0) {
         lvl_off[i + 1] = base_free;
         lvl_cnt[i + 1] = (int32_t)carry_sv;
+        lvl_boff[i + 1] = (int32_t)bbase;
+        lvl_nsb[i + 1] = (int32_t)nsb;
+        s_bnext = bbase + nsb;
         s_next_free = base_free + carry_sv;
         s_arena_next += carry_acc;
         if (s_next_free > I.cap_surv) { s_err = SLOS_ERR_CAPACITY; out->need_surv = 2 * s_next_free; }

@@ -229,6 +229,12 @@ struct Blob {
   }
 };
 
+// BatchPlanner::quantize_gap (batch_planner.cpp:136-139), host copy for the pair keys.
+double host_quantize_gap(double g) {
+  if (g <= 0) return 0.0;
+  return std::floor(g * 1000.0 + 1e-6) / 1000.0;
+}
+
 bool integral(double v) { return std::isfinite(v) && v == std::floor(v) && std::fabs(v) < 4.0e15; }
 
 struct Prep {  // host-side per-instance preparation
@@ -410,7 +416,7 @@ struct Layout {
   size_t in_bytes;
   size_t s_counts, s_mem, s_pb, s_value, s_nadm, s_parent, s_arena, s_level;
   size_t c_src, c_j, c_memo, c_flag, c_bucket, c_pos, c_aux, c_counts, c_mem, c_pb, c_value, c_nadm;
-  size_t c_bkey, c_bval, memo, bq, work, anchors, scr_bytes, atask;
+  size_t c_bkey, c_bval, memo, bq, work, anchors, scr_bytes, atask, pair, groups, s_sb, s_bcnt, k_val;
   int64_t n_atask;
   size_t memo_bytes, bkey_bytes, bval_bytes;
   size_t out, sel, ids, batches, entries, out_bytes;
@@ -509,6 +515,11 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   int64_t TT = 0;
   for (int q : valid) TT += prep[q].N;
   Ly.atask = bi.add<int32_t>(2 * TT);
+  int64_t TPair = 0;
+  for (int q : valid) TPair += (int64_t)prep[q].N * (prep[q].N + 1) / 2;
+  Ly.pair = bi.add<uint8_t>(TPair);
+  const size_t grec_hdr = dp_group_hdr_bytes();
+  const size_t grec_stride = (grec_hdr + dp_group_stride(Sc, Lmax) + 127) & ~(size_t)127;
   Ly.dec_idx = bi.add<int32_t>(TD);
   Ly.dec_tier = bi.add<int32_t>(TD);
   Ly.dec_next = bi.add<double>(TD);
@@ -556,6 +567,10 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.bq = bs.add<int32_t>(nv + 2);
   Ly.work = bs.add<unsigned char>(TW);
   Ly.anchors = bs.add<unsigned char>(TA);
+  Ly.groups = bs.add<unsigned char>((size_t)TPair * grec_stride);
+  Ly.s_sb = bs.add<int32_t>(TS);
+  Ly.s_bcnt = bs.add<uint64_t>(TS);
+  Ly.k_val = bs.add<int64_t>(TCd);
   Ly.scr_bytes = bs.bytes;
   Blob bo;
   Ly.out = bo.add<OutHdr>(nv);
@@ -593,6 +608,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   int64_t* h_pre_left = (int64_t*)hp(Ly.pre_left);
   int32_t* h_run_tier = (int32_t*)hp(Ly.run_tier);
   int64_t oD = 0, oC = 0, oP = 0, oR = 0, oS = 0, oCd = 0, oM = 0, oW = 0, oSel = 0, oIds = 0, oB = 0, oE = 0, oA = 0;
+  int64_t oPair = 0;
+  uint8_t* h_pair = (uint8_t*)hp(Ly.pair);
   std::vector<double> cost(nv);
   for (int v = 0; v < nv; ++v) {
     const int q = valid[v];
@@ -631,6 +648,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     I.cap_go = cp.go;
     I.off_anchor = oA;
     I.anchor_stride = astride[q];
+    I.off_pair = oPair;
+    I.off_group = oPair * (int64_t)grec_stride;
     for (int i = 0; i < in->n_running; ++i) {
       const slos_running& r = in->running[i];
       h_run_tier[oR + i] = r.decode_tier;
@@ -673,6 +692,42 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
         h_rf[o] = enc;
       }
     }
+    {  // memo-key sharing per DP pair (j, i): the kernel's key (a_us, raw_us), or the
+       // ms-quantised gap without running decoders (dp_scheduler.cpp:423-424,
+       // batch_planner.cpp:411); a pair whose key no other pair has gets its own keys
+      struct PK { uint64_t k0, k1; int64_t idx; };
+      std::vector<PK> keys;
+      uint8_t* hpair = h_pair + oPair;
+      std::memset(hpair, 0, (size_t)pr.N * (pr.N + 1) / 2);
+      for (int i = 0; i < pr.N; ++i) {
+        for (int j = h_fl[oC + i]; j < i; ++j) {
+          const double a = j < 0 ? in->now : h_dl[oC + j];
+          const double d = h_dl[oC + i] - a;
+          const double raw = (0.0 < d) ? d : 0.0;
+          PK k;
+          if (pr.have_rd) {
+            k.k0 = (uint64_t)std::llround(a * 1e6);
+            k.k1 = (uint64_t)std::llround(raw * 1e6);
+          } else {
+            const double gap = host_quantize_gap(host_quantize_gap(raw));
+            k.k0 = 0xFFFFFFFFFFFFFFFFULL;
+            k.k1 = (uint64_t)std::llround(gap * 1000.0);
+          }
+          k.idx = pair_index(pr.N, j + 1, i);
+          keys.push_back(k);
+        }
+      }
+      std::sort(keys.begin(), keys.end(), [](const PK& x, const PK& y) {
+        return x.k0 != y.k0 ? x.k0 < y.k0 : x.k1 < y.k1;
+      });
+      for (size_t x = 0; x < keys.size();) {
+        size_t y = x + 1;
+        while (y < keys.size() && keys[y].k0 == keys[x].k0 && keys[y].k1 == keys[x].k1) ++y;
+        if (y - x > 1)
+          for (size_t z = x; z < y; ++z) hpair[keys[z].idx] = 1;
+        x = y;
+      }
+    }
     h_sf[oC + pr.N] = 0;
     for (int x = pr.N - 1; x >= 0; --x) h_sf[oC + x] = h_sf[oC + x + 1] + h_pf[oC + x];
     cost[v] = (double)(pr.n_dec + 8) * (double)(pr.N + 1) * (double)(pr.N + 1);
@@ -689,6 +744,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     oB += cp.batch;
     oE += cp.entry;
     oA += astride[q] * (pr.N + 1);
+    oPair += (int64_t)pr.N * (pr.N + 1) / 2;
   }
   {  // anchor tasks: (instance, anchor j), j = -1 .. N-2
     int32_t* t = (int32_t*)hp(Ly.atask);
@@ -772,6 +828,11 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   A.memo = (MemoEnt*)(DS + Ly.memo);
   A.work = DS + Ly.work;
   A.anchors = DS + Ly.anchors;
+  A.pair_shared = (const uint8_t*)(DI + Ly.pair);
+  A.groups = DS + Ly.groups;
+  A.s_sb = (int32_t*)(DS + Ly.s_sb);
+  A.s_bcnt = (uint64_t*)(DS + Ly.s_bcnt);
+  A.k_val = (int64_t*)(DS + Ly.k_val);
   A.bq = (int32_t*)(DS + Ly.bq);
   A.out = (OutHdr*)(DO + Ly.out);
   A.sel = (int32_t*)(DO + Ly.sel);
@@ -787,17 +848,16 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   dp.wscr_stride = stride;
   // 3 CTAs of 256 threads per SM (the register limit at 80 regs/thread)
   const size_t kSmemBudget = 74 * 1024;
-  dp.gstride = dp_group_stride(dp.Sc, Lmax);
+  dp.grec_hdr = grec_hdr;
+  dp.grec_stride = grec_stride;
   if ((e = ws.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
     return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   dp.wscr_global = (unsigned char*)ws.d_wscr.p;
   size_t& smem = ws.smem;
-  dp.Gmax = std::max(1, std::min(maxN + 1, 32));
   dp.Tsm = 512;
-  auto fit = [&](int dec) { return dp_smem_bytes(maxN, dec, dp.Sc, Lmax, dp.Gmax, dp.Tsm, &dp.overlay_bytes); };
-  while (fit(0) > kSmemBudget && (dp.Gmax > 2 || dp.Tsm > 64)) {
+  auto fit = [&](int dec) { return dp_smem_bytes(maxN, dec, dp.Sc, Lmax, dp.Tsm, &dp.overlay_bytes); };
+  while (fit(0) > kSmemBudget && dp.Tsm > 64) {
     if (dp.Tsm > 256) dp.Tsm -= 64;
-    else if (dp.Gmax > 2) dp.Gmax /= 2;
     else dp.Tsm /= 2;
   }
   smem = fit(0);

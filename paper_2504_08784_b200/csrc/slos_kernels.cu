@@ -33,19 +33,20 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactParams p) {
 }
 
 // dynamic shared memory of dp_kernel (must mirror the carve-up in dp_kernel)
-size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Gmax, int Tsm, size_t* overlay) {
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay) {
   const size_t N = (size_t)max_N;
   size_t b = 8 * (N + 1) * 4 + 8 * (N + 2) + 4 * (N + 2) * 3 + 16;   // chain
   b += (size_t)max_dec_staged * 28 + 16;                              // decoders
   b += 8 * (size_t)Sc * kDpWarps + 16;                                // placement temporaries
-  b += sizeof(GroupHdr) * (size_t)Gmax + 128;                         // group headers
-  const size_t ov = std::max(group_var_stride(Sc, L) * (size_t)Gmax, (size_t)76 * (size_t)Tsm);
+  const size_t ov = (size_t)76 * (size_t)Tsm;
   *overlay = ov;
-  b += ov + 16;
+  b += ov + 16;                                                       // candidate states
   b += (size_t)20 * (size_t)Tsm;                                      // kept candidate arrays
-  b += sizeof(double) * (size_t)L * (size_t)Sc + 16;                  // canonical due times
+  (void)L;
   return b + 64;
 }
+
+size_t dp_group_hdr_bytes() { return (sizeof(GroupHdr) + 127) & ~(size_t)127; }
 
 size_t dp_anchor_stride(int R, int Sc, int L, int N) { return anchor_stride_bytes(R, Sc, L, N);
 }
