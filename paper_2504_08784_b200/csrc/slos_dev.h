@@ -170,6 +170,8 @@ struct BatchArgs {
   int32_t* s_sb;               // survivor: dense id of its Pareto bucket within its level
   uint64_t* s_bcnt;            // per level, per surviving bucket: its count vector
   int64_t* k_val;              // per level: fresh-pair key results (budget, or -1 = nullopt)
+  double* ctime;               // per instance: canonical due times [Lmax][Sc] (anchor_kernel)
+  int32_t* ccnt;               // per instance: canonical due counts [kMaxTiers]
   int32_t* bq;       // build queue: fallback instances first (n_inst + 2 ints; [0],[1] = counters)
   OutHdr* out;
 };
@@ -221,9 +223,11 @@ struct DpParams {
   size_t grec_hdr;          // header bytes before the variant arrays
 };
 
-// Triangular index of the pair (anchor a = j+1, chain item i), 0 <= a <= i < N.
+// Triangular index of the pair (anchor a = j+1, chain item i), 0 <= a <= i < N:
+// row-major by item, so one DP level's pairs (a = floor+1 .. i) are contiguous.
 __host__ __device__ __forceinline__ int64_t pair_index(int N, int a, int i) {
-  return (int64_t)a * N - (int64_t)a * (a - 1) / 2 + (i - a);
+  (void)N;
+  return (int64_t)i * (i + 1) / 2 + a;
 }
 
 }  // namespace slos

@@ -656,12 +656,49 @@ __global__ void __launch_bounds__(kDpThreads) anchor_kernel(DpParams prm) {
   block_build_anchor(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), Sc, ctime, ccnt,
                      min_slot, s_wsum);
   block_anchor_dues(P, D, av, j, N, ch_dl, ch_fl, a, pull, min_slot, Sc, scr, prm.anchor_scr_bytes);
-  // the gap group of every pair (j, i) this anchor opens (the DP's E1/E2, moved off
-  // its critical path): one warp per pair, record written to HBM
-  const int nG = N - j - 1;
-  for (int gi = warp_id(); gi < nG; gi += kDpWarps) {
-    const int i = j + 1 + gi;
-    if (ch_fl[i] > j) continue;  // never a DP transition
+  if (j < 0) {  // the instance's canonical due times, for group_kernel
+    double* gct = A.ctime + (size_t)v * prm.Lmax * Sc;
+    for (int x = tid; x < L * Sc; x += kDpThreads) gct[x] = ctime[x];
+    if (tid < kMaxTiers) A.ccnt[v * kMaxTiers + tid] = tid < L ? ccnt[tid] : 0;
+  }
+}
+
+// Gap group records (the DP's E1/E2, off its critical path): one warp per pair
+// (j, i), i > j >= floor_at[i], built from anchor j's cache and written to HBM.
+constexpr int kGroupWarps = 4;
+__global__ void __launch_bounds__(32 * kGroupWarps) group_kernel(DpParams prm) {
+  __shared__ PlannerDev sP;
+  __shared__ InstDev sI;
+  const BatchArgs& A = prm.a;
+  const int vi = A.atask[2 * blockIdx.x], j = A.atask[2 * blockIdx.x + 1];
+  if (threadIdx.x == 0) {
+    sI = A.inst[vi];
+    sP = A.planners[sI.planner];
+  }
+  __syncthreads();
+  const PlannerDev& P = sP;
+  const InstDev& I = sI;
+  const int N = I.N;
+  const int L = P.L;
+  const int Sc = prm.Sc;
+  const int gi = blockIdx.y * kGroupWarps + warp_id();
+  if (gi >= N - j - 1) return;
+  const int i = j + 1 + gi;
+  const double* ch_dl = A.ch_deadline + I.off_chain;
+  if (A.ch_floor[I.off_chain + i] > j) return;  // never a DP transition
+  DecView D;
+  D.n = I.have_running_decode ? I.n_dec : 0;
+  D.next = A.dec_next + I.off_dec;
+  D.backlog = A.dec_backlog + I.off_dec;
+  D.rem = A.dec_rem + I.off_dec;
+  D.tier = A.dec_tier + I.off_dec;
+  const double* ctime = A.ctime + (size_t)vi * prm.Lmax * Sc;
+  const int* ccnt = A.ccnt + vi * kMaxTiers;
+  const double min_slot = plan_predict(P, 1, 0);
+  const double pull = min_slot;
+  const double a = (j < 0) ? I.now : ch_dl[j];
+  const AnchorView av = anchor_view(A.anchors + I.off_anchor + (size_t)(j + 1) * I.anchor_stride, D.n, Sc, L);
+  {
     unsigned char* rec = A.groups + I.off_group + (size_t)pair_index(N, j + 1, i) * prm.grec_stride;
     GroupHdr* H = (GroupHdr*)rec;
     const GroupVar ga = group_var_carve(rec + prm.grec_hdr, Sc, L);
@@ -706,6 +743,7 @@ __global__ void __launch_bounds__(kDpThreads) anchor_kernel(DpParams prm) {
     if (lane_id() == 0) { H->g = g; H->v = v; H->j = j; }
   }
 }
+
 
 #ifndef SLOS_DP_MIN_BLOCKS
 #define SLOS_DP_MIN_BLOCKS 3
@@ -909,6 +947,19 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       }
       return lo;
     };
+    // the level's gap group records (pairs (jlo .. i-1, i), contiguous) staged into
+    // the candidate-state overlay, which is free until step 4
+    const bool staged = (size_t)nlev * prm.grec_stride <= prm.overlay_bytes;
+    const unsigned char* GRl = GR + (size_t)pair_index(N, jlo + 1, i) * prm.grec_stride;
+    if (staged) {
+      const uint4* src4 = (const uint4*)GRl;
+      uint4* dst4 = (uint4*)ovl;
+      const int n4 = (int)((size_t)nlev * prm.grec_stride / 16);
+      for (int x = tid; x < n4; x += kDpThreads) dst4[x] = src4[x];
+    }
+    auto rec_of = [&](int j) -> const unsigned char* {
+      return (staged ? (const unsigned char*)ovl : GRl) + (size_t)(j - jlo) * prm.grec_stride;
+    };
     // ---- 1: memo keys. A pair whose key (a_us, raw_us) is unique to it (host
     // flag) has one key per surviving source bucket: key s_kpre[k] + bucket id,
     // no table. Shared pairs use the instance's hash memo, whose first-inserted
@@ -970,7 +1021,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         uint64_t cw;
         MemoEnt* e;
         key_of(q, j, cw, e);
-        const unsigned char* rec = GR + (size_t)pair_index(N, j + 1, i) * prm.grec_stride;
+        const unsigned char* rec = rec_of(j);
         const GroupHdr& H = *(const GroupHdr*)rec;
         const GroupVar ga = group_var_carve((unsigned char*)rec + prm.grec_hdr, prm.Sc, L);
         int64_t cv[kMaxTiers];
@@ -1009,7 +1060,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         uint64_t cw;
         MemoEnt* e;
         key_of(q, j, cw, e);
-        const unsigned char* rec = GR + (size_t)pair_index(N, j + 1, i) * prm.grec_stride;
+        const unsigned char* rec = rec_of(j);
         const GroupHdr& H = *(const GroupHdr*)rec;
         const GroupVar ga = group_var_carve((unsigned char*)rec + prm.grec_hdr, prm.Sc, L);
         int64_t cv[kMaxTiers];

@@ -416,7 +416,7 @@ struct Layout {
   size_t in_bytes;
   size_t s_counts, s_mem, s_pb, s_value, s_nadm, s_parent, s_arena, s_level;
   size_t c_src, c_j, c_memo, c_flag, c_bucket, c_pos, c_aux, c_counts, c_mem, c_pb, c_value, c_nadm;
-  size_t c_bkey, c_bval, memo, bq, work, anchors, scr_bytes, atask, pair, groups, s_sb, s_bcnt, k_val;
+  size_t c_bkey, c_bval, memo, bq, work, anchors, scr_bytes, atask, pair, groups, s_sb, s_bcnt, k_val, ctime, ccnt;
   int64_t n_atask;
   size_t memo_bytes, bkey_bytes, bval_bytes;
   size_t out, sel, ids, batches, entries, out_bytes;
@@ -436,6 +436,7 @@ struct Workspace {
   DpParams dp;
   size_t smem = 0;
   size_t anchor_smem = 0;
+  int maxN = 0;
   cudaStream_t stream = nullptr;
   bool uploaded = false;
   int n_total = 0;
@@ -571,6 +572,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.s_sb = bs.add<int32_t>(TS);
   Ly.s_bcnt = bs.add<uint64_t>(TS);
   Ly.k_val = bs.add<int64_t>(TCd);
+  Ly.ctime = bs.add<double>((size_t)nv * Lmax * Sc);
+  Ly.ccnt = bs.add<int32_t>((size_t)nv * kMaxTiers);
   Ly.scr_bytes = bs.bytes;
   Blob bo;
   Ly.out = bo.add<OutHdr>(nv);
@@ -833,6 +836,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   A.s_sb = (int32_t*)(DS + Ly.s_sb);
   A.s_bcnt = (uint64_t*)(DS + Ly.s_bcnt);
   A.k_val = (int64_t*)(DS + Ly.k_val);
+  A.ctime = (double*)(DS + Ly.ctime);
+  A.ccnt = (int32_t*)(DS + Ly.ccnt);
   A.bq = (int32_t*)(DS + Ly.bq);
   A.out = (OutHdr*)(DO + Ly.out);
   A.sel = (int32_t*)(DO + Ly.sel);
@@ -874,6 +879,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   if (fit(maxDec) <= kSmemBudget) dp.dec_smem_max = maxDec;
   smem = fit(dp.dec_smem_max);
   ws.anchor_smem = anchor_smem_bytes(maxN, dp.Sc, Lmax, &dp.anchor_scr_bytes);
+  ws.maxN = maxN;
   ws.valid = valid;
   ws.nv = nv;
   ws.uploaded = true;
@@ -901,6 +907,8 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     if (!ws.ev[k]) cudaEventCreate(&ws.ev[k]);
   cudaEventRecord(ws.ev[0], s);
   if ((e = launch_anchor(dp, ws.A.n_atask, ws.anchor_smem, s)) != cudaSuccess)
+    return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  if ((e = launch_group(dp, ws.A.n_atask, ws.maxN, s)) != cudaSuccess)
     return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   cudaEventRecord(ws.ev[3], s);
   if ((e = launch_dp(dp, nv, smem, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));

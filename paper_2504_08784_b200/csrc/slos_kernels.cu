@@ -75,6 +75,13 @@ cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream
   return cudaGetLastError();
 }
 
+cudaError_t launch_group(const DpParams& prm, int n_atask, int max_N, cudaStream_t s) {
+  if (n_atask <= 0 || max_N <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)n_atask, (unsigned)((max_N + kGroupWarps - 1) / kGroupWarps));
+  group_kernel<<<grid, 32 * kGroupWarps, 0, s>>>(prm);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s) {
   if (grid <= 0) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(dp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

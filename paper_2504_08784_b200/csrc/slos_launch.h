@@ -32,6 +32,7 @@ size_t dp_warp_scr_stride(int Sc, int L);
 cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
 size_t anchor_smem_bytes(int max_N, int Sc, int L, size_t* scr);
 cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_group(const DpParams& prm, int n_atask, int max_N, cudaStream_t s);
 cudaError_t launch_build(const BuildParams& prm, int grid, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& prm, int grid, cudaStream_t s);
 cudaError_t launch_gap(const GapParams& prm, int grid, cudaStream_t s);
