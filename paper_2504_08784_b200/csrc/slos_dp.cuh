@@ -290,7 +290,7 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
   const int lane = lane_id(), w = warp_id();
   __shared__ unsigned s_mask;
   __shared__ int s_nex, s_hb, s_abl;
-  __shared__ unsigned long long s_pt[kMaxTiers];
+  __shared__ unsigned s_pt[kMaxTiers];
   __shared__ double s_minph[kDpWarps];
   if (tid == 0) {
     s_mask = 0; s_nex = 0; s_hb = 0; s_abl = 0;
@@ -300,20 +300,31 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
   double minph = INFINITY;
   unsigned mask = 0;
   int nex = 0, hb = 0, abl = 0;
+  uint64_t pt8 = 0;  // per-thread member count per tier, 8 bits each (<= 255 members per thread)
+  int it = 0;
   for (int k = tid; k < D.n; k += kDpThreads) {
+    if ((++it & 0xff) == 0) {  // keep every 8-bit tier count below 256
+      for (int l = 0; l < P.L; ++l)
+        if ((pt8 >> (8 * l)) & 0xffu) atomicAdd(&s_pt[l], (unsigned)((pt8 >> (8 * l)) & 0xffu));
+      pt8 = 0;
+    }
     const Member m = member_at(P, D.next[k], D.backlog[k], D.rem[k], D.tier[k], now, a, pull);
     av.ph[k] = m.valid ? m.phase : 0.0;
     av.bl[k] = m.valid ? m.backlog : 0;
     av.rm[k] = m.valid ? m.rem : 0;
     if (!m.valid) continue;
     ++nex;
-    atomicAdd(&s_pt[m.tier], 1ull);
+    pt8 += 1ull << (8 * m.tier);
     if (m.backlog > 0) hb = 1;
     if (m.rem > 0) {
       mask |= 1u << m.tier;
       if (m.backlog > 0) abl = 1;
       minph = dmin(minph, m.phase);
     }
+  }
+  for (int l = 0; l < P.L; ++l) {
+    const unsigned cl = __reduce_add_sync(0xffffffffu, (unsigned)((pt8 >> (8 * l)) & 0xffu));
+    if (lane == 0 && cl) atomicAdd(&s_pt[l], cl);
   }
   mask = __reduce_or_sync(0xffffffffu, mask);
   nex = __reduce_add_sync(0xffffffffu, (unsigned)nex);
@@ -604,7 +615,7 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
 // group's tail (block_anchor_dues) -- is independent of the DP's states, so all
 // anchors of all instances are built up front, one CTA per (instance, anchor),
 // instead of on the DP's level-sequential critical path.
-__global__ void __launch_bounds__(kDpThreads) anchor_kernel(DpParams prm) {
+__global__ void __launch_bounds__(kDpThreads, 3) anchor_kernel(DpParams prm) {
   extern __shared__ __align__(16) unsigned char asm_[];
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;
@@ -666,7 +677,7 @@ __global__ void __launch_bounds__(kDpThreads) anchor_kernel(DpParams prm) {
 // Gap group records (the DP's E1/E2, off its critical path): one warp per pair
 // (j, i), i > j >= floor_at[i], built from anchor j's cache and written to HBM.
 constexpr int kGroupWarps = 4;
-__global__ void __launch_bounds__(32 * kGroupWarps) group_kernel(DpParams prm) {
+__global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm) {
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;
   const BatchArgs& A = prm.a;

@@ -828,9 +828,10 @@ __device__ inline int thread_place_budget(const PlannerDev& P, const Variant& v,
   if (v.Lx == 0) {
     bool ok = true;
     int64_t b = 0;
+#pragma unroll 4
     for (int s = 0; s < S; ++s) {
       const int64_t f = cap[s] - dues_at(s);
-      if (f < 0) { ok = false; break; }
+      ok = ok && f >= 0;
       b += imin(f, P.max_chunk);
     }
     if (ok) { *budget = b; return 1; }

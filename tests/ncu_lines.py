@@ -1,6 +1,6 @@
 """Per-CUDA-source-line hot spots from an ncu report (cuda,sass source view).
 
-  python tests/ncu_lines.py gpurun_out/<rep>.ncu-rep [top]
+  python tests/ncu_lines.py gpurun_out/<rep>.ncu-rep [top] [kernel-regex]
 
 Prints the source lines with the most warp-stall samples and instructions, plus
 each line's dominant stall reasons (needs -lineinfo at compile time).
@@ -14,7 +14,8 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+    kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+    txt = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = []
     fname = "?"
