@@ -1,6 +1,6 @@
 """Distil ncu captures (gpurun_out/*.ncu-rep + launches.csv) into profiles/.
 
-  python tests/ncu_summary.py <tag>     -> profiles/<tag>_ncu_summary.{json,md}
+  python tests/ncu_summary.py <tag> [report]  -> profiles/<tag>_ncu_summary.{json,md}
                                            and profiles/ncu_summary.json (read by bench.py)
 """
 import csv
@@ -35,15 +35,22 @@ METRICS = [
 
 
 def raw(rep):
+    """{kernel short name: {metric: {value, unit}}} for every launch in the report
+    (the last launch of a kernel wins)."""
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    d = {}
-    for i, n in enumerate(hdr):
-        if n in METRICS:
-            d[n] = {"value": vals[i], "unit": units[i]}
-    return d
+    hdr, units = rows[0], rows[1]
+    ki = hdr.index("Kernel Name")
+    out = {}
+    for vals in rows[2:]:
+        name = vals[ki].split("(")[0].split("::")[-1]
+        d = {}
+        for i, n in enumerate(hdr):
+            if n in METRICS:
+                d[n] = {"value": vals[i], "unit": units[i]}
+        out[name] = d
+    return out
 
 
 def to_bytes(m):
@@ -69,10 +76,9 @@ def launches(path):
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "latest"
     summ = {"tag": tag, "kernels": {}}
-    for name, rep in (("dp_kernel", "prof_dp.ncu-rep"), ("build_kernel", "prof_build.ncu-rep")):
-        p = os.path.join(OUT, rep)
-        if os.path.exists(p):
-            m = raw(p)
+    rep = sys.argv[2] if len(sys.argv) > 2 else os.path.join(OUT, "prof.ncu-rep")
+    if os.path.exists(rep):
+        for name, m in raw(rep).items():
             summ["kernels"][name] = {k: v["value"] + " " + v["unit"] for k, v in m.items()}
             if "dram__bytes_read.sum" in m:
                 summ["kernels"][name]["dram_bytes_per_launch"] = to_bytes(m["dram__bytes_read.sum"]) + \
@@ -91,11 +97,13 @@ def main():
     os.makedirs(PROF, exist_ok=True)
     with open(os.path.join(PROF, f"{tag}_ncu_summary.json"), "w") as f:
         json.dump(summ, f, indent=1)
-    dp = summ["kernels"].get("dp_kernel", {})
+    stage = [summ["kernels"].get(k, {}).get("dram_bytes_per_launch") for k in
+             ("anchor_kernel", "group_kernel", "dp_kernel")]
     with open(os.path.join(PROF, "ncu_summary.json"), "w") as f:
-        json.dump({"kernel": "dp_kernel", "instances": 1024,
-                   "dram_bytes_per_launch": dp.get("dram_bytes_per_launch"), "source": f"{tag}_ncu_summary.json"},
-                  f, indent=1)
+        json.dump({"kernel": "dp_stage", "instances": 1024,
+                   "dram_bytes_per_launch": sum(stage) if all(x is not None for x in stage) else None,
+                   "per_kernel": dict(zip(("anchor_kernel", "group_kernel", "dp_kernel"), stage)),
+                   "source": f"{tag}_ncu_summary.json"}, f, indent=1)
     lines = [f"# ncu summary ({tag})", ""]
     for k, d in summ["kernels"].items():
         lines.append(f"## {k}")
