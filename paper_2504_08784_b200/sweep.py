@@ -46,9 +46,10 @@ class ShardSpec:
 class ShardSolver:
     """Device-resident shard of planning instances behind one slos_workspace."""
 
-    def __init__(self, lib, spec: ShardSpec, seeds, unit_value: bool = False):
+    def __init__(self, lib, spec: ShardSpec, seeds, unit_value: bool = False, batch: InstanceBatch = None):
         self.lib = lib
-        self.batch = InstanceBatch.stress(spec.family, list(seeds), spec.slo)
+        # a stress-family shard (seeds) or any prepared batch (e.g. a recorded corpus)
+        self.batch = batch if batch is not None else InstanceBatch.stress(spec.family, list(seeds), spec.slo)
         self.handle = _Handle(lib, spec.model, spec.slo, spec.cfg)
         self.n = self.batch.n
         self.unit_value = 1 if unit_value else 0

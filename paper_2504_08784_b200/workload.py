@@ -192,6 +192,74 @@ class InstanceBatch:
         return cls(inp, run, pen, blob, offs)
 
 
+    @classmethod
+    def from_corpus(cls, buf: bytes) -> "InstanceBatch":
+        """Parse a recorded-input corpus (the binary layout written by the simulator
+        recorder, oracle/ref_sim.cpp slos_sim_recorded_write) into C-ABI arrays."""
+        import struct
+        run_rec = np.dtype([("prefill_remaining", "<i8"), ("prefill_deadline", "<f8"), ("decode_tier", "<i4"),
+                            ("pad", "<i4"), ("next_due_s", "<f8"), ("backlog", "<i8"),
+                            ("decode_remaining", "<i8")])
+        pen_rec = np.dtype([("prefill_deadline", "<f8"), ("prefill_tokens", "<i8"), ("decode_tier", "<i4"),
+                            ("pad", "<i4"), ("memory_units", "<i8"), ("value", "<f8")])
+        heads, runs, pens, ids = [], [], [], []
+        off = 0
+        while off < len(buf):
+            now, th, mt, msr, nr, npn = struct.unpack_from("<ddqqii", buf, off)
+            off += 40
+            runs.append(np.frombuffer(buf, run_rec, nr, off))
+            off += nr * run_rec.itemsize
+            pens.append(np.frombuffer(buf, pen_rec, npn, off))
+            off += npn * pen_rec.itemsize
+            for _ in range(nr + npn):
+                (ln,) = struct.unpack_from("<H", buf, off)
+                ids.append(bytes(buf[off + 2:off + 2 + ln]) + b"\0")
+                off += 2 + ln
+            heads.append((now, th, mt, msr, nr, npn))
+        blob = np.frombuffer(b"".join(ids) + b"\0", np.uint8).copy()
+        offs = np.concatenate([[0], np.cumsum([len(x) for x in ids])[:-1]]).astype(np.uint64)
+        base = np.uint64(blob.ctypes.data)
+        R = sum(h[4] for h in heads)
+        Pn = sum(h[5] for h in heads)
+        run = np.zeros(max(1, R), abi.RUNNING_DTYPE)
+        pen = np.zeros(max(1, Pn), abi.PENDING_DTYPE)
+        inp = np.zeros(len(heads), abi.INPUT_DTYPE)
+        r0 = p0 = k = 0
+        for n_, (now, th, mt, msr, nr, npn) in enumerate(heads):
+            rr, pr = runs[n_], pens[n_]
+            dst = run[r0:r0 + nr]
+            dst["id"] = base + offs[k:k + nr]
+            for f in ("prefill_remaining", "prefill_deadline", "decode_tier", "next_due_s", "backlog",
+                      "decode_remaining"):
+                dst[f] = rr[f]
+            k += nr
+            dp = pen[p0:p0 + npn]
+            dp["id"] = base + offs[k:k + npn]
+            for f in ("prefill_deadline", "prefill_tokens", "decode_tier", "memory_units", "value"):
+                dp[f] = pr[f]
+            k += npn
+            inp[n_] = (now, run.ctypes.data + r0 * run.itemsize, nr, npn, pen.ctypes.data + p0 * pen.itemsize,
+                       mt, msr, th)
+            r0 += nr
+            p0 += npn
+        return cls(inp, run, pen, blob, offs)
+
+    def tiled(self, reps: int) -> "InstanceBatch":
+        """The same instances repeated `reps` times (shares every request array)."""
+        return InstanceBatch(np.tile(self.inputs, reps), self.running, self.pending, self._blob, self._id_offsets)
+
+    def subset(self, idx) -> "InstanceBatch":
+        return InstanceBatch(self.inputs[np.asarray(idx)].copy(), self.running, self.pending, self._blob,
+                             self._id_offsets)
+
+
+def load_corpus(path: str) -> InstanceBatch:
+    """A gzip'd recorded-input corpus (tests/golden/c5_*.bin.gz)."""
+    import gzip
+    with gzip.open(path, "rb") as f:
+        return InstanceBatch.from_corpus(f.read())
+
+
 # --------------------------------------------- brute-force oracle adapters ---
 
 ORACLE_REC_LEN = 41  # oracle/ref_tools.cpp encode()

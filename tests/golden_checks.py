@@ -54,3 +54,26 @@ def check_fuzz(lib, seeds=None):
         h = _Handle(lib, terms, slo, cfg)
         _cmp(plan_one(lib, h.ptr, ci.c, False), case["value"], f"fuzz {case['seed']} value")
         _cmp(plan_one(lib, h.ptr, ci.c, True), case["throughput"], f"fuzz {case['seed']} throughput")
+
+
+def check_c5(lib, groups=("ar", "spec"), limit=None):
+    """The C5 sweep corpus: inputs recorded from the reference simulator
+    (oracle/make_corpus.py), reference results as goldens."""
+    import os
+    from golden_io import GOLDEN
+    from paper_2504_08784_b200.planner import PerfTerm
+    meta = load("c5")
+    n = 0
+    for g in groups:
+        G = meta["groups"][g]
+        b = W.load_corpus(os.path.join(GOLDEN, f"c5_{g}.bin.gz"))
+        if limit:
+            b = b.subset(range(min(limit, b.n)))
+        cfg = PlannerConfig(max_chunk_tokens=2048, max_batch_tokens=16384, speculative=G["speculative"],
+                            spec_alpha=0.8, spec_max_len=8, plan_margin=0.0)
+        h = _Handle(lib, [PerfTerm(*t) for t in meta["model"]], W.TWO_TIER_SLO, cfg)
+        res = plan_many(lib, h.ptr, b)
+        for k, got in enumerate(res):
+            _cmp(got, G["ref"][k], f"c5 {g} instance {k}")
+        n += len(res)
+    return n

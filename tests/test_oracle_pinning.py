@@ -8,7 +8,7 @@ import os
 
 import pytest
 
-from golden_checks import check_fuzz, check_oracle_instances, check_stress
+from golden_checks import check_c5, check_fuzz, check_oracle_instances, check_stress
 from golden_io import load
 from paper_2504_08784_b200 import abi
 
@@ -19,6 +19,11 @@ def test_oracle_matches_reference_on_brute_force_families():
 
 def test_oracle_matches_reference_on_stress_families():
     check_stress(abi.oracle(), families=("C1", "LAT", "C2", "C3"))
+
+
+def test_oracle_matches_reference_on_c5_simulator_corpus():
+    # 4,096 inputs recorded from the reference simulator over the sweep grid
+    assert check_c5(abi.oracle()) == 4096
 
 
 def test_oracle_matches_reference_on_fuzz():

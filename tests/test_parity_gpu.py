@@ -3,7 +3,7 @@ output field of plan() -- admitted/declined id sequences, admitted_value bits,
 running_set_infeasible, every batch and entry, exact_until_s."""
 import pytest
 
-from golden_checks import check_fuzz, check_oracle_instances, check_stress
+from golden_checks import check_c5, check_fuzz, check_oracle_instances, check_stress
 from parity import diff, plan_many, plan_one
 from paper_2504_08784_b200 import abi
 from paper_2504_08784_b200 import workload as W
@@ -23,6 +23,11 @@ def test_brute_force_families_match_reference():
 @pytest.mark.parametrize("fam", ["C1", "LAT", "C2", "C3", "C4"])
 def test_stress_families_match_reference(fam):
     check_stress(abi.product(), families=(fam,))
+
+
+def test_c5_simulator_corpus_matches_reference():
+    # C5: inputs recorded from the reference simulator's sweep grid, batched
+    assert check_c5(abi.product()) == 4096
 
 
 def test_fuzz_matches_reference():
