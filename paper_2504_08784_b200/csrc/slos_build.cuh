@@ -571,37 +571,32 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
   }
 }
 
-// Plan reconstruction granularity (SLOS_BUILD_MODE): 0 = one warp per instance,
-// 4 instances per CTA; 1 = one 128-thread CTA per instance; 2 = 256 threads.
-#ifndef SLOS_BUILD_MODE
-#define SLOS_BUILD_MODE 1
-#endif
-#if SLOS_BUILD_MODE == 0
+// Plan reconstruction granularity, chosen per instance by the host: small
+// instances (few decoders) are built by one warp each, four per CTA, without CTA
+// barriers (build_kernel_warp, queue 0); large ones by a 128-thread CTA each
+// (build_kernel, queue 1).
 constexpr int kBuildWarps = 4;
-constexpr int kBuildThreads = 32 * kBuildWarps;
-constexpr int kBuildPerCta = kBuildWarps;
-#else
-constexpr int kBuildThreads = SLOS_BUILD_MODE == 1 ? 128 : 256;
-constexpr int kBuildPerCta = 1;
+constexpr int kBuildThreads = 128;
+#ifndef SLOS_BUILD_MIN_BLOCKS
+#define SLOS_BUILD_MIN_BLOCKS 3
 #endif
 
-#ifndef SLOS_BUILD_MIN_BLOCKS
-#define SLOS_BUILD_MIN_BLOCKS 1
-#endif
-__global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_kernel(BuildParams prm) {
+__global__ void __launch_bounds__(32 * kBuildWarps, 2) build_kernel_warp(BuildParams prm) {
   const BatchArgs& A = prm.a;
-#if SLOS_BUILD_MODE == 0
   __shared__ BuildShared shs[kBuildWarps];
   extern __shared__ __align__(16) unsigned char bsm[];
   const int idx = blockIdx.x * kBuildWarps + warp_id();
-  if (idx >= A.n_inst) return;  // whole warp; the engine never uses CTA barriers here
+  if (idx >= A.n_small) return;  // whole warp; the engine never uses CTA barriers here
   const int64_t per = (int64_t)(prm.smem_bytes / kBuildWarps) & ~(int64_t)255;
-  build_instance<WarpGrp>(A, shs[warp_id()], A.bq[2 + idx], bsm + per * warp_id(), per, prm.phase_cycles);
-#else
+  build_instance<WarpGrp>(A, shs[warp_id()], A.bq[4 + idx], bsm + per * warp_id(), per, prm.phase_cycles);
+}
+
+__global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_kernel(BuildParams prm) {
+  const BatchArgs& A = prm.a;
   __shared__ BuildShared sh;
   extern __shared__ __align__(16) unsigned char bsm[];
-  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.bq[2 + blockIdx.x], bsm, (int64_t)prm.smem_bytes, prm.phase_cycles);
-#endif
+  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.bq[4 + A.n_small + blockIdx.x], bsm,
+                                           (int64_t)prm.smem_bytes, prm.phase_cycles);
 }
 
 // ---- standalone gap queries (slos_tile_gap_batch) ----------------------------

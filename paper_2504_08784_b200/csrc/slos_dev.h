@@ -59,6 +59,7 @@ struct InstDev {
   int32_t last_forced;
   int32_t have_running_decode;
   int32_t values_integral;  // all chain values integral -> eps ties impossible
+  int32_t build_small;      // plan reconstruction by one warp (small instance)
   int64_t off_dec;     // into dec_* arrays
   int64_t off_chain;   // into ch_* arrays (N items, suffix has N+1)
   int64_t off_pre;     // into pre_* arrays
@@ -172,7 +173,9 @@ struct BatchArgs {
   int64_t* k_val;              // per level: fresh-pair key results (budget, or -1 = nullopt)
   double* ctime;               // per instance: canonical due times [Lmax][Sc] (anchor_kernel)
   int32_t* ccnt;               // per instance: canonical due counts [kMaxTiers]
-  int32_t* bq;       // build queue: fallback instances first (n_inst + 2 ints; [0],[1] = counters)
+  int32_t* bq;       // build queues (4 counters, then n_small + n_large ints): per queue,
+                     // fallback instances from the front, the rest from the back
+  int32_t n_small;   // instances reconstructed one warp each (build_kernel_warp), queue 0
   OutHdr* out;
 };
 
@@ -222,6 +225,17 @@ struct DpParams {
   size_t grec_stride;       // bytes per pair group record
   size_t grec_hdr;          // header bytes before the variant arrays
 };
+
+// Push an instance onto its plan-reconstruction queue: queue 0 (warp-built, small
+// instances) occupies bq[4 .. 4+n_small), queue 1 the rest; fallback instances (a
+// long sequential batch loop) are taken first, from the front.
+__device__ __forceinline__ void build_queue_push(const BatchArgs& A, int inst, bool small, bool front) {
+  const int base = small ? 4 : 4 + A.n_small;
+  const int n = small ? A.n_small : A.n_inst - A.n_small;
+  int32_t* c = A.bq + (small ? 0 : 2);
+  if (front) A.bq[base + atomicAdd(&c[0], 1)] = inst;
+  else A.bq[base + n - 1 - atomicAdd(&c[1], 1)] = inst;
+}
 
 // Triangular index of the pair (anchor a = j+1, chain item i), 0 <= a <= i < N:
 // row-major by item, so one DP level's pairs (a = floor+1 .. i) are contiguous.

@@ -1499,7 +1499,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   if (s_err) {
     if (tid == 0) {
       out->status = s_err;
-      A.bq[2 + A.n_inst - 1 - atomicAdd(&A.bq[1], 1)] = inst;
+      build_queue_push(A, inst, I.build_small != 0, false);
     }
     return;
   }
@@ -1620,8 +1620,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     out->status = 0;
     // plan-reconstruction queue: instances that fall back (a long sequential batch
     // loop) are queued from the front, the rest from the back
-    if (best < 0) A.bq[2 + atomicAdd(&A.bq[0], 1)] = inst;
-    else A.bq[2 + A.n_inst - 1 - atomicAdd(&A.bq[1], 1)] = inst;
+    build_queue_push(A, inst, I.build_small != 0, best < 0);
   }
   SLOS_PHASE(11);  // 11: terminal selection + backtrack
 }

@@ -235,6 +235,17 @@ double host_quantize_gap(double g) {
   return std::floor(g * 1000.0 + 1e-6) / 1000.0;
 }
 
+// Instances with at most this many running decoders are reconstructed by one warp
+// (measured crossover: warp-built C1 (48 decoders) and the C5 corpus are faster,
+// block-built C2 (240 decoders) is faster). SLOS_BUILD_WARP_MAX_DEC overrides.
+int build_warp_max_dec() {
+  static const int v = [] {
+    const char* e = std::getenv("SLOS_BUILD_WARP_MAX_DEC");
+    return e ? std::atoi(e) : 96;
+  }();
+  return v;
+}
+
 bool integral(double v) { return std::isfinite(v) && v == std::floor(v) && std::fabs(v) < 4.0e15; }
 
 struct Prep {  // host-side per-instance preparation
@@ -565,7 +576,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.c_bkey = bs.add<uint64_t>(2 * TCd);
   Ly.c_bval = bs.add<int32_t>(2 * TCd);
   Ly.memo = bs.add<MemoEnt>(TM);
-  Ly.bq = bs.add<int32_t>(nv + 2);
+  Ly.bq = bs.add<int32_t>(nv + 4);
   Ly.work = bs.add<unsigned char>(TW);
   Ly.anchors = bs.add<unsigned char>(TA);
   Ly.groups = bs.add<unsigned char>((size_t)TPair * grec_stride);
@@ -612,6 +623,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   int32_t* h_run_tier = (int32_t*)hp(Ly.run_tier);
   int64_t oD = 0, oC = 0, oP = 0, oR = 0, oS = 0, oCd = 0, oM = 0, oW = 0, oSel = 0, oIds = 0, oB = 0, oE = 0, oA = 0;
   int64_t oPair = 0;
+  int n_small = 0;
   uint8_t* h_pair = (uint8_t*)hp(Ly.pair);
   std::vector<double> cost(nv);
   for (int v = 0; v < nv; ++v) {
@@ -635,6 +647,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     I.last_forced = pr.last_forced;
     I.have_running_decode = pr.have_rd ? 1 : 0;
     I.values_integral = pr.values_integral ? 1 : 0;
+    I.build_small = pr.n_dec <= build_warp_max_dec() ? 1 : 0;
+    n_small += I.build_small;
     I.off_dec = oD;
     I.off_chain = oC;
     I.off_pre = oP;
@@ -839,6 +853,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   A.ctime = (double*)(DS + Ly.ctime);
   A.ccnt = (int32_t*)(DS + Ly.ccnt);
   A.bq = (int32_t*)(DS + Ly.bq);
+  A.n_small = n_small;
   A.out = (OutHdr*)(DO + Ly.out);
   A.sel = (int32_t*)(DO + Ly.sel);
   A.ids = (int32_t*)(DO + Ly.ids);
@@ -901,7 +916,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   cudaMemsetAsync(DS + Ly.c_bkey, 0, Ly.bkey_bytes, s);
   cudaMemsetAsync(DS + Ly.c_bval, 0xFF, Ly.bval_bytes, s);
   cudaMemsetAsync(DO + Ly.out, 0, sizeof(OutHdr) * nv, s);
-  cudaMemsetAsync(DS + Ly.bq, 0, 2 * sizeof(int32_t), s);
+  cudaMemsetAsync(DS + Ly.bq, 0, 4 * sizeof(int32_t), s);
   cudaError_t e;
   for (int k = 0; k < 4; ++k)
     if (!ws.ev[k]) cudaEventCreate(&ws.ev[k]);
@@ -917,7 +932,8 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   bp.a = ws.A;
   bp.smem_bytes = 44 * 1024;
   bp.phase_cycles = dp.phase_cycles ? dp.phase_cycles + 16 : nullptr;
-  if ((e = launch_build(bp, nv, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  if ((e = launch_build(bp, ws.A.n_small, nv - ws.A.n_small, s)) != cudaSuccess)
+    return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   cudaEventRecord(ws.ev[2], s);
   return SLOS_OK;
 }

@@ -90,13 +90,23 @@ cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_build(const BuildParams& prm, int grid, cudaStream_t s) {
-  if (grid <= 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)prm.smem_bytes);
-  if (e != cudaSuccess) return e;
-  build_kernel<<<(grid + kBuildPerCta - 1) / kBuildPerCta, kBuildThreads, prm.smem_bytes, s>>>(prm);
-  return cudaGetLastError();
+cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, cudaStream_t s) {
+  cudaError_t e;
+  if (n_small > 0) {
+    if ((e = cudaFuncSetAttribute(build_kernel_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)prm.smem_bytes)) != cudaSuccess)
+      return e;
+    build_kernel_warp<<<(n_small + kBuildWarps - 1) / kBuildWarps, 32 * kBuildWarps, prm.smem_bytes, s>>>(prm);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (n_large > 0) {
+    if ((e = cudaFuncSetAttribute(build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)prm.smem_bytes)) != cudaSuccess)
+      return e;
+    build_kernel<<<n_large, kBuildThreads, prm.smem_bytes, s>>>(prm);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_compact(const CompactParams& prm, int grid, cudaStream_t s) {
