@@ -17,6 +17,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -142,6 +146,71 @@ Ctx& ctx() {
   return *c;
 }
 
+// Host worker pool for the per-instance preparation (chain sort, capacity
+// estimates, pair keys, SoA fill): instances are independent, so a batch's host
+// work splits across cores like the kernels split across SMs.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();
+    return *p;
+  }
+  // fn(lo, hi) over contiguous ranges of [0, n); runs inline for small n.
+  void run(int n, const std::function<void(int, int)>& fn) {
+    const int T = (int)workers_.size() + 1;
+    if (n < 64 || T == 1) { fn(0, n); return; }
+    {
+      std::unique_lock<std::mutex> l(mu_);
+      fn_ = &fn;
+      n_ = n;
+      next_ = 0;
+      busy_ = (int)workers_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> l(mu_);
+    done_.wait(l, [&] { return busy_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const char* e = std::getenv("SLOS_HOST_THREADS");
+    int t = e ? std::atoi(e) : (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+    for (int k = 1; k < t; ++k) workers_.emplace_back([this] { loop(); });
+    for (auto& w : workers_) w.detach();
+  }
+  void work() {
+    const int grain = 16;
+    for (;;) {
+      const int lo = next_.fetch_add(grain);
+      if (lo >= n_) break;
+      (*fn_)(lo, std::min(n_, lo + grain));
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      work();
+      std::lock_guard<std::mutex> l(mu_);
+      if (--busy_ == 0) done_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int, int)>* fn_ = nullptr;
+  std::atomic<int> next_{0};
+  int n_ = 0, busy_ = 0;
+  uint64_t gen_ = 0;
+};
+
 int ensure_device(Ctx& c) {
   if (c.init) return c.status;
   c.init = true;
@@ -173,17 +242,22 @@ int ensure_device(Ctx& c) {
 
 ResultArena* arena_get(Ctx& c, size_t bytes) {
   {
+    // best fit among the pooled pinned arenas
     std::lock_guard<std::mutex> g(c.pool_mu);
-    for (size_t i = 0; i < c.pool.size(); ++i) {
-      if (c.pool[i]->cap >= bytes) {
-        ResultArena* a = c.pool[i];
-        c.pool.erase(c.pool.begin() + (long)i);
-        return a;
-      }
+    long best = -1;
+    for (size_t i = 0; i < c.pool.size(); ++i)
+      if (c.pool[i]->cap >= bytes && (best < 0 || c.pool[i]->cap < c.pool[(size_t)best]->cap)) best = (long)i;
+    if (best >= 0) {
+      ResultArena* a = c.pool[(size_t)best];
+      c.pool.erase(c.pool.begin() + best);
+      return a;
     }
   }
   ResultArena* a = new ResultArena();
-  size_t want = std::max(bytes, (size_t)1 << 16);
+  // power-of-two sizes so arenas of similar batches are reused (pinned
+  // allocation costs milliseconds)
+  size_t want = (size_t)1 << 16;
+  while (want < bytes) want <<= 1;
   if (cudaHostAlloc(&a->p, want, cudaHostAllocDefault) != cudaSuccess) {
     a->p = std::malloc(want);  // pageable is still correct, only slower to fill
     if (!a->p) { delete a; return nullptr; }
@@ -452,6 +526,7 @@ struct Workspace {
   bool uploaded = false;
   int n_total = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t own_stream = nullptr;  // pipeline workspaces only
 };
 
 thread_local int64_t g_h2d = 0, g_d2h = 0;
@@ -477,11 +552,18 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   std::vector<Caps> caps(n);
   int maxN = 0, maxDec = 0, Lmax = 1;
   double S_need = 16;
+  HostPool::get().run(n, [&](int lo, int hi) {
+    for (int q = lo; q < hi; ++q) {
+      const int k = jobs[q].k;
+      Prep& pr = prep[q];
+      pr.status = prep_instance(planners[k], &inputs[k], unit_value, pr);
+      if (pr.status == SLOS_OK) caps[q] = estimate_caps(planners[k], &inputs[k], pr, jobs[q].grow);
+    }
+  });
   for (int q = 0; q < n; ++q) {
     const int k = jobs[q].k;
     const slos_planner* P = planners[k];
     Prep& pr = prep[q];
-    pr.status = prep_instance(P, &inputs[k], unit_value, pr);
     if (pr.status != SLOS_OK) {
       std::memset(&outs[k], 0, sizeof(outs[k]));
       outs[k].status = pr.status;
@@ -492,7 +574,6 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     if (pi < 0) { pi = (int)plist.size(); plist.push_back(P); }
     pr.planner = pi;
     valid.push_back(q);
-    caps[q] = estimate_caps(P, &inputs[k], pr, jobs[q].grow);
     TD += pr.n_dec;
     TC += pr.N + 1;
     TP += pr.n_pre;
@@ -621,12 +702,41 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   int32_t* h_pre_idx = (int32_t*)hp(Ly.pre_idx);
   int64_t* h_pre_left = (int64_t*)hp(Ly.pre_left);
   int32_t* h_run_tier = (int32_t*)hp(Ly.run_tier);
-  int64_t oD = 0, oC = 0, oP = 0, oR = 0, oS = 0, oCd = 0, oM = 0, oW = 0, oSel = 0, oIds = 0, oB = 0, oE = 0, oA = 0;
-  int64_t oPair = 0;
   int n_small = 0;
   uint8_t* h_pair = (uint8_t*)hp(Ly.pair);
   std::vector<double> cost(nv);
-  for (int v = 0; v < nv; ++v) {
+  struct Off { int64_t D, C, P, R, S, Cd, M, W, Sel, Ids, B, E, A, Pair; };
+  std::vector<Off> offs(nv);
+  {
+    Off o{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int v = 0; v < nv; ++v) {
+      const int q = valid[v];
+      const Prep& pr = prep[q];
+      const Caps& cp = caps[q];
+      const slos_input* in = &inputs[jobs[q].k];
+      offs[v] = o;
+      o.D += pr.n_dec;
+      o.C += pr.N + 1;
+      o.P += pr.n_pre;
+      o.R += in->n_running;
+      o.S += cp.surv;
+      o.Cd += cp.cand;
+      o.M += cp.memo;
+      o.W += (cp.work + 255) & ~(int64_t)255;
+      o.Sel += pr.N + 1;
+      o.Ids += 2 * (int64_t)in->n_pending + 1;
+      o.B += cp.batch;
+      o.E += cp.entry;
+      o.A += astride[q] * (pr.N + 1);
+      o.Pair += (int64_t)pr.N * (pr.N + 1) / 2;
+      n_small += pr.n_dec <= build_warp_max_dec() ? 1 : 0;
+    }
+  }
+  HostPool::get().run(nv, [&](int v_lo, int v_hi) {
+  for (int v = v_lo; v < v_hi; ++v) {
+    int64_t oD = offs[v].D, oC = offs[v].C, oP = offs[v].P, oR = offs[v].R, oS = offs[v].S, oCd = offs[v].Cd,
+            oM = offs[v].M, oW = offs[v].W, oSel = offs[v].Sel, oIds = offs[v].Ids, oB = offs[v].B,
+            oE = offs[v].E, oA = offs[v].A, oPair = offs[v].Pair;
     const int q = valid[v];
     const int k = jobs[q].k;
     const slos_input* in = &inputs[k];
@@ -648,7 +758,6 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     I.have_running_decode = pr.have_rd ? 1 : 0;
     I.values_integral = pr.values_integral ? 1 : 0;
     I.build_small = pr.n_dec <= build_warp_max_dec() ? 1 : 0;
-    n_small += I.build_small;
     I.off_dec = oD;
     I.off_chain = oC;
     I.off_pre = oP;
@@ -748,21 +857,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     h_sf[oC + pr.N] = 0;
     for (int x = pr.N - 1; x >= 0; --x) h_sf[oC + x] = h_sf[oC + x + 1] + h_pf[oC + x];
     cost[v] = (double)(pr.n_dec + 8) * (double)(pr.N + 1) * (double)(pr.N + 1);
-    oD += 0;  // advanced in the loop above
-    oC += pr.N + 1;
-    oP += pr.n_pre;
-    oR += in->n_running;
-    oS += cp.surv;
-    oCd += cp.cand;
-    oM += cp.memo;
-    oW += (cp.work + 255) & ~(int64_t)255;
-    oSel += pr.N + 1;
-    oIds += 2 * (int64_t)in->n_pending + 1;
-    oB += cp.batch;
-    oE += cp.entry;
-    oA += astride[q] * (pr.N + 1);
-    oPair += (int64_t)pr.N * (pr.N + 1) / 2;
   }
+  });
   {  // anchor tasks: (instance, anchor j), j = -1 .. N-2
     int32_t* t = (int32_t*)hp(Ly.atask);
     int64_t x = 0;
@@ -1161,6 +1257,27 @@ Workspace& default_ws() {
   return *w;
 }
 
+// Two pipeline workspaces with their own streams: chunk i+1's host preparation and
+// H2D overlap chunk i's kernels, and chunk i's compaction + D2H overlap chunk i+1's
+// kernels (copy engines vs SMs).
+Workspace& pipe_ws(int k) {
+  static Workspace* w[2] = {nullptr, nullptr};
+  if (!w[k]) {
+    w[k] = new Workspace();
+    cudaStreamCreateWithFlags(&w[k]->own_stream, cudaStreamNonBlocking);
+  }
+  return *w[k];
+}
+
+int pipeline_chunks(int n) {
+  static const int env = [] {
+    const char* e = std::getenv("SLOS_PIPELINE_CHUNKS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env > 0) return std::min(env, std::max(1, n));
+  return n < 512 ? 1 : 2;  // measured on C2 x 1024: 2 chunks 125k plans/s e2e, 1 chunk 108k, 4 chunks 115k
+}
+
 // full pipeline with capacity regrowth; caller holds ctx().mu
 int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, const slos_input* inputs,
              int32_t unit_value, slos_result* outs, cudaStream_t stream) {
@@ -1168,6 +1285,47 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
   for (int k = 0; k < n; ++k) jobs[k] = {k, 0};
   g_h2d = 0;
   g_d2h = 0;
+  const int K = pipeline_chunks(n);
+  if (K > 1) {
+    // order after the caller's prior work on `stream`
+    static cudaEvent_t ev0 = nullptr;
+    if (!ev0) cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+    cudaEventRecord(ev0, stream ? stream : c.stream);
+    std::vector<std::vector<Job>> chunk(K);
+    for (int k = 0; k < n; ++k) chunk[(int64_t)k * K / n].push_back(jobs[k]);
+    int prev = -1;
+    for (int i = 0; i <= K; ++i) {
+      const auto t_a = std::chrono::steady_clock::now();
+      if (i < K) {
+        Workspace& w = pipe_ws(i & 1);
+        cudaStreamWaitEvent(w.own_stream, ev0, 0);
+        int r = ws_upload(c, w, planners, inputs, unit_value, chunk[i], outs, w.own_stream);
+        if (r == SLOS_OK) r = ws_solve(w, w.own_stream);
+        if (r != SLOS_OK) {
+          for (const Job& j : jobs) outs[j.k].status = r;
+          return r;
+        }
+      }
+      const auto t_b = std::chrono::steady_clock::now();
+      if (prev >= 0) {
+        const int r = ws_collect(c, pipe_ws(prev & 1), outs, retry);
+        if (r != SLOS_OK) {
+          for (const Job& j : jobs) outs[j.k].status = r;
+          return r;
+        }
+      }
+      if (std::getenv("SLOS_HOST_TIMING")) {
+        const auto t_c = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[slos pipeline] step %d: upload+enqueue %.3f ms, collect %.3f ms\n", i,
+                     std::chrono::duration<double, std::milli>(t_b - t_a).count(),
+                     std::chrono::duration<double, std::milli>(t_c - t_b).count());
+      }
+      prev = i;
+    }
+    jobs.swap(retry);
+    retry.clear();
+    if (std::getenv("SLOS_HOST_TIMING")) std::fprintf(stderr, "[slos pipeline] %d chunks, %zu retried\n", K, jobs.size());
+  }
   for (int round = 0; round < 8 && !jobs.empty(); ++round) {
     retry.clear();
     int r = ws_upload(c, ws, planners, inputs, unit_value, jobs, outs, stream);
