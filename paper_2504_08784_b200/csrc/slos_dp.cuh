@@ -1188,6 +1188,15 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     // its bucket rejects it, and an accepted c is pruned iff a LATER accepted
     // candidate of its bucket weakly dominates it: decided pairwise, one thread per
     // candidate over its bucket's list.
+    // Why: let W(x,y) = x.v>=y.v && x.mem<=y.mem && x.pb>=y.pb (transitive when the
+    // comparisons are exact) and rej(x,y) = W(x,y) && (x != y in (v,mem,pb) ||
+    // x.n >= y.n). If an earlier y rejects c but is not on the frontier when c
+    // arrives, y was rejected by, or later pruned by, some frontier member f with
+    // W(f,y); then W(f,c), and if f equals c in (v,mem,pb) so do y and c, with
+    // f.n >= y.n >= c.n (rejection) or f.n > y.n (f was accepted while y was on the
+    // frontier). By induction some member on c's frontier rejects c. Conversely a
+    // rejecting frontier member is an earlier candidate. Pruning removes exactly
+    // the accepted entries weakly dominated by a later accepted candidate.
     const bool pairwise = I.values_integral != 0;
     bool fastB = !pairwise && NB <= 64;
     if (pairwise) {
