@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm
 
 
 #ifndef SLOS_DP_MIN_BLOCKS
-#define SLOS_DP_MIN_BLOCKS 3
+#define SLOS_DP_MIN_BLOCKS 4
 #endif
 __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpParams prm) {
   extern __shared__ __align__(16) unsigned char dsm[];

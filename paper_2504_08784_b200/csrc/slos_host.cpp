@@ -962,18 +962,36 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   dp.Sc = Sc;
   const size_t stride = dp_warp_scr_stride(dp.Sc, Lmax);
   dp.wscr_stride = stride;
-  // 3 CTAs of 256 threads per SM (the register limit at 80 regs/thread)
-  const size_t kSmemBudget = 74 * 1024;
+  // 4 CTAs of 256 threads per SM (64 registers/thread, SLOS_DP_MIN_BLOCKS)
+  // dynamic shared memory cap per CTA (SLOS_DP_SMEM_KB overrides). Staging the
+  // decoders (read only by the rare warp fallback) costs a CTA per SM at C2 sizes,
+  // so it is off unless SLOS_DP_STAGE_DEC=1.
+  static const size_t kSmemBudget = [] {
+    const char* e = std::getenv("SLOS_DP_SMEM_KB");
+    return (size_t)(e ? std::atoi(e) : 74) * 1024;
+  }();
+  static const bool kStageDec = [] {
+    const char* e = std::getenv("SLOS_DP_STAGE_DEC");
+    return e ? std::atoi(e) != 0 : false;
+  }();
   dp.grec_hdr = grec_hdr;
   dp.grec_stride = grec_stride;
   if ((e = ws.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
     return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   dp.wscr_global = (unsigned char*)ws.d_wscr.p;
   size_t& smem = ws.smem;
-  dp.Tsm = 512;
+  // candidates per level kept in shared memory (SLOS_DP_TSM overrides). Bigger is
+  // not better: what the 4 resident CTAs leave of the SM's 228 KB stays L1 for the
+  // HBM scratch (survivors, group records, larger levels). Measured on C2 x 1024:
+  // dp_kernel 1.81 ms at 192, 1.87 at 256, 2.07 at 512 (3 CTAs), 2.39 at 640.
+  static const int kTsm = [] {
+    const char* e = std::getenv("SLOS_DP_TSM");
+    return e ? std::atoi(e) : 192;
+  }();
+  dp.Tsm = kTsm;
   auto fit = [&](int dec) { return dp_smem_bytes(maxN, dec, dp.Sc, Lmax, dp.Tsm, &dp.overlay_bytes); };
   while (fit(0) > kSmemBudget && dp.Tsm > 64) {
-    if (dp.Tsm > 256) dp.Tsm -= 64;
+    if (dp.Tsm > 256) dp.Tsm -= 32;
     else dp.Tsm /= 2;
   }
   smem = fit(0);
@@ -987,7 +1005,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     dp.phase_cycles = dev_pc;
   }
   dp.dec_smem_max = 0;
-  if (fit(maxDec) <= kSmemBudget) dp.dec_smem_max = maxDec;
+  if (kStageDec && fit(maxDec) <= kSmemBudget) dp.dec_smem_max = maxDec;
   smem = fit(dp.dec_smem_max);
   ws.anchor_smem = anchor_smem_bytes(maxN, dp.Sc, Lmax, &dp.anchor_scr_bytes);
   ws.maxN = maxN;
