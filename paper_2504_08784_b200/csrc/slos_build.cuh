@@ -10,11 +10,6 @@
 
 namespace slos {
 
-struct BuildParams {
-  BatchArgs a;
-  size_t smem_bytes;  // dynamic shared memory per CTA (per-gap working set)
-  unsigned long long* phase_cycles;  // 8 counters or nullptr (SLOS_PHASE_TIMING)
-};
 
 #define SLOS_BPHASE(k)                                                         \
   do {                                                                         \
@@ -587,7 +582,7 @@ __global__ void __launch_bounds__(32 * kBuildWarps, 2) build_kernel_warp(BuildPa
   extern __shared__ __align__(16) unsigned char bsm[];
   const int idx = blockIdx.x * kBuildWarps + warp_id();
   if (idx >= A.n_small) return;  // whole warp; the engine never uses CTA barriers here
-  const int64_t per = (int64_t)(prm.smem_bytes / kBuildWarps) & ~(int64_t)255;
+  const int64_t per = (int64_t)(prm.smem_warp / kBuildWarps) & ~(int64_t)255;
   build_instance<WarpGrp>(A, shs[warp_id()], A.bq[4 + idx], bsm + per * warp_id(), per, prm.phase_cycles);
 }
 

@@ -237,6 +237,14 @@ __device__ __forceinline__ void build_queue_push(const BatchArgs& A, int inst, b
   else A.bq[base + n - 1 - atomicAdd(&c[1], 1)] = inst;
 }
 
+// build_kernel / build_kernel_warp launch parameters.
+struct BuildParams {
+  BatchArgs a;
+  size_t smem_bytes;  // build_kernel: dynamic shared memory per CTA (per-gap working set)
+  size_t smem_warp;   // build_kernel_warp: dynamic shared memory per CTA (4 instances)
+  unsigned long long* phase_cycles;  // 8 counters or nullptr (SLOS_PHASE_TIMING)
+};
+
 // Triangular index of the pair (anchor a = j+1, chain item i), 0 <= a <= i < N:
 // row-major by item, so one DP level's pairs (a = floor+1 .. i) are contiguous.
 __host__ __device__ __forceinline__ int64_t pair_index(int N, int a, int i) {

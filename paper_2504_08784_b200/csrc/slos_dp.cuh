@@ -615,7 +615,10 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
 // group's tail (block_anchor_dues) -- is independent of the DP's states, so all
 // anchors of all instances are built up front, one CTA per (instance, anchor),
 // instead of on the DP's level-sequential critical path.
-__global__ void __launch_bounds__(kDpThreads, 3) anchor_kernel(DpParams prm) {
+#ifndef SLOS_ANCHOR_MIN_BLOCKS
+#define SLOS_ANCHOR_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kDpThreads, SLOS_ANCHOR_MIN_BLOCKS) anchor_kernel(DpParams prm) {
   extern __shared__ __align__(16) unsigned char asm_[];
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;

@@ -31,11 +31,6 @@
 #include "../../include/slos_planner.h"
 
 namespace slos {
-struct BuildParams {
-  BatchArgs a;
-  size_t smem_bytes;
-  unsigned long long* phase_cycles;
-};
 struct GapBatchOut {
   double start_s, end_s;
   int64_t capacity, spec_step, decode_tokens, prefill_budget;
@@ -1044,7 +1039,16 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   cudaEventRecord(ws.ev[1], s);
   BuildParams bp;
   bp.a = ws.A;
-  bp.smem_bytes = 44 * 1024;
+  static const size_t kBuildSmem = [] {  // per-gap working set per CTA (SLOS_BUILD_SMEM_KB)
+    const char* e = std::getenv("SLOS_BUILD_SMEM_KB");
+    return (size_t)(e ? std::atoi(e) : 44) * 1024;
+  }();
+  bp.smem_bytes = kBuildSmem;
+  static const size_t kBuildSmemWarp = [] {  // per CTA of 4 warp-built instances (SLOS_BUILD_WARP_SMEM_KB)
+    const char* e = std::getenv("SLOS_BUILD_WARP_SMEM_KB");
+    return (size_t)(e ? std::atoi(e) : 16) * 1024;
+  }();
+  bp.smem_warp = kBuildSmemWarp;
   bp.phase_cycles = dp.phase_cycles ? dp.phase_cycles + 16 : nullptr;
   if ((e = launch_build(bp, ws.A.n_small, nv - ws.A.n_small, s)) != cudaSuccess)
     return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));

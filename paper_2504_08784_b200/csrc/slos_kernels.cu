@@ -94,9 +94,9 @@ cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, cudaS
   cudaError_t e;
   if (n_small > 0) {
     if ((e = cudaFuncSetAttribute(build_kernel_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)prm.smem_bytes)) != cudaSuccess)
+                                  (int)prm.smem_warp)) != cudaSuccess)
       return e;
-    build_kernel_warp<<<(n_small + kBuildWarps - 1) / kBuildWarps, 32 * kBuildWarps, prm.smem_bytes, s>>>(prm);
+    build_kernel_warp<<<(n_small + kBuildWarps - 1) / kBuildWarps, 32 * kBuildWarps, prm.smem_warp, s>>>(prm);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if (n_large > 0) {
