@@ -1286,7 +1286,11 @@ Workspace& pipe_ws(int k) {
   static Workspace* w[2] = {nullptr, nullptr};
   if (!w[k]) {
     w[k] = new Workspace();
-    cudaStreamCreateWithFlags(&w[k]->own_stream, cudaStreamNonBlocking);
+    // the earlier chunk runs at higher priority so its D2H starts while the next
+    // chunk's kernels still run
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&w[k]->own_stream, cudaStreamNonBlocking, k == 0 ? hi : lo);
   }
   return *w[k];
 }
@@ -1313,8 +1317,18 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
     static cudaEvent_t ev0 = nullptr;
     if (!ev0) cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
     cudaEventRecord(ev0, stream ? stream : c.stream);
+    // chunk boundaries: with 2 chunks the first is larger (SLOS_PIPELINE_SPLIT, its
+    // D2H hides under the second's kernels; only the last chunk's D2H is exposed)
+    static const double split = [] {
+      const char* e = std::getenv("SLOS_PIPELINE_SPLIT");
+      return e ? std::atof(e) : 0.5;
+    }();
     std::vector<std::vector<Job>> chunk(K);
-    for (int k = 0; k < n; ++k) chunk[(int64_t)k * K / n].push_back(jobs[k]);
+    for (int k = 0; k < n; ++k) {
+      int ci = (int)((int64_t)k * K / n);
+      if (K == 2) ci = k < (int)(split * n) ? 0 : 1;
+      chunk[ci].push_back(jobs[k]);
+    }
     int prev = -1;
     for (int i = 0; i <= K; ++i) {
       const auto t_a = std::chrono::steady_clock::now();
