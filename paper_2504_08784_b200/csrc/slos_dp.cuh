@@ -282,6 +282,7 @@ __device__ inline EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D
 
 // Build the anchor cache of anchor j (gap start a) for this instance: block-wide.
 // gmax: the longest gap any later chain item can open from this anchor.
+template <int NT>
 __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D, const AnchorView& av,
                                           double a, double now, double pull, double gmax, int Sc,
                                           const double* ctime, const int* ccnt, double min_slot,
@@ -291,7 +292,7 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
   __shared__ unsigned s_mask;
   __shared__ int s_nex, s_hb, s_abl;
   __shared__ unsigned s_pt[kMaxTiers];
-  __shared__ double s_minph[kDpWarps];
+  __shared__ double s_minph[(NT / 32)];
   if (tid == 0) {
     s_mask = 0; s_nex = 0; s_hb = 0; s_abl = 0;
     for (int l = 0; l < kMaxTiers; ++l) s_pt[l] = 0;
@@ -302,7 +303,7 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
   int nex = 0, hb = 0, abl = 0;
   uint64_t pt8 = 0;  // per-thread member count per tier, 8 bits each (<= 255 members per thread)
   int it = 0;
-  for (int k = tid; k < D.n; k += kDpThreads) {
+  for (int k = tid; k < D.n; k += NT) {
     if ((++it & 0xff) == 0) {  // keep every 8-bit tier count below 256
       for (int l = 0; l < P.L; ++l)
         if ((pt8 >> (8 * l)) & 0xffu) atomicAdd(&s_pt[l], (unsigned)((pt8 >> (8 * l)) & 0xffu));
@@ -347,7 +348,7 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
     F->has_backlog = s_hb;
     F->any_bl = s_abl;
     double mp = s_minph[0];
-    for (int x = 1; x < kDpWarps; ++x) mp = dmin(mp, s_minph[x]);
+    for (int x = 1; x < (NT / 32); ++x) mp = dmin(mp, s_minph[x]);
     F->min_phase = mp;
     for (int l = 0; l < kMaxTiers; ++l) F->per_tier[l] = (int64_t)s_pt[l];
     F->t0 = s_mask ? P.tpot[__ffs(s_mask) - 1] : 0.0;
@@ -392,14 +393,14 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
   __syncthreads();
   const int Kg = F->Kg;
   // grid slot capacities (duration e_k - e_{k-1}); -1 where time2bs throws
-  for (int s = tid; s < Kg; s += kDpThreads) {
+  for (int s = tid; s < Kg; s += NT) {
     const double dur = av.ge[s] - (s == 0 ? 0.0 : av.ge[s - 1]);
     const int64_t c = plan_time2bs(P, dur, 0);
     av.gcap[s] = c < 0 ? -1 : imin(c, P.max_batch);
   }
   // canonical due times -> grid jit
   for (int l = 0; l < P.L; ++l)
-    for (int k = tid; k < ccnt[l]; k += kDpThreads) av.ccell[l * Sc + k] = jit_search(av.ge, Kg, ctime[l * Sc + k]);
+    for (int k = tid; k < ccnt[l]; k += NT) av.ccell[l * Sc + k] = jit_search(av.ge, Kg, ctime[l * Sc + k]);
   __syncthreads();
   (void)s_red;
 }
@@ -414,6 +415,7 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
 // few groups whose tail covers its cell and accumulates their GroupTail.
 // Runs only when the anchor grid is usable (grid_ok) and no member has a negative
 // backlog (tile_gap's second spill scan); otherwise the groups fall back to E2.
+template <int NT>
 __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, const AnchorView& av,
                                          int j, int N, const double* ch_dl, const int32_t* ch_fl,
                                          double a, double pull, double min_slot, int Sc,
@@ -450,16 +452,16 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
     if (tid == 0) F->dues_ok = 0;
     return;
   }
-  for (int k = tid; k < Kg; k += kDpThreads) sge[k] = av.ge[k];
-  for (int k = tid; k <= Kg; k += kDpThreads) sHc[k] = 0;
-  for (int k = tid; k < 5 * nG; k += kDpThreads) g_acc[k] = 0;
+  for (int k = tid; k < Kg; k += NT) sge[k] = av.ge[k];
+  for (int k = tid; k <= Kg; k += NT) sHc[k] = 0;
+  for (int k = tid; k < 5 * nG; k += NT) g_acc[k] = 0;
   int neg = 0;
-  for (int k = tid; k < D.n; k += kDpThreads)
+  for (int k = tid; k < D.n; k += NT)
     if (av.rm[k] > 0 && av.bl[k] < 0) neg = 1;
   __syncthreads();
   // per group: gap, horizon, Sp, tail cell range [lo, hi] (cells -1 .. Kg-1)
   double hloc = 0.0;
-  for (int gi = tid; gi < nG; gi += kDpThreads) {
+  for (int gi = tid; gi < nG; gi += NT) {
     const int i = j + 1 + gi;
     if (ch_fl[i] > j) {  // (j, i) is never a DP transition
       g_lo[gi] = 1; g_hi[gi] = 0; g_Sp[gi] = 0; g_gap[gi] = 0.0; g_hor[gi] = 0.0;
@@ -506,7 +508,7 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
     return;
   }
   // per-cell group lists (cell y = c+1): counts, exclusive offsets, items
-  for (int y = tid; y <= Kg; y += kDpThreads) {
+  for (int y = tid; y <= Kg; y += NT) {
     int n = 0;
     for (int gi = 0; gi < nG; ++gi) n += (g_lo[gi] <= y - 1 && y - 1 <= g_hi[gi]) ? 1 : 0;
     l_off[y + 1] = n;
@@ -524,7 +526,7 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
     if (tid == 0) F->dues_ok = 0;
     return;
   }
-  for (int y = tid; y <= Kg; y += kDpThreads) {
+  for (int y = tid; y <= Kg; y += NT) {
     int pos = l_off[y];
     for (int gi = 0; gi < nG; ++gi)
       if (g_lo[gi] <= y - 1 && y - 1 <= g_hi[gi]) l_item[pos++] = gi;
@@ -533,7 +535,7 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
   const double hmax = s_hmax;
   // the walk: lanes over members in lockstep (one due per lane per round)
   unsigned long long lx = 0;
-  for (int base = 0; base < D.n; base += kDpThreads) {
+  for (int base = 0; base < D.n; base += NT) {
     const int k = base + tid;
     int64_t rem = 0, issued = 0;
     double d = 0.0, tpot = 0.0;
@@ -596,7 +598,7 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
     F->Lx = (int64_t)s_lx;
     F->dues_ok = 1;
   }
-  for (int gi = tid; gi < nG; gi += kDpThreads) {
+  for (int gi = tid; gi < nG; gi += NT) {
     GroupTail t;
     t.tA = g_acc[5 * gi + 0];
     t.tB = g_acc[5 * gi + 1];
@@ -615,16 +617,20 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
 // group's tail (block_anchor_dues) -- is independent of the DP's states, so all
 // anchors of all instances are built up front, one CTA per (instance, anchor),
 // instead of on the DP's level-sequential critical path.
-#ifndef SLOS_ANCHOR_MIN_BLOCKS
-#define SLOS_ANCHOR_MIN_BLOCKS 4
+#ifndef SLOS_ANCHOR_THREADS
+#define SLOS_ANCHOR_THREADS 128
 #endif
-__global__ void __launch_bounds__(kDpThreads, SLOS_ANCHOR_MIN_BLOCKS) anchor_kernel(DpParams prm) {
+constexpr int kAnchorThreads = SLOS_ANCHOR_THREADS;
+#ifndef SLOS_ANCHOR_MIN_BLOCKS
+#define SLOS_ANCHOR_MIN_BLOCKS 8
+#endif
+__global__ void __launch_bounds__(kAnchorThreads, SLOS_ANCHOR_MIN_BLOCKS) anchor_kernel(DpParams prm) {
   extern __shared__ __align__(16) unsigned char asm_[];
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;
   __shared__ int ccnt[kMaxTiers];
   __shared__ double s_maxdl, s_minA;
-  __shared__ int64_t s_wsum[kDpWarps + 1];
+  __shared__ int64_t s_wsum[kAnchorThreads / 32 + 1];
   const BatchArgs& A = prm.a;
   const int tid = threadIdx.x;
   const int v = A.atask[2 * blockIdx.x], j = A.atask[2 * blockIdx.x + 1];
@@ -667,12 +673,12 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_ANCHOR_MIN_BLOCKS) anchor_ker
   const double pull = min_slot;
   const double a = (j < 0) ? I.now : ch_dl[j];
   const AnchorView av = anchor_view(A.anchors + I.off_anchor + (size_t)(j + 1) * I.anchor_stride, D.n, Sc, L);
-  block_build_anchor(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), Sc, ctime, ccnt,
+  block_build_anchor<kAnchorThreads>(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), Sc, ctime, ccnt,
                      min_slot, s_wsum);
-  block_anchor_dues(P, D, av, j, N, ch_dl, ch_fl, a, pull, min_slot, Sc, scr, prm.anchor_scr_bytes);
+  block_anchor_dues<kAnchorThreads>(P, D, av, j, N, ch_dl, ch_fl, a, pull, min_slot, Sc, scr, prm.anchor_scr_bytes);
   if (j < 0) {  // the instance's canonical due times, for group_kernel
     double* gct = A.ctime + (size_t)v * prm.Lmax * Sc;
-    for (int x = tid; x < L * Sc; x += kDpThreads) gct[x] = ctime[x];
+    for (int x = tid; x < L * Sc; x += kAnchorThreads) gct[x] = ctime[x];
     if (tid < kMaxTiers) A.ccnt[v * kMaxTiers + tid] = tid < L ? ccnt[tid] : 0;
   }
 }

@@ -71,7 +71,7 @@ cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream
   if (grid <= 0) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(anchor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  anchor_kernel<<<grid, kDpThreads, smem, s>>>(prm);
+  anchor_kernel<<<grid, kAnchorThreads, smem, s>>>(prm);
   return cudaGetLastError();
 }
 
