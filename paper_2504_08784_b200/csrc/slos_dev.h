@@ -224,6 +224,7 @@ struct DpParams {
   size_t anchor_scr_bytes;  // anchor_kernel: due-pass scratch (bytes)
   size_t grec_stride;       // bytes per pair group record
   size_t grec_hdr;          // header bytes before the variant arrays
+  size_t grec_stage;        // bytes of a record the DP stages (header + evaluated arrays)
 };
 
 // Push an instance onto its plan-reconstruction queue: queue 0 (warp-built, small

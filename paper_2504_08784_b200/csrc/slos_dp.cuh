@@ -969,16 +969,21 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     };
     // the level's gap group records (pairs (jlo .. i-1, i), contiguous) staged into
     // the candidate-state overlay, which is free until step 4
-    const bool staged = (size_t)nlev * prm.grec_stride <= prm.overlay_bytes;
+    // (header + cap/nx/hc of each record; the slot ends are not read by E3)
+    const bool staged = (size_t)nlev * prm.grec_stage <= prm.overlay_bytes;
     const unsigned char* GRl = GR + (size_t)pair_index(N, jlo + 1, i) * prm.grec_stride;
     if (staged) {
+      const int per4 = (int)(prm.grec_stage / 16), str4 = (int)(prm.grec_stride / 16);
       const uint4* src4 = (const uint4*)GRl;
       uint4* dst4 = (uint4*)ovl;
-      const int n4 = (int)((size_t)nlev * prm.grec_stride / 16);
-      for (int x = tid; x < n4; x += kDpThreads) dst4[x] = src4[x];
+      for (int x = tid; x < nlev * per4; x += kDpThreads) {
+        const int r = x / per4, o = x - r * per4;
+        dst4[x] = src4[(size_t)r * str4 + o];
+      }
     }
     auto rec_of = [&](int j) -> const unsigned char* {
-      return (staged ? (const unsigned char*)ovl : GRl) + (size_t)(j - jlo) * prm.grec_stride;
+      return staged ? (const unsigned char*)ovl + (size_t)(j - jlo) * prm.grec_stage
+                    : GRl + (size_t)(j - jlo) * prm.grec_stride;
     };
     // ---- 1: memo keys. A pair whose key (a_us, raw_us) is unique to it (host
     // flag) has one key per surviving source bucket: key s_kpre[k] + bucket id,

@@ -120,16 +120,22 @@ struct GroupHdr {
 };
 
 __host__ __device__ __forceinline__ size_t group_var_stride(int Sc, int L) {
-  return (((size_t)Sc * (8 + 8 + 4 + 4 * (size_t)L)) + 127) & ~(size_t)127;
+  return (((size_t)Sc * (8 + 4 + 4 * (size_t)L + 8)) + 127) & ~(size_t)127;
 }
 
+// Bytes of a group variant the DP's key evaluation reads (everything but the
+// slot ends, which are last): what a DP level stages into shared memory.
+__host__ __device__ __forceinline__ size_t group_var_eval_bytes(int Sc, int L) {
+  return (((size_t)Sc * (8 + 4 + 4 * (size_t)L)) + 15) & ~(size_t)15;
+}
+
+// layout: cap[Sc] (i64), nx[Sc] (i32), hc[L][Sc] (i32), ends[Sc] (f64)
 __device__ __forceinline__ GroupVar group_var_carve(unsigned char* base, int Sc, int L) {
   GroupVar g;
-  g.ends = (double*)base;
-  g.cap = (int64_t*)(base + (size_t)Sc * 8);
-  g.nx = (int32_t*)(base + (size_t)Sc * 16);
-  g.hc = (int32_t*)(base + (size_t)Sc * 20);
-  (void)L;
+  g.cap = (int64_t*)base;
+  g.nx = (int32_t*)(base + (size_t)Sc * 8);
+  g.hc = (int32_t*)(base + (size_t)Sc * 12);
+  g.ends = (double*)(base + (((size_t)Sc * (12 + 4 * (size_t)L) + 7) & ~(size_t)7));
   return g;
 }
 

@@ -971,6 +971,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   }();
   dp.grec_hdr = grec_hdr;
   dp.grec_stride = grec_stride;
+  dp.grec_stage = (grec_hdr + dp_group_eval_bytes(Sc, Lmax) + 15) & ~(size_t)15;
   if ((e = ws.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
     return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   dp.wscr_global = (unsigned char*)ws.d_wscr.p;

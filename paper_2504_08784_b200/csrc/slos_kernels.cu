@@ -46,7 +46,9 @@ size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size
   return b + 64;
 }
 
-size_t dp_group_hdr_bytes() { return (sizeof(GroupHdr) + 127) & ~(size_t)127; }
+size_t dp_group_hdr_bytes() { return (sizeof(GroupHdr) + 15) & ~(size_t)15; }
+
+size_t dp_group_eval_bytes(int Sc, int L) { return group_var_eval_bytes(Sc, L); }
 
 size_t dp_anchor_stride(int R, int Sc, int L, int N) { return anchor_stride_bytes(R, Sc, L, N);
 }
