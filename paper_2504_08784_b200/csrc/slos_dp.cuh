@@ -760,6 +760,22 @@ __global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm
       v.dues_done = 1;
     }
     __syncwarp();
+    // packed form for the DP's thread-per-key placement (thread_place_budget)
+    if (v.valid && v.S <= Sc && L <= 4) {
+      int big = 0;
+      for (int s = lane_id(); s < v.S; s += 32) {
+        uint32_t pk = 0;
+        for (int l = 0; l < L; ++l) {
+          const int32_t h = ga.hc[l * v.S + s];
+          if (h > 255) big = 1;
+          pk |= (uint32_t)(h & 0xff) << (8 * l);
+        }
+        ga.hcp[s] = pk;
+        ga.cnx[s] = ga.cap[s] - ga.nx[s];
+      }
+      v.packed = warp_or(big) ? 0 : 1;
+    }
+    __syncwarp();
     if (lane_id() == 0) { H->g = g; H->v = v; H->j = j; }
   }
 }
@@ -1045,6 +1061,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         int j;
         uint64_t cw;
         MemoEnt* e;
+        const long long dbg0 = prm.phase_cycles ? clock64() : 0;
         key_of(q, j, cw, e);
         const unsigned char* rec = rec_of(j);
         const GroupHdr& H = *(const GroupHdr*)rec;
@@ -1053,7 +1070,18 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
 #pragma unroll
         for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
         EvalOut r;
-        if (thread_eval_counts(P, H.g, H.v, ga, prm.Sc, cv, min_slot, r)) {
+        const long long dbg1 = prm.phase_cycles ? clock64() : 0;
+        const int fb = thread_eval_counts(P, H.g, H.v, ga, prm.Sc, cv, min_slot, r);
+        if (prm.phase_cycles) {
+          const long long dbg2 = clock64();
+          atomicAdd(&prm.phase_cycles[24], (unsigned long long)(dbg2 - dbg1));
+          atomicAdd(&prm.phase_cycles[25], 1ull);
+          atomicMax(&prm.phase_cycles[26], (unsigned long long)(dbg2 - dbg1));
+          atomicAdd(&prm.phase_cycles[27], (unsigned long long)(dbg1 - dbg0));
+          if (r.dues == 0) atomicAdd(&prm.phase_cycles[28], 1ull);
+          if (H.v.Lx > 0) atomicAdd(&prm.phase_cycles[29], 1ull);
+        }
+        if (fb) {
           Cj[atomicAdd(&s_nw, 1)] = q;
           continue;
         }
@@ -1219,6 +1247,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       int32_t* cntB = Cj;   // anchors are no longer needed this level
       int32_t* offB = Cme;  // memo slots are no longer needed after step 4
       for (int b = tid; b < NB; b += kDpThreads) cntB[b] = 0;
+      if (tid == 0) s_bovf = 0;  // reused below: a bucket of more than 32 candidates exists
       __syncthreads();
       for (int c = tid; c < T; c += kDpThreads)
         if (Cbk[c] >= 0) atomicAdd(&cntB[Cbk[c]], 1);
@@ -1237,12 +1266,57 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       __syncthreads();
       for (int c = tid; c < T; c += kDpThreads) {
         const int b = Cbk[c];
-        if (b >= 0) Blst[offB[b] + atomicAdd(&cntB[b], 1)] = c;
+        if (b >= 0) {
+          const int pos = atomicAdd(&cntB[b], 1);
+          Blst[offB[b] + pos] = c;
+          if (pos == 32) s_bovf = 1;
+        }
       }
       __syncthreads();
+      // buckets of <= 32 candidates: one warp each, members in registers, the
+      // pairwise tests over shuffles (no memory traffic in the loops)
+      {
+        const int lane = lane_id();
+        for (int b = warp_id(); b < NB; b += kDpWarps) {
+          const int n = cntB[b];
+          if (n > 32) continue;
+          int c = 0x7fffffff;
+          double xv = 0.0;
+          int64_t xm = 0, xp = 0;
+          int xn = 0;
+          if (lane < n) {
+            c = Blst[offB[b] + lane];
+            xv = Cvl[c]; xm = Cmm[c]; xp = Cpb[c]; xn = Cna[c];
+          }
+          bool acc = lane < n;
+          for (int y = 0; y < n; ++y) {
+            const int yc = __shfl_sync(0xffffffffu, c, y);
+            const double yv = __shfl_sync(0xffffffffu, xv, y);
+            const int64_t ym = __shfl_sync(0xffffffffu, xm, y);
+            const int64_t yp = __shfl_sync(0xffffffffu, xp, y);
+            const int yn = __shfl_sync(0xffffffffu, xn, y);
+            if (yc < c && yv >= xv && ym <= xm && yp >= xp) {
+              const bool equal = yv == xv && ym == xm && yp == xp;
+              if (!equal || yn >= xn) acc = false;
+            }
+          }
+          const unsigned Am = __ballot_sync(0xffffffffu, acc);
+          bool pr = false;
+          for (unsigned t = Am; t; t &= t - 1) {
+            const int y = __ffs(t) - 1;
+            const int yc = __shfl_sync(0xffffffffu, c, y);
+            const double yv = __shfl_sync(0xffffffffu, xv, y);
+            const int64_t ym = __shfl_sync(0xffffffffu, xm, y);
+            const int64_t yp = __shfl_sync(0xffffffffu, xp, y);
+            if (yc > c && yv >= xv && ym <= xm && yp >= xp) pr = true;
+          }
+          if (acc) Cfl[c] |= pr ? 6 : 2;
+        }
+      }
+      if (s_bovf) {  // larger buckets: one thread per candidate over the bucket list
       for (int c = tid; c < T; c += kDpThreads) {
         const int b = Cbk[c];
-        if (b < 0) continue;
+        if (b < 0 || cntB[b] <= 32) continue;
         const double xv = Cvl[c];
         const int64_t xm = Cmm[c], xp = Cpb[c];
         const int xn = Cna[c];
@@ -1265,6 +1339,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       for (int c = tid; c < T; c += kDpThreads) {
         if (!(Cfl[c] & 2)) continue;
         const int b = Cbk[c];
+        if (cntB[b] <= 32) continue;
         const double xv = Cvl[c];
         const int64_t xm = Cmm[c], xp = Cpb[c];
         const int32_t* lst = Blst + offB[b];
@@ -1274,6 +1349,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
           if (y <= c || !(Cfl[y] & 2)) continue;
           if (Cvl[y] >= xv && Cmm[y] <= xm && Cpb[y] >= xp) { Cfl[c] |= 4; break; }
         }
+      }
       }
     }
     if (fastB) {

@@ -222,9 +222,16 @@ __device__ inline void blk_sort_mrec(MRec* r, int n_pow2) {
 __device__ inline int gap_prefill_only(const PlannerDev& P, double gap, double min_slot,
                                        GapPlanBuf& o) {
   double t = 0.0;
+  const int64_t Cfull = imin(P.max_chunk, P.max_batch);  // see prefill_only_budget
+  const double predC = predict(P, Cfull, 0);
   for (long guard = 0; gap - t >= min_slot - kTimeEps; ++guard) {
-    int64_t size = plan_time2bs(P, gap - t, 0);
-    if (size < 0) return SLOS_ERR_INFEASIBLE_BUDGET;
+    int64_t size;
+    if (time_le(predC, (gap - t) / P.margin1)) {
+      size = Cfull;
+    } else {
+      size = plan_time2bs(P, gap - t, 0);
+      if (size < 0) return SLOS_ERR_INFEASIBLE_BUDGET;
+    }
     if (guard > 100000000L) return SLOS_ERR_INTERNAL_INCONSISTENCY;
     size = imin(size, P.max_chunk);
     const double dur = plan_predict(P, size, 0);

@@ -103,6 +103,7 @@ struct Variant {
   int valid;
   int inc;          // slot ends strictly increasing -> jit may be walked
   int dues_done;    // exact dues filled from the anchor due pass (no E2 task)
+  int packed;       // cnx/hcp valid: L <= 4 and every canonical per-slot count <= 255
 };
 
 // A group's shared variant arrays (shared memory).
@@ -111,6 +112,8 @@ struct GroupVar {
   int64_t* cap;
   int32_t* nx;
   int32_t* hc;
+  int64_t* cnx;    // cap - nx per slot (group_kernel, when packed)
+  uint32_t* hcp;   // canonical dues per slot, 8 bits per tier (tiers 0..3, when packed)
 };
 
 struct GroupHdr {
@@ -120,22 +123,26 @@ struct GroupHdr {
 };
 
 __host__ __device__ __forceinline__ size_t group_var_stride(int Sc, int L) {
-  return (((size_t)Sc * (8 + 4 + 4 * (size_t)L + 8)) + 127) & ~(size_t)127;
+  return (((size_t)Sc * (8 + 4 + 8 + 4 + 4 * (size_t)L + 8)) + 127) & ~(size_t)127;
 }
 
 // Bytes of a group variant the DP's key evaluation reads (everything but the
 // slot ends, which are last): what a DP level stages into shared memory.
 __host__ __device__ __forceinline__ size_t group_var_eval_bytes(int Sc, int L) {
-  return (((size_t)Sc * (8 + 4 + 4 * (size_t)L)) + 15) & ~(size_t)15;
+  return (((size_t)Sc * (8 + 4 + 8 + 4 + 4 * (size_t)L)) + 15) & ~(size_t)15;
 }
 
-// layout: cap[Sc] (i64), nx[Sc] (i32), hc[L][Sc] (i32), ends[Sc] (f64)
+// layout: cnx[Sc] (i64), hcp[Sc] (u32), cap[Sc] (i64), nx[Sc] (i32), hc[L][Sc] (i32),
+// ends[Sc] (f64)
 __device__ __forceinline__ GroupVar group_var_carve(unsigned char* base, int Sc, int L) {
   GroupVar g;
-  g.cap = (int64_t*)base;
-  g.nx = (int32_t*)(base + (size_t)Sc * 8);
-  g.hc = (int32_t*)(base + (size_t)Sc * 12);
-  g.ends = (double*)(base + (((size_t)Sc * (12 + 4 * (size_t)L) + 7) & ~(size_t)7));
+  const size_t S = (size_t)Sc;
+  g.cnx = (int64_t*)base;
+  g.hcp = (uint32_t*)(base + S * 8);
+  g.cap = (int64_t*)(base + ((S * 12 + 7) & ~(size_t)7));
+  g.nx = (int32_t*)((unsigned char*)g.cap + S * 8);
+  g.hc = (int32_t*)((unsigned char*)g.nx + S * 4);
+  g.ends = (double*)(((uintptr_t)((unsigned char*)g.hc + S * 4 * (size_t)L) + 7) & ~(uintptr_t)7);
   return g;
 }
 
@@ -362,6 +369,7 @@ __device__ inline void warp_group_from_anchor(const PlannerDev& P, const AnchorV
   v.cfail = 0;
   v.inc = 0;
   v.dues_done = 0;
+  v.packed = 0;
   for (int l = 0; l < kMaxTiers; ++l) v.q[l] = 0;
   if (g.gap <= kTimeEps || !F.exact_mask) return;
   v.t0 = F.t0;
@@ -705,11 +713,25 @@ __device__ inline void warp_build_canon_variant(const PlannerDev& P, double gap,
 }
 
 // prefill_only lambda (batch_planner.cpp:177-195), budget only. status!=0 on throw.
+// While the remaining budget fits a full chunk C = min(max_chunk, max_batch), the
+// step is exactly (C, plan_predict(C)): predict is monotone in the token count
+// (coefficients are validated nonnegative), so time2bs's binary search returns
+// >= C whenever predict(C) fits, and min(., max_chunk) = C. Only the tail steps
+// binary-search.
 __device__ inline int64_t prefill_only_budget(const PlannerDev& P, double gap, double min_slot,
                                               int* status) {
   double t = 0.0;
   int64_t budget = 0;
+  const int64_t C = imin(P.max_chunk, P.max_batch);
+  const double predC = predict(P, C, 0);
+  const double durC = predC * P.margin1;  // plan_predict(P, C, 0)
   for (long guard = 0; gap - t >= min_slot - kTimeEps; ++guard) {
+    if (time_le(predC, (gap - t) / P.margin1)) {  // plan_time2bs(gap - t) >= C
+      if (guard > 100000000L) { *status = SLOS_ERR_INTERNAL_INCONSISTENCY; return 0; }
+      budget += C;
+      t += durC;
+      continue;
+    }
     int64_t size = plan_time2bs(P, gap - t, 0);
     if (size < 0) { *status = SLOS_ERR_INFEASIBLE_BUDGET; return 0; }
     if (guard > 100000000L) { *status = SLOS_ERR_INTERNAL_INCONSISTENCY; return 0; }
@@ -822,13 +844,66 @@ namespace slos {
 // DP level are placed per warp at once (lanes over memo keys).
 __device__ inline int thread_place_budget(const PlannerDev& P, const Variant& v, const int64_t* cap,
                                           const int32_t* nx, const int32_t* hc, const int64_t* c,
-                                          int64_t* budget) {
+                                          int64_t* budget, const int64_t* cnx = nullptr,
+                                          const uint32_t* hcp = nullptr) {
   const int S = v.S;
   const int L = P.L;
+  if (v.packed && cnx && hcp) {
+    // n(s) = nx(s) + sum_l c_l * hc_l(s): one __dp4a over 8-bit lanes (L <= 4,
+    // canonical per-slot counts <= 255 and tier counts <= 250 both fit a byte)
+    uint32_t cpk = 0;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) if (l < L) cpk |= (uint32_t)c[l] << (8 * l);
+    if (v.Lx == 0) {
+      bool ok = true;
+      int64_t b = 0;
+#pragma unroll 4
+      for (int s = 0; s < S; ++s) {
+        const int64_t f = cnx[s] - (int64_t)__dp4a(hcp[s], cpk, 0u);
+        ok = ok && f >= 0;
+        b += imin(f, P.max_chunk);
+      }
+      if (ok) { *budget = b; return 1; }
+    }
+    int64_t capT = 0, F = 0, Dn = 0, min_diff = INT64_MAX;
+    for (int s = 0; s < S; ++s) {
+      const int64_t capv = cap[s];
+      int64_t used = v.Lx - capT;
+      used = used < 0 ? 0 : (used > capv ? capv : used);
+      capT += capv;
+      F += capv - used;
+      Dn += capv - cnx[s] + (int64_t)__dp4a(hcp[s], cpk, 0u);
+      min_diff = imin(min_diff, F - Dn);
+    }
+    if (v.Lx > capT) return 0;
+    if (min_diff < 0) return 0;
+    int64_t cap_after = 0, G_next = INT64_MAX, b = 0;
+    for (int u = S - 1; u >= 0; --u) {
+      const int64_t capv = cap[u];
+      const int64_t before = capT - cap_after - capv;
+      int64_t used = v.Lx - before;
+      used = used < 0 ? 0 : (used > capv ? capv : used);
+      const int64_t Gu = imin(F - Dn, G_next);
+      if (u + 1 < S) b += imin(G_next - Gu, P.max_chunk);
+      G_next = Gu;
+      F -= capv - used;
+      Dn -= capv - cnx[u] + (int64_t)__dp4a(hcp[u], cpk, 0u);
+      cap_after += capv;
+    }
+    b += imin(G_next, P.max_chunk);
+    *budget = b;
+    return 1;
+  }
+  // the count vector stays in registers: every tier loop is unrolled to kMaxTiers
+  // with constant indices (a runtime-bounded loop would index it in local memory)
+  int64_t cr[kMaxTiers];
+#pragma unroll
+  for (int l = 0; l < kMaxTiers; ++l) cr[l] = l < L ? c[l] : 0;
   auto dues_at = [&](int s) -> int64_t {
     int64_t n = nx ? nx[s] : 0;
-    for (int l = 0; l < L; ++l)
-      if (c[l] > 0) n += c[l] * (int64_t)hc[l * S + s];
+#pragma unroll
+    for (int l = 0; l < kMaxTiers; ++l)
+      if (cr[l] > 0) n += cr[l] * (int64_t)hc[l * S + s];
     return n;
   };
   if (v.Lx == 0) {
@@ -883,7 +958,8 @@ __device__ inline int thread_eval_counts(const PlannerDev& P, const GapGroup& g,
   if (P.speculative) return 1;
   const int L = P.L;
   unsigned cmask = 0;
-  for (int l = 0; l < L; ++l) if (c[l] > 0) cmask |= 1u << l;
+#pragma unroll
+  for (int l = 0; l < kMaxTiers; ++l) if (l < L && c[l] > 0) cmask |= 1u << l;
   if (g.gap <= kTimeEps) { o.has = !g.any_due; return 0; }
   const unsigned present = g.exact_mask | cmask;
   auto prefill_only = [&]() {
@@ -898,7 +974,8 @@ __device__ inline int thread_eval_counts(const PlannerDev& P, const GapGroup& g,
   if (!(gv.valid && gv.t0 == t0)) return 1;
   if (gv.S > Sc) { o.status = SLOS_ERR_CAPACITY; return 0; }
   int64_t Dtot = gv.Dx;
-  for (int l = 0; l < L; ++l) Dtot += c[l] * (int64_t)gv.q[l];
+#pragma unroll
+  for (int l = 0; l < kMaxTiers; ++l) if (l < L) Dtot += c[l] * (int64_t)gv.q[l];
   o.dues = Dtot;
   if (Dtot == 0) { prefill_only(); return 0; }
   if (min_slot > t0 + kTimeEps) return 0;
@@ -907,7 +984,7 @@ __device__ inline int thread_eval_counts(const PlannerDev& P, const GapGroup& g,
   if (gv.cap_err) { o.status = SLOS_ERR_INFEASIBLE_BUDGET; return 0; }
   if (gv.exact_fail || (gv.cfail & cmask)) return 0;
   int64_t b = 0;
-  o.has = thread_place_budget(P, gv, ga.cap, ga.nx, ga.hc, c, &b) != 0;
+  o.has = thread_place_budget(P, gv, ga.cap, ga.nx, ga.hc, c, &b, ga.cnx, ga.hcp) != 0;
   o.budget = o.has ? b : 0;
   return 0;
 }
