@@ -929,26 +929,37 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   for (int i = 0; i < N && !s_err; ++i) {
     const int jlo = ch_fl[i];
     const int nlev = i - jlo;  // source levels jlo+1 .. i (anchor j = level - 1)
-    if (tid == 0) {
-      int acc = 0, kacc = 0, anysh = 0;
-      for (int k = 0; k < nlev; ++k) {
-        const int lv = jlo + 1 + k;
-        s_pre[k] = acc;
-        acc += lvl_cnt[lv];
-        const uint8_t sh = PS[pair_index(N, lv, i)];
-        s_sh[k] = sh;
-        s_kpre[k] = kacc;
-        if (sh) anysh = 1;
-        else kacc += lvl_nsb[lv];
+    if (warp_id() == 0) {  // level prefixes, lanes over source levels
+      const int lane = lane_id();
+      int acc = 0, kacc = 0;
+      unsigned anysh = 0;
+      for (int base = 0; base < nlev; base += 32) {
+        const int k = base + lane;
+        int cnt = 0, kc = 0;
+        if (k < nlev) {
+          const int lv = jlo + 1 + k;
+          const uint8_t sh = PS[pair_index(N, lv, i)];
+          s_sh[k] = sh;
+          cnt = lvl_cnt[lv];
+          kc = sh ? 0 : lvl_nsb[lv];
+          anysh |= sh ? 1u : 0u;
+        }
+        const int ic = warp_incl_scan(cnt), ik = warp_incl_scan(kc);
+        if (k < nlev) { s_pre[k] = acc + ic - cnt; s_kpre[k] = kacc + ik - kc; }
+        acc += __shfl_sync(0xffffffffu, ic, 31);
+        kacc += __shfl_sync(0xffffffffu, ik, 31);
       }
-      s_pre[nlev] = acc;
-      s_kpre[nlev] = kacc;
-      s_anysh = anysh;
-      s_n_new = 0;
-      s_nb = 0;
-      s_nw = 0;
-      if (acc > Tsm && acc > capC) { s_err = SLOS_ERR_CAPACITY; out->need_cand = acc; }
-      else if (kacc > capC) { s_err = SLOS_ERR_CAPACITY; out->need_cand = kacc; }
+      anysh = __reduce_or_sync(0xffffffffu, anysh);
+      if (lane == 0) {
+        s_pre[nlev] = acc;
+        s_kpre[nlev] = kacc;
+        s_anysh = anysh != 0;
+        s_n_new = 0;
+        s_nb = 0;
+        s_nw = 0;
+        if (acc > Tsm && acc > capC) { s_err = SLOS_ERR_CAPACITY; out->need_cand = acc; }
+        else if (kacc > capC) { s_err = SLOS_ERR_CAPACITY; out->need_cand = kacc; }
+      }
     }
     __syncthreads();
     if (s_err) break;
@@ -1010,7 +1021,10 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       const int lv = jlo + 1 + k;
       const int src = (int)(lvl_off[lv] + (c - s_pre[k]));
       Csrc[c] = src;
-      if (!s_sh[k]) continue;
+      if (!s_sh[k]) {  // fresh pair: the key is (level, surviving source bucket)
+        Cme[c] = -(s_kpre[k] + Ssb[src]) - 1;
+        continue;
+      }
       const int j = lv - 1;
       const double a = (j < 0) ? I.now : ch_dl[j];
       const double raw = dmax(0.0, t_i - a);
@@ -1149,15 +1163,15 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     const bool forced = ch_fc[i] != 0;
     for (int c = tid; c < T; c += kDpThreads) {
       const int src = Csrc[c];
-      const int k = level_of(c);
+      const int me = Cme[c];
       bool has;
       int64_t val;
-      if (s_sh[k]) {
-        const MemoEnt* e = &Memo[Cme[c]];
+      if (me >= 0) {
+        const MemoEnt* e = &Memo[me];
         has = e->has != 0;
         val = e->val;
       } else {
-        val = Kv[s_kpre[k] + Ssb[src]];
+        val = Kv[-me - 1];
         has = val >= 0;
       }
       int flag = 0;
@@ -1558,9 +1572,11 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         const int fl = c < T ? Cfl[c] : 0;
         const int acc = (fl & 2) ? 1 : 0;
         const int sv = ((fl & 2) && !(fl & 4)) ? 1 : 0;
-        int64_t tot_acc, tot_sv;
-        const int64_t r_acc = block_excl_scan(acc, s_wsum, &tot_acc);
-        const int64_t r_sv = block_excl_scan(sv, s_wsum, &tot_sv);
+        // one scan for both counts: accepted in the low, surviving in the high word
+        int64_t tot2;
+        const int64_t r2 = block_excl_scan((int64_t)acc | ((int64_t)sv << 32), s_wsum, &tot2);
+        const int64_t r_acc = r2 & 0xffffffffLL, r_sv = r2 >> 32;
+        const int64_t tot_acc = tot2 & 0xffffffffLL, tot_sv = tot2 >> 32;
         if (sv) {
           const int64_t dst = base_free + carry_sv + r_sv;
           if (dst < I.cap_surv) {
