@@ -1012,6 +1012,19 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       return staged ? (const unsigned char*)ovl + (size_t)(j - jlo) * prm.grec_stage
                     : GRl + (size_t)(j - jlo) * prm.grec_stride;
     };
+    // a group's variant arrays: the staged prefix (cnx, hcp, cap) and, from the
+    // HBM record, the unpacked nx / hc / ends
+    auto var_of = [&](int j) -> GroupVar {
+      GroupVar g = group_var_carve((unsigned char*)GRl + (size_t)(j - jlo) * prm.grec_stride + prm.grec_hdr,
+                                   prm.Sc, L);
+      if (staged) {
+        const GroupVar st = group_var_carve((unsigned char*)rec_of(j) + prm.grec_hdr, prm.Sc, L);
+        g.cnx = st.cnx;
+        g.hcp = st.hcp;
+        g.cap = st.cap;
+      }
+      return g;
+    };
     // ---- 1: memo keys. A pair whose key (a_us, raw_us) is unique to it (host
     // flag) has one key per surviving source bucket: key s_kpre[k] + bucket id,
     // no table. Shared pairs use the instance's hash memo, whose first-inserted
@@ -1079,7 +1092,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         key_of(q, j, cw, e);
         const unsigned char* rec = rec_of(j);
         const GroupHdr& H = *(const GroupHdr*)rec;
-        const GroupVar ga = group_var_carve((unsigned char*)rec + prm.grec_hdr, prm.Sc, L);
+        const GroupVar ga = var_of(j);
         int64_t cv[kMaxTiers];
 #pragma unroll
         for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;
@@ -1129,7 +1142,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         key_of(q, j, cw, e);
         const unsigned char* rec = rec_of(j);
         const GroupHdr& H = *(const GroupHdr*)rec;
-        const GroupVar ga = group_var_carve((unsigned char*)rec + prm.grec_hdr, prm.Sc, L);
+        const GroupVar ga = var_of(j);
         int64_t cv[kMaxTiers];
 #pragma unroll
         for (int l = 0; l < kMaxTiers; ++l) cv[l] = l < L ? pack_get(cw, l) : 0;

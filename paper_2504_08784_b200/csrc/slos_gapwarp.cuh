@@ -126,10 +126,12 @@ __host__ __device__ __forceinline__ size_t group_var_stride(int Sc, int L) {
   return (((size_t)Sc * (8 + 4 + 8 + 4 + 4 * (size_t)L + 8)) + 127) & ~(size_t)127;
 }
 
-// Bytes of a group variant the DP's key evaluation reads (everything but the
-// slot ends, which are last): what a DP level stages into shared memory.
+// Bytes of a group variant a DP level stages into shared memory: the packed
+// placement inputs cnx / hcp and the slot capacities (the leading arrays). The
+// unpacked nx / hc are read from the HBM record when a group needs them.
 __host__ __device__ __forceinline__ size_t group_var_eval_bytes(int Sc, int L) {
-  return (((size_t)Sc * (8 + 4 + 8 + 4 + 4 * (size_t)L)) + 15) & ~(size_t)15;
+  (void)L;
+  return (((size_t)Sc * (8 + 4 + 8)) + 15) & ~(size_t)15;
 }
 
 // layout: cnx[Sc] (i64), hcp[Sc] (u32), cap[Sc] (i64), nx[Sc] (i32), hc[L][Sc] (i32),
