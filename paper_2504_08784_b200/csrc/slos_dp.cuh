@@ -405,6 +405,15 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
   (void)s_red;
 }
 
+// Cooperative copy of a plain struct into shared memory (8-byte words, all threads).
+template <class T>
+__device__ __forceinline__ void block_copy_struct(T& dst, const T& src, int tid, int nt) {
+  static_assert(sizeof(T) % 8 == 0, "8-byte words");
+  const uint64_t* s = (const uint64_t*)&src;
+  uint64_t* d = (uint64_t*)&dst;
+  for (int k = tid; k < (int)(sizeof(T) / 8); k += nt) d[k] = s[k];
+}
+
 // Anchor due pass (replaces the per-group member walks of E2): every exact member's
 // due line from anchor a is walked ONCE, up to the longest due horizon of any group
 // (j, i) this anchor opens, exactly as member_dues_warp walks it (same repeated
@@ -634,10 +643,8 @@ __global__ void __launch_bounds__(kAnchorThreads, SLOS_ANCHOR_MIN_BLOCKS) anchor
   const BatchArgs& A = prm.a;
   const int tid = threadIdx.x;
   const int v = A.atask[2 * blockIdx.x], j = A.atask[2 * blockIdx.x + 1];
-  if (tid == 0) {
-    sI = A.inst[v];
-    sP = A.planners[sI.planner];
-  }
+  block_copy_struct(sI, A.inst[v], tid, kAnchorThreads);
+  block_copy_struct(sP, A.planners[A.inst[v].planner], tid, kAnchorThreads);
   __syncthreads();
   const PlannerDev& P = sP;
   const InstDev& I = sI;
@@ -691,10 +698,8 @@ __global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm
   __shared__ InstDev sI;
   const BatchArgs& A = prm.a;
   const int vi = A.atask[2 * blockIdx.x], j = A.atask[2 * blockIdx.x + 1];
-  if (threadIdx.x == 0) {
-    sI = A.inst[vi];
-    sP = A.planners[sI.planner];
-  }
+  block_copy_struct(sI, A.inst[vi], threadIdx.x, 32 * kGroupWarps);
+  block_copy_struct(sP, A.planners[A.inst[vi].planner], threadIdx.x, 32 * kGroupWarps);
   __syncthreads();
   const PlannerDev& P = sP;
   const InstDev& I = sI;
