@@ -233,9 +233,11 @@ int slos_workspace_records(slos_workspace* ws, slos_record* out, void* stream);
  * reconstruction. CPU checkers report wall time of the whole solve in [0]. */
 int slos_workspace_kernel_ms(slos_workspace* ws, float* ms2);
 
-/* Per-kernel device time (ms) of the last solve, n <= 3 entries: [0] anchor caches
- * (anchor_kernel), [1] admission DP (dp_kernel), [2] plan reconstruction
- * (build_kernel). CPU checkers write zeros. */
+/* Device time (ms) of the last solve's stages, n <= 3 entries: [0] anchor caches
+ * and pair groups (anchor_kernel, group_kernel), [1] admission DP until its last
+ * part ends (dp_kernel; solve parts are pipelined, so earlier parts'
+ * reconstruction overlaps it), [2] the remaining plan reconstruction
+ * (build_kernel*). CPU checkers write zeros. */
 int slos_workspace_stage_ms(slos_workspace* ws, float* ms, int32_t n);
 
 /* Bytes moved host->device and device->host by the calling thread's last

@@ -581,16 +581,18 @@ __global__ void __launch_bounds__(32 * kBuildWarps, 2) build_kernel_warp(BuildPa
   __shared__ BuildShared shs[kBuildWarps];
   extern __shared__ __align__(16) unsigned char bsm[];
   const int idx = blockIdx.x * kBuildWarps + warp_id();
-  if (idx >= A.n_small) return;  // whole warp; the engine never uses CTA barriers here
+  const int q = 2 * prm.part;
+  if (idx >= A.qn[q]) return;  // whole warp; the engine never uses CTA barriers here
   const int64_t per = (int64_t)(prm.smem_warp / kBuildWarps) & ~(int64_t)255;
-  build_instance<WarpGrp>(A, shs[warp_id()], A.bq[4 + idx], bsm + per * warp_id(), per, prm.phase_cycles);
+  build_instance<WarpGrp>(A, shs[warp_id()], A.bq[A.qbase[q] + idx], bsm + per * warp_id(), per,
+                          prm.phase_cycles);
 }
 
 __global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_kernel(BuildParams prm) {
   const BatchArgs& A = prm.a;
   __shared__ BuildShared sh;
   extern __shared__ __align__(16) unsigned char bsm[];
-  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.bq[4 + A.n_small + blockIdx.x], bsm,
+  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.bq[A.qbase[2 * prm.part + 1] + blockIdx.x], bsm,
                                            (int64_t)prm.smem_bytes, prm.phase_cycles);
 }
 

@@ -24,6 +24,7 @@
 namespace slos {
 
 constexpr int kMaxTiers = 8;      // dp_scheduler.cpp:367
+constexpr int kMaxParts = 4;      // solve parts pipelined across streams
 constexpr int kMaxTerms = 8;      // PerfModel terms carried on device
 constexpr int kMaxSpecLen = 64;   // PlannerConfig::spec_max_len carried on device
 constexpr double kTimeEps = 1e-9;  // common.hpp:29
@@ -60,6 +61,7 @@ struct InstDev {
   int32_t have_running_decode;
   int32_t values_integral;  // all chain values integral -> eps ties impossible
   int32_t build_small;      // plan reconstruction by one warp (small instance)
+  int32_t part;             // solve part (dp + build launched per part, pipelined)
   int64_t off_dec;     // into dec_* arrays
   int64_t off_chain;   // into ch_* arrays (N items, suffix has N+1)
   int64_t off_pre;     // into pre_* arrays
@@ -173,9 +175,10 @@ struct BatchArgs {
   int64_t* k_val;              // per level: fresh-pair key results (budget, or -1 = nullopt)
   double* ctime;               // per instance: canonical due times [Lmax][Sc] (anchor_kernel)
   int32_t* ccnt;               // per instance: canonical due counts [kMaxTiers]
-  int32_t* bq;       // build queues (4 counters, then n_small + n_large ints): per queue,
-                     // fallback instances from the front, the rest from the back
-  int32_t n_small;   // instances reconstructed one warp each (build_kernel_warp), queue 0
+  int32_t* bq;       // build queues: 2 counters per queue, then the queue segments; per
+                     // queue, fallback instances from the front, the rest from the back
+  int32_t qbase[2 * kMaxParts];  // queue q = 2*part + (large ? 1 : 0): segment offset in bq
+  int32_t qn[2 * kMaxParts];     // and length
   OutHdr* out;
 };
 
@@ -225,15 +228,17 @@ struct DpParams {
   size_t grec_stride;       // bytes per pair group record
   size_t grec_hdr;          // header bytes before the variant arrays
   size_t grec_stage;        // bytes of a record the DP stages (header + evaluated arrays)
+  int blk0;                 // first position in `order` of this launch's part
 };
 
-// Push an instance onto its plan-reconstruction queue: queue 0 (warp-built, small
-// instances) occupies bq[4 .. 4+n_small), queue 1 the rest; fallback instances (a
+// Push an instance onto its plan-reconstruction queue: queue 2*part+0 holds the
+// part's warp-built (small) instances, 2*part+1 the rest; fallback instances (a
 // long sequential batch loop) are taken first, from the front.
-__device__ __forceinline__ void build_queue_push(const BatchArgs& A, int inst, bool small, bool front) {
-  const int base = small ? 4 : 4 + A.n_small;
-  const int n = small ? A.n_small : A.n_inst - A.n_small;
-  int32_t* c = A.bq + (small ? 0 : 2);
+__device__ __forceinline__ void build_queue_push(const BatchArgs& A, int inst, int part, bool small, bool front) {
+  const int q = 2 * part + (small ? 0 : 1);
+  const int base = A.qbase[q];
+  const int n = A.qn[q];
+  int32_t* c = A.bq + 2 * q;
   if (front) A.bq[base + atomicAdd(&c[0], 1)] = inst;
   else A.bq[base + n - 1 - atomicAdd(&c[1], 1)] = inst;
 }
@@ -243,6 +248,7 @@ struct BuildParams {
   BatchArgs a;
   size_t smem_bytes;  // build_kernel: dynamic shared memory per CTA (per-gap working set)
   size_t smem_warp;   // build_kernel_warp: dynamic shared memory per CTA (4 instances)
+  int part;           // solve part whose queues this launch drains
   unsigned long long* phase_cycles;  // 8 counters or nullptr (SLOS_PHASE_TIMING)
 };
 

@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
 
   const BatchArgs& A = prm.a;
   const int tid = threadIdx.x;
-  const int inst = A.order[blockIdx.x];
+  const int inst = A.order[prm.blk0 + blockIdx.x];
   OutHdr* out = &A.out[inst];
   if (tid == 0) {
     sP = A.planners[A.inst[inst].planner];
@@ -1632,7 +1632,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   if (s_err) {
     if (tid == 0) {
       out->status = s_err;
-      build_queue_push(A, inst, I.build_small != 0, false);
+      build_queue_push(A, inst, I.part, I.build_small != 0, false);
     }
     return;
   }
@@ -1753,7 +1753,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     out->status = 0;
     // plan-reconstruction queue: instances that fall back (a long sequential batch
     // loop) are queued from the front, the rest from the back
-    build_queue_push(A, inst, I.build_small != 0, best < 0);
+    build_queue_push(A, inst, I.part, I.build_small != 0, best < 0);
   }
   SLOS_PHASE(11);  // 11: terminal selection + backtrack
 }

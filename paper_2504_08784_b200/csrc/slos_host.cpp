@@ -315,6 +315,18 @@ int build_warp_max_dec() {
   return v;
 }
 
+// Parts of one solve whose DP / reconstruction are pipelined across streams
+// (SLOS_SOLVE_PARTS overrides; 1 disables).
+int solve_parts(int nv) {
+  static const int env = [] {
+    const char* e = std::getenv("SLOS_SOLVE_PARTS");
+    return e ? std::atoi(e) : 2;
+  }();
+  int P = std::max(1, std::min(env, kMaxParts));
+  if (nv < 128 * P) P = std::max(1, nv / 128);
+  return std::max(1, P);
+}
+
 bool integral(double v) { return std::isfinite(v) && v == std::floor(v) && std::fabs(v) < 4.0e15; }
 
 struct Prep {  // host-side per-instance preparation
@@ -522,6 +534,12 @@ struct Workspace {
   int n_total = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t own_stream = nullptr;  // pipeline workspaces only
+  int n_parts = 1;
+  int part_lo[kMaxParts + 1] = {0};
+  int qbase[2 * kMaxParts] = {0};
+  int qn[2 * kMaxParts] = {0};
+  cudaStream_t pstream[kMaxParts] = {nullptr};  // per-part streams, earlier parts higher priority
+  cudaEvent_t ev_fork = nullptr, ev_dp[kMaxParts] = {nullptr}, ev_join[kMaxParts] = {nullptr};
 };
 
 thread_local int64_t g_h2d = 0, g_d2h = 0;
@@ -652,7 +670,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.c_bkey = bs.add<uint64_t>(2 * TCd);
   Ly.c_bval = bs.add<int32_t>(2 * TCd);
   Ly.memo = bs.add<MemoEnt>(TM);
-  Ly.bq = bs.add<int32_t>(nv + 4);
+  Ly.bq = bs.add<int32_t>(nv + 4 * kMaxParts);
   Ly.work = bs.add<unsigned char>(TW);
   Ly.anchors = bs.add<unsigned char>(TA);
   Ly.groups = bs.add<unsigned char>((size_t)TPair * grec_stride);
@@ -867,6 +885,26 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     for (int v = 0; v < nv; ++v) ord[v] = v;
     std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
     for (int v = 0; v < nv; ++v) h_order[v] = ord[v];
+    // solve parts: contiguous ranges of the cost-descending order (every part gets
+    // a share of the heavy instances); each part's DP and reconstruction are
+    // launched on their own stream so one part's reconstruction overlaps the next
+    // part's DP (ws_solve)
+    const int P = solve_parts(nv);
+    ws.n_parts = P;
+    int qcount[2 * kMaxParts] = {0};
+    for (int p = 0; p <= P; ++p) ws.part_lo[p] = (int)((int64_t)p * nv / P);
+    for (int p = 0; p < P; ++p)
+      for (int x = ws.part_lo[p]; x < ws.part_lo[p + 1]; ++x) {
+        InstDev& I = hI[ord[x]];
+        I.part = p;
+        ++qcount[2 * p + (I.build_small ? 0 : 1)];
+      }
+    int qb = 4 * kMaxParts;
+    for (int q = 0; q < 2 * kMaxParts; ++q) {
+      ws.qbase[q] = qb;
+      ws.qn[q] = qcount[q];
+      qb += qcount[q];
+    }
   }
   {
     slos_record* rd = (slos_record*)hp(Ly.recdef);
@@ -944,7 +982,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   A.ctime = (double*)(DS + Ly.ctime);
   A.ccnt = (int32_t*)(DS + Ly.ccnt);
   A.bq = (int32_t*)(DS + Ly.bq);
-  A.n_small = n_small;
+  for (int q = 0; q < 2 * kMaxParts; ++q) { A.qbase[q] = ws.qbase[q]; A.qn[q] = ws.qn[q]; }
+  (void)n_small;
   A.out = (OutHdr*)(DO + Ly.out);
   A.sel = (int32_t*)(DO + Ly.sel);
   A.ids = (int32_t*)(DO + Ly.ids);
@@ -1026,18 +1065,27 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   cudaMemsetAsync(DS + Ly.c_bkey, 0, Ly.bkey_bytes, s);
   cudaMemsetAsync(DS + Ly.c_bval, 0xFF, Ly.bval_bytes, s);
   cudaMemsetAsync(DO + Ly.out, 0, sizeof(OutHdr) * nv, s);
-  cudaMemsetAsync(DS + Ly.bq, 0, 4 * sizeof(int32_t), s);
+  cudaMemsetAsync(DS + Ly.bq, 0, 4 * kMaxParts * sizeof(int32_t), s);
   cudaError_t e;
   for (int k = 0; k < 4; ++k)
     if (!ws.ev[k]) cudaEventCreate(&ws.ev[k]);
+  if (!ws.ev_fork) {
+    cudaEventCreateWithFlags(&ws.ev_fork, cudaEventDisableTiming);
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    for (int p = 0; p < kMaxParts; ++p) {
+      cudaStreamCreateWithPriority(&ws.pstream[p], cudaStreamNonBlocking, std::min(lo, hi + p));
+      cudaEventCreate(&ws.ev_dp[p]);
+      cudaEventCreateWithFlags(&ws.ev_join[p], cudaEventDisableTiming);
+    }
+  }
   cudaEventRecord(ws.ev[0], s);
   if ((e = launch_anchor(dp, ws.A.n_atask, ws.anchor_smem, s)) != cudaSuccess)
     return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   if ((e = launch_group(dp, ws.A.n_atask, ws.maxN, s)) != cudaSuccess)
     return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   cudaEventRecord(ws.ev[3], s);
-  if ((e = launch_dp(dp, nv, smem, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  cudaEventRecord(ws.ev[1], s);
+  cudaEventRecord(ws.ev_fork, s);
   BuildParams bp;
   bp.a = ws.A;
   static const size_t kBuildSmem = [] {  // per-gap working set per CTA (SLOS_BUILD_SMEM_KB)
@@ -1051,10 +1099,35 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   }();
   bp.smem_warp = kBuildSmemWarp;
   bp.phase_cycles = dp.phase_cycles ? dp.phase_cycles + 16 : nullptr;
-  if ((e = launch_build(bp, ws.A.n_small, nv - ws.A.n_small, s)) != cudaSuccess)
-    return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  // per part: admission DP, then its plan reconstruction, on the part's stream;
+  // part p's reconstruction runs while part p+1's DP still occupies SMs
+  for (int p = 0; p < ws.n_parts; ++p) {
+    const cudaStream_t sp = ws.pstream[p];
+    cudaStreamWaitEvent(sp, ws.ev_fork, 0);
+    DpParams dpp = dp;
+    dpp.blk0 = ws.part_lo[p];
+    if ((e = launch_dp(dpp, ws.part_lo[p + 1] - ws.part_lo[p], smem, sp)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    cudaEventRecord(ws.ev_dp[p], sp);
+    bp.part = p;
+    if ((e = launch_build(bp, ws.qn[2 * p], ws.qn[2 * p + 1], sp)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    cudaEventRecord(ws.ev_join[p], sp);
+    cudaStreamWaitEvent(s, ws.ev_join[p], 0);
+  }
   cudaEventRecord(ws.ev[2], s);
   return SLOS_OK;
+}
+
+// end of the admission DP over all parts (ms after ev[0])
+float dp_end_ms(Workspace& ws) {
+  float t = 0.0f;
+  for (int p = 0; p < ws.n_parts; ++p) {
+    float x = 0.0f;
+    cudaEventElapsedTime(&x, ws.ev[0], ws.ev_dp[p]);
+    t = std::max(t, x);
+  }
+  return t;
 }
 
 // Headers back, capacity regrowth list, compaction and one D2H of the results.
@@ -1489,8 +1562,10 @@ int slos_workspace_kernel_ms(slos_workspace* b, float* ms2) {
   ms2[0] = ms2[1] = 0.0f;
   if (!ws.ev[2]) return SLOS_OK;
   cudaEventSynchronize(ws.ev[2]);
-  cudaEventElapsedTime(&ms2[0], ws.ev[0], ws.ev[1]);
-  cudaEventElapsedTime(&ms2[1], ws.ev[1], ws.ev[2]);
+  float all = 0.0f;
+  cudaEventElapsedTime(&all, ws.ev[0], ws.ev[2]);
+  ms2[0] = dp_end_ms(ws);
+  ms2[1] = all - ms2[0];
   return SLOS_OK;
 }
 
@@ -1499,9 +1574,12 @@ int slos_workspace_stage_ms(slos_workspace* b, float* ms, int32_t n) {
   float t[3] = {0.0f, 0.0f, 0.0f};
   if (ws.ev[2]) {
     cudaEventSynchronize(ws.ev[2]);
+    float all = 0.0f;
+    cudaEventElapsedTime(&all, ws.ev[0], ws.ev[2]);
     cudaEventElapsedTime(&t[0], ws.ev[0], ws.ev[3]);
-    cudaEventElapsedTime(&t[1], ws.ev[3], ws.ev[1]);
-    cudaEventElapsedTime(&t[2], ws.ev[1], ws.ev[2]);
+    const float dp_end = dp_end_ms(ws);  // last part's DP (the reconstruction of earlier
+    t[1] = dp_end - t[0];                // parts overlaps it)
+    t[2] = all - dp_end;
   }
   for (int k = 0; k < n && k < 3; ++k) ms[k] = t[k];
   return SLOS_OK;
