@@ -124,11 +124,17 @@ typedef struct slos_input { /* ScheduleInput dp_scheduler.hpp:38-47 */
 /* Entry request reference: req >= 0 is running[req]; req < 0 is pending[-req-1]. */
 #define SLOS_PENDING_REF(p) (-(int32_t)(p)-1)
 
-typedef struct slos_entry { /* PlanEntry dp_scheduler.hpp:49-54 */
+/* PlanEntry dp_scheduler.hpp:49-54. Token counts are 32-bit on the wire (plans are
+ * the bulk of the device->host traffic): every count is bounded by a batch
+ * capacity, and slos_planner_create rejects max_batch_tokens / max_chunk_tokens
+ * above INT32_MAX; a plan whose count would still not fit (only possible with
+ * absurd decode backlogs in the EDF fallback) fails with SLOS_ERR_INVALID_PARAMETERS
+ * instead of truncating. The adapter widens them back to the reference's int64. */
+typedef struct slos_entry {
   int32_t req;
   int32_t spec_len;
-  int64_t prefill_tokens;
-  int64_t decode_tokens;
+  int32_t prefill_tokens;
+  int32_t decode_tokens;
 } slos_entry;
 
 typedef struct slos_batch { /* PlanBatch dp_scheduler.hpp:56-63 */

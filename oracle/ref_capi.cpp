@@ -16,6 +16,7 @@
 //   slos_expected_accepted  -> expected_accepted  batch_planner.cpp:32
 
 #include <atomic>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <ctime>
@@ -106,7 +107,13 @@ void fill_result(const slos_input* in, const ScheduleResult& res, slos_result* o
   for (int i = 0; i < in->n_running; ++i) ref.emplace(in->running[i].id, i);
   for (int i = 0; i < in->n_pending; ++i) ref.emplace(in->pending[i].id, SLOS_PENDING_REF(i));
   size_t n_entries = 0;
-  for (const auto& b : res.plan.batches) n_entries += b.entries.size();
+  for (const auto& b : res.plan.batches) {
+    n_entries += b.entries.size();
+    for (const PlanEntry& pe : b.entries)  // token counts must fit the 32-bit slos_entry
+      if (pe.prefill_tokens > INT32_MAX || pe.decode_tokens > INT32_MAX || pe.prefill_tokens < INT32_MIN ||
+          pe.decode_tokens < INT32_MIN)
+        fail("invalid-parameters", "a plan token count exceeds the 32-bit entry range");
+  }
   const size_t n_adm = res.admitted.size(), n_dec = res.declined.size(),
                n_def = res.deferred.size(), n_b = res.plan.batches.size();
   size_t bytes = sizeof(slos_batch) * n_b + sizeof(slos_entry) * n_entries +
@@ -132,8 +139,8 @@ void fill_result(const slos_input* in, const ScheduleResult& res, slos_result* o
     for (const PlanEntry& pe : b.entries) {
       entries[e].req = ref.at(pe.id);
       entries[e].spec_len = pe.spec_len;
-      entries[e].prefill_tokens = pe.prefill_tokens;
-      entries[e].decode_tokens = pe.decode_tokens;
+      entries[e].prefill_tokens = (int32_t)pe.prefill_tokens;
+      entries[e].decode_tokens = (int32_t)pe.decode_tokens;
       ++e;
     }
   }
@@ -250,6 +257,8 @@ int slos_planner_create(const slos_perf_term* terms, int32_t n_terms, const doub
     p->cfg.plan_margin = c.plan_margin;
     p->planner = std::make_unique<BatchPlanner>(p->model, p->slo, p->cfg);
     p->sched = std::make_unique<SloScheduler>(*p->planner);
+    if (c.max_chunk_tokens > INT32_MAX || c.max_batch_tokens > INT32_MAX)  // 32-bit slos_entry
+      fail("invalid-parameters", "batch and chunk caps must fit the 32-bit plan entries");
     *out = p.release();
     return SLOS_OK;
   });

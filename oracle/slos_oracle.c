@@ -260,6 +260,7 @@ int slos_planner_create(const slos_perf_term* terms, int32_t n_terms, const doub
   if (cfg) c = *cfg; else slos_planner_config_default(&c);
   /* BatchPlanner::BatchPlanner batch_planner.cpp:117-123 */
   if (c.max_chunk_tokens < 1 || c.max_batch_tokens < 1) goto fail_soft;
+  if (c.max_chunk_tokens > INT32_MAX || c.max_batch_tokens > INT32_MAX) goto fail_soft; /* 32-bit slos_entry */
   if (c.plan_margin < 0) goto fail_soft;
   slos_planner* p = calloc(1, sizeof *p);
   p->terms = malloc(sizeof(slos_perf_term) * (size_t)n_terms);
@@ -1190,6 +1191,13 @@ static void emit_result(const slos_input* in, int infeasible, double value, cons
                         int nadm, const int32_t* dec, int ndec, const splan_t* plan,
                         const slos_counters* ctr, slos_result* out) {
   (void)in;
+  for (int64_t k = 0; k < plan->e.n; ++k) /* token counts must fit the 32-bit slos_entry */
+    if (plan->e.v[k].prefill > INT32_MAX || plan->e.v[k].decode > INT32_MAX ||
+        plan->e.v[k].prefill < INT32_MIN || plan->e.v[k].decode < INT32_MIN) {
+      memset(out, 0, sizeof *out);
+      out->status = SLOS_ERR_INVALID_PARAMETERS;
+      return;
+    }
   size_t bytes = sizeof(obatch_t) + sizeof(slos_batch) * (size_t)plan->b.n +
                  sizeof(slos_entry) * (size_t)plan->e.n + sizeof(int32_t) * (size_t)(nadm + ndec) + 64;
   char* mem = calloc(1, bytes);
@@ -1208,8 +1216,8 @@ static void emit_result(const slos_input* in, int infeasible, double value, cons
   for (int64_t k = 0; k < plan->e.n; ++k) {
     e[k].req = plan->e.v[k].req;
     e[k].spec_len = plan->e.v[k].spec_len;
-    e[k].prefill_tokens = plan->e.v[k].prefill;
-    e[k].decode_tokens = plan->e.v[k].decode;
+    e[k].prefill_tokens = (int32_t)plan->e.v[k].prefill;
+    e[k].decode_tokens = (int32_t)plan->e.v[k].decode;
   }
   for (int k = 0; k < nadm; ++k) ids[k] = adm[k];
   for (int k = 0; k < ndec; ++k) ids[nadm + k] = dec[k];

@@ -96,12 +96,12 @@ class Input(C.Structure):
     ]
 
 
-class Entry(C.Structure):
+class Entry(C.Structure):  # slos_entry: 32-bit token counts on the wire
     _fields_ = [
         ("req", C.c_int32),
         ("spec_len", C.c_int32),
-        ("prefill_tokens", C.c_int64),
-        ("decode_tokens", C.c_int64),
+        ("prefill_tokens", C.c_int32),
+        ("decode_tokens", C.c_int32),
     ]
 
 
@@ -268,9 +268,19 @@ INPUT_DTYPE = np.dtype(
 ENTRY_DTYPE = np.dtype(
     {
         "names": ["req", "spec_len", "prefill_tokens", "decode_tokens"],
+        "formats": [np.int32, np.int32, np.int32, np.int32],
+        "offsets": [0, 4, 8, 12],
+        "itemsize": C.sizeof(Entry),
+    }
+)
+# The canonical (reference PlanEntry) form used by parity digests: int64 token
+# counts, independent of the wire layout.
+CANON_ENTRY_DTYPE = np.dtype(
+    {
+        "names": ["req", "spec_len", "prefill_tokens", "decode_tokens"],
         "formats": [np.int32, np.int32, np.int64, np.int64],
         "offsets": [0, 4, 8, 16],
-        "itemsize": C.sizeof(Entry),
+        "itemsize": 24,
     }
 )
 BATCH_DTYPE = np.dtype(

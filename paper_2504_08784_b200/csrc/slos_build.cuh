@@ -20,6 +20,12 @@ namespace slos {
     }                                                                          \
   } while (0)
 
+// A plan token count as a 32-bit entry field (flags values that do not fit).
+__device__ __forceinline__ int32_t tok32(int64_t v, int* err) {
+  if (v > 2147483647LL || v < -2147483647LL - 1) *err = 1;
+  return (int32_t)v;
+}
+
 struct BuildShared {
   BlockShared bs;
   GapPlanBuf o, tmp;
@@ -30,6 +36,7 @@ struct BuildShared {
   unsigned long long m_asg[SLOS_MAX_CHAIN + 1];
   int32_t m_item[SLOS_MAX_CHAIN + 1];
   int nb, nsel, edf, fill_late, err, m1;
+  int range_err;  // a plan token count outside the 32-bit entry range
   int64_t n_batch, n_entry;
   double tail_len;
 };
@@ -130,7 +137,7 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
           slos_entry e;
           e.req = A.ch_ref[o2];
           e.spec_len = 0;
-          e.prefill_tokens = spend;
+          e.prefill_tokens = tok32(spend, &sh.range_err);
           e.decode_tokens = 0;
           OE[ne] = e;
         }
@@ -167,7 +174,7 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
         e.req = owner_ref(A, sh, owner);
         e.spec_len = spec_batch ? o.spec[owner_tier(A, sh, owner)] : 0;
         e.prefill_tokens = 0;
-        e.decode_tokens = t;
+        e.decode_tokens = tok32(t, &sh.range_err);
         OE[at] = e;
       }
       if (track && owner >= I.R_total) atomicAdd(&sh.m_asg[owner - I.R_total], (unsigned long long)t);
@@ -269,7 +276,7 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
           e.req = didx[k];
           e.spec_len = 0;
           e.prefill_tokens = 0;
-          e.decode_tokens = ddue[k];
+          e.decode_tokens = tok32(ddue[k], &sh.range_err);
           OE[pos] = e;
         }
         ++pos;
@@ -316,7 +323,7 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
           slos_entry e;
           e.req = pidx[k];
           e.spec_len = 0;
-          e.prefill_tokens = take;
+          e.prefill_tokens = tok32(take, &sh.range_err);
           e.decode_tokens = 0;
           OE[pos] = e;
         }
@@ -385,6 +392,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
     sh.n_entry = 0;
     sh.edf = 0;
     sh.fill_late = 0;
+    sh.range_err = 0;
   }
   G::sync();
   const InstDev& I = sh.I;
@@ -562,6 +570,8 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
       out->status = SLOS_ERR_CAPACITY;
       out->need_batch = 2 * sh.n_batch;
       out->need_entry = 2 * sh.n_entry;
+    } else if (sh.range_err) {
+      out->status = SLOS_ERR_INVALID_PARAMETERS;
     }
   }
 }

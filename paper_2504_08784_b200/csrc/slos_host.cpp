@@ -1326,6 +1326,8 @@ int slos_planner_create(const slos_perf_term* terms, int32_t n_terms, const doub
   if (cfg) c = *cfg; else slos_planner_config_default(&c);
   if (c.max_chunk_tokens < 1 || c.max_batch_tokens < 1)
     return set_err(SLOS_ERR_INVALID_PARAMETERS, "batch and chunk caps must be positive");
+  if (c.max_chunk_tokens > INT32_MAX || c.max_batch_tokens > INT32_MAX)  // slos_entry is 32-bit
+    return set_err(SLOS_ERR_INVALID_PARAMETERS, "batch and chunk caps must fit the 32-bit plan entries");
   if (c.plan_margin < 0) return set_err(SLOS_ERR_INVALID_PARAMETERS, "plan margin must be >= 0");
   slos_planner* p = new slos_planner();
   p->terms.assign(terms, terms + n_terms);

@@ -23,10 +23,10 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactParams p) {
   slos_entry* de = (slos_entry*)(p.dst + p.eoff[k]);
   int32_t* di = (int32_t*)(p.dst + p.ioff[k]);
   for (int64_t x = threadIdx.x; x < nb; x += blockDim.x) db[x] = p.batches[I.off_batch + x];
-  // entries: 24 B each, copy as 8-byte words for coalescing
-  const uint64_t* se = (const uint64_t*)(p.entries + I.off_entry);
-  uint64_t* dw = (uint64_t*)de;
-  for (int64_t x = threadIdx.x; x < ne * 3; x += blockDim.x) dw[x] = se[x];
+  // entries: 16 B each, copied as 16-byte words
+  const uint4* se = (const uint4*)(p.entries + I.off_entry);
+  uint4* dw = (uint4*)de;
+  for (int64_t x = threadIdx.x; x < ne; x += blockDim.x) dw[x] = se[x];
   const int32_t* ids = p.ids + I.off_ids;
   for (int x = threadIdx.x; x < o.n_admitted; x += blockDim.x) di[x] = ids[x];
   for (int x = threadIdx.x; x < o.n_declined; x += blockDim.x) di[o.n_admitted + x] = ids[I.n_pending + x];

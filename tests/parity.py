@@ -32,11 +32,14 @@ def canon_c(r: abi.Result) -> dict:
         d["batches"] = bb.view(abi.BATCH_DTYPE).copy()
     else:
         d["batches"] = np.zeros(0, abi.BATCH_DTYPE)
+    # entries in the canonical int64 layout (digests are independent of the wire form)
+    ent = np.zeros(ne, abi.CANON_ENTRY_DTYPE)
     if ne:
         eb = np.ctypeslib.as_array(C.cast(r.entries, C.POINTER(C.c_uint8)), (ne * C.sizeof(abi.Entry),))
-        d["entries"] = eb.view(abi.ENTRY_DTYPE).copy()
-    else:
-        d["entries"] = np.zeros(0, abi.ENTRY_DTYPE)
+        w = eb.view(abi.ENTRY_DTYPE)
+        for f in ("req", "spec_len", "prefill_tokens", "decode_tokens"):
+            ent[f] = w[f]
+    d["entries"] = ent
     d["counters"] = (r.counters.transitions, r.counters.gap_evals, r.counters.dues,
                      r.counters.slots, r.counters.states)
     return d
