@@ -31,12 +31,18 @@ METRICS = [
     "launch__block_size",
     "sm__cycles_elapsed.avg.per_second",
     "smsp__average_warp_latency_issue_stalled_barrier",
+    "launches",
 ]
 
 
+ADDITIVE = {"gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum", "launch__grid_size"}
+
+
 def raw(rep):
-    """{kernel short name: {metric: {value, unit}}} for every launch in the report
-    (the last launch of a kernel wins)."""
+    """{kernel short name: {metric: {value, unit}}} over the launches in the report:
+    additive metrics (time, bytes, instructions, grid) are summed over a kernel's
+    launches (one solve = one launch per solve part), ratios keep the last launch."""
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
@@ -45,10 +51,18 @@ def raw(rep):
     out = {}
     for vals in rows[2:]:
         name = vals[ki].split("(")[0].split("::")[-1]
+        prev = out.get(name, {})
         d = {}
         for i, n in enumerate(hdr):
             if n in METRICS:
-                d[n] = {"value": vals[i], "unit": units[i]}
+                v = vals[i]
+                if n in ADDITIVE and n in prev:
+                    try:
+                        v = repr(float(prev[n]["value"].replace(",", "")) + float(v.replace(",", "")))
+                    except ValueError:
+                        pass
+                d[n] = {"value": v, "unit": units[i]}
+        d["launches"] = {"value": str(int(prev.get("launches", {"value": "0"})["value"]) + 1), "unit": ""}
         out[name] = d
     return out
 
