@@ -499,7 +499,9 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
     }
     g_gap[gi] = gap;
     g_hor[gi] = hor;
-    g_Sp[gi] = Sp;
+    // Sp and whether the gap end is appended as a slot (batch_planner.cpp:242-247)
+    const bool app = Sp == 0 ? time_le(min_slot, gap) : (gap - sge[Sp - 1] >= min_slot - kTimeEps);
+    g_Sp[gi] = 2 * Sp + (app ? 1 : 0);
     g_lo[gi] = Sp - 1;
     g_hi[gi] = c_hi < Sp - 1 ? Sp - 1 : c_hi;
     hloc = dmax(hloc, hor);
@@ -576,14 +578,12 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
             const int gi = l_item[q];
             if (!time_le(d, g_hor[gi])) continue;
             const double gap = g_gap[gi];
-            const int Sp = g_Sp[gi];
+            const int Sp = g_Sp[gi] >> 1;
+            const bool app = (g_Sp[gi] & 1) != 0;
             int32_t* acc = g_acc + 5 * gi;
             atomicAdd(&acc[2], 1);
             if (!time_le(d, gap)) acc[4] = 1;
             // slot: Sp-1 (Sp >= 1), or the appended slot when time_le(gap, d)
-            bool app;
-            if (Sp == 0) app = time_le(min_slot, gap);
-            else app = (gap - sge[Sp - 1] >= min_slot - kTimeEps);
             if (app && time_le(gap, d)) atomicAdd(&acc[1], 1);
             else if (Sp >= 1) atomicAdd(&acc[0], 1);
             else acc[3] = 1;
