@@ -62,6 +62,8 @@ struct InstDev {
   int32_t values_integral;  // all chain values integral -> eps ties impossible
   int32_t build_small;      // plan reconstruction by one warp (small instance)
   int32_t part;             // solve part (dp + build launched per part, pipelined)
+  int32_t direct;           // Pareto buckets through a direct count-vector table (dp_kernel)
+  int32_t dstride[kMaxTiers];  // its strides: index = sum_l count_l * dstride[l]
   int64_t off_dec;     // into dec_* arrays
   int64_t off_chain;   // into ch_* arrays (N items, suffix has N+1)
   int64_t off_pre;     // into pre_* arrays
@@ -229,6 +231,7 @@ struct DpParams {
   size_t grec_hdr;          // header bytes before the variant arrays
   size_t grec_stage;        // bytes of a record the DP stages (header + evaluated arrays)
   int blk0;                 // first position in `order` of this launch's part
+  int dtab;                 // direct bucket-table entries in shared memory (0: none)
 };
 
 // Push an instance onto its plan-reconstruction queue: queue 2*part+0 holds the

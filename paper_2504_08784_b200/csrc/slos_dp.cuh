@@ -886,6 +886,9 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   int32_t* k_new = (int32_t*)p; p += 4 * (size_t)Tsm;
   int32_t* k_grp = (int32_t*)p; p += 4 * (size_t)Tsm;
   (void)k_grp;
+  // direct count-vector -> bucket table (instances whose count space is small)
+  int32_t* dtab = (int32_t*)p; p += 4 * (size_t)prm.dtab;
+  for (int x = tid; x < prm.dtab; x += kDpThreads) dtab[x] = -1;
   // overlay layout: 8-byte arrays first
   uint64_t* o_cn = (uint64_t*)ovl;
   int64_t* o_mm = (int64_t*)(ovl + 8 * (size_t)Tsm);
@@ -1216,13 +1219,34 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       }
       Cfl[c] = flag;
     }
-    if (sm) {  // fresh level-local bucket table
+    if (sm && !I.direct) {  // fresh level-local bucket table
       for (int x = tid; x < capB; x += kDpThreads) { Bkey[x] = 0ull; Bval[x] = -1; }
     }
     __syncthreads();
     if (s_err) break;
     SLOS_PHASE(8);  // 8: candidate states
     // ---- 5: Pareto buckets ----
+    if (I.direct) {  // count vector -> dense index -> bucket id (shared-memory 32-bit atomics)
+      for (int c = tid; c < T; c += kDpThreads) {
+        int b = -1;
+        if (Cfl[c] & 1) {
+          const uint64_t key = Ccn[c];
+          int idx = 0;
+#pragma unroll
+          for (int l = 0; l < kMaxTiers; ++l) if (l < L) idx += (int)pack_get(key, l) * I.dstride[l];
+          int v = atomicCAS(&dtab[idx], -1, -2);
+          if (v == -1) {
+            b = atomicAdd(&s_nb, 1);
+            Caux[b] = idx;
+            atomicExch(&dtab[idx], b);
+          } else {
+            while (v < 0) v = atomicAdd(&dtab[idx], 0);
+            b = v;
+          }
+        }
+        Cbk[c] = b;
+      }
+    } else
     for (int c = tid; c < T; c += kDpThreads) {
       int b = -1;
       if (Cfl[c] & 1) {
@@ -1553,7 +1577,9 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
       }
     }
     __syncthreads();
-    if (!sm) {  // reset the HBM bucket hash slots claimed by this level
+    if (I.direct) {  // reset the direct-table entries claimed by this level
+      for (int b = tid; b < NB; b += kDpThreads) dtab[Caux[b]] = -1;
+    } else if (!sm) {  // reset the HBM bucket hash slots claimed by this level
       for (int b = tid; b < NB; b += kDpThreads) {
         Bkey[Caux[b]] = 0ull;
         Bval[Caux[b]] = -1;

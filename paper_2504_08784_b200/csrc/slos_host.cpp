@@ -327,6 +327,10 @@ int solve_parts(int nv) {
   return std::max(1, P);
 }
 
+// Direct bucket-table entries per DP CTA (shared memory); instances whose count
+// space prod_l (items of tier l + 1) exceeds it hash instead.
+constexpr int kDirectMax = 1024;
+
 bool integral(double v) { return std::isfinite(v) && v == std::floor(v) && std::fabs(v) < 4.0e15; }
 
 struct Prep {  // host-side per-instance preparation
@@ -771,6 +775,20 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     I.have_running_decode = pr.have_rd ? 1 : 0;
     I.values_integral = pr.values_integral ? 1 : 0;
     I.build_small = pr.n_dec <= build_warp_max_dec() ? 1 : 0;
+    {  // direct bucket table when the count-vector space is small
+      int64_t maxc[kMaxTiers] = {0};
+      for (int x = 0; x < pr.N; ++x) {
+        const int enc = pr.chain[x];
+        const int t = enc >= 0 ? in->running[enc].decode_tier : in->pending[-enc - 1].decode_tier;
+        if (t >= 0 && t < kMaxTiers) ++maxc[t];
+      }
+      int64_t D = 1;
+      for (int l = 0; l < planners[k]->L && D <= kDirectMax; ++l) {
+        I.dstride[l] = (int32_t)D;
+        D *= std::min<int64_t>(maxc[l], 250) + 1;
+      }
+      I.direct = D <= kDirectMax ? 1 : 0;
+    }
     I.off_dec = oD;
     I.off_chain = oC;
     I.off_pre = oP;
@@ -1024,7 +1042,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     return e ? std::atoi(e) : 192;
   }();
   dp.Tsm = kTsm;
-  auto fit = [&](int dec) { return dp_smem_bytes(maxN, dec, dp.Sc, Lmax, dp.Tsm, &dp.overlay_bytes); };
+  dp.dtab = kDirectMax;
+  auto fit = [&](int dec) { return dp_smem_bytes(maxN, dec, dp.Sc, Lmax, dp.Tsm, &dp.overlay_bytes, dp.dtab); };
   while (fit(0) > kSmemBudget && dp.Tsm > 64) {
     if (dp.Tsm > 256) dp.Tsm -= 32;
     else dp.Tsm /= 2;

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactParams p) {
 }
 
 // dynamic shared memory of dp_kernel (must mirror the carve-up in dp_kernel)
-size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay) {
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay, int dtab) {
   const size_t N = (size_t)max_N;
   size_t b = 8 * (N + 1) * 4 + 8 * (N + 2) + 4 * (N + 2) * 3 + 16;   // chain
   b += (size_t)max_dec_staged * 28 + 16;                              // decoders
@@ -42,6 +42,7 @@ size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size
   *overlay = ov;
   b += ov + 16;                                                       // candidate states
   b += (size_t)20 * (size_t)Tsm;                                      // kept candidate arrays
+  b += 4 * (size_t)dtab;                                              // direct bucket table
   (void)L;
   return b + 64;
 }

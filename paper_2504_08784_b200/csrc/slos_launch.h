@@ -24,7 +24,7 @@ struct CompactParams {
   unsigned char* dst;
 };
 
-size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay);
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay, int dtab);
 size_t dp_group_hdr_bytes();
 size_t dp_group_eval_bytes(int Sc, int L);
 size_t dp_group_stride(int Sc, int L);
