@@ -238,6 +238,7 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
   double t = I.now;
   bool decodes = G::or_(sh.bs, act) != 0;
   bool prefills = G::or_(sh.bs, lsum > 0 ? 1 : 0) != 0;
+  int par = 0;  // mscan buffer parity (uniform across the group)
   for (int guard = 0; guard < 100000; ++guard) {
     if (!prefills && !decodes) break;
     const bool dec_branch = decodes;
@@ -265,10 +266,10 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
         ddue[k] = due;
         if (dleft[k] > 0) still = 1;
       }
-      // one scan: entry counts in the low 32 bits, "still decoding" in the high bits
-      int64_t tot;
-      const int64_t ex = G::excl(sh.bs, (int64_t)cnt | ((int64_t)still << 32), &tot);
-      int64_t pos = e0 + (ex & 0xffffffffLL);
+      // one scan for entry positions, the batch's decode tokens and "still decoding"
+      int64_t mv[3] = {(int64_t)cnt, tok, (int64_t)still}, mex[3], mtot[3];
+      G::template mscan<3>(sh.bs, mv, mex, mtot, par);
+      int64_t pos = e0 + mex[0];
       for (int k = d0; k < d1; ++k) {
         if (ddue[k] <= 0) continue;
         if (pos < I.cap_entry) {
@@ -281,9 +282,9 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
         }
         ++pos;
       }
-      ne += tot & 0xffffffffLL;
-      dtok = G::sum64(sh.bs, tok);
-      decodes = (tot >> 32) != 0;
+      ne += mtot[0];
+      dtok = mtot[1];
+      decodes = mtot[2] != 0;
       if (cap_t0 == -2) cap_t0 = plan_time2bs(P, t0, 0);  // loop-invariant: t0 is fixed
       cap = cap_t0;
       if (cap < 0) {
@@ -298,8 +299,9 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
     // EDF prefill in order: take_k = min(left_k, max(0, free - sum_{k'<k} left_k'))
     int64_t spent = 0;
     if (prefills) {
-      int64_t tot0;
-      const int64_t before = G::excl(sh.bs, lsum, &tot0);
+      int64_t pv[1] = {lsum}, pex[1], ptot[1];
+      G::template mscan<1>(sh.bs, pv, pex, ptot, par);
+      const int64_t before = pex[0], tot0 = ptot[0];
       int cnt = 0;
       int64_t run = before, mine = 0;
       for (int k = p0; k < p1; ++k) {
@@ -309,9 +311,10 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
         if (take > 0) ++cnt;
         mine += take;
       }
-      int64_t totc;
-      const int64_t exc = G::excl(sh.bs, cnt, &totc);
-      int64_t pos = ne + exc;
+      int64_t cv[2] = {(int64_t)cnt, mine}, cex[2], ctot[2];
+      G::template mscan<2>(sh.bs, cv, cex, ctot, par);
+      const int64_t totc = ctot[0];
+      int64_t pos = ne + cex[0];
       run = before;
       for (int k = p0; k < p1; ++k) {
         const int64_t lk = pleft[k] > 0 ? pleft[k] : 0;
@@ -330,9 +333,9 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
         ++pos;
       }
       ne += totc;
-      spent = G::sum64(sh.bs, mine);
+      spent = ctot[1];
       lsum -= mine;
-      prefills = G::or_(sh.bs, lsum > 0 ? 1 : 0) != 0;
+      prefills = tot0 - spent > 0;  // every lane's pending prefill is >= 0
     }
     slos_batch b;
     b.start_s = t;

@@ -65,6 +65,7 @@ struct BlockShared {  // shared scratch of one cooperating group (a CTA or a war
   int64_t v64a, v64b;
   double vd;
   SpecSol sp;
+  int64_t mb[2][kBW][4];  // double-buffered per-warp totals of mscan (one barrier per call)
 };
 
 // Cooperative-group policies: the same engine runs on a whole CTA (BlockGrp,
@@ -117,6 +118,32 @@ struct BlockGrpT {
     __syncthreads();
     return t;
   }
+  // K simultaneous exclusive scans with ONE barrier: per-warp totals go to the
+  // buffer `par` (alternating per call, so a buffer is rewritten only after every
+  // thread has passed the barrier of the call in between, i.e. finished reading it).
+  template <int K>
+  __device__ static void mscan(BlockShared& sh, const int64_t* v, int64_t* ex, int64_t* tot, int& par) {
+    int64_t inc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) inc[k] = warp_incl_scan(v[k]);
+    if (lane_id() == 31) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) sh.mb[par][warp_id()][k] = inc[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int64_t base = 0, t = 0;
+      for (int w = 0; w < kW; ++w) {
+        const int64_t x = sh.mb[par][w][k];
+        if (w < warp_id()) base += x;
+        t += x;
+      }
+      ex[k] = base + inc[k] - v[k];
+      tot[k] = t;
+    }
+    par ^= 1;
+  }
   // exclusive scan (one value per thread); *tot = group total
   __device__ static int64_t excl(BlockShared& sh, int64_t v, int64_t* tot) {
     const int64_t inc = warp_incl_scan(v);
@@ -156,6 +183,16 @@ struct WarpGrp {
     *tot = __shfl_sync(0xffffffffu, inc, 31);
     __syncwarp();
     return inc - v;
+  }
+  template <int K>
+  __device__ static void mscan(BlockShared&, const int64_t* v, int64_t* ex, int64_t* tot, int&) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t inc = warp_incl_scan(v[k]);
+      tot[k] = __shfl_sync(0xffffffffu, inc, 31);
+      ex[k] = inc - v[k];
+    }
+    __syncwarp();
   }
 };
 
