@@ -239,6 +239,23 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
   bool decodes = G::or_(sh.bs, act) != 0;
   bool prefills = G::or_(sh.bs, lsum > 0 ? 1 : 0) != 0;
   int par = 0;  // mscan buffer parity (uniform across the group)
+  // per-lane decoder state in registers when the lane owns at most kR decoders
+  constexpr int kR = 4;
+  const bool regs = d1 - d0 <= kR;
+  double rn[kR], rt[kR];
+  int64_t rb[kR], rl[kR], rd[kR];
+  int32_t ri[kR];
+#pragma unroll
+  for (int q = 0; q < kR; ++q) {
+    const int k = d0 + q;
+    const bool in = regs && k < d1;
+    rn[q] = in ? dnext[k] : 0.0;
+    rt[q] = in ? dtp[k] : 0.0;
+    rb[q] = in ? dbl[k] : 0;
+    rl[q] = in ? dleft[k] : 0;
+    rd[q] = 0;
+    ri[q] = in ? didx[k] : 0;
+  }
   for (int guard = 0; guard < 100000; ++guard) {
     if (!prefills && !decodes) break;
     const bool dec_branch = decodes;
@@ -248,6 +265,28 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
       const double slot_end = t + t0;
       int cnt = 0, still = 0;
       int64_t tok = 0;
+      if (regs) {  // the lane's decoders live in registers (no shared-memory round trips)
+#pragma unroll
+        for (int q = 0; q < kR; ++q) {
+          if (q >= d1 - d0) break;
+          int64_t due = 0;
+          if (rl[q] > 0) {
+            due = imin(rb[q], rl[q]);
+            rb[q] -= due;
+            while (rl[q] - due > 0 && time_le(rn[q], slot_end)) {
+              ++due;
+              rn[q] += rt[q];
+            }
+            if (due > 0) {
+              rl[q] -= due;
+              ++cnt;
+              tok += due;
+            }
+          }
+          rd[q] = due;
+          if (rl[q] > 0) still = 1;
+        }
+      } else {
       for (int k = d0; k < d1; ++k) {
         int64_t due = 0;
         if (dleft[k] > 0) {
@@ -266,10 +305,27 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
         ddue[k] = due;
         if (dleft[k] > 0) still = 1;
       }
+      }
       // one scan for entry positions, the batch's decode tokens and "still decoding"
       int64_t mv[3] = {(int64_t)cnt, tok, (int64_t)still}, mex[3], mtot[3];
       G::template mscan<3>(sh.bs, mv, mex, mtot, par);
       int64_t pos = e0 + mex[0];
+      if (regs) {
+#pragma unroll
+        for (int q = 0; q < kR; ++q) {
+          if (q >= d1 - d0) break;
+          if (rd[q] <= 0) continue;
+          if (pos < I.cap_entry) {
+            slos_entry e;
+            e.req = ri[q];
+            e.spec_len = 0;
+            e.prefill_tokens = 0;
+            e.decode_tokens = tok32(rd[q], &sh.range_err);
+            OE[pos] = e;
+          }
+          ++pos;
+        }
+      } else {
       for (int k = d0; k < d1; ++k) {
         if (ddue[k] <= 0) continue;
         if (pos < I.cap_entry) {
@@ -281,6 +337,7 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
           OE[pos] = e;
         }
         ++pos;
+      }
       }
       ne += mtot[0];
       dtok = mtot[1];
@@ -558,7 +615,12 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
       out->n_declined = I.n_pending;
     }
     G::sync();
+    const long long fb0 = clock64();
     group_edf_fallback<G>(A, sh, ar, out);
+    if (phase_cycles && tid == 0) {  // debug: fallback wall cycles and batches
+      atomicAdd(&phase_cycles[14], (unsigned long long)(clock64() - fb0));
+      atomicAdd(&phase_cycles[15], (unsigned long long)sh.n_batch);
+    }
     SLOS_BPHASE(5);  // 5: fallback
     if (sh.err) {
       if (tid == 0) out->status = sh.err;

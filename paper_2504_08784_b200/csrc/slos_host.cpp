@@ -1184,6 +1184,7 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
     std::fprintf(stderr, "[slos build phases] total %.3e cycles:", (double)bt);
     for (int k = 0; k < 6; ++k) std::fprintf(stderr, " %s %.1f%%", bn[k], 100.0 * (double)pc[16 + k] / (double)(bt ? bt : 1));
     std::fprintf(stderr, " | max instance %.3e cycles over %llu instances\n", (double)pc[22], pc[23]);
+    std::fprintf(stderr, "[slos fallback] %.3e cycles over %llu batches\n", (double)pc[30], pc[31]);
     std::fprintf(stderr, "[slos E3a] keys %llu, eval mean %.0f max %llu cycles, key_of mean %.0f; dues==0 %llu, Lx>0 %llu\n",
                  pc[25], (double)pc[24] / (double)(pc[25] ? pc[25] : 1), pc[26],
                  (double)pc[27] / (double)(pc[25] ? pc[25] : 1), pc[28], pc[29]);
