@@ -273,8 +273,12 @@ void arena_release(ResultArena* a) {
     return;
   }
   {
+    // keep up to 16 pinned arenas / 8 GiB for reuse: pinned allocation and release
+    // cost milliseconds and a pipelined batch holds one arena per chunk
     std::lock_guard<std::mutex> g(c.pool_mu);
-    if (c.pool.size() < 4) {
+    size_t held = 0;
+    for (const ResultArena* x : c.pool) held += x->cap;
+    if (c.pool.size() < 16 && held + a->cap <= ((size_t)8 << 30)) {
       c.pool.push_back(a);
     } else {
       cudaFreeHost(a->p);
