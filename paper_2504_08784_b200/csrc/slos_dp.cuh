@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   __shared__ uint8_t s_sh[SLOS_MAX_CHAIN + 2];      // source level's pair is memo-shared
   __shared__ int64_t s_wsum[kDpWarps + 1];
   __shared__ unsigned long long s_ctr[5];
-  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_nw, s_bovf, s_anysh;
+  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_nw, s_bovf, s_anysh, s_nsb;
   __shared__ int64_t s_next_free, s_arena_next, s_bnext;
 
   const BatchArgs& A = prm.a;
@@ -1183,6 +1183,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     const int tier_i = ch_tr[i];
     const bool forced = ch_fc[i] != 0;
     for (int c = tid; c < T; c += kDpThreads) {
+      Cj[c] = 0;  // bucket sizes of step 5 (the E3b key list is consumed)
       const int src = Csrc[c];
       const int me = Cme[c];
       bool has;
@@ -1243,6 +1244,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
             while (v < 0) v = atomicAdd(&dtab[idx], 0);
             b = v;
           }
+          atomicAdd(&Cj[b], 1);  // bucket size (Cj zeroed in step 4)
         }
         Cbk[c] = b;
       }
@@ -1269,6 +1271,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
           }
           h = (h + 1) & (uint64_t)(capB - 1);
         }
+        atomicAdd(&Cj[b], 1);  // bucket size (Cj zeroed in step 4)
       }
       Cbk[c] = b;
     }
@@ -1300,24 +1303,19 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     if (pairwise) {
       // unordered bucket lists (counting sort without stability: "earlier" is the
       // candidate index itself)
-      int32_t* cntB = Cj;   // anchors are no longer needed this level
+      int32_t* cntB = Cj;   // bucket sizes, counted while the buckets were assigned
       int32_t* offB = Cme;  // memo slots are no longer needed after step 4
-      for (int b = tid; b < NB; b += kDpThreads) cntB[b] = 0;
-      if (tid == 0) s_bovf = 0;  // reused below: a bucket of more than 32 candidates exists
-      __syncthreads();
-      for (int c = tid; c < T; c += kDpThreads)
-        if (Cbk[c] >= 0) atomicAdd(&cntB[Cbk[c]], 1);
-      __syncthreads();
-      {
-        int64_t carry = 0;
-        for (int base = 0; base < NB; base += kDpThreads) {
-          const int b = base + tid;
-          const int64_t x = b < NB ? cntB[b] : 0;
-          int64_t tot;
-          const int64_t ex = block_excl_scan(x, s_wsum, &tot);
-          if (b < NB) { offB[b] = (int32_t)(carry + ex); cntB[b] = 0; }
-          carry += tot;
+      if (warp_id() == 0) {  // bucket offsets: one warp (NB is small), sizes reset for the scatter
+        const int lane = lane_id();
+        int carry = 0;
+        for (int base = 0; base < NB; base += 32) {
+          const int b = base + lane;
+          const int x = b < NB ? cntB[b] : 0;
+          const int inc = warp_incl_scan(x);
+          if (b < NB) { offB[b] = carry + inc - x; cntB[b] = 0; }
+          carry += __shfl_sync(0xffffffffu, inc, 31);
         }
+        if (lane == 0) s_bovf = 0;  // reused below: a bucket of more than 32 candidates exists
       }
       __syncthreads();
       for (int c = tid; c < T; c += kDpThreads) {
@@ -1598,31 +1596,46 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         if ((fl & 2) && !(fl & 4)) hsb[Cbk[c]] = 1;
       }
       __syncthreads();
-      int64_t nsb = 0;
-      for (int base = 0; base < NB; base += kDpThreads) {
-        const int b = base + tid;
-        const int64_t x = b < NB ? hsb[b] : 0;
-        int64_t tot;
-        const int64_t ex = block_excl_scan(x, s_wsum, &tot);
-        if (b < NB) sbid[b] = (int32_t)(nsb + ex);
-        nsb += tot;
+      const int lane = lane_id(), w = warp_id();
+      if (w == 0) {  // surviving-bucket dense ids: one warp (NB is small)
+        int carry = 0;
+        for (int base = 0; base < NB; base += 32) {
+          const int b = base + lane;
+          const int x = b < NB ? hsb[b] : 0;
+          const int inc = warp_incl_scan(x);
+          if (b < NB) sbid[b] = carry + inc - x;
+          carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) s_nsb = carry;
       }
+      // accepted / surviving ranks in candidate order: every warp scans a contiguous
+      // range (one barrier for the whole level instead of one scan per 256 candidates);
+      // packed value: accepted in the low, surviving in the high word
+      const int per = (T + kDpWarps - 1) / kDpWarps;
+      const int lo = min(T, w * per), hi = min(T, lo + per);
+      auto packed = [&](int c) -> int64_t {
+        const int fl = c < hi ? Cfl[c] : 0;
+        return (int64_t)((fl & 2) ? 1 : 0) | ((int64_t)(((fl & 2) && !(fl & 4)) ? 1 : 0) << 32);
+      };
+      int64_t wt = 0;
+      for (int base = lo; base < hi; base += 32) wt += warp_sum(packed(base + lane));
+      if (lane == 0) s_wsum[w] = wt;
       __syncthreads();
+      int64_t carry = 0, total = 0;
+      for (int x = 0; x < kDpWarps; ++x) {
+        if (x < w) carry += s_wsum[x];
+        total += s_wsum[x];
+      }
       const int64_t bbase = s_bnext;
-      int64_t carry_acc = 0, carry_sv = 0;
       const int64_t base_free = s_next_free;
-      for (int base = 0; base < T; base += kDpThreads) {
-        const int c = base + tid;
-        const int fl = c < T ? Cfl[c] : 0;
-        const int acc = (fl & 2) ? 1 : 0;
-        const int sv = ((fl & 2) && !(fl & 4)) ? 1 : 0;
-        // one scan for both counts: accepted in the low, surviving in the high word
-        int64_t tot2;
-        const int64_t r2 = block_excl_scan((int64_t)acc | ((int64_t)sv << 32), s_wsum, &tot2);
-        const int64_t r_acc = r2 & 0xffffffffLL, r_sv = r2 >> 32;
-        const int64_t tot_acc = tot2 & 0xffffffffLL, tot_sv = tot2 >> 32;
-        if (sv) {
-          const int64_t dst = base_free + carry_sv + r_sv;
+      for (int base = lo; base < hi; base += 32) {
+        const int c = base + lane;
+        const int64_t v = packed(c);
+        const int64_t inc = warp_incl_scan(v);
+        const int64_t ex = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+        if (v >> 32) {  // a survivor
+          const int64_t dst = base_free + (ex >> 32);
           if (dst < I.cap_surv) {
             const int sb = sbid[Cbk[c]];
             Sc_[dst] = Ccn[c];
@@ -1631,23 +1644,24 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
             Sv_[dst] = Cvl[c];
             Sn_[dst] = Cna[c];
             Spar[dst] = Csrc[c];
-            Sar[dst] = (int32_t)(s_arena_next + carry_acc + r_acc);
+            Sar[dst] = (int32_t)(s_arena_next + (ex & 0xffffffffLL));
             Sit[dst] = i;
             Ssb[dst] = sb;
             Bc[bbase + sb] = Ccn[c];  // every survivor of the bucket writes the same counts
           }
         }
-        carry_acc += tot_acc;
-        carry_sv += tot_sv;
       }
+      __syncthreads();  // every warp has read s_next_free / s_arena_next / s_bnext
       if (tid == 0) {
+        const int64_t tot_acc = total & 0xffffffffLL, tot_sv = total >> 32;
+        const int nsb = s_nsb;
         lvl_off[i + 1] = base_free;
-        lvl_cnt[i + 1] = (int32_t)carry_sv;
+        lvl_cnt[i + 1] = (int32_t)tot_sv;
         lvl_boff[i + 1] = (int32_t)bbase;
-        lvl_nsb[i + 1] = (int32_t)nsb;
+        lvl_nsb[i + 1] = nsb;
         s_bnext = bbase + nsb;
-        s_next_free = base_free + carry_sv;
-        s_arena_next += carry_acc;
+        s_next_free = base_free + tot_sv;
+        s_arena_next += tot_acc;
         if (s_next_free > I.cap_surv) { s_err = SLOS_ERR_CAPACITY; out->need_surv = 2 * s_next_free; }
       }
     }
