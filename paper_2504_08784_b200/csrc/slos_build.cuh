@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(32 * kBuildWarps, 2) build_kernel_warp(BuildPa
   __shared__ BuildShared shs[kBuildWarps];
   extern __shared__ __align__(16) unsigned char bsm[];
   const int idx = blockIdx.x * kBuildWarps + warp_id();
-  const int q = 2 * prm.part;
+  const int q = kBuildKinds * prm.part;
   if (idx >= A.qn[q]) return;  // whole warp; the engine never uses CTA barriers here
   const int64_t per = (int64_t)(prm.smem_warp / kBuildWarps) & ~(int64_t)255;
   build_instance<WarpGrp>(A, shs[warp_id()], A.bq[A.qbase[q] + idx], bsm + per * warp_id(), per,
@@ -667,8 +667,18 @@ __global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_ke
   const BatchArgs& A = prm.a;
   __shared__ BuildShared sh;
   extern __shared__ __align__(16) unsigned char bsm[];
-  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.bq[A.qbase[2 * prm.part + 1] + blockIdx.x], bsm,
+  build_instance<BlockGrpT<kBuildThreads>>(A, sh, A.bq[A.qbase[kBuildKinds * prm.part + 1] + blockIdx.x], bsm,
                                            (int64_t)prm.smem_bytes, prm.phase_cycles);
+}
+
+// Very large instances (thousands of running decoders, the C4 family): twice the
+// threads per instance, one CTA per SM.
+__global__ void __launch_bounds__(2 * kBuildThreads, 1) build_kernel_big(BuildParams prm) {
+  const BatchArgs& A = prm.a;
+  __shared__ BuildShared sh;
+  extern __shared__ __align__(16) unsigned char bsm[];
+  build_instance<BlockGrpT<2 * kBuildThreads>>(A, sh, A.bq[A.qbase[kBuildKinds * prm.part + 2] + blockIdx.x], bsm,
+                                               (int64_t)prm.smem_bytes, prm.phase_cycles);
 }
 
 // ---- standalone gap queries (slos_tile_gap_batch) ----------------------------

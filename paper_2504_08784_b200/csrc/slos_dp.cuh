@@ -1672,7 +1672,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   if (s_err) {
     if (tid == 0) {
       out->status = s_err;
-      build_queue_push(A, inst, I.part, I.build_small != 0, false);
+      build_queue_push(A, inst, I.part, I.build_kind, false);
     }
     return;
   }
@@ -1793,7 +1793,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     out->status = 0;
     // plan-reconstruction queue: instances that fall back (a long sequential batch
     // loop) are queued from the front, the rest from the back
-    build_queue_push(A, inst, I.part, I.build_small != 0, best < 0);
+    build_queue_push(A, inst, I.part, I.build_kind, best < 0);
   }
   SLOS_PHASE(11);  // 11: terminal selection + backtrack
 }

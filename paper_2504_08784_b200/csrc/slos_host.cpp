@@ -335,6 +335,16 @@ int solve_parts(int nv) {
 // space prod_l (items of tier l + 1) exceeds it hash instead.
 constexpr int kDirectMax = 1024;
 
+// Instances with at least this many running decoders are reconstructed by a
+// 256-thread CTA (SLOS_BUILD_BIG_MIN_DEC overrides).
+int build_big_min_dec() {
+  static const int v = [] {
+    const char* e = std::getenv("SLOS_BUILD_BIG_MIN_DEC");
+    return e ? std::atoi(e) : 1024;
+  }();
+  return v;
+}
+
 bool integral(double v) { return std::isfinite(v) && v == std::floor(v) && std::fabs(v) < 4.0e15; }
 
 struct Prep {  // host-side per-instance preparation
@@ -544,8 +554,8 @@ struct Workspace {
   cudaStream_t own_stream = nullptr;  // pipeline workspaces only
   int n_parts = 1;
   int part_lo[kMaxParts + 1] = {0};
-  int qbase[2 * kMaxParts] = {0};
-  int qn[2 * kMaxParts] = {0};
+  int qbase[kQueues] = {0};
+  int qn[kQueues] = {0};
   cudaStream_t pstream[kMaxParts] = {nullptr};  // per-part streams, earlier parts higher priority
   cudaEvent_t ev_fork = nullptr, ev_dp[kMaxParts] = {nullptr}, ev_join[kMaxParts] = {nullptr};
 };
@@ -678,7 +688,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.c_bkey = bs.add<uint64_t>(2 * TCd);
   Ly.c_bval = bs.add<int32_t>(2 * TCd);
   Ly.memo = bs.add<MemoEnt>(TM);
-  Ly.bq = bs.add<int32_t>(nv + 4 * kMaxParts);
+  Ly.bq = bs.add<int32_t>(nv + 2 * kQueues);
   Ly.work = bs.add<unsigned char>(TW);
   Ly.anchors = bs.add<unsigned char>(TA);
   Ly.groups = bs.add<unsigned char>((size_t)TPair * grec_stride);
@@ -750,7 +760,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       o.E += cp.entry;
       o.A += astride[q] * (pr.N + 1);
       o.Pair += (int64_t)pr.N * (pr.N + 1) / 2;
-      n_small += pr.n_dec <= build_warp_max_dec() ? 1 : 0;
+      n_small += pr.n_dec <= build_warp_max_dec() ? 1 : 0;  // (informational)
     }
   }
   HostPool::get().run(nv, [&](int v_lo, int v_hi) {
@@ -778,7 +788,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     I.last_forced = pr.last_forced;
     I.have_running_decode = pr.have_rd ? 1 : 0;
     I.values_integral = pr.values_integral ? 1 : 0;
-    I.build_small = pr.n_dec <= build_warp_max_dec() ? 1 : 0;
+    I.build_kind = pr.n_dec <= build_warp_max_dec() ? 0 : (pr.n_dec < build_big_min_dec() ? 1 : 2);
     {  // direct bucket table when the count-vector space is small
       int64_t maxc[kMaxTiers] = {0};
       for (int x = 0; x < pr.N; ++x) {
@@ -913,16 +923,16 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     // part's DP (ws_solve)
     const int P = solve_parts(nv);
     ws.n_parts = P;
-    int qcount[2 * kMaxParts] = {0};
+    int qcount[kQueues] = {0};
     for (int p = 0; p <= P; ++p) ws.part_lo[p] = (int)((int64_t)p * nv / P);
     for (int p = 0; p < P; ++p)
       for (int x = ws.part_lo[p]; x < ws.part_lo[p + 1]; ++x) {
         InstDev& I = hI[ord[x]];
         I.part = p;
-        ++qcount[2 * p + (I.build_small ? 0 : 1)];
+        ++qcount[kBuildKinds * p + I.build_kind];
       }
-    int qb = 4 * kMaxParts;
-    for (int q = 0; q < 2 * kMaxParts; ++q) {
+    int qb = 2 * kQueues;  // the counters come first
+    for (int q = 0; q < kQueues; ++q) {
       ws.qbase[q] = qb;
       ws.qn[q] = qcount[q];
       qb += qcount[q];
@@ -1004,7 +1014,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   A.ctime = (double*)(DS + Ly.ctime);
   A.ccnt = (int32_t*)(DS + Ly.ccnt);
   A.bq = (int32_t*)(DS + Ly.bq);
-  for (int q = 0; q < 2 * kMaxParts; ++q) { A.qbase[q] = ws.qbase[q]; A.qn[q] = ws.qn[q]; }
+  for (int q = 0; q < kQueues; ++q) { A.qbase[q] = ws.qbase[q]; A.qn[q] = ws.qn[q]; }
   (void)n_small;
   A.out = (OutHdr*)(DO + Ly.out);
   A.sel = (int32_t*)(DO + Ly.sel);
@@ -1088,7 +1098,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   cudaMemsetAsync(DS + Ly.c_bkey, 0, Ly.bkey_bytes, s);
   cudaMemsetAsync(DS + Ly.c_bval, 0xFF, Ly.bval_bytes, s);
   cudaMemsetAsync(DO + Ly.out, 0, sizeof(OutHdr) * nv, s);
-  cudaMemsetAsync(DS + Ly.bq, 0, 4 * kMaxParts * sizeof(int32_t), s);
+  cudaMemsetAsync(DS + Ly.bq, 0, 2 * kQueues * sizeof(int32_t), s);
   cudaError_t e;
   for (int k = 0; k < 4; ++k)
     if (!ws.ev[k]) cudaEventCreate(&ws.ev[k]);
@@ -1133,7 +1143,8 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     cudaEventRecord(ws.ev_dp[p], sp);
     bp.part = p;
-    if ((e = launch_build(bp, ws.qn[2 * p], ws.qn[2 * p + 1], sp)) != cudaSuccess)
+    const int q0 = kBuildKinds * p;
+    if ((e = launch_build(bp, ws.qn[q0], ws.qn[q0 + 1], ws.qn[q0 + 2], sp)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     cudaEventRecord(ws.ev_join[p], sp);
     cudaStreamWaitEvent(s, ws.ev_join[p], 0);

@@ -93,7 +93,7 @@ cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, cudaStream_t s) {
+cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, int n_big, cudaStream_t s) {
   cudaError_t e;
   if (n_small > 0) {
     if ((e = cudaFuncSetAttribute(build_kernel_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -107,6 +107,13 @@ cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, cudaS
                                   (int)prm.smem_bytes)) != cudaSuccess)
       return e;
     build_kernel<<<n_large, kBuildThreads, prm.smem_bytes, s>>>(prm);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (n_big > 0) {
+    if ((e = cudaFuncSetAttribute(build_kernel_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)prm.smem_bytes)) != cudaSuccess)
+      return e;
+    build_kernel_big<<<n_big, 2 * kBuildThreads, prm.smem_bytes, s>>>(prm);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
