@@ -233,6 +233,7 @@ struct DpParams {
   size_t grec_hdr;          // header bytes before the variant arrays
   size_t grec_stage;        // bytes of a record the DP stages (header + evaluated arrays)
   int blk0;                 // first position in `order` of this launch's part
+  int task0;                // first anchor task of this launch (anchor / group kernels)
   int dtab;                 // direct bucket-table entries in shared memory (0: none)
 };
 

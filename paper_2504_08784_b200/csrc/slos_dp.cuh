@@ -642,7 +642,8 @@ __global__ void __launch_bounds__(kAnchorThreads, SLOS_ANCHOR_MIN_BLOCKS) anchor
   __shared__ int64_t s_wsum[kAnchorThreads / 32 + 1];
   const BatchArgs& A = prm.a;
   const int tid = threadIdx.x;
-  const int v = A.atask[2 * blockIdx.x], j = A.atask[2 * blockIdx.x + 1];
+  const int task = prm.task0 + blockIdx.x;
+  const int v = A.atask[2 * task], j = A.atask[2 * task + 1];
   block_copy_struct(sI, A.inst[v], tid, kAnchorThreads);
   block_copy_struct(sP, A.planners[A.inst[v].planner], tid, kAnchorThreads);
   __syncthreads();
@@ -697,7 +698,8 @@ __global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;
   const BatchArgs& A = prm.a;
-  const int vi = A.atask[2 * blockIdx.x], j = A.atask[2 * blockIdx.x + 1];
+  const int task = prm.task0 + blockIdx.x;
+  const int vi = A.atask[2 * task], j = A.atask[2 * task + 1];
   block_copy_struct(sI, A.inst[vi], threadIdx.x, 32 * kGroupWarps);
   block_copy_struct(sP, A.planners[A.inst[vi].planner], threadIdx.x, 32 * kGroupWarps);
   __syncthreads();

@@ -554,6 +554,8 @@ struct Workspace {
   cudaStream_t own_stream = nullptr;  // pipeline workspaces only
   int n_parts = 1;
   int part_lo[kMaxParts + 1] = {0};
+  int atask_lo[kMaxParts + 1] = {0};  // anchor-task range of each part
+  cudaEvent_t ev_anc[kMaxParts] = {nullptr};
   int qbase[kQueues] = {0};
   int qn[kQueues] = {0};
   cudaStream_t pstream[kMaxParts] = {nullptr};  // per-part streams, earlier parts higher priority
@@ -904,13 +906,6 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     cost[v] = (double)(pr.n_dec + 8) * (double)(pr.N + 1) * (double)(pr.N + 1);
   }
   });
-  {  // anchor tasks: (instance, anchor j), j = -1 .. N-2
-    int32_t* t = (int32_t*)hp(Ly.atask);
-    int64_t x = 0;
-    for (int v = 0; v < nv; ++v)
-      for (int j = -1; j < prep[valid[v]].N - 1; ++j) { t[2 * x] = v; t[2 * x + 1] = j; ++x; }
-    Ly.n_atask = x;
-  }
   int32_t* h_order = (int32_t*)hp(Ly.order);
   {
     std::vector<int> ord(nv);
@@ -937,6 +932,19 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       ws.qn[q] = qcount[q];
       qb += qcount[q];
     }
+    // anchor tasks (instance, anchor j), j = -1 .. N-2, grouped by solve part so each
+    // part's anchor/group kernels run on its own stream ahead of its DP
+    int32_t* t = (int32_t*)hp(Ly.atask);
+    int64_t x = 0;
+    for (int p = 0; p < P; ++p) {
+      ws.atask_lo[p] = (int)x;
+      for (int y = ws.part_lo[p]; y < ws.part_lo[p + 1]; ++y) {
+        const int v = ord[y];
+        for (int j = -1; j < prep[valid[v]].N - 1; ++j) { t[2 * x] = v; t[2 * x + 1] = j; ++x; }
+      }
+    }
+    ws.atask_lo[P] = (int)x;
+    Ly.n_atask = x;
   }
   {
     slos_record* rd = (slos_record*)hp(Ly.recdef);
@@ -1109,15 +1117,11 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     for (int p = 0; p < kMaxParts; ++p) {
       cudaStreamCreateWithPriority(&ws.pstream[p], cudaStreamNonBlocking, std::min(lo, hi + p));
       cudaEventCreate(&ws.ev_dp[p]);
+      cudaEventCreate(&ws.ev_anc[p]);
       cudaEventCreateWithFlags(&ws.ev_join[p], cudaEventDisableTiming);
     }
   }
   cudaEventRecord(ws.ev[0], s);
-  if ((e = launch_anchor(dp, ws.A.n_atask, ws.anchor_smem, s)) != cudaSuccess)
-    return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  if ((e = launch_group(dp, ws.A.n_atask, ws.maxN, s)) != cudaSuccess)
-    return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  cudaEventRecord(ws.ev[3], s);
   cudaEventRecord(ws.ev_fork, s);
   BuildParams bp;
   bp.a = ws.A;
@@ -1137,6 +1141,14 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   for (int p = 0; p < ws.n_parts; ++p) {
     const cudaStream_t sp = ws.pstream[p];
     cudaStreamWaitEvent(sp, ws.ev_fork, 0);
+    DpParams dpa = dp;  // the part's anchor caches and pair groups
+    dpa.task0 = ws.atask_lo[p];
+    const int nt = ws.atask_lo[p + 1] - ws.atask_lo[p];
+    if ((e = launch_anchor(dpa, nt, ws.anchor_smem, sp)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    if ((e = launch_group(dpa, nt, ws.maxN, sp)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    cudaEventRecord(ws.ev_anc[p], sp);
     DpParams dpp = dp;
     dpp.blk0 = ws.part_lo[p];
     if ((e = launch_dp(dpp, ws.part_lo[p + 1] - ws.part_lo[p], smem, sp)) != cudaSuccess)
@@ -1613,9 +1625,13 @@ int slos_workspace_stage_ms(slos_workspace* b, float* ms, int32_t n) {
     cudaEventSynchronize(ws.ev[2]);
     float all = 0.0f;
     cudaEventElapsedTime(&all, ws.ev[0], ws.ev[2]);
-    cudaEventElapsedTime(&t[0], ws.ev[0], ws.ev[3]);
-    const float dp_end = dp_end_ms(ws);  // last part's DP (the reconstruction of earlier
-    t[1] = dp_end - t[0];                // parts overlaps it)
+    for (int p = 0; p < ws.n_parts; ++p) {  // anchor stage: until the last part's groups
+      float x = 0.0f;
+      cudaEventElapsedTime(&x, ws.ev[0], ws.ev_anc[p]);
+      t[0] = std::max(t[0], x);
+    }
+    const float dp_end = dp_end_ms(ws);  // last part's DP (parts overlap: stages are
+    t[1] = dp_end - t[0];                // timed to their last part's end)
     t[2] = all - dp_end;
   }
   for (int k = 0; k < n && k < 3; ++k) ms[k] = t[k];
