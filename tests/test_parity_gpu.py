@@ -47,6 +47,23 @@ def test_c2_batch_matches_oracle_with_reference_counters():
     assert not bad, bad[:4]
 
 
+def test_c2_1024_pipelined_matches_reference():
+    """The bench batch itself: 1024 C2 instances through slos_plan_batch, which runs
+    as two pipelined chunks, each solved in two stream-pipelined parts with all three
+    reconstruction kinds' queues, against the compiled reference (16 host threads)."""
+    import os
+    if not os.path.exists(abi.REF_LIB):
+        pytest.skip("oracle/_ref not built")
+    F = W.FAMILIES["C2"]
+    b = W.InstanceBatch.stress(F["spec"], range(5000, 6024))
+    prod, ref = abi.product(), abi.reference()
+    hp, hr = _Handle(prod, F["model"], W.TWO_TIER_SLO, F["cfg"]), _Handle(ref, F["model"], W.TWO_TIER_SLO, F["cfg"])
+    P = plan_many(prod, hp.ptr, b)
+    R = plan_many(ref, hr.ptr, b)
+    bad = [(k, diff(P[k], R[k])) for k in range(b.n) if diff(P[k], R[k])]
+    assert not bad, bad[:4]
+
+
 def test_fresh_fuzz_matches_oracle():
     from fuzz import random_case
     prod, ora = abi.product(), abi.oracle()
