@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--instances", type=int, default=PER_RANK)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="C2", choices=["C2", "C5"],
+                    help="C2 (default, BASELINE configs[1]) or C5: the recorded capacity-sweep "
+                         "corpus, 65,536 instances sharded across the ranks (configs[4])")
     return ap.parse_args()
 
 
@@ -108,6 +111,34 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+C5_TOTAL = 65536
+
+
+def c5_shard(lib, rank: int, world: int):
+    """configs[4]: the C5 corpus (tests/golden/c5_*.bin.gz, schedule() inputs recorded
+    from the reference simulator's sweep grid, 2,048 per planner configuration) tiled
+    to 65,536 instances, half AR (chatbot/coder/summarizer/toolllm) and half
+    speculative (reasoning), sharded contiguously across the ranks (strong scaling).
+    Returns (batch, per-instance handles, shard size)."""
+    from paper_2504_08784_b200 import workload as W
+    from paper_2504_08784_b200.planner import PerfTerm, PlannerConfig, _Handle
+    from paper_2504_08784_b200.sweep import shard_range
+    gold = os.path.join(ROOT, "tests", "golden")
+    model = [PerfTerm(2.5e-5, 2e-3, 0.006), PerfTerm(0.0, 0.0, 0.02)]  # the desk model
+    parts, hs = [], []
+    for g, spec in (("ar", False), ("spec", True)):
+        b = W.load_corpus(os.path.join(gold, f"c5_{g}.bin.gz"))
+        half = C5_TOTAL // 2
+        parts.append(b.tiled((half + b.n - 1) // b.n).subset(range(half)))
+        cfg = PlannerConfig(max_chunk_tokens=2048, max_batch_tokens=16384, speculative=spec, spec_alpha=0.8,
+                            spec_max_len=8)
+        hs.append((_Handle(lib, model, W.TWO_TIER_SLO, cfg), half))
+    full = W.InstanceBatch.concat(parts)
+    sh = shard_range(C5_TOTAL, rank, world)
+    handles = [hs[0][0]] * hs[0][1] + [hs[1][0]] * hs[1][1]
+    return full.subset(sh), [handles[k] for k in sh], len(sh)
+
+
 def family():
     from paper_2504_08784_b200 import workload as W
     from paper_2504_08784_b200.sweep import ShardSpec
@@ -140,11 +171,52 @@ def cpu_reference_rate(n_inst: int, seeds_base: int = 0):
     return batch.n / dt, kind, cores, dt
 
 
+def cpu_reference_rate_c5(n_inst: int = 8192):
+    """The reference CPU planner over the first n_inst instances of the C5 workload
+    (all host cores). Returns (plans/sec, kind, cores, seconds, n)."""
+    from paper_2504_08784_b200 import abi
+    if os.path.exists(abi.REF_LIB):
+        lib, kind = abi.reference(), "reference"
+        cores = int(os.environ.get("SLOS_REF_THREADS", os.cpu_count() or 1))
+    else:
+        lib, kind, cores = abi.oracle(), "port", 1
+    b, handles, _ = c5_shard(lib, 0, 1)
+    idx = list(range(0, C5_TOTAL, C5_TOTAL // n_inst))  # both halves, every recorded source
+    sub = b.subset(idx)
+    hs = (C.c_void_p * len(idx))(*[handles[k].ptr for k in idx])
+    outs = (abi.Result * len(idx))()
+    t = time.perf_counter()
+    lib.slos_plan_batch(hs, len(idx), C.c_void_p(sub.inputs_ptr()), 0, outs, None)
+    dt = time.perf_counter() - t
+    for k in range(len(idx)):
+        lib.slos_result_free(C.byref(outs[k]))
+    return len(idx) / dt, kind, cores, dt, len(idx)
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     ncores = int(os.environ.get("SLOS_REF_THREADS", os.cpu_count() or 1))
+    if args.workload == "C5":  # configs[4] corpus: the reference over all host cores
+        for _ in range(args.warmup):
+            cpu_reference_rate_c5()
+        rates = [cpu_reference_rate_c5() for _ in range(args.steps)]
+        value = sum(r[0] for r in rates) / len(rates)
+        kind, cores, n5 = rates[0][1], rates[0][2], rates[0][4]
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n5 / value,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp64+int64",
+            "data": "schedule() inputs recorded from the reference simulator's capacity-sweep grid",
+            "config": {"workload": "C5: bursty capacity-sweep corpus (BASELINE configs[4])",
+                       "instances_per_step": n5, "parallelism": f"{cores} host threads"},
+            "cpu_baseline": {"value": value, "unit": "plans/s", "cores": cores, "kind": kind,
+                             "sample": f"{n5} C5 instances per step"},
+            "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
     sample = max(2 * ncores, 8)  # ~0.5 s of all-core reference work per step
     for _ in range(args.warmup):
         cpu_reference_rate(sample)
@@ -194,8 +266,13 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = abi.product()
     spec, F = family()
-    per = args.instances
-    solver = ShardSolver(lib, spec, weak_seeds(rank, per))
+    c5 = args.workload == "C5"
+    if c5:
+        batch5, handles5, per = c5_shard(lib, rank, world)
+        solver = ShardSolver(lib, spec, None, batch=batch5, handles=handles5)
+    else:
+        per = args.instances
+        solver = ShardSolver(lib, spec, weak_seeds(rank, per))
     stream = torch.cuda.Stream()
     sptr = stream.cuda_stream
     rec = torch.empty((per, C.sizeof(abi.Record)), dtype=torch.uint8, device="cuda")
@@ -240,7 +317,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, anc_tot, dp_tot, build_tot = (float(x) for x in t.tolist())
     recs = records_view(allrec)
-    n_all = per * world
+    n_all = per * world if not c5 else len(recs)
     assert len(recs) == n_all and (recs["status"] == 0).all(), "solve produced error records"
     value = n_all * args.steps / (total_ms / 1e3)
 
@@ -252,7 +329,7 @@ def run_ours(args):
 
     # ---- e2e: the reference-facing C-ABI call with host inputs ----
     batch = solver.batch
-    hs = (C.c_void_p * per)(*([solver.handle.ptr] * per))
+    hs = solver._hs
     outs2 = (abi.Result * per)()
     for _ in range(max(2, args.warmup // 2)):
         lib.slos_plan_batch(hs, per, C.c_void_p(batch.inputs_ptr()), 0, outs2, sptr)
@@ -312,10 +389,15 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             ncores = int(os.environ.get("SLOS_REF_THREADS", os.cpu_count() or 1))
-            sample = max(16 * ncores, 32)
-            r, kind, cores, dt = cpu_reference_rate(sample, seeds_base=0)
-            cpu = {"value": r, "unit": "plans/s", "cores": cores, "kind": kind,
-                   "sample": f"{sample} C2 instances (seeds 0..{sample - 1}), {dt:.1f} s wall"}
+            if c5:
+                r, kind, cores, dt, n5 = cpu_reference_rate_c5()
+                cpu = {"value": r, "unit": "plans/s", "cores": cores, "kind": kind,
+                       "sample": f"{n5} C5 corpus instances (mixed AR / speculative), {dt:.1f} s wall"}
+            else:
+                sample = max(16 * ncores, 32)
+                r, kind, cores, dt = cpu_reference_rate(sample, seeds_base=0)
+                cpu = {"value": r, "unit": "plans/s", "cores": cores, "kind": kind,
+                       "sample": f"{sample} C2 instances (seeds 0..{sample - 1}), {dt:.1f} s wall"}
         line = {
             "metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -344,6 +426,14 @@ def run_ours(args):
             "clocks": ck,
             "check": {"statuses_ok": bool(ok), "mean_admitted": adm},
         }
+        if c5:  # configs[4]: the sharded sweep corpus, strong scaling
+            line["scaling"] = "strong"
+            line["data"] = ("schedule() inputs recorded from the reference simulator's capacity-sweep grid "
+                            "(tests/golden/c5_*.bin.gz, 4,096 distinct, tiled)")
+            line["config"]["workload"] = ("C5: bursty capacity-sweep corpus, 65,536 instances (32,768 AR + "
+                                          "32,768 speculative) sharded across the GPUs (BASELINE configs[4])")
+            line["config"]["parallelism"] = f"{world} GPU(s), one process each, strong scaling"
+            line["config"]["instances_per_gpu"] = per
         print(json.dumps(line), flush=True)
     solver.close()
     if world > 1:

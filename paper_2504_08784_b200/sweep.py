@@ -46,7 +46,8 @@ class ShardSpec:
 class ShardSolver:
     """Device-resident shard of planning instances behind one slos_workspace."""
 
-    def __init__(self, lib, spec: ShardSpec, seeds, unit_value: bool = False, batch: InstanceBatch = None):
+    def __init__(self, lib, spec: ShardSpec, seeds, unit_value: bool = False, batch: InstanceBatch = None,
+                 handles=None):
         self.lib = lib
         # a stress-family shard (seeds) or any prepared batch (e.g. a recorded corpus)
         self.batch = batch if batch is not None else InstanceBatch.stress(spec.family, list(seeds), spec.slo)
@@ -58,7 +59,11 @@ class ShardSolver:
         if st != abi.SLOS_OK:
             raise RuntimeError(lib.slos_last_error().decode())
         self.ws = ws
-        self._hs = (C.c_void_p * self.n)(*([self.handle.ptr] * self.n))
+        # one planner handle for every instance, or one per instance (mixed planner
+        # configurations, e.g. the C5 corpus' speculative and AR instances)
+        self._handles = handles
+        ptrs = [h.ptr for h in handles] if handles is not None else [self.handle.ptr] * self.n
+        self._hs = (C.c_void_p * self.n)(*ptrs)
         self._outs = (abi.Result * self.n)()
 
     def upload(self, stream=None) -> None:

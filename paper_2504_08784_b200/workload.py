@@ -244,13 +244,26 @@ class InstanceBatch:
             p0 += npn
         return cls(inp, run, pen, blob, offs)
 
+    @classmethod
+    def concat(cls, parts) -> "InstanceBatch":
+        """Instances of several batches in one (the request arrays stay where they are;
+        the new batch keeps the parts alive)."""
+        out = cls(np.concatenate([p.inputs for p in parts]), parts[0].running, parts[0].pending,
+                  parts[0]._blob, parts[0]._id_offsets)
+        out._parts = list(parts)
+        return out
+
     def tiled(self, reps: int) -> "InstanceBatch":
         """The same instances repeated `reps` times (shares every request array)."""
-        return InstanceBatch(np.tile(self.inputs, reps), self.running, self.pending, self._blob, self._id_offsets)
+        out = InstanceBatch(np.tile(self.inputs, reps), self.running, self.pending, self._blob, self._id_offsets)
+        out._parts = [self]
+        return out
 
     def subset(self, idx) -> "InstanceBatch":
-        return InstanceBatch(self.inputs[np.asarray(idx)].copy(), self.running, self.pending, self._blob,
-                             self._id_offsets)
+        out = InstanceBatch(self.inputs[np.asarray(idx)].copy(), self.running, self.pending, self._blob,
+                            self._id_offsets)
+        out._parts = [self]
+        return out
 
 
 def load_corpus(path: str) -> InstanceBatch:
