@@ -373,7 +373,8 @@ int prep_instance(const slos_planner* P, const slos_input* in, int unit_value, P
   const int L = P->L;
   if (L > 8) return set_err(SLOS_ERR_INVALID_PARAMETERS, "at most 8 SLO tiers supported");
   if (!P->device_ok) return set_err(SLOS_ERR_RANGE, "planner not representable on device");
-  std::vector<ChainKey> ch;
+  thread_local std::vector<ChainKey> ch;  // capacity kept across calls
+  ch.clear();
   ch.reserve((size_t)in->n_running + (size_t)in->n_pending);
   for (int i = 0; i < in->n_running; ++i) {
     const slos_running& r = in->running[i];
@@ -585,6 +586,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   std::vector<Caps> caps(n);
   int maxN = 0, maxDec = 0, Lmax = 1;
   double S_need = 16;
+  const auto t_a = std::chrono::steady_clock::now();
   HostPool::get().run(n, [&](int lo, int hi) {
     for (int q = lo; q < hi; ++q) {
       const int k = jobs[q].k;
@@ -624,6 +626,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     Lmax = std::max(Lmax, P->L);
     S_need = std::max(S_need, std::ceil(pr.span / P->tpot[0]) + 8);
   }
+  const auto t_b = std::chrono::steady_clock::now();
   const int nv = (int)valid.size();
   if (nv == 0) return SLOS_OK;
   const int Sc = (int)std::min<double>(S_need, 1 << 20);
@@ -765,6 +768,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       n_small += pr.n_dec <= build_warp_max_dec() ? 1 : 0;  // (informational)
     }
   }
+  const auto t_c = std::chrono::steady_clock::now();
   HostPool::get().run(nv, [&](int v_lo, int v_hi) {
   for (int v = v_lo; v < v_hi; ++v) {
     int64_t oD = offs[v].D, oC = offs[v].C, oP = offs[v].P, oR = offs[v].R, oS = offs[v].S, oCd = offs[v].Cd,
@@ -906,11 +910,27 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     cost[v] = (double)(pr.n_dec + 8) * (double)(pr.N + 1) * (double)(pr.N + 1);
   }
   });
+  const auto t_d = std::chrono::steady_clock::now();
   int32_t* h_order = (int32_t*)hp(Ly.order);
   {
+    // launch order, heaviest first (load balance only: results do not depend on it).
+    // Large batches bucket by log2(cost) instead of sorting (O(n), stable).
     std::vector<int> ord(nv);
-    for (int v = 0; v < nv; ++v) ord[v] = v;
-    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    if (nv <= 4096) {
+      for (int v = 0; v < nv; ++v) ord[v] = v;
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    } else {
+      constexpr int kB = 64;
+      int cnt[kB + 1] = {0};
+      std::vector<uint8_t> key(nv);
+      for (int v = 0; v < nv; ++v) {
+        const int e = std::min(kB - 1, std::max(0, std::ilogb(std::max(1.0, cost[v]))));
+        key[v] = (uint8_t)(kB - 1 - e);
+        ++cnt[key[v] + 1];
+      }
+      for (int b = 0; b < kB; ++b) cnt[b + 1] += cnt[b];
+      for (int v = 0; v < nv; ++v) ord[cnt[key[v]]++] = v;
+    }
     for (int v = 0; v < nv; ++v) h_order[v] = ord[v];
     // solve parts: contiguous ranges of the cost-descending order (every part gets
     // a share of the heavy instances); each part's DP and reconstruction are
@@ -953,6 +973,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     int32_t* rm = (int32_t*)hp(Ly.recmap);
     for (int v = 0; v < nv; ++v) rm[v] = valid[v];
   }
+  const auto t_e = std::chrono::steady_clock::now();
   ws.n_total = n;
   g_h2d += (int64_t)Ly.in_bytes;
   // ---- device pipeline ----
@@ -961,6 +982,14 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   unsigned char* DO = (unsigned char*)ws.d_out.p;
   cudaStream_t s = ws.stream;
   cudaMemcpyAsync(DI, H, Ly.in_bytes, cudaMemcpyHostToDevice, s);
+  if (std::getenv("SLOS_HOST_TIMING")) {
+    const auto t_f = std::chrono::steady_clock::now();
+    auto ms = [](std::chrono::steady_clock::time_point x, std::chrono::steady_clock::time_point y) {
+      return std::chrono::duration<double, std::milli>(y - x).count();
+    };
+    std::fprintf(stderr, "[slos upload] n %d: prep %.3f, totals %.3f, layout %.3f, fill %.3f, order/parts %.3f, h2d %.3f ms\n",
+                 n, ms(t_a, t_b), 0.0, ms(t_b, t_c), ms(t_c, t_d), ms(t_d, t_e), ms(t_e, t_f));
+  }
   Ly.memo_bytes = sizeof(MemoEnt) * (size_t)TM;
   Ly.bkey_bytes = sizeof(uint64_t) * 2 * (size_t)TCd;
   Ly.bval_bytes = sizeof(int32_t) * 2 * (size_t)TCd;
