@@ -560,6 +560,7 @@ struct Workspace {
   int qbase[kQueues] = {0};
   int qn[kQueues] = {0};
   cudaStream_t pstream[kMaxParts] = {nullptr};  // per-part streams, earlier parts higher priority
+  cudaStream_t astream = nullptr;                // anchor / group kernels of every part
   cudaEvent_t ev_fork = nullptr, ev_dp[kMaxParts] = {nullptr}, ev_join[kMaxParts] = {nullptr};
 };
 
@@ -1143,8 +1144,9 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     cudaEventCreateWithFlags(&ws.ev_fork, cudaEventDisableTiming);
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&ws.astream, cudaStreamNonBlocking, hi);
     for (int p = 0; p < kMaxParts; ++p) {
-      cudaStreamCreateWithPriority(&ws.pstream[p], cudaStreamNonBlocking, std::min(lo, hi + p));
+      cudaStreamCreateWithPriority(&ws.pstream[p], cudaStreamNonBlocking, std::min(lo, hi + 1 + p));
       cudaEventCreate(&ws.ev_dp[p]);
       cudaEventCreate(&ws.ev_anc[p]);
       cudaEventCreateWithFlags(&ws.ev_join[p], cudaEventDisableTiming);
@@ -1167,17 +1169,23 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   bp.phase_cycles = dp.phase_cycles ? dp.phase_cycles + 16 : nullptr;
   // per part: admission DP, then its plan reconstruction, on the part's stream;
   // part p's reconstruction runs while part p+1's DP still occupies SMs
+  // anchor caches and pair groups of every part, in part order, on the highest-
+  // priority stream (throughput kernels: they fill the SMs the latency-bound DP
+  // leaves idle and put each part's DP on its critical path as early as possible)
+  cudaStreamWaitEvent(ws.astream, ws.ev_fork, 0);
   for (int p = 0; p < ws.n_parts; ++p) {
-    const cudaStream_t sp = ws.pstream[p];
-    cudaStreamWaitEvent(sp, ws.ev_fork, 0);
-    DpParams dpa = dp;  // the part's anchor caches and pair groups
+    DpParams dpa = dp;
     dpa.task0 = ws.atask_lo[p];
     const int nt = ws.atask_lo[p + 1] - ws.atask_lo[p];
-    if ((e = launch_anchor(dpa, nt, ws.anchor_smem, sp)) != cudaSuccess)
+    if ((e = launch_anchor(dpa, nt, ws.anchor_smem, ws.astream)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-    if ((e = launch_group(dpa, nt, ws.maxN, sp)) != cudaSuccess)
+    if ((e = launch_group(dpa, nt, ws.maxN, ws.astream)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-    cudaEventRecord(ws.ev_anc[p], sp);
+    cudaEventRecord(ws.ev_anc[p], ws.astream);
+  }
+  for (int p = 0; p < ws.n_parts; ++p) {
+    const cudaStream_t sp = ws.pstream[p];
+    cudaStreamWaitEvent(sp, ws.ev_anc[p], 0);
     DpParams dpp = dp;
     dpp.blk0 = ws.part_lo[p];
     if ((e = launch_dp(dpp, ws.part_lo[p + 1] - ws.part_lo[p], smem, sp)) != cudaSuccess)
