@@ -124,18 +124,56 @@ typedef struct slos_input { /* ScheduleInput dp_scheduler.hpp:38-47 */
 /* Entry request reference: req >= 0 is running[req]; req < 0 is pending[-req-1]. */
 #define SLOS_PENDING_REF(p) (-(int32_t)(p)-1)
 
-/* PlanEntry dp_scheduler.hpp:49-54. Token counts are 32-bit on the wire (plans are
- * the bulk of the device->host traffic): every count is bounded by a batch
- * capacity, and slos_planner_create rejects max_batch_tokens / max_chunk_tokens
- * above INT32_MAX; a plan whose count would still not fit (only possible with
- * absurd decode backlogs in the EDF fallback) fails with SLOS_ERR_INVALID_PARAMETERS
- * instead of truncating. The adapter widens them back to the reference's int64. */
+/* PlanEntry dp_scheduler.hpp:49-54, 8 bytes on the wire (plans are the bulk of the
+ * device->host traffic). Every entry the planner emits is EITHER a prefill chunk
+ * (decode_tokens = spec_len = 0) OR a decode allocation (prefill_tokens = 0):
+ * dp_scheduler.cpp:150,163,178,229,288,343. So one 32-bit token count and a kind
+ * bit carry it:
+ *   ref bits  0-23  request reference (SLOS_PENDING_REF convention, 24-bit signed)
+ *   ref bits 24-30  spec_len of a decode entry (0 = autoregressive)
+ *   ref bit  31     1 = decode entry, 0 = prefill entry
+ *   tokens          prefill_tokens (prefill entry) or decode_tokens (decode entry)
+ * The limits that keep this lossless are enforced, never truncated: slos_plan*
+ * rejects n_running or n_pending >= SLOS_ENTRY_MAX_REQS, slos_planner_create
+ * rejects max_batch_tokens / max_chunk_tokens above INT32_MAX and speculative
+ * spec_max_len above SLOS_ENTRY_MAX_SPEC, and a plan whose count would still not
+ * fit (only possible with absurd decode backlogs in the EDF fallback) fails with
+ * SLOS_ERR_INVALID_PARAMETERS. Read entries through the accessors below; the
+ * adapter widens the counts back to the reference's int64. */
 typedef struct slos_entry {
-  int32_t req;
-  int32_t spec_len;
-  int32_t prefill_tokens;
-  int32_t decode_tokens;
+  uint32_t ref;
+  int32_t tokens;
 } slos_entry;
+
+#define SLOS_ENTRY_MAX_REQS (1 << 23)
+#define SLOS_ENTRY_MAX_SPEC 127
+
+#if defined(__CUDACC__)
+#define SLOS_ENTRY_FN static inline __host__ __device__
+#else
+#define SLOS_ENTRY_FN static inline
+#endif
+SLOS_ENTRY_FN int32_t slos_entry_req(const slos_entry* e) { return ((int32_t)(e->ref << 8)) >> 8; }
+SLOS_ENTRY_FN int32_t slos_entry_is_decode(const slos_entry* e) { return (int32_t)(e->ref >> 31); }
+SLOS_ENTRY_FN int32_t slos_entry_spec_len(const slos_entry* e) { return (int32_t)((e->ref >> 24) & 0x7Fu); }
+SLOS_ENTRY_FN int64_t slos_entry_prefill_tokens(const slos_entry* e) {
+  return slos_entry_is_decode(e) ? 0 : (int64_t)e->tokens;
+}
+SLOS_ENTRY_FN int64_t slos_entry_decode_tokens(const slos_entry* e) {
+  return slos_entry_is_decode(e) ? (int64_t)e->tokens : 0;
+}
+SLOS_ENTRY_FN slos_entry slos_entry_prefill(int32_t req, int32_t tokens) {
+  slos_entry e;
+  e.ref = (uint32_t)req & 0xFFFFFFu;
+  e.tokens = tokens;
+  return e;
+}
+SLOS_ENTRY_FN slos_entry slos_entry_decode(int32_t req, int32_t tokens, int32_t spec_len) {
+  slos_entry e;
+  e.ref = ((uint32_t)req & 0xFFFFFFu) | ((uint32_t)spec_len & 0x7Fu) << 24 | 0x80000000u;
+  e.tokens = tokens;
+  return e;
+}
 
 typedef struct slos_batch { /* PlanBatch dp_scheduler.hpp:56-63 */
   double start_s;

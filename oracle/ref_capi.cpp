@@ -109,10 +109,15 @@ void fill_result(const slos_input* in, const ScheduleResult& res, slos_result* o
   size_t n_entries = 0;
   for (const auto& b : res.plan.batches) {
     n_entries += b.entries.size();
-    for (const PlanEntry& pe : b.entries)  // token counts must fit the 32-bit slos_entry
+    for (const PlanEntry& pe : b.entries) {  // the 8-byte slos_entry (include/slos_planner.h)
       if (pe.prefill_tokens > INT32_MAX || pe.decode_tokens > INT32_MAX || pe.prefill_tokens < INT32_MIN ||
           pe.decode_tokens < INT32_MIN)
         fail("invalid-parameters", "a plan token count exceeds the 32-bit entry range");
+      if (pe.spec_len < 0 || pe.spec_len > SLOS_ENTRY_MAX_SPEC)
+        fail("invalid-parameters", "a plan spec_len exceeds the entry range");
+      if (pe.prefill_tokens != 0 && (pe.decode_tokens != 0 || pe.spec_len != 0))
+        fail("internal-inconsistency", "a plan entry carries both prefill and decode tokens");
+    }
   }
   const size_t n_adm = res.admitted.size(), n_dec = res.declined.size(),
                n_def = res.deferred.size(), n_b = res.plan.batches.size();
@@ -137,10 +142,10 @@ void fill_result(const slos_input* in, const ScheduleResult& res, slos_result* o
     batches[k].first_entry = (int64_t)e;
     batches[k].n_entries = (int64_t)b.entries.size();
     for (const PlanEntry& pe : b.entries) {
-      entries[e].req = ref.at(pe.id);
-      entries[e].spec_len = pe.spec_len;
-      entries[e].prefill_tokens = (int32_t)pe.prefill_tokens;
-      entries[e].decode_tokens = (int32_t)pe.decode_tokens;
+      const int32_t rq = ref.at(pe.id);
+      entries[e] = (pe.decode_tokens != 0 || pe.spec_len != 0)
+                       ? slos_entry_decode(rq, (int32_t)pe.decode_tokens, pe.spec_len)
+                       : slos_entry_prefill(rq, (int32_t)pe.prefill_tokens);
       ++e;
     }
   }
@@ -259,6 +264,8 @@ int slos_planner_create(const slos_perf_term* terms, int32_t n_terms, const doub
     p->sched = std::make_unique<SloScheduler>(*p->planner);
     if (c.max_chunk_tokens > INT32_MAX || c.max_batch_tokens > INT32_MAX)  // 32-bit slos_entry
       fail("invalid-parameters", "batch and chunk caps must fit the 32-bit plan entries");
+    if (c.speculative && c.spec_max_len > SLOS_ENTRY_MAX_SPEC)  // 7-bit entry spec_len
+      fail("invalid-parameters", "spec_max_len must fit the plan entry format");
     *out = p.release();
     return SLOS_OK;
   });
@@ -269,6 +276,8 @@ void slos_planner_destroy(slos_planner* p) { delete p; }
 int slos_plan(slos_planner* p, const slos_input* in, int32_t unit_value, slos_result* out) {
   std::memset(out, 0, sizeof(*out));
   int st = guarded([&] {
+    if (in->n_running >= SLOS_ENTRY_MAX_REQS || in->n_pending >= SLOS_ENTRY_MAX_REQS)  // 24-bit entry refs
+      fail("invalid-parameters", "too many requests for the plan entry format");
     ScheduleInput s = to_input(in);
     ScheduleResult r = unit_value ? p->sched->schedule_throughput(s) : p->sched->schedule(s);
     fill_result(in, r, out);

@@ -119,10 +119,10 @@ class GpuSloScheduler : public Scheduler {
       pb.prefill_budget_left = cb.prefill_budget_left;
       for (int64_t e = cb.first_entry; e < cb.first_entry + cb.n_entries; ++e) {
         PlanEntry pe;
-        pe.id = id(r.entries[e].req);
-        pe.prefill_tokens = r.entries[e].prefill_tokens;
-        pe.decode_tokens = r.entries[e].decode_tokens;
-        pe.spec_len = r.entries[e].spec_len;
+        pe.id = id(slos_entry_req(&r.entries[e]));
+        pe.prefill_tokens = slos_entry_prefill_tokens(&r.entries[e]);
+        pe.decode_tokens = slos_entry_decode_tokens(&r.entries[e]);
+        pe.spec_len = slos_entry_spec_len(&r.entries[e]);
         pb.entries.push_back(std::move(pe));
       }
       out.plan.batches.push_back(std::move(pb));

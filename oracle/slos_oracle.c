@@ -261,6 +261,7 @@ int slos_planner_create(const slos_perf_term* terms, int32_t n_terms, const doub
   /* BatchPlanner::BatchPlanner batch_planner.cpp:117-123 */
   if (c.max_chunk_tokens < 1 || c.max_batch_tokens < 1) goto fail_soft;
   if (c.max_chunk_tokens > INT32_MAX || c.max_batch_tokens > INT32_MAX) goto fail_soft; /* 32-bit slos_entry */
+  if (c.speculative && c.spec_max_len > SLOS_ENTRY_MAX_SPEC) goto fail_soft;             /* 7-bit spec_len */
   if (c.plan_margin < 0) goto fail_soft;
   slos_planner* p = calloc(1, sizeof *p);
   p->terms = malloc(sizeof(slos_perf_term) * (size_t)n_terms);
@@ -1191,13 +1192,17 @@ static void emit_result(const slos_input* in, int infeasible, double value, cons
                         int nadm, const int32_t* dec, int ndec, const splan_t* plan,
                         const slos_counters* ctr, slos_result* out) {
   (void)in;
-  for (int64_t k = 0; k < plan->e.n; ++k) /* token counts must fit the 32-bit slos_entry */
-    if (plan->e.v[k].prefill > INT32_MAX || plan->e.v[k].decode > INT32_MAX ||
-        plan->e.v[k].prefill < INT32_MIN || plan->e.v[k].decode < INT32_MIN) {
+  for (int64_t k = 0; k < plan->e.n; ++k) { /* the 8-byte slos_entry (include/slos_planner.h) */
+    const int bad = plan->e.v[k].prefill > INT32_MAX || plan->e.v[k].decode > INT32_MAX ||
+                    plan->e.v[k].prefill < INT32_MIN || plan->e.v[k].decode < INT32_MIN ||
+                    plan->e.v[k].spec_len < 0 || plan->e.v[k].spec_len > SLOS_ENTRY_MAX_SPEC;
+    const int both = plan->e.v[k].prefill != 0 && (plan->e.v[k].decode != 0 || plan->e.v[k].spec_len != 0);
+    if (bad || both) {
       memset(out, 0, sizeof *out);
-      out->status = SLOS_ERR_INVALID_PARAMETERS;
+      out->status = bad ? SLOS_ERR_INVALID_PARAMETERS : SLOS_ERR_INTERNAL_INCONSISTENCY;
       return;
     }
+  }
   size_t bytes = sizeof(obatch_t) + sizeof(slos_batch) * (size_t)plan->b.n +
                  sizeof(slos_entry) * (size_t)plan->e.n + sizeof(int32_t) * (size_t)(nadm + ndec) + 64;
   char* mem = calloc(1, bytes);
@@ -1214,10 +1219,9 @@ static void emit_result(const slos_input* in, int infeasible, double value, cons
     b[k].n_entries = plan->b.v[k].n_entries;
   }
   for (int64_t k = 0; k < plan->e.n; ++k) {
-    e[k].req = plan->e.v[k].req;
-    e[k].spec_len = plan->e.v[k].spec_len;
-    e[k].prefill_tokens = (int32_t)plan->e.v[k].prefill;
-    e[k].decode_tokens = (int32_t)plan->e.v[k].decode;
+    e[k] = (plan->e.v[k].decode != 0 || plan->e.v[k].spec_len != 0)
+               ? slos_entry_decode(plan->e.v[k].req, (int32_t)plan->e.v[k].decode, plan->e.v[k].spec_len)
+               : slos_entry_prefill(plan->e.v[k].req, (int32_t)plan->e.v[k].prefill);
   }
   for (int k = 0; k < nadm; ++k) ids[k] = adm[k];
   for (int k = 0; k < ndec; ++k) ids[nadm + k] = dec[k];
@@ -1243,6 +1247,8 @@ static void emit_result(const slos_input* in, int infeasible, double value, cons
 static void run(const slos_planner* p, const slos_input* in, int unit_value, slos_result* out) {
   const int L = p->L;
   if (L > 8) fail(SLOS_ERR_INVALID_PARAMETERS, "at most 8 SLO tiers supported");
+  if (in->n_running >= SLOS_ENTRY_MAX_REQS || in->n_pending >= SLOS_ENTRY_MAX_REQS) /* 24-bit entry refs */
+    fail(SLOS_ERR_INVALID_PARAMETERS, "too many requests for the plan entry format");
   const int64_t cap_chain = (int64_t)in->n_running + in->n_pending;
   chain_t* chain = malloc(sizeof(chain_t) * (size_t)(cap_chain + 1));
   int N = 0;

@@ -96,13 +96,35 @@ class Input(C.Structure):
     ]
 
 
-class Entry(C.Structure):  # slos_entry: 32-bit token counts on the wire
+class Entry(C.Structure):
+    """slos_entry: 8 bytes on the wire (include/slos_planner.h). `ref` packs the
+    24-bit signed request reference, the 7-bit spec_len and the decode bit; `tokens`
+    is the prefill or decode count. The properties mirror the header's accessors."""
     _fields_ = [
-        ("req", C.c_int32),
-        ("spec_len", C.c_int32),
-        ("prefill_tokens", C.c_int32),
-        ("decode_tokens", C.c_int32),
+        ("ref", C.c_uint32),
+        ("tokens", C.c_int32),
     ]
+
+    @property
+    def req(self) -> int:
+        r = self.ref & 0xFFFFFF
+        return r - (1 << 24) if r & 0x800000 else r
+
+    @property
+    def is_decode(self) -> bool:
+        return bool(self.ref >> 31)
+
+    @property
+    def spec_len(self) -> int:
+        return (self.ref >> 24) & 0x7F
+
+    @property
+    def prefill_tokens(self) -> int:
+        return 0 if self.is_decode else int(self.tokens)
+
+    @property
+    def decode_tokens(self) -> int:
+        return int(self.tokens) if self.is_decode else 0
 
 
 class Batch(C.Structure):
@@ -267,9 +289,9 @@ INPUT_DTYPE = np.dtype(
 )
 ENTRY_DTYPE = np.dtype(
     {
-        "names": ["req", "spec_len", "prefill_tokens", "decode_tokens"],
-        "formats": [np.int32, np.int32, np.int32, np.int32],
-        "offsets": [0, 4, 8, 12],
+        "names": ["ref", "tokens"],
+        "formats": [np.uint32, np.int32],
+        "offsets": [0, 4],
         "itemsize": C.sizeof(Entry),
     }
 )
@@ -283,6 +305,21 @@ CANON_ENTRY_DTYPE = np.dtype(
         "itemsize": 24,
     }
 )
+
+
+def canon_entries(wire: np.ndarray) -> np.ndarray:
+    """Wire entries (ENTRY_DTYPE) -> CANON_ENTRY_DTYPE, vectorised Entry accessors."""
+    ref = wire["ref"].astype(np.uint32)
+    tok = wire["tokens"].astype(np.int64)
+    dec = (ref >> np.uint32(31)).astype(bool)
+    out = np.zeros(len(wire), CANON_ENTRY_DTYPE)
+    out["req"] = ((ref << np.uint32(8)).view(np.int32) >> 8)
+    out["spec_len"] = ((ref >> np.uint32(24)) & np.uint32(0x7F)).astype(np.int32)
+    out["prefill_tokens"] = np.where(dec, 0, tok)
+    out["decode_tokens"] = np.where(dec, tok, 0)
+    return out
+
+
 BATCH_DTYPE = np.dtype(
     {
         "names": ["start_s", "end_s", "capacity_tokens", "spec_step", "prefill_budget_left",

@@ -21,6 +21,16 @@ namespace slos {
   } while (0)
 
 // A plan token count as a 32-bit entry field (flags values that do not fit).
+// Plan entries (include/slos_planner.h): a range violation flags the plan
+// (SLOS_ERR_INVALID_PARAMETERS) instead of truncating.
+__device__ __forceinline__ int32_t tok32(int64_t v, int* err);
+__device__ __forceinline__ slos_entry entry_prefill(int32_t req, int64_t tok, int* err) {
+  return slos_entry_prefill(req, tok32(tok, err));
+}
+__device__ __forceinline__ slos_entry entry_decode(int32_t req, int64_t tok, int spec, int* err) {
+  if (spec < 0 || spec > SLOS_ENTRY_MAX_SPEC) *err = 1;
+  return slos_entry_decode(req, tok32(tok, err), spec);
+}
 __device__ __forceinline__ int32_t tok32(int64_t v, int* err) {
   if (v > 2147483647LL || v < -2147483647LL - 1) *err = 1;
   return (int32_t)v;
@@ -134,12 +144,7 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
         const int64_t o2 = I.off_chain + sh.m_item[mi];
         if (sh.m_left[mi] == 0 && end_abs > A.ch_deadline[o2] + kTimeEps) sh.fill_late = 1;
         if (ne < I.cap_entry) {
-          slos_entry e;
-          e.req = A.ch_ref[o2];
-          e.spec_len = 0;
-          e.prefill_tokens = tok32(spend, &sh.range_err);
-          e.decode_tokens = 0;
-          OE[ne] = e;
+          OE[ne] = entry_prefill(A.ch_ref[o2], spend, &sh.range_err);
         }
         ++ne;
       }
@@ -170,12 +175,8 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
       const int64_t t = o.own[2 * (gb.first_owner + q) + 1];
       const int64_t at = e0 + q;
       if (at < I.cap_entry) {
-        slos_entry e;
-        e.req = owner_ref(A, sh, owner);
-        e.spec_len = spec_batch ? o.spec[owner_tier(A, sh, owner)] : 0;
-        e.prefill_tokens = 0;
-        e.decode_tokens = tok32(t, &sh.range_err);
-        OE[at] = e;
+        OE[at] = entry_decode(owner_ref(A, sh, owner), t, spec_batch ? o.spec[owner_tier(A, sh, owner)] : 0,
+                              &sh.range_err);
       }
       if (track && owner >= I.R_total) atomicAdd(&sh.m_asg[owner - I.R_total], (unsigned long long)t);
     }
@@ -316,12 +317,7 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
           if (q >= d1 - d0) break;
           if (rd[q] <= 0) continue;
           if (pos < I.cap_entry) {
-            slos_entry e;
-            e.req = ri[q];
-            e.spec_len = 0;
-            e.prefill_tokens = 0;
-            e.decode_tokens = tok32(rd[q], &sh.range_err);
-            OE[pos] = e;
+            OE[pos] = entry_decode(ri[q], rd[q], 0, &sh.range_err);
           }
           ++pos;
         }
@@ -329,12 +325,7 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
       for (int k = d0; k < d1; ++k) {
         if (ddue[k] <= 0) continue;
         if (pos < I.cap_entry) {
-          slos_entry e;
-          e.req = didx[k];
-          e.spec_len = 0;
-          e.prefill_tokens = 0;
-          e.decode_tokens = tok32(ddue[k], &sh.range_err);
-          OE[pos] = e;
+          OE[pos] = entry_decode(didx[k], ddue[k], 0, &sh.range_err);
         }
         ++pos;
       }
@@ -380,12 +371,7 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
         if (take <= 0) continue;
         pleft[k] -= take;
         if (pos < I.cap_entry) {
-          slos_entry e;
-          e.req = pidx[k];
-          e.spec_len = 0;
-          e.prefill_tokens = tok32(take, &sh.range_err);
-          e.decode_tokens = 0;
-          OE[pos] = e;
+          OE[pos] = entry_prefill(pidx[k], take, &sh.range_err);
         }
         ++pos;
       }

@@ -101,6 +101,7 @@ struct OutHdr {
   int64_t ctr[5];        // transitions, gap_evals, dues, slots, states
   int64_t need_surv, need_cand, need_memo, need_batch, need_entry, need_work;
   int64_t dbg_cycles;  // build_kernel cycles of this instance (phase timing only)
+  int64_t dbg_dp_cycles;  // dp_kernel cycles of this instance (phase timing only)
 };
 
 // Memo table entry (gap_budget memo, dp_scheduler.cpp:414-435).

@@ -935,6 +935,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   __syncthreads();
 
   long long ph_t0_ = clock64();
+  const long long ph_start_ = ph_t0_;
   SLOS_PHASE(0);  // 0: instance load / setup
   for (int i = 0; i < N && !s_err; ++i) {
     const int jlo = ch_fl[i];
@@ -1798,6 +1799,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     build_queue_push(A, inst, I.part, I.build_kind, best < 0);
   }
   SLOS_PHASE(11);  // 11: terminal selection + backtrack
+  if (prm.phase_cycles && tid == 0) out->dbg_dp_cycles = clock64() - ph_start_;
 }
 
 }  // namespace slos

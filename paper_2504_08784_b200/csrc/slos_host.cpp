@@ -372,6 +372,8 @@ struct ChainKey {
 int prep_instance(const slos_planner* P, const slos_input* in, int unit_value, Prep& pr) {
   const int L = P->L;
   if (L > 8) return set_err(SLOS_ERR_INVALID_PARAMETERS, "at most 8 SLO tiers supported");
+  if (in->n_running >= SLOS_ENTRY_MAX_REQS || in->n_pending >= SLOS_ENTRY_MAX_REQS)  // 24-bit entry refs
+    return set_err(SLOS_ERR_INVALID_PARAMETERS, "too many requests for the plan entry format");
   if (!P->device_ok) return set_err(SLOS_ERR_RANGE, "planner not representable on device");
   thread_local std::vector<ChainKey> ch;  // capacity kept across calls
   ch.clear();
@@ -562,9 +564,22 @@ struct Workspace {
   cudaStream_t pstream[kMaxParts] = {nullptr};  // per-part streams, earlier parts higher priority
   cudaStream_t astream = nullptr;                // anchor / group kernels of every part
   cudaEvent_t ev_fork = nullptr, ev_dp[kMaxParts] = {nullptr}, ev_join[kMaxParts] = {nullptr};
+  // per-part collection (plan_all): each part's headers are copied on its stream
+  // right after its reconstruction, so its compaction and D2H overlap later parts
+  bool part_collect = false;
+  std::vector<int32_t> ord;  // instance order: part p = ord[part_lo[p] .. part_lo[p+1])
+  PinBuf h_hdr[kMaxParts], h_offs[kMaxParts];
+  DevBuf d_packp[kMaxParts];
+  cudaEvent_t ev_hdr[kMaxParts] = {nullptr}, ev_d2h[kMaxParts] = {nullptr};
 };
 
 thread_local int64_t g_h2d = 0, g_d2h = 0;
+
+bool host_timing() {
+  static const bool on = std::getenv("SLOS_HOST_TIMING") != nullptr;
+  return on;
+}
+
 
 // Host preparation + one H2D copy; the instances become device-resident.
 int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_input* inputs,
@@ -933,6 +948,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       for (int v = 0; v < nv; ++v) ord[cnt[key[v]]++] = v;
     }
     for (int v = 0; v < nv; ++v) h_order[v] = ord[v];
+    ws.ord.assign(ord.begin(), ord.end());
     // solve parts: contiguous ranges of the cost-descending order (every part gets
     // a share of the heavy instances); each part's DP and reconstruction are
     // launched on their own stream so one part's reconstruction overlaps the next
@@ -1195,6 +1211,12 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     const int q0 = kBuildKinds * p;
     if ((e = launch_build(bp, ws.qn[q0], ws.qn[q0 + 1], ws.qn[q0 + 2], sp)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    if (ws.part_collect) {  // this part's headers, as soon as its reconstruction ends
+      if ((e = ws.h_hdr[p].ensure(sizeof(OutHdr) * nv)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+      if (!ws.ev_hdr[p]) cudaEventCreateWithFlags(&ws.ev_hdr[p], cudaEventDisableTiming);
+      cudaMemcpyAsync(ws.h_hdr[p].p, DO + Ly.out, sizeof(OutHdr) * nv, cudaMemcpyDeviceToHost, sp);
+      cudaEventRecord(ws.ev_hdr[p], sp);
+    }
     cudaEventRecord(ws.ev_join[p], sp);
     cudaStreamWaitEvent(s, ws.ev_join[p], 0);
   }
@@ -1213,25 +1235,11 @@ float dp_end_ms(Workspace& ws) {
   return t;
 }
 
-// Headers back, capacity regrowth list, compaction and one D2H of the results.
-int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry) {
-  if (!ws.uploaded || ws.nv == 0) return SLOS_OK;
+void print_phase_debug(Workspace& ws, const std::vector<OutHdr>& hdr) {
   const int nv = ws.nv;
   const std::vector<int>& valid = ws.valid;
   const std::vector<Job>& jobs = ws.jobs;
-  const Layout& Ly = ws.Ly;
-  const BatchArgs& A = ws.A;
-  const cudaStream_t s = ws.stream;
-  unsigned char* DO = (unsigned char*)ws.d_out.p;
-  cudaError_t e;
-  // ---- headers back, capacity check ----
-  if ((e = ws.h_small.ensure(sizeof(OutHdr) * nv)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  OutHdr* hO = (OutHdr*)ws.h_small.p;
-  cudaMemcpyAsync(hO, DO + Ly.out, sizeof(OutHdr) * nv, cudaMemcpyDeviceToHost, s);
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  std::vector<OutHdr> hdr(hO, hO + nv);
-  g_d2h += (int64_t)(sizeof(OutHdr) * (size_t)nv);
-  if (ws.dp.phase_cycles) {
+  {
     unsigned long long pc[32];
     cudaMemcpy(pc, ws.dp.phase_cycles, sizeof pc, cudaMemcpyDeviceToHost);
     unsigned long long tot = 0;
@@ -1261,12 +1269,36 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
                    jobs[valid[idx[r]]].k, (double)h.dbg_cycles, (long long)h.n_batches, (long long)h.n_entries,
                    h.infeasible, h.n_admitted, (long long)h.ctr[0]);
     }
+    std::sort(idx.begin(), idx.end(), [&](int x, int y) { return hdr[x].dbg_dp_cycles > hdr[y].dbg_dp_cycles; });
+    double dsum = 0.0;
+    for (int v = 0; v < nv; ++v) dsum += (double)hdr[v].dbg_dp_cycles;
+    auto q = [&](double f) { return (double)hdr[idx[std::min(nv - 1, (int)(f * nv))]].dbg_dp_cycles; };
+    std::fprintf(stderr, "[slos dp instances] mean %.3e p10 %.3e p50 %.3e p90 %.3e max %.3e cycles\n", dsum / nv, q(0.9),
+                 q(0.5), q(0.1), q(0.0));
+    for (int r = 0; r < std::min(nv, 6); ++r) {
+      const OutHdr& h = hdr[idx[r]];
+      std::fprintf(stderr, "  slow dp #%d: job %d cycles %.3e T %lld gap_evals %lld dues %lld states %lld admitted %d\n", r,
+                   jobs[valid[idx[r]]].k, (double)h.dbg_dp_cycles, (long long)h.ctr[0], (long long)h.ctr[1],
+                   (long long)h.ctr[2], (long long)h.ctr[4], h.n_admitted);
+    }
   }
-  // packed offsets
-  std::vector<int64_t> boff(nv, 0), eoff(nv, 0), ioff(nv, 0);
+}
+
+// One set of instances (positions x -> instance v = vlist[x]): capacity regrowth
+// list, packed offsets, compaction on `s` and one async D2H into a result arena;
+// fills the slos_result of each instance (the caller synchronises `s`).
+int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h, const int32_t* vlist_d, int n,
+                PinBuf& h_offs, DevBuf& d_pack, cudaStream_t s, slos_result* outs, std::vector<Job>& retry) {
+  const std::vector<int>& valid = ws.valid;
+  const std::vector<Job>& jobs = ws.jobs;
+  const BatchArgs& A = ws.A;
+  cudaError_t e;
+  auto vof = [&](int x) { return vlist_h ? vlist_h[x] : x; };
+  std::vector<int64_t> boff(n, 0), eoff(n, 0), ioff(n, 0);
   size_t packed = 0;
-  std::vector<int> good;
-  for (int v = 0; v < nv; ++v) {
+  int good = 0;
+  for (int x = 0; x < n; ++x) {
+    const int v = vof(x);
     const int q = valid[v];
     const OutHdr& h = hdr[v];
     if (h.status == SLOS_ERR_CAPACITY && jobs[q].grow < 6) {
@@ -1274,28 +1306,27 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
       continue;
     }
     if (h.status != SLOS_OK) continue;
-    good.push_back(v);
+    ++good;
     packed = (packed + 15) & ~(size_t)15;
-    boff[v] = (int64_t)packed;
+    boff[x] = (int64_t)packed;
     packed += sizeof(slos_batch) * (size_t)h.n_batches;
     packed = (packed + 15) & ~(size_t)15;
-    eoff[v] = (int64_t)packed;
+    eoff[x] = (int64_t)packed;
     packed += sizeof(slos_entry) * (size_t)h.n_entries;
     packed = (packed + 15) & ~(size_t)15;
-    ioff[v] = (int64_t)packed;
+    ioff[x] = (int64_t)packed;
     packed += sizeof(int32_t) * (size_t)(h.n_admitted + h.n_declined);
   }
   ResultArena* ra = nullptr;
-  if (!good.empty()) {
-    const size_t offs_bytes = sizeof(int64_t) * 3 * (size_t)nv;
-    if ((e = ws.d_pack.ensure(packed + offs_bytes + 256)) != cudaSuccess)
-      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-    if ((e = ws.h_small.ensure(offs_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-    int64_t* ho = (int64_t*)ws.h_small.p;
-    std::memcpy(ho, boff.data(), sizeof(int64_t) * nv);
-    std::memcpy(ho + nv, eoff.data(), sizeof(int64_t) * nv);
-    std::memcpy(ho + 2 * nv, ioff.data(), sizeof(int64_t) * nv);
-    unsigned char* DP_ = (unsigned char*)ws.d_pack.p;
+  if (good) {
+    const size_t offs_bytes = sizeof(int64_t) * 3 * (size_t)n;
+    if ((e = d_pack.ensure(packed + offs_bytes + 256)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    if ((e = h_offs.ensure(offs_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    int64_t* ho = (int64_t*)h_offs.p;
+    std::memcpy(ho, boff.data(), sizeof(int64_t) * n);
+    std::memcpy(ho + n, eoff.data(), sizeof(int64_t) * n);
+    std::memcpy(ho + 2 * n, ioff.data(), sizeof(int64_t) * n);
+    unsigned char* DP_ = (unsigned char*)d_pack.p;
     const size_t offs_at = (packed + 255) & ~(size_t)255;
     cudaMemcpyAsync(DP_ + offs_at, ho, offs_bytes, cudaMemcpyHostToDevice, s);
     CompactParams cpp;
@@ -1304,19 +1335,21 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
     cpp.batches = A.batches;
     cpp.entries = A.entries;
     cpp.ids = A.ids;
+    cpp.vlist = vlist_d;
     cpp.boff = (const int64_t*)(DP_ + offs_at);
-    cpp.eoff = cpp.boff + nv;
-    cpp.ioff = cpp.boff + 2 * nv;
+    cpp.eoff = cpp.boff + n;
+    cpp.ioff = cpp.boff + 2 * n;
     cpp.dst = DP_;
-    if ((e = launch_compact(cpp, nv, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    if ((e = launch_compact(cpp, n, s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     ra = arena_get(c, packed + 64);
     if (!ra) return set_err(SLOS_ERR_ALLOC, "result arena");
-    cudaMemcpyAsync(ra->p, DP_, packed, cudaMemcpyDeviceToHost, s);
+    if ((e = cudaMemcpyAsync(ra->p, DP_, packed, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     g_d2h += (int64_t)packed;
     g_h2d += (int64_t)offs_bytes;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   }
-  for (int v = 0; v < nv; ++v) {
+  for (int x = 0; x < n; ++x) {
+    const int v = vof(x);
     const int q = valid[v];
     const int k = jobs[q].k;
     const OutHdr& h = hdr[v];
@@ -1331,13 +1364,13 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
     r.n_admitted = h.n_admitted;
     r.n_declined = h.n_declined;
     r.n_deferred = 0;
-    r.admitted = (const int32_t*)(base + ioff[v]);
+    r.admitted = (const int32_t*)(base + ioff[x]);
     r.declined = r.admitted + h.n_admitted;
     r.deferred = r.declined + h.n_declined;
     r.n_batches = h.n_batches;
-    r.batches = (const slos_batch*)(base + boff[v]);
+    r.batches = (const slos_batch*)(base + boff[x]);
     r.n_entries = h.n_entries;
-    r.entries = (const slos_entry*)(base + eoff[v]);
+    r.entries = (const slos_entry*)(base + eoff[x]);
     r.exact_until_s = h.exact_until;
     r.counters.transitions = h.ctr[0];
     r.counters.gap_evals = h.ctr[1];
@@ -1347,6 +1380,56 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
     arena_addref(ra);
     r.owner_ = ra;
   }
+  return SLOS_OK;
+}
+
+// Headers back, capacity regrowth list, compaction and the D2H of the results.
+// With per-part headers (ws.part_collect, copied by ws_solve on each part's
+// stream) a part's compaction and D2H start as soon as ITS reconstruction ends,
+// under the later parts' kernels; otherwise one set over the whole workspace.
+int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry) {
+  if (!ws.uploaded || ws.nv == 0) return SLOS_OK;
+  const int nv = ws.nv;
+  cudaError_t e;
+  if (ws.part_collect) {
+    for (int p = 0; p < ws.n_parts; ++p) {
+      if ((e = cudaEventSynchronize(ws.ev_hdr[p])) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+      g_d2h += (int64_t)(sizeof(OutHdr) * (size_t)nv);
+      const int lo = ws.part_lo[p], n = ws.part_lo[p + 1] - lo;
+      const int r = collect_set(c, ws, (const OutHdr*)ws.h_hdr[p].p, ws.ord.data() + lo, ws.A.order + lo, n,
+                                ws.h_offs[p], ws.d_packp[p], ws.pstream[p], outs, retry);
+      if (r != SLOS_OK) return r;
+      if (host_timing()) {
+        if (!ws.ev_d2h[p]) cudaEventCreate(&ws.ev_d2h[p]);
+        cudaEventRecord(ws.ev_d2h[p], ws.pstream[p]);
+      }
+    }
+    for (int p = 0; p < ws.n_parts; ++p)
+      if ((e = cudaStreamSynchronize(ws.pstream[p])) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    if (host_timing()) {
+      for (int p = 0; p < ws.n_parts; ++p) {
+        float a = 0.0f, b = 0.0f, d = 0.0f;
+        cudaEventElapsedTime(&a, ws.ev[0], ws.ev_dp[p]);
+        cudaEventElapsedTime(&b, ws.ev[0], ws.ev_d2h[p]);
+        cudaEventElapsedTime(&d, ws.ev[0], ws.ev[2]);
+        std::fprintf(stderr, "[slos collect] part %d: dp end %.3f ms, d2h end %.3f ms (solve end %.3f ms)\n", p, a, b, d);
+      }
+    }
+    return SLOS_OK;
+  }
+  const Layout& Ly = ws.Ly;
+  const cudaStream_t s = ws.stream;
+  unsigned char* DO = (unsigned char*)ws.d_out.p;
+  if ((e = ws.h_small.ensure(sizeof(OutHdr) * nv)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  OutHdr* hO = (OutHdr*)ws.h_small.p;
+  cudaMemcpyAsync(hO, DO + Ly.out, sizeof(OutHdr) * nv, cudaMemcpyDeviceToHost, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  std::vector<OutHdr> hdr(hO, hO + nv);
+  g_d2h += (int64_t)(sizeof(OutHdr) * (size_t)nv);
+  if (ws.dp.phase_cycles) print_phase_debug(ws, hdr);
+  const int r = collect_set(c, ws, hdr.data(), nullptr, nullptr, nv, ws.h_offs[0], ws.d_pack, s, outs, retry);
+  if (r != SLOS_OK) return r;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   return SLOS_OK;
 }
 
@@ -1412,6 +1495,8 @@ int slos_planner_create(const slos_perf_term* terms, int32_t n_terms, const doub
     return set_err(SLOS_ERR_INVALID_PARAMETERS, "batch and chunk caps must be positive");
   if (c.max_chunk_tokens > INT32_MAX || c.max_batch_tokens > INT32_MAX)  // slos_entry is 32-bit
     return set_err(SLOS_ERR_INVALID_PARAMETERS, "batch and chunk caps must fit the 32-bit plan entries");
+  if (c.speculative && c.spec_max_len > SLOS_ENTRY_MAX_SPEC)  // 7-bit entry spec_len
+    return set_err(SLOS_ERR_INVALID_PARAMETERS, "spec_max_len must fit the plan entry format");
   if (c.plan_margin < 0) return set_err(SLOS_ERR_INVALID_PARAMETERS, "plan margin must be >= 0");
   slos_planner* p = new slos_planner();
   p->terms.assign(terms, terms + n_terms);
@@ -1467,6 +1552,14 @@ int pipeline_chunks(int n) {
   return n < 512 ? 1 : 2;  // measured on C2 x 1024: 2 chunks 125k plans/s e2e, 1 chunk 108k, 4 chunks 115k
 }
 
+bool part_collect_enabled() {  // SLOS_PART_COLLECT=0: one collection per workspace
+  static const bool on = [] {
+    const char* e = std::getenv("SLOS_PART_COLLECT");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 // full pipeline with capacity regrowth; caller holds ctx().mu
 int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, const slos_input* inputs,
              int32_t unit_value, slos_result* outs, cudaStream_t stream) {
@@ -1498,6 +1591,7 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
       if (i < K) {
         Workspace& w = pipe_ws(i & 1);
         cudaStreamWaitEvent(w.own_stream, ev0, 0);
+        w.part_collect = part_collect_enabled();
         int r = ws_upload(c, w, planners, inputs, unit_value, chunk[i], outs, w.own_stream);
         if (r == SLOS_OK) r = ws_solve(w, w.own_stream);
         if (r != SLOS_OK) {
@@ -1525,6 +1619,7 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
     retry.clear();
     if (std::getenv("SLOS_HOST_TIMING")) std::fprintf(stderr, "[slos pipeline] %d chunks, %zu retried\n", K, jobs.size());
   }
+  ws.part_collect = part_collect_enabled();
   for (int round = 0; round < 8 && !jobs.empty(); ++round) {
     retry.clear();
     int r = ws_upload(c, ws, planners, inputs, unit_value, jobs, outs, stream);

@@ -14,22 +14,23 @@ namespace slos {
 // Pack each instance's batches / entries / admitted+declined ids densely so the
 // host copies exactly the bytes of the results (one D2H).
 __global__ void __launch_bounds__(256) compact_kernel(CompactParams p) {
-  const int k = blockIdx.x;
+  const int x = blockIdx.x;
+  const int k = p.vlist ? p.vlist[x] : x;
   const InstDev& I = p.inst[k];
   const OutHdr& o = p.out[k];
   if (o.status != 0) return;
   const int64_t nb = o.n_batches, ne = o.n_entries;
-  slos_batch* db = (slos_batch*)(p.dst + p.boff[k]);
-  slos_entry* de = (slos_entry*)(p.dst + p.eoff[k]);
-  int32_t* di = (int32_t*)(p.dst + p.ioff[k]);
-  for (int64_t x = threadIdx.x; x < nb; x += blockDim.x) db[x] = p.batches[I.off_batch + x];
-  // entries: 16 B each, copied as 16-byte words
-  const uint4* se = (const uint4*)(p.entries + I.off_entry);
-  uint4* dw = (uint4*)de;
-  for (int64_t x = threadIdx.x; x < ne; x += blockDim.x) dw[x] = se[x];
+  slos_batch* db = (slos_batch*)(p.dst + p.boff[x]);
+  slos_entry* de = (slos_entry*)(p.dst + p.eoff[x]);
+  int32_t* di = (int32_t*)(p.dst + p.ioff[x]);
+  for (int64_t y = threadIdx.x; y < nb; y += blockDim.x) db[y] = p.batches[I.off_batch + y];
+  // entries: 8 B each, copied as 8-byte words
+  const uint2* se = (const uint2*)(p.entries + I.off_entry);
+  uint2* dw = (uint2*)de;
+  for (int64_t y = threadIdx.x; y < ne; y += blockDim.x) dw[y] = se[y];
   const int32_t* ids = p.ids + I.off_ids;
-  for (int x = threadIdx.x; x < o.n_admitted; x += blockDim.x) di[x] = ids[x];
-  for (int x = threadIdx.x; x < o.n_declined; x += blockDim.x) di[o.n_admitted + x] = ids[I.n_pending + x];
+  for (int y = threadIdx.x; y < o.n_admitted; y += blockDim.x) di[y] = ids[y];
+  for (int y = threadIdx.x; y < o.n_declined; y += blockDim.x) di[o.n_admitted + y] = ids[I.n_pending + y];
 }
 
 // dynamic shared memory of dp_kernel (must mirror the carve-up in dp_kernel)

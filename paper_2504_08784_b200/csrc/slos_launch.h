@@ -18,7 +18,8 @@ struct CompactParams {
   const slos_batch* batches;
   const slos_entry* entries;
   const int32_t* ids;
-  const int64_t* boff;  // byte offsets into dst
+  const int32_t* vlist;  // position -> instance (nullptr: identity)
+  const int64_t* boff;  // byte offsets into dst, per position
   const int64_t* eoff;
   const int64_t* ioff;
   unsigned char* dst;

@@ -443,8 +443,7 @@ def _convert(inp: ScheduleInput, r: abi.Result) -> ScheduleResult:
                        int(cb.prefill_budget_left))
         for e in range(cb.first_entry, cb.first_entry + cb.n_entries):
             ce = r.entries[e]
-            pb.entries.append(PlanEntry(rid(ce.req), int(ce.prefill_tokens),
-                                        int(ce.decode_tokens), int(ce.spec_len)))
+            pb.entries.append(PlanEntry(rid(ce.req), ce.prefill_tokens, ce.decode_tokens, ce.spec_len))
         out.plan.batches.append(pb)
     c = r.counters
     out.counters = dict(transitions=c.transitions, gap_evals=c.gap_evals, dues=c.dues,

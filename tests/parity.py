@@ -36,9 +36,7 @@ def canon_c(r: abi.Result) -> dict:
     ent = np.zeros(ne, abi.CANON_ENTRY_DTYPE)
     if ne:
         eb = np.ctypeslib.as_array(C.cast(r.entries, C.POINTER(C.c_uint8)), (ne * C.sizeof(abi.Entry),))
-        w = eb.view(abi.ENTRY_DTYPE)
-        for f in ("req", "spec_len", "prefill_tokens", "decode_tokens"):
-            ent[f] = w[f]
+        ent = abi.canon_entries(eb.view(abi.ENTRY_DTYPE))
     d["entries"] = ent
     d["counters"] = (r.counters.transitions, r.counters.gap_evals, r.counters.dues,
                      r.counters.slots, r.counters.states)

@@ -15,7 +15,8 @@ HEADER = os.path.join(abi.ROOT, "include", "slos_planner.h")
 
 
 def declared():
-    src = open(HEADER).read()
+    # header-only inline accessors (SLOS_ENTRY_FN) are not exported symbols
+    src = "\n".join(l for l in open(HEADER).read().splitlines() if not l.startswith("SLOS_ENTRY_FN") and "return " not in l)
     return sorted(set(re.findall(r"^[a-z_ ]*?[\w\*]+\s+\**(slos_\w+)\(", src, re.M)))
 
 
