@@ -1393,7 +1393,11 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         if (acc) Cfl[c] |= 2;
       }
       __syncthreads();
-      for (int c = tid; c < T; c += kDpThreads) {
+      // pruned marks (bit 4) are held back until every thread has read the accepted
+      // marks (bit 2) of its bucket: no thread writes a flag word another reads
+      uint32_t pm = 0;
+      int it = 0;
+      for (int c = tid; c < T; c += kDpThreads, ++it) {
         if (!(Cfl[c] & 2)) continue;
         const int b = Cbk[c];
         if (cntB[b] <= 32) continue;
@@ -1404,9 +1408,16 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         for (int q = 0; q < n; ++q) {
           const int y = lst[q];
           if (y <= c || !(Cfl[y] & 2)) continue;
-          if (Cvl[y] >= xv && Cmm[y] <= xm && Cpb[y] >= xp) { Cfl[c] |= 4; break; }
+          if (Cvl[y] >= xv && Cmm[y] <= xm && Cpb[y] >= xp) {
+            if (it < 32) pm |= 1u << it;
+            else Cfl[c] |= 4;  // levels beyond 32 x kDpThreads (HBM arrays): bit 2 is never cleared
+            break;
+          }
         }
       }
+      __syncthreads();
+      for (int k = 0; pm; ++k, pm >>= 1)
+        if (pm & 1u) Cfl[tid + k * kDpThreads] |= 4;
       }
     }
     if (fastB) {
