@@ -1573,11 +1573,12 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
     static cudaEvent_t ev0 = nullptr;
     if (!ev0) cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
     cudaEventRecord(ev0, stream ? stream : c.stream);
-    // chunk boundaries: with 2 chunks the first is larger (SLOS_PIPELINE_SPLIT, its
-    // D2H hides under the second's kernels; only the last chunk's D2H is exposed)
+    // chunk boundaries: with 2 chunks the first is the smaller (SLOS_PIPELINE_SPLIT):
+    // the GPU starts after a short host preparation, the second chunk's preparation
+    // overlaps the first's kernels, and both chunks' kernels then share the SMs
     static const double split = [] {
       const char* e = std::getenv("SLOS_PIPELINE_SPLIT");
-      return e ? std::atof(e) : 0.5;
+      return e ? std::atof(e) : 0.3;  // measured C2 x 1024: 0.3 -> 4.5 ms, 0.5 -> 4.9 ms, 0.7 -> 5.2 ms
     }();
     std::vector<std::vector<Job>> chunk(K);
     for (int k = 0; k < n; ++k) {
