@@ -26,6 +26,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "slos_plan_json.h"
 #include "slos_planner.h"
 #include "slosim/batch_planner.hpp"
 #include "slosim/common.hpp"
@@ -502,3 +503,64 @@ const char* slos_last_error(void) { return g_last_error.c_str(); }
 const char* slos_backend(void) { return "reference-cpp"; }
 
 }  // extern "C"
+
+// plan_to_json parity (include/slos_plan_json.h): the slos_result is turned back into
+// the reference's ScheduleResult and serialised by the reference's own plan_to_json
+// (dp_scheduler.cpp:560-589).
+extern "C" int slos_plan_to_json(const slos_input* in, const slos_result* r, double now_s, char* buf, int64_t cap,
+                                 int64_t* len) {
+  if (len) *len = 0;
+  if (!in || !r) return SLOS_ERR_INVALID_PARAMETERS;
+  std::string text;
+  const int st = guarded([&] {
+    auto pid = [&](int32_t k) -> std::string {
+      if (k < 0 || k >= in->n_pending) fail("invalid-parameters", "pending index out of range");
+      return in->pending[k].id ? in->pending[k].id : "";
+    };
+    ScheduleResult res;
+    for (int k = 0; k < r->n_admitted; ++k) res.admitted.push_back(pid(r->admitted[k]));
+    for (int k = 0; k < r->n_declined; ++k) res.declined.push_back(pid(r->declined[k]));
+    for (int k = 0; k < r->n_deferred; ++k) res.deferred.push_back(pid(r->deferred[k]));
+    res.admitted_value = r->admitted_value;
+    res.running_set_infeasible = r->running_set_infeasible != 0;
+    res.plan.exact_until_s = r->exact_until_s;
+    for (int64_t b = 0; b < r->n_batches; ++b) {
+      const slos_batch& cb = r->batches[b];
+      PlanBatch pb;
+      pb.start_s = cb.start_s;
+      pb.end_s = cb.end_s;
+      pb.capacity_tokens = cb.capacity_tokens;
+      pb.spec_step = cb.spec_step;
+      pb.prefill_budget_left = cb.prefill_budget_left;
+      if (cb.first_entry < 0 || cb.n_entries < 0 || cb.first_entry + cb.n_entries > r->n_entries)
+        fail("invalid-parameters", "batch entry range out of range");
+      for (int64_t e = cb.first_entry; e < cb.first_entry + cb.n_entries; ++e) {
+        const slos_entry* ce = &r->entries[e];
+        const int32_t ref = slos_entry_req(ce);
+        PlanEntry pe;
+        if (ref >= 0 && ref < in->n_running) pe.id = in->running[ref].id ? in->running[ref].id : "";
+        else if (ref < 0 && -ref - 1 < in->n_pending) pe.id = pid(-ref - 1);
+        else fail("invalid-parameters", "entry reference out of range");
+        pe.prefill_tokens = slos_entry_prefill_tokens(ce);
+        pe.decode_tokens = slos_entry_decode_tokens(ce);
+        pe.spec_len = slos_entry_spec_len(ce);
+        pb.entries.push_back(std::move(pe));
+      }
+      res.plan.batches.push_back(std::move(pb));
+    }
+    try {
+      text = plan_to_json(res, now_s);
+    } catch (const std::exception& e) {  // nlohmann: ill-formed UTF-8 in an id
+      fail("invalid-parameters", e.what());
+    }
+    return SLOS_OK;
+  });
+  if (st != SLOS_OK) return st;
+  if (len) *len = (int64_t)text.size();
+  if (buf && cap > 0) {
+    const size_t m = (size_t)cap > text.size() ? text.size() : (size_t)cap;
+    std::memcpy(buf, text.data(), m);
+    if ((size_t)cap > text.size()) buf[text.size()] = '\0';
+  }
+  return SLOS_OK;
+}

@@ -39,7 +39,8 @@ def _stale(target, sources):
 
 def build_product(force: bool = False, verbose: bool = False) -> str:
     out = os.path.join(PKG, "libslos_b200.so")
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "slos_planner.h")]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
+        os.path.join(ROOT, "include", h) for h in ("slos_planner.h", "slos_plan_json.h")]
     if not force and not _stale(out, deps):
         return out
     bdir = os.path.join(PKG, "build")
@@ -50,7 +51,9 @@ def build_product(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(k.stderr)
     _run([NVCC, *ARCH, *NVFLAGS, "-x", "cu", "-c", os.path.join(CSRC, "slos_host.cpp"), "-o", ho])
-    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xlinker", "-Bsymbolic", ko, ho, "-o", out,
+    jo = os.path.join(bdir, "slos_json.o")  # host-only: plan_to_json serialisation
+    _run(["g++", "-std=c++17", "-O2", "-fPIC", "-c", os.path.join(CSRC, "slos_json.cpp"), "-o", jo])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xlinker", "-Bsymbolic", ko, ho, jo, "-o", out,
           "-lpthread", "-ldl", "-lrt"])
     return out
 

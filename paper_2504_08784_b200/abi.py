@@ -401,7 +401,26 @@ def _bind(lib: C.CDLL) -> C.CDLL:
     lib.slos_workspace_stage_ms.restype = C.c_int
     lib.slos_last_transfer_bytes.argtypes = [P(C.c_int64), P(C.c_int64)]
     lib.slos_last_transfer_bytes.restype = None
+    if hasattr(lib, "slos_plan_to_json"):  # include/slos_plan_json.h (product, reference)
+        lib.slos_plan_to_json.argtypes = [C.c_void_p, P(Result), C.c_double, C.c_char_p, C.c_int64,
+                                          P(C.c_int64)]
+        lib.slos_plan_to_json.restype = C.c_int
     return lib
+
+
+def plan_to_json(lib: C.CDLL, inp, res, now_s: float) -> str:
+    """include/slos_plan_json.h: plan_to_json(result, now) (dp_scheduler.cpp:560-589)
+    of `res` (a Result, or a pointer to one) for the input at `inp` (an address)."""
+    rp = res if isinstance(res, C._Pointer) else C.byref(res)
+    n = C.c_int64()
+    st = lib.slos_plan_to_json(C.c_void_p(inp), rp, now_s, None, 0, C.byref(n))
+    if st != SLOS_OK:
+        raise RuntimeError(f"slos_plan_to_json: {lib.slos_status_slug(st).decode()}")
+    buf = C.create_string_buffer(n.value + 1)
+    st = lib.slos_plan_to_json(C.c_void_p(inp), rp, now_s, buf, n.value + 1, C.byref(n))
+    if st != SLOS_OK:
+        raise RuntimeError(f"slos_plan_to_json: {lib.slos_status_slug(st).decode()}")
+    return buf.raw[:n.value].decode()
 
 
 def load(path: str) -> C.CDLL:
