@@ -261,6 +261,8 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
     if (!prefills && !decodes) break;
     const bool dec_branch = decodes;
     const int64_t e0 = ne;
+    int64_t pre_before = 0, pre_tot = 0;
+    bool have_pre = false;
     int64_t free, dtok = 0, cap = 0;
     if (dec_branch) {
       const double slot_end = t + t0;
@@ -307,9 +309,13 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
         if (dleft[k] > 0) still = 1;
       }
       }
-      // one scan for entry positions, the batch's decode tokens and "still decoding"
-      int64_t mv[3] = {(int64_t)cnt, tok, (int64_t)still}, mex[3], mtot[3];
-      G::template mscan<3>(sh.bs, mv, mex, mtot, par);
+      // one scan for entry positions, the batch's decode tokens, "still decoding" and
+      // the prefill EDF prefix (pending prefill before this lane's range)
+      int64_t mv[4] = {(int64_t)cnt, tok, (int64_t)still, lsum}, mex[4], mtot[4];
+      G::template mscan<4>(sh.bs, mv, mex, mtot, par);
+      pre_before = mex[3];
+      pre_tot = mtot[3];
+      have_pre = true;
       int64_t pos = e0 + mex[0];
       if (regs) {
 #pragma unroll
@@ -347,9 +353,13 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
     // EDF prefill in order: take_k = min(left_k, max(0, free - sum_{k'<k} left_k'))
     int64_t spent = 0;
     if (prefills) {
-      int64_t pv[1] = {lsum}, pex[1], ptot[1];
-      G::template mscan<1>(sh.bs, pv, pex, ptot, par);
-      const int64_t before = pex[0], tot0 = ptot[0];
+      if (!have_pre) {
+        int64_t pv[1] = {lsum}, pex[1], ptot[1];
+        G::template mscan<1>(sh.bs, pv, pex, ptot, par);
+        pre_before = pex[0];
+        pre_tot = ptot[0];
+      }
+      const int64_t before = pre_before, tot0 = pre_tot;
       int cnt = 0;
       int64_t run = before, mine = 0;
       for (int k = p0; k < p1; ++k) {
