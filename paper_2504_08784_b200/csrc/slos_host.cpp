@@ -150,22 +150,34 @@ class HostPool {
     static HostPool* p = new HostPool();
     return *p;
   }
-  // fn(lo, hi) over contiguous ranges of [0, n); runs inline for small n.
+  // fn(lo, hi) over contiguous ranges of [0, n); runs inline for small n. Workers
+  // spin for a short while after each job before sleeping, so the back-to-back
+  // jobs of one upload do not pay a thread wake-up each.
   void run(int n, const std::function<void(int, int)>& fn) {
     const int T = (int)workers_.size() + 1;
     if (n < 64 || T == 1) { fn(0, n); return; }
+    fn_ = &fn;
+    n_ = n;
+    next_.store(0, std::memory_order_relaxed);
+    // chunks: ~8 per thread, at least 16 items (one shared counter: small chunks of
+    // cheap items would serialise on it)
+    grain_ = std::max(16, n / (8 * T));
+    busy_.store((int)workers_.size(), std::memory_order_relaxed);
     {
-      std::unique_lock<std::mutex> l(mu_);
-      fn_ = &fn;
-      n_ = n;
-      next_ = 0;
-      busy_ = (int)workers_.size();
-      ++gen_;
+      std::lock_guard<std::mutex> l(mu_);
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     work();
-    std::unique_lock<std::mutex> l(mu_);
-    done_.wait(l, [&] { return busy_ == 0; });
+    // wait for the workers (spinning: they are normally already awake)
+    const auto t0 = std::chrono::steady_clock::now();
+    while (busy_.load(std::memory_order_acquire) != 0) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200)) {
+        std::unique_lock<std::mutex> l(mu_);
+        done_.wait(l, [&] { return busy_.load(std::memory_order_acquire) == 0; });
+        break;
+      }
+    }
     fn_ = nullptr;
   }
 
@@ -177,7 +189,7 @@ class HostPool {
     for (auto& w : workers_) w.detach();
   }
   void work() {
-    const int grain = 16;
+    const int grain = grain_;
     for (;;) {
       const int lo = next_.fetch_add(grain);
       if (lo >= n_) break;
@@ -187,23 +199,33 @@ class HostPool {
   void loop() {
     uint64_t seen = 0;
     for (;;) {
-      {
+      // a new job: spin ~0.5 ms first, then sleep on the condition variable
+      const auto t0 = std::chrono::steady_clock::now();
+      uint64_t g = gen_.load(std::memory_order_acquire);
+      while (g == seen && std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(500))
+        g = gen_.load(std::memory_order_acquire);
+      if (g == seen) {
         std::unique_lock<std::mutex> l(mu_);
-        cv_.wait(l, [&] { return gen_ != seen; });
-        seen = gen_;
+        cv_.wait(l, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+        g = gen_.load(std::memory_order_acquire);
       }
+      seen = g;
       work();
-      std::lock_guard<std::mutex> l(mu_);
-      if (--busy_ == 0) done_.notify_all();
+      if (busy_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+        std::lock_guard<std::mutex> l(mu_);
+        done_.notify_all();
+      }
     }
   }
   std::vector<std::thread> workers_;
+  int grain_ = 16;
   std::mutex mu_;
   std::condition_variable cv_, done_;
   const std::function<void(int, int)>* fn_ = nullptr;
   std::atomic<int> next_{0};
-  int n_ = 0, busy_ = 0;
-  uint64_t gen_ = 0;
+  int n_ = 0;
+  std::atomic<int> busy_{0};
+  std::atomic<uint64_t> gen_{0};
 };
 
 int ensure_device(Ctx& c) {
@@ -287,7 +309,6 @@ void arena_release(ResultArena* a) {
   }
 }
 
-void arena_addref(ResultArena* a) { ++a->refs; }
 
 // ------------------------------------------------------------ blob layout ---
 
@@ -370,6 +391,14 @@ struct ChainKey {
 };
 
 int prep_instance(const slos_planner* P, const slos_input* in, int unit_value, Prep& pr) {
+  // Prep objects are reused across calls (their vectors keep their capacity)
+  pr.planner = 0;
+  pr.N = pr.n_dec = pr.n_pre = 0;
+  pr.last_forced = -1;
+  pr.have_rd = false;
+  pr.values_integral = true;
+  pr.span = pr.tail_bound = 0.0;
+  pr.max_rem = 0;
   const int L = P->L;
   if (L > 8) return set_err(SLOS_ERR_INVALID_PARAMETERS, "at most 8 SLO tiers supported");
   if (in->n_running >= SLOS_ENTRY_MAX_REQS || in->n_pending >= SLOS_ENTRY_MAX_REQS)  // 24-bit entry refs
@@ -415,7 +444,8 @@ int prep_instance(const slos_planner* P, const slos_input* in, int unit_value, P
   }
   pr.span = std::max(0.0, maxdl - mindl);
   struct PreKey { int idx; double ddl; const char* id; };
-  std::vector<PreKey> pre;
+  thread_local std::vector<PreKey> pre;  // capacity kept across calls
+  pre.clear();
   double tb = 0.0;
   for (int i = 0; i < in->n_running; ++i) {
     const slos_running& r = in->running[i];
@@ -571,6 +601,7 @@ struct Workspace {
   PinBuf h_hdr[kMaxParts], h_offs[kMaxParts];
   DevBuf d_packp[kMaxParts];
   cudaEvent_t ev_hdr[kMaxParts] = {nullptr}, ev_d2h[kMaxParts] = {nullptr};
+  std::vector<Prep> prep;  // host preparation, reused across uploads
 };
 
 thread_local int64_t g_h2d = 0, g_d2h = 0;
@@ -595,11 +626,14 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   const int n = (int)jobs.size();
   if (n == 0) return SLOS_OK;
   // ---- host preparation ----
-  std::vector<Prep> prep(n);
+  std::vector<Prep>& prep = ws.prep;  // reused: no per-instance heap traffic per call
+  if (prep.size() < (size_t)n) prep.resize((size_t)n);
   std::vector<const slos_planner*> plist;
   std::vector<int> valid;
   int64_t TD = 0, TC = 0, TP = 0, TR = 0, TS = 0, TCd = 0, TM = 0, TW = 0, TSel = 0, TIds = 0, TB = 0, TE = 0;
-  std::vector<Caps> caps(n);
+  thread_local std::vector<Caps> caps_tl;  // lambdas below see it through the reference
+  std::vector<Caps>& caps = caps_tl;  // per-call scratch kept across calls: large fresh
+  caps.resize((size_t)n);                // vectors would page-fault on every call
   int maxN = 0, maxDec = 0, Lmax = 1;
   double S_need = 16;
   const auto t_a = std::chrono::steady_clock::now();
@@ -647,11 +681,17 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   if (nv == 0) return SLOS_OK;
   const int Sc = (int)std::min<double>(S_need, 1 << 20);
   int64_t TA = 0;
-  std::vector<int64_t> astride(n, 0);
-  for (int q : valid) {
-    astride[q] = (int64_t)dp_anchor_stride(prep[q].n_dec, Sc, Lmax, prep[q].N);
-    TA += astride[q] * (prep[q].N + 1);
-  }
+  thread_local std::vector<int64_t> astride_tl;  // lambdas below see it through the reference
+  std::vector<int64_t>& astride = astride_tl;
+  astride.resize((size_t)n);
+  HostPool::get().run((int)valid.size(), [&](int lo, int hi) {
+    for (int x = lo; x < hi; ++x) {
+      const int q = valid[x];
+      astride[q] = (int64_t)dp_anchor_stride(prep[q].n_dec, Sc, Lmax, prep[q].N);
+    }
+  });
+  for (int q : valid) TA += astride[q] * (prep[q].N + 1);
+  const auto t_b1 = std::chrono::steady_clock::now();
   Layout& Ly = ws.Ly;
   Blob bi;
   Ly.planners = bi.add<PlannerDev>(plist.size());
@@ -727,11 +767,13 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.entries = bo.add<slos_entry>(TE);
   Ly.out_bytes = bo.bytes;
 
+  const auto t_b2 = std::chrono::steady_clock::now();
   cudaError_t e;
   if ((e = ws.h_in.ensure(Ly.in_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   if ((e = ws.d_in.ensure(Ly.in_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   if ((e = ws.d_scr.ensure(Ly.scr_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   if ((e = ws.d_out.ensure(Ly.out_bytes)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  const auto t_b3 = std::chrono::steady_clock::now();
   unsigned char* H = (unsigned char*)ws.h_in.p;
   auto hp = [&](size_t off) { return H + off; };
   PlannerDev* hP = (PlannerDev*)hp(Ly.planners);
@@ -756,32 +798,51 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   int32_t* h_run_tier = (int32_t*)hp(Ly.run_tier);
   int n_small = 0;
   uint8_t* h_pair = (uint8_t*)hp(Ly.pair);
-  std::vector<double> cost(nv);
+  thread_local std::vector<double> cost_tl;  // lambdas below see it through the reference
+  std::vector<double>& cost = cost_tl;
+  thread_local std::vector<uint8_t> kind_v_tl;  // lambdas below see it through the reference
+  std::vector<uint8_t>& kind_v = kind_v_tl;  // compact copies for the serial ordering passes
+  thread_local std::vector<int32_t> N_v_tl;  // lambdas below see it through the reference
+  std::vector<int32_t>& N_v = N_v_tl;
+  cost.resize((size_t)nv);
+  kind_v.resize((size_t)nv);
+  N_v.resize((size_t)nv);
   struct Off { int64_t D, C, P, R, S, Cd, M, W, Sel, Ids, B, E, A, Pair; };
-  std::vector<Off> offs(nv);
+  thread_local std::vector<Off> offs_tl;  // lambdas below see it through the reference
+  std::vector<Off>& offs = offs_tl;
+  offs.resize((size_t)nv);
   {
+    // per-instance sizes in parallel (the inputs are scattered), then one compact
+    // serial exclusive scan
+    HostPool::get().run(nv, [&](int lo, int hi) {
+      for (int v = lo; v < hi; ++v) {
+        const int q = valid[v];
+        const Prep& pr = prep[q];
+        const Caps& cp = caps[q];
+        const slos_input* in = &inputs[jobs[q].k];
+        Off& o = offs[v];
+        o.D = pr.n_dec;
+        o.C = pr.N + 1;
+        o.P = pr.n_pre;
+        o.R = in->n_running;
+        o.S = cp.surv;
+        o.Cd = cp.cand;
+        o.M = cp.memo;
+        o.W = (cp.work + 255) & ~(int64_t)255;
+        o.Sel = pr.N + 1;
+        o.Ids = 2 * (int64_t)in->n_pending + 1;
+        o.B = cp.batch;
+        o.E = cp.entry;
+        o.A = astride[q] * (pr.N + 1);
+        o.Pair = (int64_t)pr.N * (pr.N + 1) / 2;
+      }
+    });
     Off o{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int v = 0; v < nv; ++v) {
-      const int q = valid[v];
-      const Prep& pr = prep[q];
-      const Caps& cp = caps[q];
-      const slos_input* in = &inputs[jobs[q].k];
+      const Off x = offs[v];
       offs[v] = o;
-      o.D += pr.n_dec;
-      o.C += pr.N + 1;
-      o.P += pr.n_pre;
-      o.R += in->n_running;
-      o.S += cp.surv;
-      o.Cd += cp.cand;
-      o.M += cp.memo;
-      o.W += (cp.work + 255) & ~(int64_t)255;
-      o.Sel += pr.N + 1;
-      o.Ids += 2 * (int64_t)in->n_pending + 1;
-      o.B += cp.batch;
-      o.E += cp.entry;
-      o.A += astride[q] * (pr.N + 1);
-      o.Pair += (int64_t)pr.N * (pr.N + 1) / 2;
-      n_small += pr.n_dec <= build_warp_max_dec() ? 1 : 0;  // (informational)
+      o.D += x.D; o.C += x.C; o.P += x.P; o.R += x.R; o.S += x.S; o.Cd += x.Cd; o.M += x.M;
+      o.W += x.W; o.Sel += x.Sel; o.Ids += x.Ids; o.B += x.B; o.E += x.E; o.A += x.A; o.Pair += x.Pair;
     }
   }
   const auto t_c = std::chrono::steady_clock::now();
@@ -811,6 +872,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     I.have_running_decode = pr.have_rd ? 1 : 0;
     I.values_integral = pr.values_integral ? 1 : 0;
     I.build_kind = pr.n_dec <= build_warp_max_dec() ? 0 : (pr.n_dec < build_big_min_dec() ? 1 : 2);
+    kind_v[v] = (uint8_t)I.build_kind;
+    N_v[v] = pr.N;
     {  // direct bucket table when the count-vector space is small
       int64_t maxc[kMaxTiers] = {0};
       for (int x = 0; x < pr.N; ++x) {
@@ -931,14 +994,18 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   {
     // launch order, heaviest first (load balance only: results do not depend on it).
     // Large batches bucket by log2(cost) instead of sorting (O(n), stable).
-    std::vector<int> ord(nv);
+    thread_local std::vector<int32_t> ord_tl;  // lambdas below see it through the reference
+    std::vector<int32_t>& ord = ord_tl;
+    ord.resize((size_t)nv);
     if (nv <= 4096) {
       for (int v = 0; v < nv; ++v) ord[v] = v;
       std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
     } else {
       constexpr int kB = 64;
       int cnt[kB + 1] = {0};
-      std::vector<uint8_t> key(nv);
+      thread_local std::vector<uint8_t> key_tl;
+      std::vector<uint8_t>& key = key_tl;
+      key.resize((size_t)nv);
       for (int v = 0; v < nv; ++v) {
         const int e = std::min(kB - 1, std::max(0, std::ilogb(std::max(1.0, cost[v]))));
         key[v] = (uint8_t)(kB - 1 - e);
@@ -947,7 +1014,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       for (int b = 0; b < kB; ++b) cnt[b + 1] += cnt[b];
       for (int v = 0; v < nv; ++v) ord[cnt[key[v]]++] = v;
     }
-    for (int v = 0; v < nv; ++v) h_order[v] = ord[v];
+    std::memcpy(h_order, ord.data(), sizeof(int32_t) * (size_t)nv);
     ws.ord.assign(ord.begin(), ord.end());
     // solve parts: contiguous ranges of the cost-descending order (every part gets
     // a share of the heavy instances); each part's DP and reconstruction are
@@ -958,11 +1025,14 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     int qcount[kQueues] = {0};
     for (int p = 0; p <= P; ++p) ws.part_lo[p] = (int)((int64_t)p * nv / P);
     for (int p = 0; p < P; ++p)
-      for (int x = ws.part_lo[p]; x < ws.part_lo[p + 1]; ++x) {
-        InstDev& I = hI[ord[x]];
-        I.part = p;
-        ++qcount[kBuildKinds * p + I.build_kind];
+      for (int x = ws.part_lo[p]; x < ws.part_lo[p + 1]; ++x) ++qcount[kBuildKinds * p + kind_v[ord[x]]];
+    HostPool::get().run(nv, [&](int lo, int hi) {
+      int p = 0;
+      for (int x = lo; x < hi; ++x) {
+        while (x >= ws.part_lo[p + 1]) ++p;
+        hI[ord[x]].part = p;
       }
+    });
     int qb = 2 * kQueues;  // the counters come first
     for (int q = 0; q < kQueues; ++q) {
       ws.qbase[q] = qb;
@@ -972,23 +1042,29 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     // anchor tasks (instance, anchor j), j = -1 .. N-2, grouped by solve part so each
     // part's anchor/group kernels run on its own stream ahead of its DP
     int32_t* t = (int32_t*)hp(Ly.atask);
-    int64_t x = 0;
-    for (int p = 0; p < P; ++p) {
-      ws.atask_lo[p] = (int)x;
-      for (int y = ws.part_lo[p]; y < ws.part_lo[p + 1]; ++y) {
+    thread_local std::vector<int64_t> aoff_tl;  // lambdas below see it through the reference
+    std::vector<int64_t>& aoff = aoff_tl;  // first task of the instance at order position y
+    aoff.resize((size_t)nv + 1);
+    aoff[0] = 0;
+    for (int y = 0; y < nv; ++y) aoff[y + 1] = aoff[y] + N_v[ord[y]];
+    for (int p = 0; p <= P; ++p) ws.atask_lo[p] = (int)aoff[ws.part_lo[p]];
+    HostPool::get().run(nv, [&](int lo, int hi) {
+      for (int y = lo; y < hi; ++y) {
         const int v = ord[y];
-        for (int j = -1; j < prep[valid[v]].N - 1; ++j) { t[2 * x] = v; t[2 * x + 1] = j; ++x; }
+        int64_t x = aoff[y];
+        for (int j = -1; j < N_v[v] - 1; ++j, ++x) { t[2 * x] = v; t[2 * x + 1] = j; }
       }
-    }
-    ws.atask_lo[P] = (int)x;
-    Ly.n_atask = x;
+    });
+    Ly.n_atask = aoff[nv];
   }
   {
     slos_record* rd = (slos_record*)hp(Ly.recdef);
-    std::memset(rd, 0, sizeof(slos_record) * (size_t)n);
-    for (int q = 0; q < n; ++q) rd[q].status = prep[q].status;
+    HostPool::get().run(n, [&](int lo, int hi) {
+      std::memset(rd + lo, 0, sizeof(slos_record) * (size_t)(hi - lo));
+      for (int q = lo; q < hi; ++q) rd[q].status = prep[q].status;
+    });
     int32_t* rm = (int32_t*)hp(Ly.recmap);
-    for (int v = 0; v < nv; ++v) rm[v] = valid[v];
+    std::memcpy(rm, valid.data(), sizeof(int32_t) * (size_t)nv);
   }
   const auto t_e = std::chrono::steady_clock::now();
   ws.n_total = n;
@@ -1004,8 +1080,9 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     auto ms = [](std::chrono::steady_clock::time_point x, std::chrono::steady_clock::time_point y) {
       return std::chrono::duration<double, std::milli>(y - x).count();
     };
-    std::fprintf(stderr, "[slos upload] n %d: prep %.3f, totals %.3f, layout %.3f, fill %.3f, order/parts %.3f, h2d %.3f ms\n",
-                 n, ms(t_a, t_b), 0.0, ms(t_b, t_c), ms(t_c, t_d), ms(t_d, t_e), ms(t_e, t_f));
+    std::fprintf(stderr, "[slos upload] n %d: prep %.3f, totals %.3f, layout %.3f (strides %.3f blobs %.3f ensure %.3f), fill %.3f, order/parts %.3f, h2d %.3f ms\n",
+                 n, ms(t_a, t_b), 0.0, ms(t_b, t_c), ms(t_b, t_b1), ms(t_b1, t_b2), ms(t_b2, t_b3), ms(t_c, t_d),
+                 ms(t_d, t_e), ms(t_e, t_f));
   }
   Ly.memo_bytes = sizeof(MemoEnt) * (size_t)TM;
   Ly.bkey_bytes = sizeof(uint64_t) * 2 * (size_t)TCd;
@@ -1294,7 +1371,13 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
   const BatchArgs& A = ws.A;
   cudaError_t e;
   auto vof = [&](int x) { return vlist_h ? vlist_h[x] : x; };
-  std::vector<int64_t> boff(n, 0), eoff(n, 0), ioff(n, 0);
+  thread_local std::vector<int64_t> boff_tl, eoff_tl, ioff_tl;  // kept across calls (no page faults)
+  std::vector<int64_t>& boff = boff_tl;  // the pool's lambdas see them through these references
+  std::vector<int64_t>& eoff = eoff_tl;
+  std::vector<int64_t>& ioff = ioff_tl;
+  boff.assign((size_t)n, 0);
+  eoff.assign((size_t)n, 0);
+  ioff.assign((size_t)n, 0);
   size_t packed = 0;
   int good = 0;
   for (int x = 0; x < n; ++x) {
@@ -1348,7 +1431,9 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
     g_d2h += (int64_t)packed;
     g_h2d += (int64_t)offs_bytes;
   }
-  for (int x = 0; x < n; ++x) {
+  if (ra) ra->refs += good;  // one reference per result that points into the arena
+  HostPool::get().run(n, [&](int lo, int hi) {
+  for (int x = lo; x < hi; ++x) {
     const int v = vof(x);
     const int q = valid[v];
     const int k = jobs[q].k;
@@ -1377,9 +1462,9 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
     r.counters.dues = h.ctr[2];
     r.counters.slots = h.ctr[3];
     r.counters.states = h.ctr[4];
-    arena_addref(ra);
     r.owner_ = ra;
   }
+  });
   return SLOS_OK;
 }
 
