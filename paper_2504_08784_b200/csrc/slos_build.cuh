@@ -257,8 +257,135 @@ __device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, A
     rd[q] = 0;
     ri[q] = in ? didx[k] : 0;
   }
+  bool tail_try = true;
   for (int guard = 0; guard < 100000; ++guard) {
     if (!prefills && !decodes) break;
+    if (!prefills && tail_try) {
+      tail_try = false;
+      // ---- the decode-only tail in closed time (dp_scheduler.cpp:138-169 with no
+      // prefill left). While every batch lasts exactly t0 (predict(decode tokens) <=
+      // t0), batch k starts at t + t0 + ... + t0 (the sequential loop's own additions),
+      // so each decoder's dues per batch follow from its own state alone: decoders in
+      // parallel over all batches, then batches in parallel for the totals, entry
+      // positions and records. A batch that would outlast t0 (or no room for the due
+      // matrix) voids the attempt and the sequential loop below runs unchanged. ----
+      if (cap_t0 == -2) cap_t0 = plan_time2bs(P, t0, 0);
+      auto st_get = [&](int k, int q, double& n_, double& tp_, int64_t& b_, int64_t& l_) {
+        if (regs) {  // constant register indices (a runtime index would demote them to local memory)
+#pragma unroll
+          for (int qq = 0; qq < kR; ++qq)
+            if (qq == q) { n_ = rn[qq]; tp_ = rt[qq]; b_ = rb[qq]; l_ = rl[qq]; }
+        } else {
+          n_ = dnext[k]; tp_ = dtp[k]; b_ = dbl[k]; l_ = dleft[k];
+        }
+      };
+      // the per-batch dues of one decoder, batch by batch (exactly the sequential step)
+      auto step = [&](double tt, double& n_, double tp_, int64_t& b_, int64_t& l_) -> int64_t {
+        if (l_ <= 0) return 0;
+        int64_t due = imin(b_, l_);
+        b_ -= due;
+        const double slot_end = tt + t0;
+        while (l_ - due > 0 && time_le(n_, slot_end)) { ++due; n_ += tp_; }
+        if (due > 0) l_ -= due;
+        return due;
+      };
+      const int64_t left_guard = 100000 - guard;
+      int64_t klast = -1;  // last batch with a due, over this lane's decoders
+#pragma unroll 1
+      for (int k = d0; k < d1; ++k) {
+        double n_, tp_;
+        int64_t b_, l_;
+        st_get(k, k - d0, n_, tp_, b_, l_);
+        double tt = t;
+        for (int64_t kb = 0; l_ > 0 && kb <= left_guard; ++kb) {
+          step(tt, n_, tp_, b_, l_);
+          if (l_ <= 0) klast = kb > klast ? kb : klast;
+          tt = tt + t0;
+        }
+        if (l_ > 0) klast = left_guard + 1;  // never finishes inside the guard
+      }
+      const int64_t K = (int64_t)(-G::min(sh.bs, -(double)klast)) + 1;
+      Arena a2 = ar;
+      // dues per (decoder, batch) as bytes (a due above 255 voids the attempt)
+      uint8_t* Dm = (uint8_t*)a2.take((int64_t)nd * (K > 0 ? K : 1));
+      int64_t* Bt = (int64_t*)a2.take(sizeof(int64_t) * 3 * (size_t)(K > 0 ? K : 1));
+      const bool room = !a2.over() && K > 0 && K <= left_guard && cap_t0 >= 0;
+      if (room) {
+        // pass 1: the due matrix, decoder-major
+        int wide = 0;
+#pragma unroll 1
+        for (int k = d0; k < d1; ++k) {
+          double n_, tp_;
+          int64_t b_, l_;
+          st_get(k, k - d0, n_, tp_, b_, l_);
+          double tt = t;
+          uint8_t* row = Dm + (size_t)k * (size_t)K;
+          for (int64_t kb = 0; kb < K; ++kb) {
+            const int64_t due = step(tt, n_, tp_, b_, l_);
+            if (due > 255) wide = 1;
+            row[kb] = (uint8_t)due;
+            tt = tt + t0;
+          }
+        }
+        G::sync();
+        // pass 2: per batch (contiguous batch ranges per lane): tokens, entries, and
+        // whether the batch outlasts t0
+        const int64_t kper = (K + NT - 1) / NT, k0 = imin(K, (int64_t)lane * kper), k1 = imin(K, k0 + kper);
+        int bad = 0;
+        int64_t lcnt = 0;
+        for (int64_t kb = k0; kb < k1; ++kb) {
+          int64_t tok = 0, cnt = 0;
+          for (int d = 0; d < nd; ++d) {
+            const int64_t x = (int64_t)Dm[(size_t)d * (size_t)K + kb];
+            tok += x;
+            cnt += x > 0 ? 1 : 0;
+          }
+          if (tok > 0 && plan_predict(P, tok, 0) > t0) bad = 1;
+          if (wide) bad = 1;
+          Bt[3 * kb] = tok;
+          Bt[3 * kb + 1] = cnt;
+          lcnt += cnt;
+        }
+        if (!G::or_(sh.bs, bad)) {
+          int64_t cv[1] = {lcnt}, cex[1], ctot[1];
+          G::template mscan<1>(sh.bs, cv, cex, ctot, par);
+          // pass 3: entries and batch records of this lane's batches
+          double tt = t;
+          for (int64_t kb = 0; kb < k0; ++kb) tt = tt + t0;
+          int64_t pos = ne + cex[0];
+          for (int64_t kb = k0; kb < k1; ++kb) {
+            const int64_t first = pos;
+            for (int d = 0; d < nd; ++d) {
+              const int64_t x = (int64_t)Dm[(size_t)d * (size_t)K + kb];
+              if (x <= 0) continue;
+              if (pos < I.cap_entry) OE[pos] = entry_decode(didx[d], x, 0, &sh.range_err);
+              ++pos;
+            }
+            const int64_t tok = Bt[3 * kb];
+            slos_batch b;
+            b.start_s = tt;
+            b.end_s = tt + t0;
+            b.capacity_tokens = imax(cap_t0, tok);
+            b.spec_step = 0;
+            b.prefill_budget_left = imax(0, imin(cap_t0 - tok, chunk_cap));
+            b.first_entry = first;
+            b.n_entries = pos - first;
+            if (nb + kb < I.cap_batch) OB[nb + kb] = b;
+            tt = b.end_s;
+          }
+          // every lane advances the same sequence to the tail's end
+          double te = t;
+          for (int64_t kb = 0; kb < K; ++kb) te = te + t0;
+          t = te;
+          nb += K;
+          ne += ctot[0];
+          decodes = false;
+          G::sync();
+          break;
+        }
+      }
+      G::sync();  // the attempt is void: the due matrix is scratch, the state untouched
+    }
     const bool dec_branch = decodes;
     const int64_t e0 = ne;
     int64_t pre_before = 0, pre_tot = 0;
