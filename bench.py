@@ -331,7 +331,7 @@ def run_ours(args):
     batch = solver.batch
     hs = solver._hs
     outs2 = (abi.Result * per)()
-    for _ in range(max(2, args.warmup // 2)):
+    for _ in range(max(3, args.warmup)):  # pinned result arenas and host pools warm
         lib.slos_plan_batch(hs, per, C.c_void_p(batch.inputs_ptr()), 0, outs2, sptr)
         for k in range(per):
             lib.slos_result_free(C.byref(outs2[k]))
