@@ -25,6 +25,8 @@
 
 namespace slos {
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
 constexpr int kDpThreads = 256;
 constexpr int kNumPhases = 12;
 
@@ -806,12 +808,15 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   __shared__ unsigned long long s_ctr[5];
   __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_nw, s_bovf, s_anysh, s_nsb;
   __shared__ int64_t s_next_free, s_arena_next, s_bnext;
+  __shared__ __align__(8) uint64_t s_mbar;  // completion of a level's record staging (TMA bulk copies)
 
   const BatchArgs& A = prm.a;
   const int tid = threadIdx.x;
   const int inst = A.order[prm.blk0 + blockIdx.x];
   OutHdr* out = &A.out[inst];
   if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_mbar)), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
     sP = A.planners[A.inst[inst].planner];
     sI = A.inst[inst];
     s_err = 0;
@@ -936,6 +941,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
 
   long long ph_t0_ = clock64();
   const long long ph_start_ = ph_t0_;
+  uint32_t mb_phase = 0;  // parity of the staging barrier's current phase
   SLOS_PHASE(0);  // 0: instance load / setup
   for (int i = 0; i < N && !s_err; ++i) {
     const int jlo = ch_fl[i];
@@ -1010,14 +1016,20 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     // (header + cap/nx/hc of each record; the slot ends are not read by E3)
     const bool staged = (size_t)nlev * prm.grec_stage <= prm.overlay_bytes;
     const unsigned char* GRl = GR + (size_t)pair_index(N, jlo + 1, i) * prm.grec_stride;
-    if (staged) {
-      const int per4 = (int)(prm.grec_stage / 16), str4 = (int)(prm.grec_stride / 16);
-      const uint4* src4 = (const uint4*)GRl;
-      uint4* dst4 = (uint4*)ovl;
-      for (int x = tid; x < nlev * per4; x += kDpThreads) {
-        const int r = x / per4, o = x - r * per4;
-        dst4[x] = src4[(size_t)r * str4 + o];
-      }
+    if (staged && tid == 0) {
+      // one TMA bulk copy per record (global -> shared, completion on s_mbar); it runs
+      // under the candidate enumeration below, which does not read the records. The
+      // overlay's last generic-proxy use is behind the level barrier above.
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t mb = smem_u32(&s_mbar);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                   "r"((uint32_t)((size_t)nlev * prm.grec_stage))
+                   : "memory");
+      for (int r = 0; r < nlev; ++r)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(ovl + (size_t)r * prm.grec_stage)),
+                     "l"(GRl + (size_t)r * prm.grec_stride), "r"((uint32_t)prm.grec_stage), "r"(mb)
+                     : "memory");
     }
     auto rec_of = [&](int j) -> const unsigned char* {
       return staged ? (const unsigned char*)ovl + (size_t)(j - jlo) * prm.grec_stage
@@ -1062,6 +1074,15 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
         k1 = (uint64_t)llround(gap * 1000.0);
       }
       Cme[c] = memo_find_insert(Memo, I.cap_memo, k0, k1, Sc_[src], c, X0, &s_n_new, &s_n_used, &s_ovf);
+    }
+    if (staged) {  // the level's records have landed (every thread waits: no copy outlives the level)
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(smem_u32(&s_mbar)), "r"(mb_phase)
+                     : "memory");
+      mb_phase ^= 1u;
     }
     __syncthreads();
     if (s_ovf) {
