@@ -794,13 +794,16 @@ __global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_ke
                                            (int64_t)prm.smem_bytes, prm.phase_cycles);
 }
 
-// Very large instances (thousands of running decoders, the C4 family): twice the
-// threads per instance, one CTA per SM.
-__global__ void __launch_bounds__(2 * kBuildThreads, 1) build_kernel_big(BuildParams prm) {
+// Very large instances (thousands of running decoders, the C4 family): four times
+// the threads per instance, one CTA per SM.
+#ifndef SLOS_BUILD_BIG_THREADS  // measured on C4 x 64: 512 threads 1.33 ms, 256 threads 1.46 ms
+#define SLOS_BUILD_BIG_THREADS (4 * kBuildThreads)
+#endif
+__global__ void __launch_bounds__(SLOS_BUILD_BIG_THREADS, 1) build_kernel_big(BuildParams prm) {
   const BatchArgs& A = prm.a;
   __shared__ BuildShared sh;
   extern __shared__ __align__(16) unsigned char bsm[];
-  build_instance<BlockGrpT<2 * kBuildThreads>>(A, sh, A.bq[A.qbase[kBuildKinds * prm.part + 2] + blockIdx.x], bsm,
+  build_instance<BlockGrpT<SLOS_BUILD_BIG_THREADS>>(A, sh, A.bq[A.qbase[kBuildKinds * prm.part + 2] + blockIdx.x], bsm,
                                                (int64_t)prm.smem_bytes, prm.phase_cycles);
 }
 

@@ -22,7 +22,7 @@
 namespace slos {
 
 constexpr int kBT = 256;  // block size of build / gap kernels
-constexpr int kBW = kBT / 32;
+constexpr int kBW = 16;  // BlockShared capacity: groups of up to 512 threads
 
 struct MemBuf {  // exact census members (SoA), census order
   double* ph;

@@ -114,7 +114,7 @@ cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, int n
     if ((e = cudaFuncSetAttribute(build_kernel_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)prm.smem_bytes)) != cudaSuccess)
       return e;
-    build_kernel_big<<<n_big, 2 * kBuildThreads, prm.smem_bytes, s>>>(prm);
+    build_kernel_big<<<n_big, SLOS_BUILD_BIG_THREADS, prm.smem_bytes, s>>>(prm);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
