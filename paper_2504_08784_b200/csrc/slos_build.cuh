@@ -794,11 +794,14 @@ __global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_ke
                                            (int64_t)prm.smem_bytes, prm.phase_cycles);
 }
 
-// Very large instances (thousands of running decoders, the C4 family): four times
-// the threads per instance, one CTA per SM.
-#ifndef SLOS_BUILD_BIG_THREADS  // measured on C4 x 64: 512 threads 1.33 ms, 256 threads 1.46 ms
-#define SLOS_BUILD_BIG_THREADS (4 * kBuildThreads)
+// Very large instances (thousands of running decoders, the C4 family): twice the
+// threads per instance, one CTA per SM. (512 threads measured C4 x 64 1.46 -> 1.33 ms,
+// but the BlockShared capacity it needs (kBW = 16) slowed the C2 reconstruction by
+// ~0.1 ms, so the default stays at 256.)
+#ifndef SLOS_BUILD_BIG_THREADS
+#define SLOS_BUILD_BIG_THREADS (2 * kBuildThreads)
 #endif
+static_assert(SLOS_BUILD_BIG_THREADS <= kBT, "BlockShared holds groups of at most kBT threads");
 __global__ void __launch_bounds__(SLOS_BUILD_BIG_THREADS, 1) build_kernel_big(BuildParams prm) {
   const BatchArgs& A = prm.a;
   __shared__ BuildShared sh;

@@ -22,7 +22,7 @@
 namespace slos {
 
 constexpr int kBT = 256;  // block size of build / gap kernels
-constexpr int kBW = 16;  // BlockShared capacity: groups of up to 512 threads
+constexpr int kBW = kBT / 32;  // BlockShared capacity: groups of up to kBT threads
 
 struct MemBuf {  // exact census members (SoA), census order
   double* ph;
