@@ -93,3 +93,44 @@ def test_errors_are_status_codes():
     with pytest.raises(Error) as e:
         sched.schedule(many)
     assert e.value.code == "invalid-parameters"
+
+
+def test_c2_bench_seeds_with_the_infeasible_instance_match_reference():
+    """Seeds 0..1023 (the bench batch) include an instance whose running set is
+    infeasible: its 496-batch EDF fallback takes the closed-time decode tail."""
+    import os
+    if not os.path.exists(abi.REF_LIB):
+        pytest.skip("oracle/_ref not built")
+    F = W.FAMILIES["C2"]
+    b = W.InstanceBatch.stress(F["spec"], range(0, 1024))
+    prod, ref = abi.product(), abi.reference()
+    hp, hr = _Handle(prod, F["model"], W.TWO_TIER_SLO, F["cfg"]), _Handle(ref, F["model"], W.TWO_TIER_SLO, F["cfg"])
+    P = plan_many(prod, hp.ptr, b)
+    R = plan_many(ref, hr.ptr, b)
+    assert any(r["infeasible"] for r in R)
+    bad = [(k, diff(P[k], R[k])) for k in range(b.n) if diff(P[k], R[k])]
+    assert not bad, bad[:4]
+
+
+def test_c5_corpus_tiled_matches_reference():
+    """The C5 corpus tiled (65,536 AR instances: the 4-chunk host pipeline; 32,768
+    speculative: 2 chunks) with per-part collection, every result against the
+    reference's golden summary."""
+    import gzip
+    import json
+    import os
+    from golden_checks import _cmp
+    from paper_2504_08784_b200.planner import PerfTerm, PlannerConfig
+    GOLDEN = os.path.join(abi.ROOT, "tests", "golden")
+    meta = json.load(gzip.open(os.path.join(GOLDEN, "c5.json.gz"), "rt"))
+    prod = abi.product()
+    for g in ("ar", "spec"):
+        G = meta["groups"][g]
+        base = W.load_corpus(os.path.join(GOLDEN, f"c5_{g}.bin.gz"))
+        b = base.tiled(32 if g == "ar" else 16)
+        cfg = PlannerConfig(max_chunk_tokens=2048, max_batch_tokens=16384, speculative=G["speculative"],
+                            spec_alpha=0.8, spec_max_len=8, plan_margin=0.0)
+        h = _Handle(prod, [PerfTerm(*t) for t in meta["model"]], W.TWO_TIER_SLO, cfg)
+        res = plan_many(prod, h.ptr, b)
+        for k, got in enumerate(res):
+            _cmp(got, G["ref"][k % base.n], f"c5 {g} tiled instance {k}")
