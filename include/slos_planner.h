@@ -284,6 +284,11 @@ int slos_workspace_kernel_ms(slos_workspace* ws, float* ms2);
  * (build_kernel*). CPU checkers write zeros. */
 int slos_workspace_stage_ms(slos_workspace* ws, float* ms, int32_t n);
 
+/* Number of kernels the last solve launched (anchor / group / DP per solve part and
+ * one per non-empty reconstruction queue; the records and compaction kernels are
+ * separate calls). CPU checkers write 0. */
+int slos_workspace_launches(slos_workspace* ws, int64_t* n);
+
 /* Bytes moved host->device and device->host by the calling thread's last
  * slos_plan_batch / slos_workspace_* sequence. */
 void slos_last_transfer_bytes(int64_t* h2d, int64_t* d2h);

@@ -49,8 +49,20 @@ def dump(name, obj):
 
 
 def main():
+    only = set(sys.argv[1:])  # optional section filter: uniforms oracle stress fuzz
     lib, raw = reflib()
     # 1. RNG pin (acceptance_main.cpp:577 draws)
+    if not only or "uniforms" in only:
+        _uniforms(raw)
+    if not only or "oracle" in only:
+        _oracle(lib, raw)
+    if not only or "stress" in only:
+        _stress(lib)
+    if not only or "fuzz" in only:
+        _fuzz(lib)
+
+
+def _uniforms(raw):
     uni = {}
     for seed in (88, 0, 1, 2024, 123456789):
         a = np.zeros(600)
@@ -58,6 +70,8 @@ def main():
         uni[str(seed)] = [int(x) for x in a.view(np.uint64)]
     dump("uniforms", uni)
 
+
+def _oracle(lib, raw):
     # 2. brute-force oracle instance families (test_dp_scheduler.cpp / acceptance_main.cpp)
     fams = {}
     for seed, count, unit in ((424242, 250, False), (20240817, 300, False), (171717, 60, False),
@@ -88,10 +102,14 @@ def main():
         fams[f"{seed}"] = dict(seed=seed, unit_value=unit, items=items)
     dump("oracle_instances", fams)
 
+
+def _stress(lib):
     # 3. stress families C1-C4 + the reference latency criterion
     stress = {}
+    # C4 (2032 decoders, the 256-thread reconstruction and HBM-spill DP levels) on 32
+    # seeds: ~3 s per plan in the reference, ~15 s on 8 host threads
     for fam, seeds in (("C1", range(16)), ("LAT", range(16)), ("C2", range(6)), ("C3", range(16)),
-                       ("C4", range(1))):
+                       ("C4", range(32))):
         F = W.FAMILIES[fam]
         b = W.InstanceBatch.stress(F["spec"], list(seeds))
         h = _Handle(lib, F["model"], W.TWO_TIER_SLO, F["cfg"])
@@ -100,6 +118,8 @@ def main():
         print(fam, "admitted", [len(r["admitted"]) for r in res][:8])
     dump("stress", stress)
 
+
+def _fuzz(lib):
     # 4. structural fuzz (tests/fuzz.py), value and throughput objectives
     fz = []
     for seed in range(1000):

@@ -36,6 +36,11 @@
 
 using namespace slosim;
 
+#ifdef SLOS_REF_INSTR
+// oracle/instrument_ref.py: the reference sources patched with work counters
+namespace slos_instr { extern thread_local long long T, G, D, S, snap[5]; extern thread_local int on; }
+#endif
+
 struct slos_planner {
   PerfModel model;
   SloConfig slo;
@@ -280,7 +285,44 @@ int slos_plan(slos_planner* p, const slos_input* in, int32_t unit_value, slos_re
     if (in->n_running >= SLOS_ENTRY_MAX_REQS || in->n_pending >= SLOS_ENTRY_MAX_REQS)  // 24-bit entry refs
       fail("invalid-parameters", "too many requests for the plan entry format");
     ScheduleInput s = to_input(in);
+#ifdef SLOS_REF_INSTR
+    // a fresh BatchPlanner per plan (cold prefill_budget memo, acceptance_main.cpp:606),
+    // so the memo-miss counter G is a per-plan quantity
+    BatchPlanner fresh(p->model, p->slo, p->cfg);
+    SloScheduler sched(fresh);
+    ScheduleResult r = unit_value ? sched.schedule_throughput(s) : sched.schedule(s);
+    fill_result(in, r, out);
+    out->counters.transitions = slos_instr::snap[0];
+    out->counters.gap_evals = slos_instr::snap[1];
+    out->counters.dues = slos_instr::snap[2];
+    out->counters.slots = slos_instr::snap[3];
+    out->counters.states = slos_instr::snap[4];
+#else
     ScheduleResult r = unit_value ? p->sched->schedule_throughput(s) : p->sched->schedule(s);
+    fill_result(in, r, out);
+#endif
+    return SLOS_OK;
+  });
+  out->status = st;
+  return st;
+}
+
+// Single-thread latency as the reference's own criterion measures it
+// (acceptance_main.cpp:606-609): a FRESH BatchPlanner + SloScheduler per instance
+// (cold memo), and only schedule() inside the clock.
+int slos_ref_schedule_timed(slos_planner* p, const slos_input* in, int32_t unit_value, slos_result* out,
+                            double* seconds) {
+  std::memset(out, 0, sizeof(*out));
+  *seconds = 0.0;
+  int st = guarded([&] {
+    ScheduleInput s = to_input(in);
+    BatchPlanner planner(p->model, p->slo, p->cfg);
+    SloScheduler sched(planner);
+    timespec a, b;
+    clock_gettime(CLOCK_MONOTONIC, &a);
+    ScheduleResult r = unit_value ? sched.schedule_throughput(s) : sched.schedule(s);
+    clock_gettime(CLOCK_MONOTONIC, &b);
+    *seconds = (double)(b.tv_sec - a.tv_sec) + 1e-9 * (double)(b.tv_nsec - a.tv_nsec);
     fill_result(in, r, out);
     return SLOS_OK;
   });
@@ -472,6 +514,12 @@ int slos_workspace_records(slos_workspace* b, slos_record* out, void* stream) {
   }
   return SLOS_OK;
 }
+int slos_workspace_launches(slos_workspace* b, int64_t* n) {
+  (void)b;
+  *n = 0;  // no device kernels in the CPU reference
+  return SLOS_OK;
+}
+
 int slos_workspace_stage_ms(slos_workspace* b, float* ms, int32_t n) {
   (void)b;
   for (int k = 0; k < n; ++k) ms[k] = 0.0f;

@@ -73,6 +73,31 @@ void slos_ref_uniforms(uint64_t seed, int32_t n, double* out) {
   for (int i = 0; i < n; ++i) out[i] = u(rng);
 }
 
+// The reference's stress generator (acceptance_main.cpp:577-605), generalised to
+// G(n_dec, n_new, seed, tiers) as SURVEY.md §8 d0 defines it: std::mt19937_64(seed)
+// and uniform_real_distribution(0, 1) draws consumed in the harness's order. It
+// lets bench.py's reference arm build its inputs from oracle/_ref alone (same
+// outputs as the product's generator, paper_2504_08784_b200/csrc/slos_workload.c).
+void slos_ref_stress(uint64_t seed, int32_t n_dec, int32_t n_new, int32_t two_tier,
+                     const double* tpot_tiers, double now, int32_t* dec_tier, double* dec_next_due,
+                     int64_t* dec_remaining, double* new_deadline, int64_t* new_prefill,
+                     int32_t* new_tier, int64_t* new_memory, double* new_value) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u(0.0, 1.0);
+  for (int32_t i = 0; i < n_dec; ++i) {
+    dec_tier[i] = two_tier ? i % 2 : 0;
+    dec_next_due[i] = now + u(rng) * tpot_tiers[dec_tier[i]];
+    dec_remaining[i] = 50 + (int64_t)(u(rng) * 200.0);
+  }
+  for (int32_t i = 0; i < n_new; ++i) {
+    new_deadline[i] = now + 0.3 + 0.9 * u(rng);
+    new_prefill[i] = 200 + (int64_t)(u(rng) * 700.0);
+    new_tier[i] = two_tier ? i % 2 : 0;
+    new_memory[i] = 20 + (int64_t)(u(rng) * 60.0);
+    new_value[i] = 1.0 + (int64_t)(u(rng) * 8.0);
+  }
+}
+
 void slos_ref_oracle_instances(uint64_t seed, int32_t count, int64_t* records) {
   std::mt19937_64 rng(seed);
   for (int i = 0; i < count; ++i) encode(oracle::random_instance(rng), records + (size_t)i * kRec);

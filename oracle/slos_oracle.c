@@ -1733,6 +1733,12 @@ int slos_workspace_records(slos_workspace* b, slos_record* out, void* stream) {
   }
   return SLOS_OK;
 }
+int slos_workspace_launches(slos_workspace* b, int64_t* n) {
+  (void)b;
+  *n = 0; /* no device kernels in the CPU checker */
+  return SLOS_OK;
+}
+
 int slos_workspace_stage_ms(slos_workspace* b, float* ms, int32_t n) {
   (void)b;
   for (int k = 0; k < n; ++k) ms[k] = 0.0f;

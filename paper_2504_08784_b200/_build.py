@@ -58,6 +58,17 @@ def build_product(force: bool = False, verbose: bool = False) -> str:
     return out
 
 
+def build_probe(force: bool = False) -> str:
+    """libslos_probe.so: the shared-memory bandwidth probe bench.py measures the
+    DP stage's roofline peak with (a measurement tool, not the planner ABI)."""
+    out = os.path.join(PKG, "libslos_probe.so")
+    src = os.path.join(CSRC, "slos_probe.cu")
+    if force or _stale(out, [src]):
+        _run([NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+              src, "-o", out])
+    return out
+
+
 def build_workload(force: bool = False) -> str:
     out = os.path.join(PKG, "libslos_workload.so")
     src = os.path.join(CSRC, "slos_workload.c")
@@ -80,6 +91,7 @@ def build_all(force: bool = False, verbose: bool = False) -> None:
     build_workload(force)
     build_oracle(force)
     build_product(force, verbose)
+    build_probe(force)
 
 
 if __name__ == "__main__":

@@ -397,6 +397,8 @@ def _bind(lib: C.CDLL) -> C.CDLL:
     lib.slos_workspace_records.restype = C.c_int
     lib.slos_workspace_kernel_ms.argtypes = [C.c_void_p, P(C.c_float)]
     lib.slos_workspace_kernel_ms.restype = C.c_int
+    lib.slos_workspace_launches.argtypes = [C.c_void_p, P(C.c_int64)]
+    lib.slos_workspace_launches.restype = C.c_int
     lib.slos_workspace_stage_ms.argtypes = [C.c_void_p, P(C.c_float), C.c_int32]
     lib.slos_workspace_stage_ms.restype = C.c_int
     lib.slos_last_transfer_bytes.argtypes = [P(C.c_int64), P(C.c_int64)]
@@ -462,3 +464,26 @@ def workload() -> C.CDLL:
         lib.slos_wl_stress.restype = None
         _LIBS[path] = lib
     return _LIBS[path]
+
+
+def reference_stress_gen():  # test infrastructure / reference bench arm only
+    """slos_ref_stress from oracle/_ref/libslos_ref.so: the reference harness's
+    G(...) generator (acceptance_main.cpp:577-605), same signature as slos_wl_stress."""
+    lib = reference()
+    f = lib.slos_ref_stress
+    P = C.POINTER
+    f.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, P(C.c_double), C.c_double, P(C.c_int32),
+                  P(C.c_double), P(C.c_int64), P(C.c_double), P(C.c_int64), P(C.c_int32), P(C.c_int64),
+                  P(C.c_double)]
+    f.restype = None
+    return f
+
+
+def reference_schedule_timed():  # test infrastructure / reference bench arm only
+    """slos_ref_schedule_timed: one reference schedule() with a fresh planner, timed
+    inside (acceptance_main.cpp:606-609). Returns the bound function."""
+    lib = reference()
+    f = lib.slos_ref_schedule_timed
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(Result), C.POINTER(C.c_double)]
+    f.restype = C.c_int
+    return f

@@ -130,6 +130,7 @@ struct Ctx {
   int status = SLOS_OK;
   std::string why;
   cudaStream_t stream = nullptr;
+  size_t smem_optin = 0;  // opt-in dynamic shared memory per CTA (227 KB on B200)
   DevBuf d_in, d_scr, d_out, d_pack, d_wscr, d_small;
   PinBuf h_in, h_small;
   std::mutex pool_mu;
@@ -247,6 +248,9 @@ int ensure_device(Ctx& c) {
     c.why = std::string("device ") + prop.name + " is not sm_100 (B200)";
     return c.status;
   }
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  c.smem_optin = (size_t)optin;
   e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     c.status = SLOS_ERR_CUDA;
@@ -390,6 +394,13 @@ struct ChainKey {
   int enc;
 };
 
+// prep_instance runs on HostPool workers: its message goes into the Prep and the
+// calling thread reports it (g_err is thread-local)
+int prep_err(Prep& pr, int code, const char* msg) {
+  pr.why = std::string(slos_status_slug(code)) + ": " + msg;
+  return code;
+}
+
 int prep_instance(const slos_planner* P, const slos_input* in, int unit_value, Prep& pr) {
   // Prep objects are reused across calls (their vectors keep their capacity)
   pr.planner = 0;
@@ -400,10 +411,10 @@ int prep_instance(const slos_planner* P, const slos_input* in, int unit_value, P
   pr.span = pr.tail_bound = 0.0;
   pr.max_rem = 0;
   const int L = P->L;
-  if (L > 8) return set_err(SLOS_ERR_INVALID_PARAMETERS, "at most 8 SLO tiers supported");
+  if (L > 8) return prep_err(pr, SLOS_ERR_INVALID_PARAMETERS, "at most 8 SLO tiers supported");
   if (in->n_running >= SLOS_ENTRY_MAX_REQS || in->n_pending >= SLOS_ENTRY_MAX_REQS)  // 24-bit entry refs
-    return set_err(SLOS_ERR_INVALID_PARAMETERS, "too many requests for the plan entry format");
-  if (!P->device_ok) return set_err(SLOS_ERR_RANGE, "planner not representable on device");
+    return prep_err(pr, SLOS_ERR_INVALID_PARAMETERS, "too many requests for the plan entry format");
+  if (!P->device_ok) return prep_err(pr, SLOS_ERR_RANGE, "planner not representable on device");
   thread_local std::vector<ChainKey> ch;  // capacity kept across calls
   ch.clear();
   ch.reserve((size_t)in->n_running + (size_t)in->n_pending);
@@ -416,15 +427,15 @@ int prep_instance(const slos_planner* P, const slos_input* in, int unit_value, P
     const slos_pending& p = in->pending[i];
     ch.push_back({false, p.id ? p.id : "", p.prefill_deadline, -(i + 1)});
   }
-  if (ch.size() > 250) return set_err(SLOS_ERR_INVALID_PARAMETERS, "admission chain too large");
+  if (ch.size() > 250) return prep_err(pr, SLOS_ERR_INVALID_PARAMETERS, "admission chain too large");
   for (const ChainKey& k : ch) {
     const int tier = k.enc >= 0 ? in->running[k.enc].decode_tier : in->pending[-k.enc - 1].decode_tier;
-    if (tier < 0 || tier >= L) return set_err(SLOS_ERR_INVALID_PARAMETERS, "bad SLO tier");
+    if (tier < 0 || tier >= L) return prep_err(pr, SLOS_ERR_INVALID_PARAMETERS, "bad SLO tier");
   }
   for (int i = 0; i < in->n_running; ++i) {
     const slos_running& r = in->running[i];
     if (r.prefill_remaining <= 0 && r.decode_remaining > 0 && (r.decode_tier < 0 || r.decode_tier >= L))
-      return set_err(SLOS_ERR_INVALID_PARAMETERS, "vector::_M_range_check: running decode tier");
+      return prep_err(pr, SLOS_ERR_INVALID_PARAMETERS, "vector::_M_range_check: running decode tier");
   }
   std::stable_sort(ch.begin(), ch.end(), [](const ChainKey& a, const ChainKey& b) {
     if (std::abs(a.deadline - b.deadline) > kTimeEps) return a.deadline < b.deadline;
@@ -582,6 +593,8 @@ struct Workspace {
   int maxN = 0;
   cudaStream_t stream = nullptr;
   bool uploaded = false;
+  bool solved = false;  // ev[2] marks the end of a solve
+  int64_t launches = 0;  // kernels launched by the last solve
   int n_total = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t own_stream = nullptr;  // pipeline workspaces only
@@ -652,6 +665,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     if (pr.status != SLOS_OK) {
       std::memset(&outs[k], 0, sizeof(outs[k]));
       outs[k].status = pr.status;
+      g_err = pr.why;
       continue;
     }
     int pi = -1;
@@ -1207,6 +1221,15 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   if (kStageDec && fit(maxDec) <= kSmemBudget) dp.dec_smem_max = maxDec;
   smem = fit(dp.dec_smem_max);
   ws.anchor_smem = anchor_smem_bytes(maxN, dp.Sc, Lmax, &dp.anchor_scr_bytes);
+  if (S_need > (double)(1 << 20) || smem > c.smem_optin || ws.anchor_smem > c.smem_optin) {
+    // the slot grid of the widest deadline span does not fit a CTA's shared memory;
+    // plan_all solves wide instances in their own slot classes, so only an instance
+    // that alone exceeds it lands here (per-instance SLOS_ERR_RANGE, never a launch failure)
+    ws.uploaded = false;
+    ws.nv = 0;
+    return set_err(SLOS_ERR_RANGE, "deadline span needs a slot grid of " + std::to_string((int64_t)S_need) +
+                                       " slots, more than a CTA's shared memory holds");
+  }
   ws.maxN = maxN;
   ws.valid = valid;
   ws.nv = nv;
@@ -1247,6 +1270,12 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   }
   cudaEventRecord(ws.ev[0], s);
   cudaEventRecord(ws.ev_fork, s);
+  ws.launches = 0;  // kernels this solve launches (slos_workspace_launches)
+  for (int p = 0; p < ws.n_parts; ++p) {
+    const int nt = ws.atask_lo[p + 1] - ws.atask_lo[p];
+    ws.launches += (nt > 0) + (nt > 0 && ws.maxN > 0) + (ws.part_lo[p + 1] > ws.part_lo[p]);
+    for (int kd = 0; kd < kBuildKinds; ++kd) ws.launches += ws.qn[kBuildKinds * p + kd] > 0;
+  }
   BuildParams bp;
   bp.a = ws.A;
   static const size_t kBuildSmem = [] {  // per-gap working set per CTA (SLOS_BUILD_SMEM_KB)
@@ -1298,6 +1327,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     cudaStreamWaitEvent(s, ws.ev_join[p], 0);
   }
   cudaEventRecord(ws.ev[2], s);
+  ws.solved = true;
   return SLOS_OK;
 }
 
@@ -1507,6 +1537,9 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
   unsigned char* DO = (unsigned char*)ws.d_out.p;
   if ((e = ws.h_small.ensure(sizeof(OutHdr) * nv)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   OutHdr* hO = (OutHdr*)ws.h_small.p;
+  // the headers are final only after the last solve's kernels, which may have run on
+  // another stream than the upload's (slos_workspace_solve takes its own stream)
+  if (ws.solved) cudaStreamWaitEvent(s, ws.ev[2], 0);
   cudaMemcpyAsync(hO, DO + Ly.out, sizeof(OutHdr) * nv, cudaMemcpyDeviceToHost, s);
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   std::vector<OutHdr> hdr(hO, hO + nv);
@@ -1648,13 +1681,114 @@ bool part_collect_enabled() {  // SLOS_PART_COLLECT=0: one collection per worksp
   return on;
 }
 
+// Slot-grid need of one instance: ws_upload sizes every kernel's shared-memory slot
+// grid (Sc) by the widest deadline span of its batch (prep_instance's span), so a
+// single outlier -- a far-future pending deadline, a late forced prefill -- must not
+// size everybody's grid. Same span as prep_instance (chain deadlines and now).
+double slot_need(const slos_planner* P, const slos_input* in) {
+  double maxdl = in->now, mindl = in->now;
+  for (int i = 0; i < in->n_running; ++i)
+    if (in->running[i].prefill_remaining > 0) {
+      maxdl = std::max(maxdl, in->running[i].prefill_deadline);
+      mindl = std::min(mindl, in->running[i].prefill_deadline);
+    }
+  for (int i = 0; i < in->n_pending; ++i) {
+    maxdl = std::max(maxdl, in->pending[i].prefill_deadline);
+    mindl = std::min(mindl, in->pending[i].prefill_deadline);
+  }
+  const double t0 = P->L > 0 ? P->tpot[0] : 1.0;
+  const double s = std::ceil(std::max(0.0, maxdl - mindl) / t0) + 8;
+  return std::isfinite(s) ? s : 1e18;
+}
+
+// Instances whose grid needs more slots than this are solved apart, in classes of
+// similar width (SLOS_NARROW_SLOTS overrides).
+double narrow_slots() {
+  static const double v = [] {
+    const char* e = std::getenv("SLOS_NARROW_SLOTS");
+    return e ? std::atof(e) : 512.0;
+  }();
+  return v;
+}
+
+// Solve `jobs` with capacity regrowth (up to 8 rounds) in one workspace.
+int solve_rounds(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_input* inputs,
+                 int32_t unit_value, slos_result* outs, cudaStream_t stream, std::vector<Job> jobs) {
+  std::vector<Job> retry;
+  ws.part_collect = part_collect_enabled();
+  for (int round = 0; round < 8 && !jobs.empty(); ++round) {
+    retry.clear();
+    int r = ws_upload(c, ws, planners, inputs, unit_value, jobs, outs, stream);
+    if (r == SLOS_OK) r = ws_solve(ws, stream);
+    if (r == SLOS_OK) r = ws_collect(c, ws, outs, retry);
+    if (r != SLOS_OK) {
+      for (const Job& j : jobs) outs[j.k].status = r;
+      return r;
+    }
+    jobs.swap(retry);
+  }
+  for (const Job& j : jobs) {
+    std::memset(&outs[j.k], 0, sizeof(outs[j.k]));
+    outs[j.k].status = SLOS_ERR_CAPACITY;
+  }
+  return SLOS_OK;
+}
+
+// Wide instances (slot_need > narrow_slots()), sorted by need, in classes whose widest
+// member needs at most twice the narrowest; a class the shared memory cannot hold is
+// retried one instance at a time so only the instances that alone exceed it fail.
+int solve_wide(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_input* inputs,
+               int32_t unit_value, slos_result* outs, cudaStream_t stream,
+               std::vector<std::pair<double, int>>& wide) {
+  std::sort(wide.begin(), wide.end());
+  size_t a = 0;
+  while (a < wide.size()) {
+    size_t b = a + 1;
+    while (b < wide.size() && wide[b].first <= 2.0 * wide[a].first) ++b;
+    std::vector<Job> cls;
+    for (size_t x = a; x < b; ++x) cls.push_back({wide[x].second, 0});
+    int r = solve_rounds(c, ws, planners, inputs, unit_value, outs, stream, cls);
+    if (r == SLOS_ERR_RANGE && cls.size() > 1) {
+      for (const Job& j : cls) {
+        r = solve_rounds(c, ws, planners, inputs, unit_value, outs, stream, {j});
+        if (r != SLOS_OK && r != SLOS_ERR_RANGE) return r;
+      }
+    } else if (r != SLOS_OK && r != SLOS_ERR_RANGE) {
+      return r;
+    }
+    a = b;
+  }
+  return SLOS_OK;
+}
+
 // full pipeline with capacity regrowth; caller holds ctx().mu
 int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, const slos_input* inputs,
              int32_t unit_value, slos_result* outs, cudaStream_t stream) {
-  std::vector<Job> jobs(n), retry;
-  for (int k = 0; k < n; ++k) jobs[k] = {k, 0};
   g_h2d = 0;
   g_d2h = 0;
+  std::vector<Job> jobs, retry;
+  std::vector<std::pair<double, int>> wide;
+  {
+    thread_local std::vector<double> need;
+    need.resize((size_t)n);
+    HostPool::get().run(n, [&](int lo, int hi) {
+      for (int k = lo; k < hi; ++k) need[k] = slot_need(planners[k], &inputs[k]);
+    });
+    const double lim = narrow_slots();
+    jobs.reserve((size_t)n);
+    for (int k = 0; k < n; ++k) {
+      if (need[k] > lim) wide.push_back({need[k], k});
+      else jobs.push_back({k, 0});
+    }
+  }
+  if (!wide.empty()) {
+    const int r = solve_wide(c, ws, planners, inputs, unit_value, outs, stream, wide);
+    if (r != SLOS_OK) {
+      for (int k = 0; k < n; ++k) outs[k].status = r;
+      return r;
+    }
+  }
+  n = (int32_t)jobs.size();
   const int K = pipeline_chunks(n);
   if (K > 1) {
     // order after the caller's prior work on `stream`
@@ -1673,7 +1807,7 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
       int ci = (int)((int64_t)k * K / n);
       if (K == 2) ci = k < (int)(split * n) ? 0 : 1;
       chunk[ci].push_back(jobs[k]);
-    }
+    }  // (jobs[k].k: the caller's instance index)
     int prev = -1;
     for (int i = 0; i <= K; ++i) {
       const auto t_a = std::chrono::steady_clock::now();
@@ -1708,23 +1842,9 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
     retry.clear();
     if (std::getenv("SLOS_HOST_TIMING")) std::fprintf(stderr, "[slos pipeline] %d chunks, %zu retried\n", K, jobs.size());
   }
-  ws.part_collect = part_collect_enabled();
-  for (int round = 0; round < 8 && !jobs.empty(); ++round) {
-    retry.clear();
-    int r = ws_upload(c, ws, planners, inputs, unit_value, jobs, outs, stream);
-    if (r == SLOS_OK) r = ws_solve(ws, stream);
-    if (r == SLOS_OK) r = ws_collect(c, ws, outs, retry);
-    if (r != SLOS_OK) {
-      for (const Job& j : jobs) outs[j.k].status = r;
-      return r;
-    }
-    jobs.swap(retry);
-  }
-  for (const Job& j : jobs) {
-    std::memset(&outs[j.k], 0, sizeof(outs[j.k]));
-    outs[j.k].status = SLOS_ERR_CAPACITY;
-  }
-  return SLOS_OK;
+  const int r = solve_rounds(c, ws, planners, inputs, unit_value, outs, stream, std::move(jobs));
+  if (r == SLOS_ERR_RANGE) return SLOS_OK;  // per-instance statuses already set
+  return r;
 }
 }  // namespace
 
@@ -1732,6 +1852,7 @@ extern "C" {
 
 int slos_plan_batch(slos_planner* const* planners, int32_t n, const slos_input* inputs,
                     int32_t unit_value, slos_result* outs, void* stream) {
+  g_err.clear();  // a message always belongs to this call
   for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
   Ctx& c = ctx();
   std::lock_guard<std::mutex> g(c.mu);
@@ -1768,6 +1889,7 @@ void slos_workspace_destroy(slos_workspace* b) {
 
 int slos_workspace_upload(slos_workspace* b, slos_planner* const* planners, int32_t n, const slos_input* inputs,
                       int32_t unit_value, slos_result* outs, void* stream) {
+  g_err.clear();  // a message always belongs to this call
   for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
   Ctx& c = ctx();
   std::lock_guard<std::mutex> g(c.mu);
@@ -1782,12 +1904,14 @@ int slos_workspace_upload(slos_workspace* b, slos_planner* const* planners, int3
 }
 
 int slos_workspace_solve(slos_workspace* b, void* stream) {
+  g_err.clear();  // a message always belongs to this call
   Ctx& c = ctx();
   std::lock_guard<std::mutex> g(c.mu);
   return ws_solve(b->ws, (cudaStream_t)stream);
 }
 
 int slos_workspace_download(slos_workspace* b, slos_result* outs, void* stream) {
+  g_err.clear();  // a message always belongs to this call
   Ctx& c = ctx();
   std::lock_guard<std::mutex> g(c.mu);
   std::vector<Job> retry;
@@ -1814,6 +1938,7 @@ int slos_workspace_download(slos_workspace* b, slos_result* outs, void* stream) 
 }
 
 int slos_workspace_records(slos_workspace* b, slos_record* out, void* stream) {
+  g_err.clear();  // a message always belongs to this call
   Ctx& c = ctx();
   std::lock_guard<std::mutex> g(c.mu);
   Workspace& ws = b->ws;
@@ -1836,6 +1961,13 @@ int slos_workspace_kernel_ms(slos_workspace* b, float* ms2) {
   cudaEventElapsedTime(&all, ws.ev[0], ws.ev[2]);
   ms2[0] = dp_end_ms(ws);
   ms2[1] = all - ms2[0];
+  return SLOS_OK;
+}
+
+int slos_workspace_launches(slos_workspace* b, int64_t* n) {
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  *n = b->ws.launches;
   return SLOS_OK;
 }
 
@@ -1884,6 +2016,7 @@ void slos_result_free(slos_result* r) {
 // ---- tile_gap primitives (K1) ----------------------------------------------
 
 int slos_tile_gap_batch(slos_planner* p, int32_t n, const slos_gap_query* qs, slos_gap_result* outs) {
+  g_err.clear();  // a message always belongs to this call
   for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
   if (n <= 0) return SLOS_OK;
   Ctx& c = ctx();

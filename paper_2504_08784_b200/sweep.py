@@ -51,7 +51,7 @@ class ShardSolver:
         self.lib = lib
         # a stress-family shard (seeds) or any prepared batch (e.g. a recorded corpus)
         self.batch = batch if batch is not None else InstanceBatch.stress(spec.family, list(seeds), spec.slo)
-        self.handle = _Handle(lib, spec.model, spec.slo, spec.cfg)
+        self.handle = _Handle(lib, spec.model, spec.slo, spec.cfg) if spec is not None else None
         self.n = self.batch.n
         self.unit_value = 1 if unit_value else 0
         ws = C.c_void_p()
@@ -107,6 +107,12 @@ class ShardSolver:
         self.lib.slos_workspace_stage_ms(self.ws, ms, 3)
         return [float(x) for x in ms]
 
+    def launches(self) -> int:
+        """Kernels the last solve launched (0 for the CPU checkers)."""
+        n = C.c_int64()
+        self.lib.slos_workspace_launches(self.ws, C.byref(n))
+        return int(n.value)
+
     def download(self, stream=None):
         st = self.lib.slos_workspace_download(self.ws, self._outs, stream)
         if st != abi.SLOS_OK:
@@ -123,19 +129,30 @@ class ShardSolver:
             self.ws = None
 
 
-def gather_records(local, world: int, group=None):
-    """All-gather fixed-size record tensors (uint8 [n, 88]) from every rank."""
+def gather_records(local, world: int, group=None, n_total: int = None):
+    """All-gather fixed-size record tensors (uint8 [n, 88]) from every rank.
+
+    With n_total given, the ranks hold the uneven contiguous shards of
+    shard_range(n_total, r, world): each pads to ceil(n_total / world) rows for
+    the collective and the padding is trimmed after it, so any world size works."""
     import torch
     import torch.distributed as dist
     if world == 1:
         return local
-    out = torch.empty((world * local.shape[0], local.shape[1]), dtype=local.dtype, device=local.device)
+    rows = local.shape[0] if n_total is None else -(-n_total // world)
+    if local.shape[0] != rows:
+        pad = torch.zeros((rows, local.shape[1]), dtype=local.dtype, device=local.device)
+        pad[: local.shape[0]].copy_(local)
+        local = pad
+    out = torch.empty((world * rows, local.shape[1]), dtype=local.dtype, device=local.device)
     if local.is_cuda:
         dist.all_gather_into_tensor(out, local, group=group)
     else:  # gloo (CPU tests)
         parts = list(out.chunk(world, dim=0))
         dist.all_gather(parts, local, group=group)
         out = torch.cat(parts, dim=0)
+    if n_total is not None and rows * world != n_total:
+        out = torch.cat([out[r * rows: r * rows + len(shard_range(n_total, r, world))] for r in range(world)])
     return out
 
 

@@ -60,14 +60,18 @@ def uniforms(seed: int, n: int) -> np.ndarray:
     return out
 
 
-def stress_arrays(spec: StressSpec, seed: int, slo: SloConfig = TWO_TIER_SLO) -> dict:
+def stress_arrays(spec: StressSpec, seed: int, slo: SloConfig = TWO_TIER_SLO, gen=None) -> dict:
+    """G(n_dec, n_new, seed) arrays. `gen` is the generator entry point: the
+    product-side slos_wl_stress by default, or abi.reference_stress_gen() (the
+    reference harness's own std::mt19937_64 draws, oracle/_ref) for bench.py's
+    reference arm, which must not map any repo library."""
     P = C.POINTER
     tp = (C.c_double * len(slo.tpot_tiers_s))(*slo.tpot_tiers_s)
     a = dict(dec_tier=np.zeros(spec.n_dec, np.int32), dec_next_due=np.zeros(spec.n_dec),
              dec_remaining=np.zeros(spec.n_dec, np.int64), new_deadline=np.zeros(spec.n_new),
              new_prefill=np.zeros(spec.n_new, np.int64), new_tier=np.zeros(spec.n_new, np.int32),
              new_memory=np.zeros(spec.n_new, np.int64), new_value=np.zeros(spec.n_new))
-    abi.workload().slos_wl_stress(
+    (gen or abi.workload().slos_wl_stress)(
         seed, spec.n_dec, spec.n_new, 1 if spec.two_tier else 0, tp, spec.now,
         a["dec_tier"].ctypes.data_as(P(C.c_int32)), a["dec_next_due"].ctypes.data_as(P(C.c_double)),
         a["dec_remaining"].ctypes.data_as(P(C.c_int64)),
@@ -152,7 +156,7 @@ class InstanceBatch:
         return out
 
     @classmethod
-    def stress(cls, spec: StressSpec, seeds, slo: SloConfig = TWO_TIER_SLO) -> "InstanceBatch":
+    def stress(cls, spec: StressSpec, seeds, slo: SloConfig = TWO_TIER_SLO, gen=None) -> "InstanceBatch":
         """Vectorised G(...) batch: no per-request Python objects."""
         seeds = list(seeds)
         n = len(seeds)
@@ -167,7 +171,7 @@ class InstanceBatch:
         run = np.zeros(max(1, n * R), abi.RUNNING_DTYPE)
         pen = np.zeros(max(1, n * Pn), abi.PENDING_DTYPE)
         for k, s in enumerate(seeds):
-            a = stress_arrays(spec, s, slo)
+            a = stress_arrays(spec, s, slo, gen)
             rr = run[k * R:(k + 1) * R]
             rr["id"] = base + offs[:R]
             rr["decode_tier"] = a["dec_tier"]

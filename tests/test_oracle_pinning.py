@@ -68,3 +68,22 @@ def test_oracle_matches_live_reference_on_fresh_fuzz():
             a = plan_one(ref, hr.ptr, ci.c, uv)
             b = plan_one(ora, ho.ptr, ci.c, uv)
             assert not diff(a, b), (seed, uv, diff(a, b))
+
+
+def test_oracle_work_counters_equal_instrumented_reference():
+    """T/G/D/S/states (the roofline numerator) of the C oracle equal
+    the counters measured inside the reference itself (oracle/instrument_ref.py:
+    the reference sources patched with counters in a /tmp copy)."""
+    from parity import plan_many
+    from paper_2504_08784_b200 import workload as W
+    from paper_2504_08784_b200.planner import _Handle
+    g = load("counters")
+    ora = abi.oracle()
+    for fam, take in (("C1", 16), ("LAT", 16), ("C3", 16), ("C2", 8)):
+        F = W.FAMILIES[fam]
+        seeds = g[fam]["seeds"][:take]
+        b = W.InstanceBatch.stress(F["spec"], seeds)
+        h = _Handle(ora, F["model"], W.TWO_TIER_SLO, F["cfg"])
+        res = plan_many(ora, h.ptr, b)
+        for k, r in enumerate(res):
+            assert list(r["counters"]) == g[fam]["counters"][k], (fam, seeds[k])

@@ -134,3 +134,96 @@ def test_c5_corpus_tiled_matches_reference():
         res = plan_many(prod, h.ptr, b)
         for k, got in enumerate(res):
             _cmp(got, G["ref"][k % base.n], f"c5 {g} tiled instance {k}")
+
+
+def test_work_counters_equal_instrumented_reference():
+    """The product's T/G/D/S/states equal the counters measured inside the
+    reference itself (tests/golden/counters.json.gz, oracle/instrument_ref.py):
+    C2 bench seeds 0..63, C1/LAT/C3 stress seeds, C4 seeds 0..7."""
+    from golden_io import load
+    g = load("counters")
+    prod = abi.product()
+    for fam, G in g.items():
+        F = W.FAMILIES[fam]
+        b = W.InstanceBatch.stress(F["spec"], G["seeds"])
+        h = _Handle(prod, F["model"], W.TWO_TIER_SLO, F["cfg"])
+        res = plan_many(prod, h.ptr, b)
+        bad = [(G["seeds"][k], list(r["counters"]), G["counters"][k]) for k, r in enumerate(res)
+               if list(r["counters"]) != G["counters"][k]]
+        assert not bad, (fam, bad[:3])
+
+
+def test_c4_32_seeds_pipelined_match_reference():
+    """C4 (2032 running decoders, budget 8192, b200-synthetic model) on all 32 golden
+    seeds, tiled x16 = 512 instances so slos_plan_batch runs its two-chunk pipeline
+    with two stream-pipelined solve parts and the 256-thread reconstruction."""
+    from golden_checks import _cmp
+    from golden_io import load
+    st = load("stress")["C4"]
+    assert len(st["seeds"]) >= 32
+    F = W.FAMILIES["C4"]
+    base = W.InstanceBatch.stress(F["spec"], st["seeds"])
+    b = base.tiled(16)
+    prod = abi.product()
+    h = _Handle(prod, F["model"], W.TWO_TIER_SLO, F["cfg"])
+    res = plan_many(prod, h.ptr, b)
+    for k, got in enumerate(res):
+        _cmp(got, st["ref"][k % base.n], f"C4 seed {st['seeds'][k % base.n]} (tile {k // base.n})")
+
+
+def test_device_resident_workspace_path_matches_reference():
+    """The path bench.py's `value` times: slos_workspace_upload once, solve twice
+    (the second solve re-runs the resident batch), download -- C2 x 1024 (seeds
+    0..1023) against the compiled reference, every field bit-exact, plus the
+    88-byte records the multi-GPU gather carries."""
+    import ctypes as C
+    import os
+
+    import torch
+    from parity import canon_c
+    from paper_2504_08784_b200.sweep import ShardSolver, ShardSpec, records_view
+    if not os.path.exists(abi.REF_LIB):
+        pytest.skip("oracle/_ref not built")
+    F = W.FAMILIES["C2"]
+    prod, ref = abi.product(), abi.reference()
+    solver = ShardSolver(prod, ShardSpec(F["spec"], F["model"], F["cfg"]), range(1024))
+    stream = torch.cuda.Stream()
+    rec = torch.empty((1024, C.sizeof(abi.Record)), dtype=torch.uint8, device="cuda")
+    solver.upload(stream.cuda_stream)
+    solver.converge(rec, stream.cuda_stream)
+    solver.solve(stream.cuda_stream)
+    solver.records(rec.data_ptr(), stream.cuda_stream)
+    outs = solver.download(stream.cuda_stream)
+    P = [canon_c(outs[k]) for k in range(1024)]
+    solver.free_results()
+    solver.close()
+    hr = _Handle(ref, F["model"], W.TWO_TIER_SLO, F["cfg"])
+    R = plan_many(ref, hr.ptr, solver.batch)
+    bad = [(k, diff(P[k], R[k])) for k in range(1024) if diff(P[k], R[k])]
+    assert not bad, bad[:4]
+    torch.cuda.synchronize()
+    rv = records_view(rec)
+    for k in (0, 1, 511, 1023):
+        assert rv["n_admitted"][k] == len(R[k]["admitted"]) and rv["n_entries"][k] == len(R[k]["entries"])
+        assert rv["status"][k] == 0
+
+
+def test_long_deadline_span_is_isolated():
+    """An instance whose pending deadline lies far in the future needs a wide slot
+    grid. It is solved in its own slot class: it must not resize (or fail) the
+    launch of the ordinary instances beside it. A span of 80 s (1,608 slots at the
+    50 ms tier) still plans bit-exactly like the oracle; a span of 5,000 s (100k
+    slots, more than a CTA's shared memory) is a per-instance SLOS_ERR_RANGE."""
+    F = W.FAMILIES["C1"]
+    ins = [W.stress_instance(F["spec"], s) for s in range(6)]
+    ins[2].pending[3].prefill_deadline = ins[2].now + 80.0
+    ins[4].pending[0].prefill_deadline = ins[4].now + 5000.0
+    b = W.InstanceBatch.from_inputs(ins)
+    prod, ora = abi.product(), abi.oracle()
+    hp, ho = _Handle(prod, F["model"], W.TWO_TIER_SLO, F["cfg"]), _Handle(ora, F["model"], W.TWO_TIER_SLO, F["cfg"])
+    P = plan_many(prod, hp.ptr, b)
+    keep = [0, 1, 2, 3, 5]
+    O = plan_many(ora, ho.ptr, b.subset(keep))
+    for x, k in enumerate(keep):
+        assert not diff(P[k], O[x], counters=True), (k, diff(P[k], O[x], counters=True))
+    assert P[4]["status"] == abi.SLOS_ERR_RANGE

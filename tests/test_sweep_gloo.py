@@ -73,3 +73,39 @@ def test_two_rank_gather_equals_single_process(tmp_path):
     solver.close()
     assert got.tobytes() == want.tobytes()
     assert (got["status"] == 0).all() and got["n_entries"].min() > 0
+
+
+def _uneven_worker(rank, world, port, outdir, n_total):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lib = abi.oracle()
+    mine = shard_range(n_total, rank, world)
+    solver = ShardSolver(lib, _spec(), mine)
+    solver.upload()
+    solver.solve()
+    rec = torch.zeros((len(mine), C.sizeof(abi.Record)), dtype=torch.uint8)
+    solver.records(rec.data_ptr())
+    allrec = gather_records(rec, world, n_total=n_total)
+    if rank == 0:
+        np.save(os.path.join(outdir, "gathered.npy"), allrec.numpy())
+    solver.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_three_rank_uneven_strong_scaling_gather(tmp_path):
+    """Strong scaling with a total the world size does not divide (7 over 3 ranks:
+    shards of 3, 2, 2): the padded gather returns exactly the 7 records in order."""
+    world, n_total = 3, 7
+    mp.spawn(_uneven_worker, args=(world, _free_port(), str(tmp_path), n_total), nprocs=world, join=True)
+    got = np.load(tmp_path / "gathered.npy").reshape(-1).view(abi.RECORD_DTYPE)
+    lib = abi.oracle()
+    solver = ShardSolver(lib, _spec(), range(n_total))
+    solver.upload()
+    solver.solve()
+    rec = torch.zeros((n_total, C.sizeof(abi.Record)), dtype=torch.uint8)
+    solver.records(rec.data_ptr())
+    want = records_view(rec)
+    solver.close()
+    assert len(got) == n_total and got.tobytes() == want.tobytes()
