@@ -667,10 +667,10 @@ def run_ours(args):
         achieved = alg / dp_avg_s / 1e9
         probe = smem_peak()
         nominal = 148 * 128 * f_mhz * 1e6 / 1e9
-        if probe:  # measured LDS.128 bandwidth, scaled to the clock the DP ran at
-            peak = probe[0] * (f_mhz / probe[1]) if probe[1] > 0 else probe[0]
-            peak_src = (f"measured: libslos_probe.so LDS.128 stream on all SMs, {probe[0]:.0f} GB/s at "
-                        f"{probe[1]:.0f} MHz, scaled to the median SM clock under load")
+        if probe:  # measured LDS.128 bandwidth (the probe runs at the same boost clock)
+            peak = probe[0]
+            peak_src = (f"measured: libslos_probe.so LDS.128 stream on all SMs, {probe[0]:.0f} GB/s "
+                        f"(probe SM clock estimate {probe[1]:.0f} MHz)")
         else:
             peak, peak_src = nominal, "nominal 148 SM x 128 B/clk x median SM clock (probe not built)"
         ncu = load_ncu_traffic()

@@ -1769,7 +1769,8 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
   std::vector<Job> jobs, retry;
   std::vector<std::pair<double, int>> wide;
   {
-    thread_local std::vector<double> need;
+    thread_local std::vector<double> need_tl;  // the workers see it through the reference
+    std::vector<double>& need = need_tl;
     need.resize((size_t)n);
     HostPool::get().run(n, [&](int lo, int hi) {
       for (int k = lo; k < hi; ++k) need[k] = slot_need(planners[k], &inputs[k]);

@@ -5,7 +5,7 @@
 // measures what the pipe actually delivers on the box: every CTA streams 16-byte
 // conflict-free loads (LDS.128) out of a 16 KB shared buffer, 8 CTAs of 256 threads
 // per SM on all SMs, timed with CUDA events, with the SM clock measured in the same
-// launch (clock64 delta / elapsed time). bench.py reads it once per run.
+// launch (the longest CTA's clock64 delta / elapsed time). bench.py reads it once per run.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kThreads) smem_read_kernel(int iters, uint4* s
   }
   const long long t1 = clock64();
   if (acc.x == 0x12345678u && acc.y == 1u) sink[blockIdx.x] = acc;  // keep the loads
-  if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = t1 - t0;
+  if (threadIdx.x == 0) atomicMax((unsigned long long*)cycles, (unsigned long long)(t1 - t0));
 }
 
 }  // namespace
@@ -54,6 +54,7 @@ extern "C" int slos_probe_smem(int iters, double* gbs, double* sm_mhz) {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   smem_read_kernel<<<grid, kThreads>>>(iters / 8, sink, cyc);  // warm-up
+  cudaMemset(cyc, 0, sizeof(long long));
   cudaEventRecord(a);
   smem_read_kernel<<<grid, kThreads>>>(iters, sink, cyc);
   cudaEventRecord(b);
@@ -64,7 +65,7 @@ extern "C" int slos_probe_smem(int iters, double* gbs, double* sm_mhz) {
   cudaMemcpy(&c, cyc, sizeof c, cudaMemcpyDeviceToHost);
   const double bytes = (double)grid * kThreads * (double)iters * 4.0 * sizeof(uint4);
   *gbs = bytes / (ms * 1e-3) / 1e9;
-  *sm_mhz = (double)c / (ms * 1e-3) / 1e6;  // one CTA's loop ~ the whole launch
+  *sm_mhz = (double)c / (ms * 1e-3) / 1e6;  // the longest CTA's loop ~ the whole launch (one wave)
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(sink);
