@@ -293,6 +293,30 @@ int slos_workspace_launches(slos_workspace* ws, int64_t* n);
  * slos_plan_batch / slos_workspace_* sequence. */
 void slos_last_transfer_bytes(int64_t* h2d, int64_t* d2h);
 
+/* ---- the plan broker: concurrent schedule() calls -> one batched launch --------
+ * The reference calls `Scheduler::schedule` synchronously, one replica at a time
+ * (sim_executor.cpp:344); many replicas / simulations / sweep points running in
+ * their own threads each block in schedule(). The broker turns those concurrent
+ * calls into ONE slos_plan_batch (SURVEY.md §8 b: "a broker aggregates concurrent
+ * schedule() calls into one launch").
+ * Protocol: a client thread is ACTIVE while it computes and may still call
+ * slos_broker_plan. slos_broker_join() marks the calling client active,
+ * slos_broker_leave() marks it inactive (it will not plan until it joins again).
+ * slos_broker_plan() queues one plan and blocks the (still registered) client;
+ * as soon as no registered client is active, the thread that made it so runs
+ * every queued plan as one batch and wakes their callers, which are active again.
+ * Results are exactly those of slos_plan (plans are independent). The CPU
+ * checkers implement slos_broker_plan as an immediate slos_plan. */
+typedef struct slos_broker slos_broker;
+int slos_broker_create(int32_t unit_value, slos_broker** out);
+void slos_broker_destroy(slos_broker* broker);
+void slos_broker_join(slos_broker* broker);
+void slos_broker_leave(slos_broker* broker);
+int slos_broker_plan(slos_broker* broker, slos_planner* planner, const slos_input* input,
+                     slos_result* out);
+/* flushes = batched launches so far, plans = plans served */
+void slos_broker_stats(slos_broker* broker, int64_t* flushes, int64_t* plans);
+
 /* ---- batch planner primitives (batch_planner.hpp:68-134, perf_model.hpp:25-61) */
 
 typedef struct slos_decode_member { /* DecodeMember batch_planner.hpp:19-25 */

@@ -531,6 +531,28 @@ int slos_workspace_kernel_ms(slos_workspace* b, float* ms2) {
   ms2[1] = 0.0f;
   return SLOS_OK;
 }
+// ---- plan broker: the CPU reference plans immediately (no batching) ----
+struct slos_broker {
+  int32_t unit_value = 0;
+  std::atomic<int64_t> plans{0};
+};
+int slos_broker_create(int32_t unit_value, slos_broker** out) {
+  *out = new slos_broker();
+  (*out)->unit_value = unit_value;
+  return SLOS_OK;
+}
+void slos_broker_destroy(slos_broker* b) { delete b; }
+void slos_broker_join(slos_broker* b) { (void)b; }
+void slos_broker_leave(slos_broker* b) { (void)b; }
+int slos_broker_plan(slos_broker* b, slos_planner* p, const slos_input* in, slos_result* out) {
+  b->plans.fetch_add(1);
+  return slos_plan(p, in, b->unit_value, out);
+}
+void slos_broker_stats(slos_broker* b, int64_t* flushes, int64_t* plans) {
+  *plans = b->plans.load();
+  *flushes = *plans;
+}
+
 void slos_last_transfer_bytes(int64_t* h2d, int64_t* d2h) {
   *h2d = 0;
   *d2h = 0;

@@ -1750,6 +1750,29 @@ int slos_workspace_kernel_ms(slos_workspace* b, float* ms2) {
   ms2[1] = 0.0f;
   return SLOS_OK;
 }
+/* ---- plan broker: the CPU checker plans immediately (no batching) ---- */
+struct slos_broker {
+  int32_t unit_value;
+  int64_t plans;
+};
+int slos_broker_create(int32_t unit_value, slos_broker** out) {
+  *out = (slos_broker*)calloc(1, sizeof(slos_broker));
+  if (!*out) return SLOS_ERR_ALLOC;
+  (*out)->unit_value = unit_value;
+  return SLOS_OK;
+}
+void slos_broker_destroy(slos_broker* b) { free(b); }
+void slos_broker_join(slos_broker* b) { (void)b; }
+void slos_broker_leave(slos_broker* b) { (void)b; }
+int slos_broker_plan(slos_broker* b, slos_planner* p, const slos_input* in, slos_result* out) {
+  __atomic_fetch_add(&b->plans, 1, __ATOMIC_RELAXED);
+  return slos_plan(p, in, b->unit_value, out);
+}
+void slos_broker_stats(slos_broker* b, int64_t* flushes, int64_t* plans) {
+  *plans = __atomic_load_n(&b->plans, __ATOMIC_RELAXED);
+  *flushes = *plans;
+}
+
 void slos_last_transfer_bytes(int64_t* h2d, int64_t* d2h) {
   *h2d = 0;
   *d2h = 0;

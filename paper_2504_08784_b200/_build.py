@@ -40,7 +40,7 @@ def _stale(target, sources):
 def build_product(force: bool = False, verbose: bool = False) -> str:
     out = os.path.join(PKG, "libslos_b200.so")
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
-        os.path.join(ROOT, "include", h) for h in ("slos_planner.h", "slos_plan_json.h")]
+        os.path.join(ROOT, "include", h) for h in ("slos_planner.h", "slos_plan_json.h", "slos_route.h")]
     if not force and not _stale(out, deps):
         return out
     bdir = os.path.join(PKG, "build")
@@ -53,7 +53,9 @@ def build_product(force: bool = False, verbose: bool = False) -> str:
     _run([NVCC, *ARCH, *NVFLAGS, "-x", "cu", "-c", os.path.join(CSRC, "slos_host.cpp"), "-o", ho])
     jo = os.path.join(bdir, "slos_json.o")  # host-only: plan_to_json serialisation
     _run(["g++", "-std=c++17", "-O2", "-fPIC", "-c", os.path.join(CSRC, "slos_json.cpp"), "-o", jo])
-    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xlinker", "-Bsymbolic", ko, ho, jo, "-o", out,
+    ro = os.path.join(bdir, "slos_route.o")  # host-only: batched routing rounds over slos_plan_batch
+    _run(["g++", "-std=c++17", "-O2", "-fPIC", "-c", os.path.join(CSRC, "slos_route.cpp"), "-o", ro])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xlinker", "-Bsymbolic", ko, ho, jo, ro, "-o", out,
           "-lpthread", "-ldl", "-lrt"])
     return out
 
@@ -87,9 +89,17 @@ def build_oracle(force: bool = False) -> str:
     return os.path.join(odir, "liboracle_slos.so")
 
 
+def build_integration(force: bool = False) -> None:
+    """integration/_build/libslos_lockstep.so: the lockstep routing / sweep driver over
+    the reference's simulator sources (compiled where they lie), when present."""
+    if os.path.isdir(os.environ.get("SLOS_REF", "/root/reference/proj")):
+        _run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "integration")])
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_workload(force)
     build_oracle(force)
+    build_integration(force)
     build_product(force, verbose)
     build_probe(force)
 

@@ -1992,6 +1992,97 @@ int slos_workspace_stage_ms(slos_workspace* b, float* ms, int32_t n) {
   return SLOS_OK;
 }
 
+// ---- the plan broker (include/slos_planner.h) --------------------------------
+}  // extern "C"
+
+struct slos_broker {
+  struct Req {
+    slos_planner* p;
+    slos_input in;
+    slos_result* out;
+    bool done;
+  };
+  std::mutex mu;
+  std::condition_variable cv;
+  int32_t unit_value = 0;
+  int active = 0;
+  bool flushing = false;
+  std::vector<Req*> queue;
+  int64_t flushes = 0, plans = 0;
+};
+
+namespace {
+// Called with the lock held by the thread that made `active` reach zero: run every
+// queued plan as one slos_plan_batch (outside the lock, so clients may keep queueing
+// for the next batch), then wake the callers, which are active again.
+void broker_flush(slos_broker* b, std::unique_lock<std::mutex>& lk) {
+  while (b->active == 0 && !b->flushing && !b->queue.empty()) {
+    b->flushing = true;
+    std::vector<slos_broker::Req*> batch;
+    batch.swap(b->queue);
+    lk.unlock();
+    const int n = (int)batch.size();
+    std::vector<slos_planner*> ps((size_t)n);
+    std::vector<slos_input> ins((size_t)n);
+    std::vector<slos_result> outs((size_t)n);
+    for (int k = 0; k < n; ++k) {
+      ps[k] = batch[k]->p;
+      ins[k] = batch[k]->in;
+    }
+    const int st = slos_plan_batch(ps.data(), n, ins.data(), b->unit_value, outs.data(), nullptr);
+    lk.lock();
+    for (int k = 0; k < n; ++k) {
+      *batch[k]->out = outs[k];
+      if (st != SLOS_OK && outs[k].status == SLOS_OK) batch[k]->out->status = st;
+      batch[k]->done = true;
+    }
+    b->active += n;
+    b->flushing = false;
+    b->flushes += 1;
+    b->plans += n;
+    b->cv.notify_all();
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int slos_broker_create(int32_t unit_value, slos_broker** out) {
+  *out = new slos_broker();
+  (*out)->unit_value = unit_value;
+  return SLOS_OK;
+}
+
+void slos_broker_destroy(slos_broker* b) { delete b; }
+
+void slos_broker_join(slos_broker* b) {
+  std::lock_guard<std::mutex> g(b->mu);
+  b->active += 1;
+}
+
+void slos_broker_leave(slos_broker* b) {
+  std::unique_lock<std::mutex> lk(b->mu);
+  b->active -= 1;
+  broker_flush(b, lk);
+}
+
+int slos_broker_plan(slos_broker* b, slos_planner* p, const slos_input* in, slos_result* out) {
+  std::unique_lock<std::mutex> lk(b->mu);
+  slos_broker::Req r{p, *in, out, false};
+  b->queue.push_back(&r);
+  b->active -= 1;
+  broker_flush(b, lk);
+  b->cv.wait(lk, [&] { return r.done; });
+  if (out->status != SLOS_OK && g_err.empty()) set_err(out->status, "plan failed");
+  return out->status;
+}
+
+void slos_broker_stats(slos_broker* b, int64_t* flushes, int64_t* plans) {
+  std::lock_guard<std::mutex> g(b->mu);
+  *flushes = b->flushes;
+  *plans = b->plans;
+}
+
 void slos_last_transfer_bytes(int64_t* h2d, int64_t* d2h) {
   *h2d = g_h2d;
   *d2h = g_d2h;

@@ -156,29 +156,36 @@ class InstanceBatch:
         return out
 
     @classmethod
-    def stress(cls, spec: StressSpec, seeds, slo: SloConfig = TWO_TIER_SLO, gen=None) -> "InstanceBatch":
-        """Vectorised G(...) batch: no per-request Python objects."""
+    def stress(cls, spec: StressSpec, seeds, slo: SloConfig = TWO_TIER_SLO, gen=None,
+               unique_ids: bool = False) -> "InstanceBatch":
+        """Vectorised G(...) batch: no per-request Python objects. With unique_ids
+        every instance's ids carry an "i<k>/" prefix (requests that move between
+        instances, e.g. routed to another replica, stay distinguishable)."""
         seeds = list(seeds)
         n = len(seeds)
         R, Pn = spec.n_dec, spec.n_new
         rid = [f"run-{i}".encode() + b"\0" for i in range(R)]
         pid = [f"new-{i}".encode() + b"\0" for i in range(Pn)]
-        # ids are identical across instances: one copy, shared pointers
-        blob = np.frombuffer(b"".join(rid + pid) + b"\0", np.uint8).copy()
-        lens = [len(x) for x in rid + pid]
+        if unique_ids:
+            names = [f"i{k}/".encode() + x for k in range(n) for x in rid + pid]
+        else:  # ids are identical across instances: one copy, shared pointers
+            names = rid + pid
+        blob = np.frombuffer(b"".join(names) + b"\0", np.uint8).copy()
+        lens = [len(x) for x in names]
         offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
         base = np.uint64(blob.ctypes.data)
         run = np.zeros(max(1, n * R), abi.RUNNING_DTYPE)
         pen = np.zeros(max(1, n * Pn), abi.PENDING_DTYPE)
         for k, s in enumerate(seeds):
             a = stress_arrays(spec, s, slo, gen)
+            o = offs[k * (R + Pn):(k + 1) * (R + Pn)] if unique_ids else offs
             rr = run[k * R:(k + 1) * R]
-            rr["id"] = base + offs[:R]
+            rr["id"] = base + o[:R]
             rr["decode_tier"] = a["dec_tier"]
             rr["next_due_s"] = a["dec_next_due"]
             rr["decode_remaining"] = a["dec_remaining"]
             pp = pen[k * Pn:(k + 1) * Pn]
-            pp["id"] = base + offs[R:]
+            pp["id"] = base + o[R:]
             pp["prefill_deadline"] = a["new_deadline"]
             pp["prefill_tokens"] = a["new_prefill"]
             pp["decode_tier"] = a["new_tier"]
