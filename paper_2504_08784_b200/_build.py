@@ -37,20 +37,22 @@ def _stale(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def build_product(force: bool = False, verbose: bool = False) -> str:
-    out = os.path.join(PKG, "libslos_b200.so")
+def build_product(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """The product library; `defines`/`out` build an experiment variant elsewhere
+    (e.g. -DSLOS_DP_THREADS=128 into exp/, selected with SLOS_PRODUCT_LIB)."""
+    out = out or os.path.join(PKG, "libslos_b200.so")
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
         os.path.join(ROOT, "include", h) for h in ("slos_planner.h", "slos_plan_json.h", "slos_route.h")]
     if not force and not _stale(out, deps):
         return out
-    bdir = os.path.join(PKG, "build")
+    bdir = os.path.join(PKG, "build") if not defines else os.path.join(os.path.dirname(out), "build")
     os.makedirs(bdir, exist_ok=True)
     ko = os.path.join(bdir, "slos_kernels.o")
     ho = os.path.join(bdir, "slos_host.o")
-    k = _run([NVCC, *ARCH, *NVFLAGS, "-Xptxas", "-v", "-c", os.path.join(CSRC, "slos_kernels.cu"), "-o", ko])
+    k = _run([NVCC, *ARCH, *NVFLAGS, *defines, "-Xptxas", "-v", "-c", os.path.join(CSRC, "slos_kernels.cu"), "-o", ko])
     if verbose:
         sys.stderr.write(k.stderr)
-    _run([NVCC, *ARCH, *NVFLAGS, "-x", "cu", "-c", os.path.join(CSRC, "slos_host.cpp"), "-o", ho])
+    _run([NVCC, *ARCH, *NVFLAGS, *defines, "-x", "cu", "-c", os.path.join(CSRC, "slos_host.cpp"), "-o", ho])
     jo = os.path.join(bdir, "slos_json.o")  # host-only: plan_to_json serialisation
     _run(["g++", "-std=c++17", "-O2", "-fPIC", "-c", os.path.join(CSRC, "slos_json.cpp"), "-o", jo])
     ro = os.path.join(bdir, "slos_route.o")  # host-only: batched routing rounds over slos_plan_batch

@@ -567,9 +567,9 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
   const int tid = G::rank();
   OutHdr* out = &A.out[inst];
   if (out->status != 0) return;
+  block_copy_struct(sh.P, A.planners[A.inst[inst].planner], tid, G::kSize);
+  block_copy_struct(sh.I, A.inst[inst], tid, G::kSize);
   if (tid == 0) {
-    sh.P = A.planners[A.inst[inst].planner];
-    sh.I = A.inst[inst];
     sh.err = 0;
     sh.n_batch = 0;
     sh.n_entry = 0;
@@ -680,6 +680,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
       if (tid == 0) sh.err = 0;
     }
     if (!fallback) {  // decode tail :302-349
+      SLOS_BPHASE(0);  // 0: setup / previous gap bookkeeping
       const double t_last = sh.bounds[sh.nb - 1];
       const int m = build_members_at<G>(A, sh, t_last, pull, E);
       double tl = 0.0, capv = 0.0;
@@ -703,12 +704,14 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
         sh.m1 = mm;
       }
       G::sync();
+      SLOS_BPHASE(1);  // 1: census (members_at + chain lines)
       const double tlen = quantize_gap(tail_len);
       if (tlen > kTimeEps && sh.m1 > 0) {
         MemBuf EE = E;
         EE.M = sh.m1;
         Arena ar2 = ar;
         block_tile_gap<G>(P, sh.bs, tlen, tail_len, zero, EE, true, ar2, sh.o, sh.tmp);
+        SLOS_BPHASE(2);  // 2: tile_gap
         if (sh.o.status) {
           if (tid == 0) { out->status = sh.o.status; out->need_work = sh.o.need_work; }
           return;
@@ -719,6 +722,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
         }
         if (!sh.o.feasible) fallback = true;
         else emit_gap<G>(A, sh, t_last, false, ar);
+        SLOS_BPHASE(3);  // 3: emission
       }
     }
     SLOS_BPHASE(4);  // 4: decode tail
@@ -773,8 +777,11 @@ constexpr int kBuildThreads = 128;
 #ifndef SLOS_BUILD_MIN_BLOCKS
 #define SLOS_BUILD_MIN_BLOCKS 3
 #endif
+#ifndef SLOS_BUILD_WARP_MIN_BLOCKS
+#define SLOS_BUILD_WARP_MIN_BLOCKS 4
+#endif
 
-__global__ void __launch_bounds__(32 * kBuildWarps, 2) build_kernel_warp(BuildParams prm) {
+__global__ void __launch_bounds__(32 * kBuildWarps, SLOS_BUILD_WARP_MIN_BLOCKS) build_kernel_warp(BuildParams prm) {
   const BatchArgs& A = prm.a;
   __shared__ BuildShared shs[kBuildWarps];
   extern __shared__ __align__(16) unsigned char bsm[];

@@ -219,4 +219,14 @@ __device__ inline SpecSol solve_spec(const PlannerDev& P, const int64_t* counts)
   return best;
 }
 
+// Cooperative copy of a header struct (planner, instance) into shared memory:
+// nt threads, 8-byte words (one thread copying ~1 KB serialises ~100 loads).
+template <class T>
+__device__ __forceinline__ void block_copy_struct(T& dst, const T& src, int tid, int nt) {
+  static_assert(sizeof(T) % 8 == 0, "8-byte words");
+  const uint64_t* s = (const uint64_t*)&src;
+  uint64_t* d = (uint64_t*)&dst;
+  for (int k = tid; k < (int)(sizeof(T) / 8); k += nt) d[k] = s[k];
+}
+
 }  // namespace slos

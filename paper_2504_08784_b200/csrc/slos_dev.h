@@ -65,6 +65,7 @@ struct InstDev {
   int32_t build_kind;       // plan reconstruction: 0 one warp, 1 a 128-thread CTA, 2 a 256-thread CTA
   int32_t part;             // solve part (dp + build launched per part, pipelined)
   int32_t direct;           // Pareto buckets through a direct count-vector table (dp_kernel)
+  int32_t has_shared;       // some DP pair's memo key recurs: dp_kernel clears its memo slice
   int32_t dstride[kMaxTiers];  // its strides: index = sum_l count_l * dstride[l]
   int64_t off_dec;     // into dec_* arrays
   int64_t off_chain;   // into ch_* arrays (N items, suffix has N+1)

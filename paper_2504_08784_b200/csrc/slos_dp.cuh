@@ -27,7 +27,10 @@ namespace slos {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-constexpr int kDpThreads = 256;
+#ifndef SLOS_DP_THREADS
+#define SLOS_DP_THREADS 256
+#endif
+constexpr int kDpThreads = SLOS_DP_THREADS;
 constexpr int kNumPhases = 12;
 
 // Optional per-phase cycle accounting (DpParams.phase_cycles != nullptr): thread 0
@@ -49,20 +52,21 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 }
 
 // ---- block-wide helpers (kDpThreads threads) --------------------------------
+template <int NW>
 __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* wsum, int64_t* total) {
   const int lane = lane_id(), w = warp_id();
   const int64_t inc = warp_incl_scan(v);
   if (lane == 31) wsum[w] = inc;
   __syncthreads();
   if (w == 0) {
-    int64_t x = lane < kDpWarps ? wsum[lane] : 0;
+    int64_t x = lane < NW ? wsum[lane] : 0;
     const int64_t xi = warp_incl_scan(x);
-    if (lane < kDpWarps) wsum[lane] = xi - x;
-    if (lane == kDpWarps - 1) wsum[kDpWarps] = xi;
+    if (lane < NW) wsum[lane] = xi - x;
+    if (lane == NW - 1) wsum[NW] = xi;
   }
   __syncthreads();
   const int64_t r = inc - v + wsum[w];
-  *total = wsum[kDpWarps];
+  *total = wsum[NW];
   __syncthreads();
   return r;
 }
@@ -408,13 +412,6 @@ __device__ inline void block_build_anchor(const PlannerDev& P, const DecView& D,
 }
 
 // Cooperative copy of a plain struct into shared memory (8-byte words, all threads).
-template <class T>
-__device__ __forceinline__ void block_copy_struct(T& dst, const T& src, int tid, int nt) {
-  static_assert(sizeof(T) % 8 == 0, "8-byte words");
-  const uint64_t* s = (const uint64_t*)&src;
-  uint64_t* d = (uint64_t*)&dst;
-  for (int k = tid; k < (int)(sizeof(T) / 8); k += nt) d[k] = s[k];
-}
 
 // Anchor due pass (replaces the per-group member walks of E2): every exact member's
 // due line from anchor a is walked ONCE, up to the longest due horizon of any group
@@ -793,20 +790,27 @@ __global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm
 #ifndef SLOS_DP_MIN_BLOCKS
 #define SLOS_DP_MIN_BLOCKS 4
 #endif
-__global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpParams prm) {
+// NT threads per CTA, chain levels up to MAXC. dp_kernel is the 256-thread form;
+// dp_kernel_small (64 threads, 16 CTAs per SM) takes instances whose levels are a
+// few dozen candidates (the C5 sweep family): the DP is a level-sequential latency
+// chain, so throughput follows the instances resident per SM, not threads per instance.
+template <int NT, int MINB, int MAXC>
+__device__ __forceinline__ void dp_body(const DpParams& prm) {
+  constexpr int kDpThreads = NT;
+  constexpr int kDpWarps = NT / 32;
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;
-  __shared__ int64_t lvl_off[SLOS_MAX_CHAIN + 2];
-  __shared__ int32_t lvl_cnt[SLOS_MAX_CHAIN + 2];
-  __shared__ int32_t lvl_boff[SLOS_MAX_CHAIN + 2];  // per level: first surviving-bucket slot
-  __shared__ int32_t lvl_nsb[SLOS_MAX_CHAIN + 2];   // per level: surviving buckets
-  __shared__ int32_t s_pre[SLOS_MAX_CHAIN + 2];     // candidate prefix over source levels
-  __shared__ int32_t s_kpre[SLOS_MAX_CHAIN + 2];    // fresh-key prefix over source levels
-  __shared__ uint8_t s_sh[SLOS_MAX_CHAIN + 2];      // source level's pair is memo-shared
+  __shared__ int64_t lvl_off[MAXC + 2];
+  __shared__ int32_t lvl_cnt[MAXC + 2];
+  __shared__ int32_t lvl_boff[MAXC + 2];  // per level: first surviving-bucket slot
+  __shared__ int32_t lvl_nsb[MAXC + 2];   // per level: surviving buckets
+  __shared__ int32_t s_pre[MAXC + 2];     // candidate prefix over source levels
+  __shared__ int32_t s_kpre[MAXC + 2];    // fresh-key prefix over source levels
+  __shared__ uint8_t s_sh[MAXC + 2];      // source level's pair is memo-shared
   __shared__ int64_t s_wsum[kDpWarps + 1];
   __shared__ unsigned long long s_ctr[5];
-  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_nw, s_bovf, s_anysh, s_nsb;
+  __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_nw, s_bovf, s_anysh, s_nsb, s_bkinit;
   __shared__ int64_t s_next_free, s_arena_next, s_bnext;
   __shared__ __align__(8) uint64_t s_mbar;  // completion of a level's record staging (TMA bulk copies)
 
@@ -814,14 +818,15 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   const int tid = threadIdx.x;
   const int inst = A.order[prm.blk0 + blockIdx.x];
   OutHdr* out = &A.out[inst];
+  block_copy_struct(sI, A.inst[inst], tid, kDpThreads);  // 8-byte words, every thread
+  block_copy_struct(sP, A.planners[A.inst[inst].planner], tid, kDpThreads);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_mbar)), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
-    sP = A.planners[A.inst[inst].planner];
-    sI = A.inst[inst];
     s_err = 0;
     s_ovf = 0;
     s_n_used = 0;
+    s_bkinit = 0;
     for (int k = 0; k < 5; ++k) s_ctr[k] = 0;
   }
   __syncthreads();
@@ -926,6 +931,11 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   unsigned char* GR = A.groups + I.off_group;
   const int64_t capC = I.cap_cand;
 
+  if (I.has_shared) {  // the instance's memo table starts empty (state 0), 8-byte words
+    uint64_t* mw = (uint64_t*)Memo;
+    const int64_t nw = I.cap_memo * (int64_t)(sizeof(MemoEnt) / 8);
+    for (int64_t x = tid; x < nw; x += kDpThreads) mw[x] = 0ull;
+  }
   if (tid == 0) {
     Sc_[0] = 0; Sm_[0] = 0; Sp_[0] = 0; Sv_[0] = 0.0; Sn_[0] = 0; Spar[0] = -1; Sar[0] = 0; Sit[0] = -1;
     Ssb[0] = 0; Bc[0] = 0;
@@ -1246,8 +1256,11 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
     }
     if (sm && !I.direct) {  // fresh level-local bucket table
       for (int x = tid; x < capB; x += kDpThreads) { Bkey[x] = 0ull; Bval[x] = -1; }
+    } else if (!sm && !I.direct && !s_bkinit) {  // first HBM level: clear the instance's
+      for (int64_t x = tid; x < capB; x += kDpThreads) { Bkey[x] = 0ull; Bval[x] = -1; }  // hash once
     }
     __syncthreads();
+    if (!sm && !I.direct && tid == 0) s_bkinit = 1;  // later HBM levels reset the slots they claim
     if (s_err) break;
     SLOS_PHASE(8);  // 8: candidate states
     // ---- 5: Pareto buckets ----
@@ -1533,7 +1546,7 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
           const int b = base + tid;
           const int64_t x = b < NB ? cntB[b] : 0;
           int64_t tot;
-          const int64_t ex = block_excl_scan(x, s_wsum, &tot);
+          const int64_t ex = block_excl_scan<kDpWarps>(x, s_wsum, &tot);
           if (b < NB) { offB[b] = (int32_t)(carry + ex); cntB[b] = 0; }
           carry += tot;
         }
@@ -1832,6 +1845,23 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
   }
   SLOS_PHASE(11);  // 11: terminal selection + backtrack
   if (prm.phase_cycles && tid == 0) out->dbg_dp_cycles = clock64() - ph_start_;
+}
+
+
+__global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpParams prm) {
+  dp_body<kDpThreads, SLOS_DP_MIN_BLOCKS, SLOS_MAX_CHAIN>(prm);
+}
+
+#ifndef SLOS_DP_SMALL_THREADS
+#define SLOS_DP_SMALL_THREADS 64
+#endif
+#ifndef SLOS_DP_SMALL_MIN_BLOCKS
+#define SLOS_DP_SMALL_MIN_BLOCKS 16
+#endif
+constexpr int kDpSmallThreads = SLOS_DP_SMALL_THREADS;
+constexpr int kDpSmallMaxChain = 16;  // chain items of a small-kernel instance (host: cost < 2048)
+__global__ void __launch_bounds__(kDpSmallThreads, SLOS_DP_SMALL_MIN_BLOCKS) dp_kernel_small(DpParams prm) {
+  dp_body<kDpSmallThreads, SLOS_DP_SMALL_MIN_BLOCKS, kDpSmallMaxChain>(prm);
 }
 
 }  // namespace slos

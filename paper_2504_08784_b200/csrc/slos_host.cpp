@@ -359,6 +359,18 @@ int solve_parts(int nv) {
 // Direct bucket-table entries per DP CTA (shared memory); instances whose count
 // space prod_l (items of tier l + 1) exceeds it hash instead.
 constexpr int kDirectMax = 1024;
+// Instances with (n_dec + 8) * (N + 1)^2 < kSmallCost (chain <= 14 items, a few
+// dozen decoders: the C5 sweep family) run their admission DP in dp_kernel_small,
+// 64-thread CTAs at 16 per SM; their direct bucket table holds kDirectSmall entries.
+constexpr double kSmallCost = 2048.0;
+constexpr int kDirectSmall = 256;
+bool dp_small_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SLOS_DP_SMALL");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
 
 // Instances with at least this many running decoders are reconstructed by a
 // 256-thread CTA (SLOS_BUILD_BIG_MIN_DEC overrides).
@@ -514,9 +526,11 @@ Caps estimate_caps(const slos_planner* P, const slos_input* in, const Prep& pr, 
   const int64_t M = pr.n_dec + pr.N + 1;
   const int64_t g = (int64_t)1 << (2 * grow);
   const int64_t N1 = pr.N + 1;
-  c.surv = std::max<int64_t>(4096, 16 * N1 * N1) * g;
-  c.cand = pow2_at_least(std::max<int64_t>(1024, 4 * N1 * N1) * g);
-  c.memo = pow2_at_least(std::max<int64_t>(4096, 8 * N1 * N1) * g);
+  // small chains get small arenas (the DP clears its memo and bucket-hash slices
+  // itself, so their size is write traffic per solve); overflow regrows (grow)
+  c.surv = std::max<int64_t>(256, 16 * N1 * N1) * g;
+  c.cand = pow2_at_least(std::max<int64_t>(64, 4 * N1 * N1) * g);
+  c.memo = pow2_at_least(std::max<int64_t>(64, 8 * N1 * N1) * g);
   c.gb = (S + 8) << (2 * grow);
   c.go = M * c.gb;
   // plan output: gaps + tail, or the fallback (until every line completes)
@@ -589,6 +603,9 @@ struct Workspace {
   BatchArgs A;
   DpParams dp;
   size_t smem = 0;
+  DpParams dp_small;              // dp_kernel_small (instances of cost < kSmallCost)
+  size_t smem_small = 0;
+  int small_lo[kMaxParts] = {0};  // first order position of each part that is small
   size_t anchor_smem = 0;
   int maxN = 0;
   cudaStream_t stream = nullptr;
@@ -895,12 +912,15 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
         const int t = enc >= 0 ? in->running[enc].decode_tier : in->pending[-enc - 1].decode_tier;
         if (t >= 0 && t < kMaxTiers) ++maxc[t];
       }
+      const bool small = dp_small_enabled() &&
+                         (double)(pr.n_dec + 8) * (double)(pr.N + 1) * (double)(pr.N + 1) < kSmallCost;
+      const int dmax = small ? kDirectSmall : kDirectMax;
       int64_t D = 1;
-      for (int l = 0; l < planners[k]->L && D <= kDirectMax; ++l) {
+      for (int l = 0; l < planners[k]->L && D <= dmax; ++l) {
         I.dstride[l] = (int32_t)D;
         D *= std::min<int64_t>(maxc[l], 250) + 1;
       }
-      I.direct = D <= kDirectMax ? 1 : 0;
+      I.direct = D <= dmax ? 1 : 0;
     }
     I.off_dec = oD;
     I.off_chain = oC;
@@ -993,8 +1013,10 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       for (size_t x = 0; x < keys.size();) {
         size_t y = x + 1;
         while (y < keys.size() && keys[y].k0 == keys[x].k0 && keys[y].k1 == keys[x].k1) ++y;
-        if (y - x > 1)
+        if (y - x > 1) {
           for (size_t z = x; z < y; ++z) hpair[keys[z].idx] = 1;
+          I.has_shared = 1;
+        }
         x = y;
       }
     }
@@ -1038,6 +1060,14 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     ws.n_parts = P;
     int qcount[kQueues] = {0};
     for (int p = 0; p <= P; ++p) ws.part_lo[p] = (int)((int64_t)p * nv / P);
+    // the small instances are a suffix of each part (cost-descending order; the
+    // bucketed order keys on ilogb(cost) and kSmallCost is a power of two)
+    for (int p = 0; p < P; ++p) {
+      int x = ws.part_lo[p + 1];
+      if (dp_small_enabled())
+        while (x > ws.part_lo[p] && cost[ord[x - 1]] < kSmallCost) --x;
+      ws.small_lo[p] = x;
+    }
     for (int p = 0; p < P; ++p)
       for (int x = ws.part_lo[p]; x < ws.part_lo[p + 1]; ++x) ++qcount[kBuildKinds * p + kind_v[ord[x]]];
     HostPool::get().run(nv, [&](int lo, int hi) {
@@ -1220,6 +1250,19 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   dp.dec_smem_max = 0;
   if (kStageDec && fit(maxDec) <= kSmemBudget) dp.dec_smem_max = maxDec;
   smem = fit(dp.dec_smem_max);
+  {  // dp_kernel_small: 64 threads, 16 CTAs per SM -> ~13 KB of shared memory each
+    DpParams& ds = ws.dp_small;
+    ds = dp;
+    ds.dec_smem_max = 0;
+    ds.dtab = kDirectSmall;
+    static const int kTsmSmall = [] {
+      const char* e = std::getenv("SLOS_DP_SMALL_TSM");
+      return e ? std::atoi(e) : 48;
+    }();
+    ds.Tsm = kTsmSmall;
+    ws.smem_small = dp_smem_bytes(std::min(maxN, kDpSmallMaxChainHost), 0, ds.Sc, Lmax, ds.Tsm, &ds.overlay_bytes,
+                                  ds.dtab, true);
+  }
   ws.anchor_smem = anchor_smem_bytes(maxN, dp.Sc, Lmax, &dp.anchor_scr_bytes);
   if (S_need > (double)(1 << 20) || smem > c.smem_optin || ws.anchor_smem > c.smem_optin) {
     // the slot grid of the widest deadline span does not fit a CTA's shared memory;
@@ -1248,14 +1291,17 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   unsigned char* DO = (unsigned char*)ws.d_out.p;
   const Layout& Ly = ws.Ly;
   // scratch init is part of every solve (memo tables, bucket hashes, headers)
-  cudaMemsetAsync(DS + Ly.memo, 0, Ly.memo_bytes, s);
-  cudaMemsetAsync(DS + Ly.c_bkey, 0, Ly.bkey_bytes, s);
-  cudaMemsetAsync(DS + Ly.c_bval, 0xFF, Ly.bval_bytes, s);
+  for (int k = 0; k < 4; ++k)
+    if (!ws.ev[k]) cudaEventCreate(&ws.ev[k]);
+  cudaEventRecord(ws.ev[1], s);  // start of the solve (scratch init), stage_ms[3]
+  if (host_timing())
+    std::fprintf(stderr, "[slos solve] nv %d: memset memo %.1f MB, bkey %.1f MB, bval %.1f MB, hdr %.1f MB\n", nv,
+                 Ly.memo_bytes / 1e6, Ly.bkey_bytes / 1e6, Ly.bval_bytes / 1e6, sizeof(OutHdr) * (double)nv / 1e6);
+  // (the memo tables and HBM bucket hashes are cleared by dp_kernel, per instance
+  // and only when used: a batch-wide memset wrote GBs for small instances)
   cudaMemsetAsync(DO + Ly.out, 0, sizeof(OutHdr) * nv, s);
   cudaMemsetAsync(DS + Ly.bq, 0, 2 * kQueues * sizeof(int32_t), s);
   cudaError_t e;
-  for (int k = 0; k < 4; ++k)
-    if (!ws.ev[k]) cudaEventCreate(&ws.ev[k]);
   if (!ws.ev_fork) {
     cudaEventCreateWithFlags(&ws.ev_fork, cudaEventDisableTiming);
     int lo = 0, hi = 0;
@@ -1273,7 +1319,8 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   ws.launches = 0;  // kernels this solve launches (slos_workspace_launches)
   for (int p = 0; p < ws.n_parts; ++p) {
     const int nt = ws.atask_lo[p + 1] - ws.atask_lo[p];
-    ws.launches += (nt > 0) + (nt > 0 && ws.maxN > 0) + (ws.part_lo[p + 1] > ws.part_lo[p]);
+    ws.launches += (nt > 0) + (nt > 0 && ws.maxN > 0) + (ws.small_lo[p] > ws.part_lo[p]) +
+                   (ws.part_lo[p + 1] > ws.small_lo[p]);
     for (int kd = 0; kd < kBuildKinds; ++kd) ws.launches += ws.qn[kBuildKinds * p + kd] > 0;
   }
   BuildParams bp;
@@ -1310,7 +1357,12 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     cudaStreamWaitEvent(sp, ws.ev_anc[p], 0);
     DpParams dpp = dp;
     dpp.blk0 = ws.part_lo[p];
-    if ((e = launch_dp(dpp, ws.part_lo[p + 1] - ws.part_lo[p], smem, sp)) != cudaSuccess)
+    if ((e = launch_dp(dpp, ws.small_lo[p] - ws.part_lo[p], smem, sp)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    DpParams dps = ws.dp_small;
+    dps.blk0 = ws.small_lo[p];
+    dps.task0 = dpp.task0;
+    if ((e = launch_dp(dps, ws.part_lo[p + 1] - ws.small_lo[p], ws.smem_small, sp, true)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     cudaEventRecord(ws.ev_dp[p], sp);
     bp.part = p;
@@ -1370,6 +1422,17 @@ void print_phase_debug(Workspace& ws, const std::vector<OutHdr>& hdr) {
     std::vector<int> idx(nv);
     for (int v = 0; v < nv; ++v) idx[v] = v;
     std::sort(idx.begin(), idx.end(), [&](int x, int y) { return hdr[x].dbg_cycles > hdr[y].dbg_cycles; });
+    {
+      double bsum = 0.0, esum = 0.0, nbs = 0.0;
+      for (int v = 0; v < nv; ++v) {
+        bsum += (double)hdr[v].dbg_cycles;
+        esum += (double)hdr[v].n_entries;
+        nbs += (double)hdr[v].n_batches;
+      }
+      auto bq = [&](double f) { return (double)hdr[idx[std::min(nv - 1, (int)(f * nv))]].dbg_cycles; };
+      std::fprintf(stderr, "[slos build instances] mean %.3e p50 %.3e p90 %.3e max %.3e cycles; mean batches %.1f entries %.1f\n",
+                   bsum / nv, bq(0.5), bq(0.1), bq(0.0), nbs / nv, esum / nv);
+    }
     for (int r = 0; r < std::min(nv, 6); ++r) {
       const OutHdr& h = hdr[idx[r]];
       std::fprintf(stderr, "  slow build #%d: job %d cycles %.3e batches %lld entries %lld infeasible %d admitted %d T %lld\n", r,
@@ -1988,7 +2051,10 @@ int slos_workspace_stage_ms(slos_workspace* b, float* ms, int32_t n) {
     t[1] = dp_end - t[0];                // timed to their last part's end)
     t[2] = all - dp_end;
   }
+  float t3 = 0.0f;  // scratch init (memsets) before the kernels
+  if (ws.ev[2]) cudaEventElapsedTime(&t3, ws.ev[1], ws.ev[0]);
   for (int k = 0; k < n && k < 3; ++k) ms[k] = t[k];
+  if (n > 3) ms[3] = t3;
   return SLOS_OK;
 }
 

@@ -25,13 +25,15 @@ struct CompactParams {
   unsigned char* dst;
 };
 
-size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay, int dtab);
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay, int dtab,
+                     bool small = false);
+constexpr int kDpSmallMaxChainHost = 16;  // dp_kernel_small: chain items (kDpSmallMaxChain)
 size_t dp_group_hdr_bytes();
 size_t dp_group_eval_bytes(int Sc, int L);
 size_t dp_group_stride(int Sc, int L);
 size_t dp_anchor_stride(int R, int Sc, int L, int N);
 size_t dp_warp_scr_stride(int Sc, int L);
-cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s, bool small = false);
 size_t anchor_smem_bytes(int max_N, int Sc, int L, size_t* scr);
 cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_group(const DpParams& prm, int n_atask, int max_N, cudaStream_t s);

@@ -102,9 +102,9 @@ class ShardSolver:
         return float(ms[0]), float(ms[1])
 
     def stage_ms(self):
-        """[anchor_kernel, dp_kernel, build_kernel] device ms of the last solve."""
-        ms = (C.c_float * 3)()
-        self.lib.slos_workspace_stage_ms(self.ws, ms, 3)
+        """[anchor_kernel, dp_kernel, build_kernel, scratch init] device ms of the last solve."""
+        ms = (C.c_float * 4)()
+        self.lib.slos_workspace_stage_ms(self.ws, ms, 4)
         return [float(x) for x in ms]
 
     def launches(self) -> int:
