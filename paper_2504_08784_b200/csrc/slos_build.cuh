@@ -41,10 +41,13 @@ struct BuildShared {
   GapPlanBuf o, tmp;
   PlannerDev P;
   InstDev I;
-  double bounds[SLOS_MAX_CHAIN + 2];
-  int64_t m_left[SLOS_MAX_CHAIN + 1];
-  unsigned long long m_asg[SLOS_MAX_CHAIN + 1];
-  int32_t m_item[SLOS_MAX_CHAIN + 1];
+  // per selected chain item (N + 2 entries; carved from the group's arena, so the
+  // static shared footprint of a reconstruction warp does not scale with the
+  // longest chain the ABI allows)
+  double* bounds;
+  int64_t* m_left;
+  unsigned long long* m_asg;
+  int32_t* m_item;
   int nb, nsel, edf, fill_late, err, m1;
   int range_err;  // a plan token count outside the 32-bit entry range
   int64_t n_batch, n_entry;
@@ -606,12 +609,17 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
   E.bl = (int64_t*)ar.take(sizeof(int64_t) * Mmax);
   E.rm = (int64_t*)ar.take(sizeof(int64_t) * Mmax);
   E.tr = (int32_t*)ar.take(sizeof(int32_t) * Mmax);
+  double* ch_bounds = (double*)ar.take(sizeof(double) * (I.N + 2));
+  int64_t* ch_left = (int64_t*)ar.take(sizeof(int64_t) * (I.N + 2));
+  unsigned long long* ch_asg = (unsigned long long*)ar.take(sizeof(unsigned long long) * (I.N + 2));
+  int32_t* ch_item = (int32_t*)ar.take(sizeof(int32_t) * (I.N + 2));
   E.ow = (int32_t*)ar.take(sizeof(int32_t) * Mmax);
   if (ga.over() || ar.over()) {
     if (tid == 0) { out->status = SLOS_ERR_CAPACITY; out->need_work = ar.need(); }
     return;
   }
   if (tid == 0) {
+    sh.bounds = ch_bounds; sh.m_left = ch_left; sh.m_asg = ch_asg; sh.m_item = ch_item;
     sh.o.b = gb; sh.o.cap_b = (int32_t)I.cap_gb; sh.o.own = go; sh.o.cap_own = (int32_t)I.cap_go;
     sh.tmp.b = tb; sh.tmp.cap_b = (int32_t)I.cap_gb; sh.tmp.own = nullptr; sh.tmp.cap_own = 0;
   }

@@ -544,7 +544,7 @@ Caps estimate_caps(const slos_planner* P, const slos_input* in, const Prep& pr, 
   c.batch = std::max<int64_t>((pr.N + 2) * (S + 4), std::min<int64_t>(fb_batches, 100000)) * (grow + 1) + 64;
   c.entry = std::max<int64_t>(c.batch * (pr.n_dec + pr.N + 1) / 2, 1024) * (grow + 1);
   const int64_t engine = S * (M + 1) * 4 + S * (64 + 8 * P->L) + M * 48 + 64 * M + (1 << 16);
-  c.work = (M * 32 + 2 * c.gb * (int64_t)sizeof(GapBatchOut) + 16 * c.go + engine) * (grow + 1);
+  c.work = (M * 32 + (pr.N + 2) * 32 + 2 * c.gb * (int64_t)sizeof(GapBatchOut) + 16 * c.go + engine) * (grow + 1);
   return c;
 }
 
