@@ -32,6 +32,28 @@ __device__ __forceinline__ double predict(const PlannerDev& P, int64_t n, int64_
 __device__ __forceinline__ int64_t time2bs(const PlannerDev& P, double budget, int64_t s,
                                            int64_t max_tokens) {
   if (!time_le(predict(P, 1, s), budget)) return -1;
+  // With every k1 >= 0, predict(n, s) is non-decreasing in n (each rounded term
+  // k1*n + k2*s + b is, and so is their max), so the reference's binary search
+  // returns the largest n in [1, max_tokens] with time_le(predict(n), budget).
+  // Start from the real-valued solution of each term and step to that boundary
+  // with the exact predicate; a guess more than a few steps off (never seen)
+  // falls through to the binary search itself.
+  bool mono = true;
+  int64_t n = max_tokens;
+  for (int t = 0; t < P.n_terms; ++t) {
+    if (P.k1[t] < 0.0) { mono = false; break; }
+    if (P.k1[t] > 0.0) {
+      const double r = (budget + kTimeEps - P.k2[t] * (double)s - P.b[t]) / P.k1[t];
+      const int64_t g = r < 1.0 ? 1 : (r >= (double)max_tokens ? max_tokens : (int64_t)r);
+      n = imin(n, g);
+    }
+  }
+  if (mono) {
+    int steps = 0;
+    while (n < max_tokens && time_le(predict(P, n + 1, s), budget) && ++steps < 8) ++n;
+    while (n > 1 && !time_le(predict(P, n, s), budget) && ++steps < 8) --n;
+    if (steps < 8) return n;
+  }
   int64_t lo = 1, hi = max_tokens;
   while (lo < hi) {
     const int64_t mid = lo + (hi - lo + 1) / 2;

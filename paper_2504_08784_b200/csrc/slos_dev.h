@@ -227,6 +227,7 @@ struct DpParams {
   int dec_smem_max;    // stage decoders in smem when n_dec <= this
   unsigned char* wscr_global;  // per-CTA-slot warp scratch when not in smem (nullptr = smem)
   size_t wscr_stride;  // bytes per warp in wscr_global
+  int wscr_warps;      // warp slots per launch-order position in wscr_global
   unsigned long long* phase_cycles;  // kNumPhases counters, or nullptr
   int Tsm;             // candidates per level kept in shared memory
   size_t overlay_bytes;  // group-variant / candidate-state overlay (bytes)

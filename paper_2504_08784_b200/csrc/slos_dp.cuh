@@ -811,7 +811,6 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
   __shared__ int64_t s_wsum[kDpWarps + 1];
   __shared__ unsigned long long s_ctr[5];
   __shared__ int s_err, s_n_new, s_n_used, s_ovf, s_nb, s_best, s_nw, s_bovf, s_anysh, s_nsb, s_bkinit;
-  __shared__ int64_t s_next_free, s_arena_next, s_bnext;
   __shared__ __align__(8) uint64_t s_mbar;  // completion of a level's record staging (TMA bulk copies)
 
   const BatchArgs& A = prm.a;
@@ -883,7 +882,9 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
   }
   // per-warp scratch for the rare private-variant / speculative paths (global);
   // the placement temporaries live in shared memory
-  unsigned char* wbase = prm.wscr_global + ((size_t)blockIdx.x * kDpWarps + warp_id()) * prm.wscr_stride;
+  // (slot = launch-order position: CTAs of concurrent launches never share one)
+  unsigned char* wbase =
+      prm.wscr_global + ((size_t)(prm.blk0 + blockIdx.x) * prm.wscr_warps + warp_id()) * prm.wscr_stride;
   WarpScr W = warp_scr_carve(wbase, prm.Sc, prm.Lmax);
   W.tmp = (int64_t*)p + (size_t)warp_id() * prm.Sc;
   p += sizeof(int64_t) * (size_t)prm.Sc * kDpWarps;
@@ -896,8 +897,7 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
   int32_t* k_j = (int32_t*)p; p += 4 * (size_t)Tsm;
   int32_t* k_me = (int32_t*)p; p += 4 * (size_t)Tsm;
   int32_t* k_new = (int32_t*)p; p += 4 * (size_t)Tsm;
-  int32_t* k_grp = (int32_t*)p; p += 4 * (size_t)Tsm;
-  (void)k_grp;
+  int32_t* k_grp = (int32_t*)p; p += 4 * (size_t)Tsm;  // direct instances: bucket sizes of a level
   // direct count-vector -> bucket table (instances whose count space is small)
   int32_t* dtab = (int32_t*)p; p += 4 * (size_t)prm.dtab;
   for (int x = tid; x < prm.dtab; x += kDpThreads) dtab[x] = -1;
@@ -943,11 +943,10 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
     lvl_cnt[0] = 1;
     lvl_boff[0] = 0;
     lvl_nsb[0] = 1;
-    s_next_free = 1;
-    s_arena_next = 1;
-    s_bnext = 1;
   }
   __syncthreads();
+  // arena bookkeeping: block-uniform, advanced identically by every thread
+  int64_t r_next_free = 1, r_arena_next = 1, r_bnext = 1;
 
   long long ph_t0_ = clock64();
   const long long ph_start_ = ph_t0_;
@@ -1010,6 +1009,9 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
     uint64_t* Bkey = sm ? o_bkey : A.c_bkey + 2 * I.off_cand;
     int32_t* Bval = sm ? o_bval : A.c_bval + 2 * I.off_cand;
     const int64_t capB = sm ? 2 * (int64_t)Tsm : 2 * capC;
+    const bool direct = I.direct != 0;
+    int32_t* Bcnt = sm ? k_grp : A.c_bval + 2 * I.off_cand;                   // direct: bucket sizes
+    int32_t* hsbA = sm ? k_new : (int32_t*)(A.k_val + I.off_cand);           // per bucket: keeps a survivor
     if (tid == 0) s_ctr[0] += (unsigned long long)T;
     const double t_i = ch_dl[i];
     // source level index of candidate c: last k with s_pre[k] <= c
@@ -1063,6 +1065,7 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
     // no table. Shared pairs use the instance's hash memo, whose first-inserted
     // candidate decides under µs key collisions (dp_scheduler.cpp:423-435). ----
     for (int c = tid; c < T; c += kDpThreads) {
+      if (direct) Bcnt[c] = 0;  // step 5's bucket sizes (no other use of the array this level)
       const int k = level_of(c);
       const int lv = jlo + 1 + k;
       const int src = (int)(lvl_off[lv] + (c - s_pre[k]));
@@ -1217,7 +1220,7 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
     const int tier_i = ch_tr[i];
     const bool forced = ch_fc[i] != 0;
     for (int c = tid; c < T; c += kDpThreads) {
-      Cj[c] = 0;  // bucket sizes of step 5 (the E3b key list is consumed)
+      if (!direct) Cj[c] = 0;  // bucket sizes of step 5 (the E3b key list is consumed)
       const int src = Csrc[c];
       const int me = Cme[c];
       bool has;
@@ -1231,10 +1234,11 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
         has = val >= 0;
       }
       int flag = 0;
+      uint64_t nc = 0;
       if (has) {
         const int64_t avail = Sp_[src] + val;
         if (avail >= ch_pf[i]) {
-          const uint64_t nc = pack_add(Sc_[src], tier_i);
+          nc = pack_add(Sc_[src], tier_i);
           if (pack_get(nc, tier_i) > 250) atomicCAS(&s_err, 0, SLOS_ERR_INTERNAL_INCONSISTENCY);
           int64_t mem = Sm_[src];
           bool ok = true;
@@ -1253,25 +1257,12 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
         }
       }
       Cfl[c] = flag;
-    }
-    if (sm && !I.direct) {  // fresh level-local bucket table
-      for (int x = tid; x < capB; x += kDpThreads) { Bkey[x] = 0ull; Bval[x] = -1; }
-    } else if (!sm && !I.direct && !s_bkinit) {  // first HBM level: clear the instance's
-      for (int64_t x = tid; x < capB; x += kDpThreads) { Bkey[x] = 0ull; Bval[x] = -1; }  // hash once
-    }
-    __syncthreads();
-    if (!sm && !I.direct && tid == 0) s_bkinit = 1;  // later HBM levels reset the slots they claim
-    if (s_err) break;
-    SLOS_PHASE(8);  // 8: candidate states
-    // ---- 5: Pareto buckets ----
-    if (I.direct) {  // count vector -> dense index -> bucket id (shared-memory 32-bit atomics)
-      for (int c = tid; c < T; c += kDpThreads) {
+      if (direct) {  // ---- 5 (fused): count vector -> dense index -> bucket id (shared-memory 32-bit atomics)
         int b = -1;
-        if (Cfl[c] & 1) {
-          const uint64_t key = Ccn[c];
+        if (flag) {
           int idx = 0;
 #pragma unroll
-          for (int l = 0; l < kMaxTiers; ++l) if (l < L) idx += (int)pack_get(key, l) * I.dstride[l];
+          for (int l = 0; l < kMaxTiers; ++l) if (l < L) idx += (int)pack_get(nc, l) * I.dstride[l];
           int v = atomicCAS(&dtab[idx], -1, -2);
           if (v == -1) {
             b = atomicAdd(&s_nb, 1);
@@ -1281,39 +1272,52 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
             while (v < 0) v = atomicAdd(&dtab[idx], 0);
             b = v;
           }
+          atomicAdd(&Bcnt[b], 1);  // bucket size (Bcnt zeroed in step 1)
+        }
+        Cbk[c] = b;
+      }
+    }
+    if (!direct) {
+      if (sm) {  // fresh level-local bucket table
+        for (int x = tid; x < capB; x += kDpThreads) { Bkey[x] = 0ull; Bval[x] = -1; }
+      } else if (!s_bkinit) {  // first HBM level: clear the instance's hash once
+        for (int64_t x = tid; x < capB; x += kDpThreads) { Bkey[x] = 0ull; Bval[x] = -1; }
+      }
+      __syncthreads();
+      if (!sm && tid == 0) s_bkinit = 1;  // later HBM levels reset the slots they claim
+      SLOS_PHASE(8);  // 8: candidate states
+      // ---- 5: Pareto buckets (hash of the count vector) ----
+      for (int c = tid; c < T; c += kDpThreads) {
+        int b = -1;
+        if (Cfl[c] & 1) {
+          const uint64_t key = Ccn[c];
+          uint64_t h = mix64(key) & (uint64_t)(capB - 1);
+          for (;;) {
+            const unsigned long long old = atomicCAS((unsigned long long*)&Bkey[h], 0ull,
+                                                     (unsigned long long)key);
+            if (old == 0ull) {
+              b = atomicAdd(&s_nb, 1);
+              Caux[b] = (int32_t)h;
+              atomicExch(&Bval[h], b);
+              break;
+            }
+            if (old == key) {
+              int x;
+              do { x = atomicAdd(&Bval[h], 0); } while (x < 0);
+              b = x;
+              break;
+            }
+            h = (h + 1) & (uint64_t)(capB - 1);
+          }
           atomicAdd(&Cj[b], 1);  // bucket size (Cj zeroed in step 4)
         }
         Cbk[c] = b;
       }
-    } else
-    for (int c = tid; c < T; c += kDpThreads) {
-      int b = -1;
-      if (Cfl[c] & 1) {
-        const uint64_t key = Ccn[c];
-        uint64_t h = mix64(key) & (uint64_t)(capB - 1);
-        for (;;) {
-          const unsigned long long old = atomicCAS((unsigned long long*)&Bkey[h], 0ull,
-                                                   (unsigned long long)key);
-          if (old == 0ull) {
-            b = atomicAdd(&s_nb, 1);
-            Caux[b] = (int32_t)h;
-            atomicExch(&Bval[h], b);
-            break;
-          }
-          if (old == key) {
-            int x;
-            do { x = atomicAdd(&Bval[h], 0); } while (x < 0);
-            b = x;
-            break;
-          }
-          h = (h + 1) & (uint64_t)(capB - 1);
-        }
-        atomicAdd(&Cj[b], 1);  // bucket size (Cj zeroed in step 4)
-      }
-      Cbk[c] = b;
     }
     __syncthreads();
+    if (s_err) break;
     const int NB = s_nb;
+    for (int b = tid; b < NB; b += kDpThreads) hsbA[b] = 0;  // read after the next barrier
     SLOS_PHASE(12);  // 12 (sub of buckets): bucket hashing
     // try_insert replay (dp_scheduler.cpp:445-465). Fast path: one warp per bucket
     // finds its candidates in creation order by ballots over the level and keeps
@@ -1340,7 +1344,7 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
     if (pairwise) {
       // unordered bucket lists (counting sort without stability: "earlier" is the
       // candidate index itself)
-      int32_t* cntB = Cj;   // bucket sizes, counted while the buckets were assigned
+      int32_t* cntB = direct ? Bcnt : Cj;   // bucket sizes, counted while the buckets were assigned
       int32_t* offB = Cme;  // memo slots are no longer needed after step 4
       if (warp_id() == 0) {  // bucket offsets: one warp (NB is small), sizes reset for the scatter
         const int lane = lane_id();
@@ -1402,6 +1406,7 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
             if (yc > c && yv >= xv && ym <= xm && yp >= xp) pr = true;
           }
           if (acc) Cfl[c] |= pr ? 6 : 2;
+          if (__any_sync(0xffffffffu, acc && !pr) && lane == 0) hsbA[b] = 1;
         }
       }
       if (s_bovf) {  // larger buckets: one thread per candidate over the bucket list
@@ -1439,15 +1444,18 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
         const int64_t xm = Cmm[c], xp = Cpb[c];
         const int32_t* lst = Blst + offB[b];
         const int n = cntB[b];
+        bool pruned = false;
         for (int q = 0; q < n; ++q) {
           const int y = lst[q];
           if (y <= c || !(Cfl[y] & 2)) continue;
           if (Cvl[y] >= xv && Cmm[y] <= xm && Cpb[y] >= xp) {
             if (it < 32) pm |= 1u << it;
             else Cfl[c] |= 4;  // levels beyond 32 x kDpThreads (HBM arrays): bit 2 is never cleared
+            pruned = true;
             break;
           }
         }
+        if (!pruned) hsbA[b] = 1;
       }
       __syncthreads();
       for (int k = 0; pm; ++k, pm >>= 1)
@@ -1623,27 +1631,28 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
       }
     }
     __syncthreads();
-    if (I.direct) {  // reset the direct-table entries claimed by this level
+    if (!pairwise) {  // register / list paths: mark the buckets that keep a survivor
+      for (int c = tid; c < T; c += kDpThreads) {
+        const int fl = Cfl[c];
+        if ((fl & 2) && !(fl & 4)) hsbA[Cbk[c]] = 1;
+      }
+      __syncthreads();
+    }
+    // reset the bucket-table entries claimed by this level (read again only after
+    // the level's last barrier)
+    if (direct) {
       for (int b = tid; b < NB; b += kDpThreads) dtab[Caux[b]] = -1;
-    } else if (!sm) {  // reset the HBM bucket hash slots claimed by this level
+    } else if (!sm) {
       for (int b = tid; b < NB; b += kDpThreads) {
         Bkey[Caux[b]] = 0ull;
         Bval[Caux[b]] = -1;
       }
     }
-    __syncthreads();
     SLOS_PHASE(9);  // 9: Pareto buckets
     // ---- 6: arena ids, survivors and their surviving-bucket ids ----
     {
-      int32_t* hsb = Cj;   // per bucket: has a survivor -> dense id
+      const int32_t* hsb = hsbA;  // per bucket: has a survivor -> dense id
       int32_t* sbid = Cme;
-      for (int b = tid; b < NB; b += kDpThreads) hsb[b] = 0;
-      __syncthreads();
-      for (int c = tid; c < T; c += kDpThreads) {
-        const int fl = Cfl[c];
-        if ((fl & 2) && !(fl & 4)) hsb[Cbk[c]] = 1;
-      }
-      __syncthreads();
       const int lane = lane_id(), w = warp_id();
       if (w == 0) {  // surviving-bucket dense ids: one warp (NB is small)
         int carry = 0;
@@ -1674,8 +1683,8 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
         if (x < w) carry += s_wsum[x];
         total += s_wsum[x];
       }
-      const int64_t bbase = s_bnext;
-      const int64_t base_free = s_next_free;
+      const int64_t bbase = r_bnext;
+      const int64_t base_free = r_next_free;
       for (int base = lo; base < hi; base += 32) {
         const int c = base + lane;
         const int64_t v = packed(c);
@@ -1692,25 +1701,26 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
             Sv_[dst] = Cvl[c];
             Sn_[dst] = Cna[c];
             Spar[dst] = Csrc[c];
-            Sar[dst] = (int32_t)(s_arena_next + (ex & 0xffffffffLL));
+            Sar[dst] = (int32_t)(r_arena_next + (ex & 0xffffffffLL));
             Sit[dst] = i;
             Ssb[dst] = sb;
             Bc[bbase + sb] = Ccn[c];  // every survivor of the bucket writes the same counts
           }
         }
       }
-      __syncthreads();  // every warp has read s_next_free / s_arena_next / s_bnext
+      // level bookkeeping: every thread advances its copies, thread 0 publishes the
+      // level's ranges (read after the barrier below)
+      const int64_t tot_acc = total & 0xffffffffLL, tot_sv = total >> 32;
+      const int nsb = s_nsb;
+      r_bnext = bbase + nsb;
+      r_next_free = base_free + tot_sv;
+      r_arena_next += tot_acc;
       if (tid == 0) {
-        const int64_t tot_acc = total & 0xffffffffLL, tot_sv = total >> 32;
-        const int nsb = s_nsb;
         lvl_off[i + 1] = base_free;
         lvl_cnt[i + 1] = (int32_t)tot_sv;
         lvl_boff[i + 1] = (int32_t)bbase;
         lvl_nsb[i + 1] = nsb;
-        s_bnext = bbase + nsb;
-        s_next_free = base_free + tot_sv;
-        s_arena_next += tot_acc;
-        if (s_next_free > I.cap_surv) { s_err = SLOS_ERR_CAPACITY; out->need_surv = 2 * s_next_free; }
+        if (r_next_free > I.cap_surv) { s_err = SLOS_ERR_CAPACITY; out->need_surv = 2 * r_next_free; }
       }
     }
     __syncthreads();
@@ -1727,7 +1737,7 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
   // ---- terminal selection (dp_scheduler.cpp:504-522) ----
   const int lv0 = I.last_forced + 1;
   const int64_t t_lo = lvl_off[lv0];
-  const int64_t t_hi = s_next_free;
+  const int64_t t_hi = r_next_free;
   if (I.values_integral) {
     // total order: value desc, n_admitted desc, mem asc, pb desc, arena asc
     int64_t best = -1;
@@ -1805,7 +1815,7 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
     out->ctr[1] = (int64_t)s_ctr[1];
     out->ctr[2] = (int64_t)s_ctr[2];
     out->ctr[3] = (int64_t)s_ctr[3];
-    out->ctr[4] = s_arena_next - 1;
+    out->ctr[4] = r_arena_next - 1;
     if (best < 0) {  // dp_scheduler.cpp:525-530
       out->infeasible = 1;
       out->n_sel = 0;
@@ -1859,6 +1869,17 @@ __global__ void __launch_bounds__(kDpThreads, SLOS_DP_MIN_BLOCKS) dp_kernel(DpPa
 #define SLOS_DP_SMALL_MIN_BLOCKS 16
 #endif
 constexpr int kDpSmallThreads = SLOS_DP_SMALL_THREADS;
+#ifndef SLOS_DP_BIG_THREADS
+#define SLOS_DP_BIG_THREADS 512
+#endif
+// dp_kernel_big: 512 threads (one CTA per SM, up to 128 registers, no spills) for
+// the instances whose levels carry the most candidates and buckets (thousands of
+// running decoders, the C4 family: a few dozen instances leave most SMs idle, so
+// the per-instance latency is the whole stage).
+constexpr int kDpBigThreads = SLOS_DP_BIG_THREADS;
+__global__ void __launch_bounds__(kDpBigThreads, 1) dp_kernel_big(DpParams prm) {
+  dp_body<kDpBigThreads, 1, SLOS_MAX_CHAIN>(prm);
+}
 constexpr int kDpSmallMaxChain = 16;  // chain items of a small-kernel instance (host: cost < 2048)
 __global__ void __launch_bounds__(kDpSmallThreads, SLOS_DP_SMALL_MIN_BLOCKS) dp_kernel_small(DpParams prm) {
   dp_body<kDpSmallThreads, SLOS_DP_SMALL_MIN_BLOCKS, kDpSmallMaxChain>(prm);

@@ -363,6 +363,17 @@ constexpr int kDirectMax = 1024;
 // dozen decoders: the C5 sweep family) run their admission DP in dp_kernel_small,
 // 64-thread CTAs at 16 per SM; their direct bucket table holds kDirectSmall entries.
 constexpr double kSmallCost = 2048.0;
+// Instances with cost >= kBigCost (thousands of running decoders: the C4 family) run
+// their admission DP in dp_kernel_big (512 threads, one CTA per SM); SLOS_DP_BIG_COST
+// overrides (0 disables). A power of two, so the big instances are a prefix of the
+// log2-bucketed cost-descending launch order.
+double dp_big_cost() {
+  static const double v = [] {
+    const char* e = std::getenv("SLOS_DP_BIG_COST");
+    return e ? std::atof(e) : 262144.0;
+  }();
+  return v;
+}
 constexpr int kDirectSmall = 256;
 bool dp_small_enabled() {
   static const bool on = [] {
@@ -606,6 +617,10 @@ struct Workspace {
   DpParams dp_small;              // dp_kernel_small (instances of cost < kSmallCost)
   size_t smem_small = 0;
   int small_lo[kMaxParts] = {0};  // first order position of each part that is small
+  int big_hi[kMaxParts] = {0};    // end of each part's big prefix (dp_kernel_big)
+  DpParams dp_big;                // dp_kernel_big
+  size_t smem_big = 0;
+  bool any_big = false;
   size_t anchor_smem = 0;
   int maxN = 0;
   cudaStream_t stream = nullptr;
@@ -1067,6 +1082,10 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       if (dp_small_enabled())
         while (x > ws.part_lo[p] && cost[ord[x - 1]] < kSmallCost) --x;
       ws.small_lo[p] = x;
+      int y = ws.part_lo[p];
+      if (dp_big_cost() > 0)
+        while (y < x && cost[ord[y]] >= dp_big_cost()) ++y;
+      ws.big_hi[p] = y;
     }
     for (int p = 0; p < P; ++p)
       for (int x = ws.part_lo[p]; x < ws.part_lo[p + 1]; ++x) ++qcount[kBuildKinds * p + kind_v[ord[x]]];
@@ -1218,7 +1237,10 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   dp.grec_hdr = grec_hdr;
   dp.grec_stride = grec_stride;
   dp.grec_stage = (grec_hdr + dp_group_eval_bytes(Sc, Lmax) + 15) & ~(size_t)15;
-  if ((e = ws.d_wscr.ensure(stride * 8 * (size_t)nv)) != cudaSuccess)
+  ws.any_big = false;
+  for (int p = 0; p < ws.n_parts; ++p) ws.any_big = ws.any_big || ws.big_hi[p] > ws.part_lo[p];
+  dp.wscr_warps = ws.any_big ? kDpMaxWarpsHost : 8;
+  if ((e = ws.d_wscr.ensure(stride * (size_t)dp.wscr_warps * (size_t)nv)) != cudaSuccess)
     return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   dp.wscr_global = (unsigned char*)ws.d_wscr.p;
   size_t& smem = ws.smem;
@@ -1263,8 +1285,26 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     ws.smem_small = dp_smem_bytes(std::min(maxN, kDpSmallMaxChainHost), 0, ds.Sc, Lmax, ds.Tsm, &ds.overlay_bytes,
                                   ds.dtab, true);
   }
+  {  // dp_kernel_big: one 512-thread CTA per SM, so a large level stays on chip
+    DpParams& db = ws.dp_big;
+    db = dp;
+    db.dec_smem_max = 0;
+    static const int kTsmBig = [] {
+      const char* e = std::getenv("SLOS_DP_BIG_TSM");
+      return e ? std::atoi(e) : 1024;
+    }();
+    static const size_t kSmemBig = [] {
+      const char* e = std::getenv("SLOS_DP_BIG_SMEM_KB");
+      return (size_t)(e ? std::atoi(e) : 200) * 1024;
+    }();
+    db.Tsm = kTsmBig;
+    auto fitb = [&] { return dp_smem_bytes(maxN, 0, db.Sc, Lmax, db.Tsm, &db.overlay_bytes, db.dtab, 2); };
+    while (fitb() > std::min(kSmemBig, (size_t)c.smem_optin) && db.Tsm > 64) db.Tsm -= 64;
+    ws.smem_big = fitb();
+  }
   ws.anchor_smem = anchor_smem_bytes(maxN, dp.Sc, Lmax, &dp.anchor_scr_bytes);
-  if (S_need > (double)(1 << 20) || smem > c.smem_optin || ws.anchor_smem > c.smem_optin) {
+  if (S_need > (double)(1 << 20) || smem > c.smem_optin || ws.anchor_smem > c.smem_optin ||
+      (ws.any_big && ws.smem_big > c.smem_optin)) {
     // the slot grid of the widest deadline span does not fit a CTA's shared memory;
     // plan_all solves wide instances in their own slot classes, so only an instance
     // that alone exceeds it lands here (per-instance SLOS_ERR_RANGE, never a launch failure)
@@ -1319,7 +1359,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   ws.launches = 0;  // kernels this solve launches (slos_workspace_launches)
   for (int p = 0; p < ws.n_parts; ++p) {
     const int nt = ws.atask_lo[p + 1] - ws.atask_lo[p];
-    ws.launches += (nt > 0) + (nt > 0 && ws.maxN > 0) + (ws.small_lo[p] > ws.part_lo[p]) +
+    ws.launches += (nt > 0) + (nt > 0 && ws.maxN > 0) + (ws.big_hi[p] > ws.part_lo[p]) + (ws.small_lo[p] > ws.big_hi[p]) +
                    (ws.part_lo[p + 1] > ws.small_lo[p]);
     for (int kd = 0; kd < kBuildKinds; ++kd) ws.launches += ws.qn[kBuildKinds * p + kd] > 0;
   }
@@ -1355,14 +1395,18 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   for (int p = 0; p < ws.n_parts; ++p) {
     const cudaStream_t sp = ws.pstream[p];
     cudaStreamWaitEvent(sp, ws.ev_anc[p], 0);
+    DpParams dpb = ws.dp_big;
+    dpb.blk0 = ws.part_lo[p];
+    if ((e = launch_dp(dpb, ws.big_hi[p] - ws.part_lo[p], ws.smem_big, sp, 2)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     DpParams dpp = dp;
-    dpp.blk0 = ws.part_lo[p];
-    if ((e = launch_dp(dpp, ws.small_lo[p] - ws.part_lo[p], smem, sp)) != cudaSuccess)
+    dpp.blk0 = ws.big_hi[p];
+    if ((e = launch_dp(dpp, ws.small_lo[p] - ws.big_hi[p], smem, sp)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     DpParams dps = ws.dp_small;
     dps.blk0 = ws.small_lo[p];
     dps.task0 = dpp.task0;
-    if ((e = launch_dp(dps, ws.part_lo[p + 1] - ws.small_lo[p], ws.smem_small, sp, true)) != cudaSuccess)
+    if ((e = launch_dp(dps, ws.part_lo[p + 1] - ws.small_lo[p], ws.smem_small, sp, 1)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     cudaEventRecord(ws.ev_dp[p], sp);
     bp.part = p;

@@ -34,8 +34,8 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactParams p) {
 }
 
 // dynamic shared memory of dp_kernel (must mirror the carve-up in dp_kernel)
-size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay, int dtab, bool small) {
-  const int nwarps = small ? kDpSmallThreads / 32 : kDpWarps;
+size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay, int dtab, int kind) {
+  const int nwarps = kind == 1 ? kDpSmallThreads / 32 : (kind == 2 ? kDpBigThreads / 32 : kDpWarps);
   const size_t N = (size_t)max_N;
   size_t b = 8 * (N + 1) * 4 + 8 * (N + 2) + 4 * (N + 2) * 3 + 16;   // chain
   b += (size_t)max_dec_staged * 28 + 16;                              // decoders
@@ -87,9 +87,15 @@ cudaError_t launch_group(const DpParams& prm, int n_atask, int max_N, cudaStream
   return cudaGetLastError();
 }
 
-cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s, bool small) {
+cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s, int kind) {
   if (grid <= 0) return cudaSuccess;
-  if (small) {
+  if (kind == 2) {
+    cudaError_t e = cudaFuncSetAttribute(dp_kernel_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dp_kernel_big<<<grid, kDpBigThreads, smem, s>>>(prm);
+    return cudaGetLastError();
+  }
+  if (kind == 1) {
     cudaError_t e = cudaFuncSetAttribute(dp_kernel_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dp_kernel_small<<<grid, kDpSmallThreads, smem, s>>>(prm);

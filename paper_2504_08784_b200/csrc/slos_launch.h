@@ -25,15 +25,17 @@ struct CompactParams {
   unsigned char* dst;
 };
 
+// kind: 0 dp_kernel, 1 dp_kernel_small, 2 dp_kernel_big
 size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay, int dtab,
-                     bool small = false);
+                     int kind = 0);
+constexpr int kDpMaxWarpsHost = 16;  // warps of the widest DP kernel (dp_kernel_big)
 constexpr int kDpSmallMaxChainHost = 16;  // dp_kernel_small: chain items (kDpSmallMaxChain)
 size_t dp_group_hdr_bytes();
 size_t dp_group_eval_bytes(int Sc, int L);
 size_t dp_group_stride(int Sc, int L);
 size_t dp_anchor_stride(int R, int Sc, int L, int N);
 size_t dp_warp_scr_stride(int Sc, int L);
-cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s, bool small = false);
+cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s, int kind = 0);
 size_t anchor_smem_bytes(int max_N, int Sc, int L, size_t* scr);
 cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_group(const DpParams& prm, int n_atask, int max_N, cudaStream_t s);
