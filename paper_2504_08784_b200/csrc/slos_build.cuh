@@ -783,7 +783,7 @@ __device__ inline void build_instance(const BatchArgs& A, BuildShared& sh, int i
 constexpr int kBuildWarps = 4;
 constexpr int kBuildThreads = 128;
 #ifndef SLOS_BUILD_MIN_BLOCKS
-#define SLOS_BUILD_MIN_BLOCKS 3
+#define SLOS_BUILD_MIN_BLOCKS 4  // <= 128 registers: a C2 part's 512 instances build in one wave
 #endif
 #ifndef SLOS_BUILD_WARP_MIN_BLOCKS
 #define SLOS_BUILD_WARP_MIN_BLOCKS 4
@@ -822,7 +822,7 @@ __global__ void __launch_bounds__(SLOS_BUILD_BIG_THREADS, 1) build_kernel_big(Bu
   __shared__ BuildShared sh;
   extern __shared__ __align__(16) unsigned char bsm[];
   build_instance<BlockGrpT<SLOS_BUILD_BIG_THREADS>>(A, sh, A.bq[A.qbase[kBuildKinds * prm.part + 2] + blockIdx.x], bsm,
-                                               (int64_t)prm.smem_bytes, prm.phase_cycles);
+                                               (int64_t)prm.smem_big, prm.phase_cycles);
 }
 
 // ---- standalone gap queries (slos_tile_gap_batch) ----------------------------

@@ -257,6 +257,7 @@ struct BuildParams {
   BatchArgs a;
   size_t smem_bytes;  // build_kernel: dynamic shared memory per CTA (per-gap working set)
   size_t smem_warp;   // build_kernel_warp: dynamic shared memory per CTA (4 instances)
+  size_t smem_big;    // build_kernel_big: dynamic shared memory per CTA (one CTA per SM)
   int part;           // solve part whose queues this launch drains
   unsigned long long* phase_cycles;  // 8 counters or nullptr (SLOS_PHASE_TIMING)
 };

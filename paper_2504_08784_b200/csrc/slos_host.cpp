@@ -1365,11 +1365,19 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   }
   BuildParams bp;
   bp.a = ws.A;
-  static const size_t kBuildSmem = [] {  // per-gap working set per CTA (SLOS_BUILD_SMEM_KB)
+  // per-gap working set per CTA (SLOS_BUILD_SMEM_KB). Measured C2 x 1024 with 4
+  // CTAs per SM (128 registers): build stage 0.69 ms at 44 KB, 0.61 at 32, 0.57 at
+  // 24, 1.03 at 16 (gaps spill to HBM); at 3 CTAs per SM (168 registers) 0.81-0.83.
+  static const size_t kBuildSmem = [] {
     const char* e = std::getenv("SLOS_BUILD_SMEM_KB");
-    return (size_t)(e ? std::atoi(e) : 44) * 1024;
+    return (size_t)(e ? std::atoi(e) : 24) * 1024;
   }();
   bp.smem_bytes = kBuildSmem;
+  static const size_t kBuildSmemBig = [] {  // build_kernel_big (SLOS_BUILD_BIG_SMEM_KB)
+    const char* e = std::getenv("SLOS_BUILD_BIG_SMEM_KB");
+    return (size_t)(e ? std::atoi(e) : 44) * 1024;
+  }();
+  bp.smem_big = kBuildSmemBig;
   static const size_t kBuildSmemWarp = [] {  // per CTA of 4 warp-built instances (SLOS_BUILD_WARP_SMEM_KB)
     const char* e = std::getenv("SLOS_BUILD_WARP_SMEM_KB");
     return (size_t)(e ? std::atoi(e) : 16) * 1024;

@@ -125,9 +125,9 @@ cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, int n
   }
   if (n_big > 0) {
     if ((e = cudaFuncSetAttribute(build_kernel_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)prm.smem_bytes)) != cudaSuccess)
+                                  (int)prm.smem_big)) != cudaSuccess)
       return e;
-    build_kernel_big<<<n_big, SLOS_BUILD_BIG_THREADS, prm.smem_bytes, s>>>(prm);
+    build_kernel_big<<<n_big, SLOS_BUILD_BIG_THREADS, prm.smem_big, s>>>(prm);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
