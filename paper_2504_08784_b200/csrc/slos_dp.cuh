@@ -787,6 +787,37 @@ __global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm
 }
 
 
+// try_insert's closed form for one bucket of n <= 64 candidates held by a warp
+// (lane r: members r and 32 + r; cn = candidate index * 256 + n_admitted): member
+// x is rejected iff an EARLIER candidate y weakly dominates it, unless they are
+// equal in (value, memory, budget) and y admits fewer; pm[k] collects the LATER
+// candidates that weakly dominate member k (it is pruned iff one is accepted).
+template <typename TV, typename TM>
+__device__ __forceinline__ void bucket_pair_tests(int n, const int (&cn)[2], const TV (&v)[2], const TM (&m)[2],
+                                                  const TM (&p)[2], bool (&acc)[2], uint64_t (&pm)[2]) {
+  for (int y = 0; y < n; ++y) {
+    const int src = y & 31;
+    const bool hi = y >= 32;  // warp-uniform
+    const int ycn = __shfl_sync(0xffffffffu, hi ? cn[1] : cn[0], src);
+    const TV yv = __shfl_sync(0xffffffffu, hi ? v[1] : v[0], src);
+    const TM ym = __shfl_sync(0xffffffffu, hi ? m[1] : m[0], src);
+    const TM yp = __shfl_sync(0xffffffffu, hi ? p[1] : p[0], src);
+    const int yc = ycn >> 8;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (yv >= v[k] && ym <= m[k] && yp >= p[k]) {
+        const int c = cn[k] >> 8;
+        if (yc < c) {
+          const bool equal = yv == v[k] && ym == m[k] && yp == p[k];
+          if (!equal || (ycn & 255) >= (cn[k] & 255)) acc[k] = false;
+        } else if (yc > c) {
+          pm[k] |= 1ull << y;
+        }
+      }
+    }
+  }
+}
+
 #ifndef SLOS_DP_MIN_BLOCKS
 #define SLOS_DP_MIN_BLOCKS 4
 #endif
@@ -1364,55 +1395,62 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
         if (b >= 0) {
           const int pos = atomicAdd(&cntB[b], 1);
           Blst[offB[b] + pos] = c;
-          if (pos == 32) s_bovf = 1;
+          if (pos == 64) s_bovf = 1;
         }
       }
       __syncthreads();
-      // buckets of <= 32 candidates: one warp each, members in registers, the
-      // pairwise tests over shuffles (no memory traffic in the loops)
+      // buckets of <= 64 candidates: one warp each, members in registers (lane r
+      // holds members r and 32 + r), every pair tested once over shuffles (no
+      // memory traffic in the loop); 32-bit operands whenever the bucket's values,
+      // memory and budgets fit (4 shuffles per member instead of 7)
       {
         const int lane = lane_id();
         for (int b = warp_id(); b < NB; b += kDpWarps) {
           const int n = cntB[b];
-          if (n > 32) continue;
-          int c = 0x7fffffff;
-          double xv = 0.0;
-          int64_t xm = 0, xp = 0;
-          int xn = 0;
-          if (lane < n) {
-            c = Blst[offB[b] + lane];
-            xv = Cvl[c]; xm = Cmm[c]; xp = Cpb[c]; xn = Cna[c];
-          }
-          bool acc = lane < n;
-          for (int y = 0; y < n; ++y) {
-            const int yc = __shfl_sync(0xffffffffu, c, y);
-            const double yv = __shfl_sync(0xffffffffu, xv, y);
-            const int64_t ym = __shfl_sync(0xffffffffu, xm, y);
-            const int64_t yp = __shfl_sync(0xffffffffu, xp, y);
-            const int yn = __shfl_sync(0xffffffffu, xn, y);
-            if (yc < c && yv >= xv && ym <= xm && yp >= xp) {
-              const bool equal = yv == xv && ym == xm && yp == xp;
-              if (!equal || yn >= xn) acc = false;
+          if (n > 64) continue;
+          int cc[2] = {-1, -1}, cn[2] = {-1, -1};
+          double xv[2] = {0.0, 0.0};
+          int64_t xm[2] = {0, 0}, xp[2] = {0, 0};
+          bool fit = true;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            if (32 * k + lane < n) {
+              const int c = Blst[offB[b] + 32 * k + lane];
+              cc[k] = c;
+              xv[k] = Cvl[c]; xm[k] = Cmm[c]; xp[k] = Cpb[c];
+              cn[k] = c * 256 + Cna[c];  // candidate index (< 2^23) and n_admitted (<= 250)
+              fit = fit && fabs(xv[k]) < 2147483647.0 && xm[k] >= INT32_MIN && xm[k] <= INT32_MAX &&
+                    xp[k] >= INT32_MIN && xp[k] <= INT32_MAX;
             }
           }
-          const unsigned Am = __ballot_sync(0xffffffffu, acc);
-          bool pr = false;
-          for (unsigned t = Am; t; t &= t - 1) {
-            const int y = __ffs(t) - 1;
-            const int yc = __shfl_sync(0xffffffffu, c, y);
-            const double yv = __shfl_sync(0xffffffffu, xv, y);
-            const int64_t ym = __shfl_sync(0xffffffffu, xm, y);
-            const int64_t yp = __shfl_sync(0xffffffffu, xp, y);
-            if (yc > c && yv >= xv && ym <= xm && yp >= xp) pr = true;
+          bool acc[2] = {true, true};
+          uint64_t pm[2] = {0ull, 0ull};
+          if (__all_sync(0xffffffffu, fit)) {
+            const int v32[2] = {(int)xv[0], (int)xv[1]};
+            const int m32[2] = {(int)xm[0], (int)xm[1]};
+            const int p32[2] = {(int)xp[0], (int)xp[1]};
+            bucket_pair_tests(n, cn, v32, m32, p32, acc, pm);
+          } else {
+            bucket_pair_tests(n, cn, xv, xm, xp, acc, pm);
           }
-          if (acc) Cfl[c] |= pr ? 6 : 2;
-          if (__any_sync(0xffffffffu, acc && !pr) && lane == 0) hsbA[b] = 1;
+          const uint64_t Am = (uint64_t)__ballot_sync(0xffffffffu, acc[0] && lane < n) |
+                              ((uint64_t)__ballot_sync(0xffffffffu, acc[1] && 32 + lane < n) << 32);
+          bool surv = false;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            if (32 * k + lane < n && acc[k]) {
+              const bool pr = (pm[k] & Am) != 0;
+              Cfl[cc[k]] |= pr ? 6 : 2;
+              surv = surv || !pr;
+            }
+          }
+          if (__any_sync(0xffffffffu, surv) && lane == 0) hsbA[b] = 1;
         }
       }
       if (s_bovf) {  // larger buckets: one thread per candidate over the bucket list
       for (int c = tid; c < T; c += kDpThreads) {
         const int b = Cbk[c];
-        if (b < 0 || cntB[b] <= 32) continue;
+        if (b < 0 || cntB[b] <= 64) continue;
         const double xv = Cvl[c];
         const int64_t xm = Cmm[c], xp = Cpb[c];
         const int xn = Cna[c];
@@ -1439,7 +1477,7 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
       for (int c = tid; c < T; c += kDpThreads, ++it) {
         if (!(Cfl[c] & 2)) continue;
         const int b = Cbk[c];
-        if (cntB[b] <= 32) continue;
+        if (cntB[b] <= 64) continue;
         const double xv = Cvl[c];
         const int64_t xm = Cmm[c], xp = Cpb[c];
         const int32_t* lst = Blst + offB[b];
