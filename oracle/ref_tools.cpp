@@ -7,6 +7,9 @@
 //                              (acceptance_main.cpp:577-605); pins our C generator.
 //   slos_ref_oracle_instances  the reference's brute-force instance generator
 //                              (tests/oracle.cpp:67-102) serialised as int64 records.
+//   slos_ref_trace             slosim::scale_scenario + slosim::generate_trace (the
+//                              reference's own code) into include/slos_trace.h's layout,
+//                              the checker of the product's batched trace generator.
 //   slos_ref_oracle_best_value / slos_ref_oracle_subset_feasible
 //                              tests/oracle.cpp:8-65 on such a record.
 
@@ -15,6 +18,12 @@
 #include <vector>
 
 #include "oracle.hpp"
+#include "slos_trace.h"
+#include "slosim/common.hpp"
+#include "slosim/metrics.hpp"
+#include "slosim/workload.hpp"
+#include <cstdlib>
+#include <cstring>
 
 using namespace slosim;
 
@@ -111,6 +120,80 @@ int32_t slos_ref_oracle_subset_feasible(const int64_t* record, const int32_t* ad
                                         int32_t n) {
   std::vector<int> a(admitted, admitted + n);
   return oracle::subset_feasible(decode(record), a) ? 1 : 0;
+}
+
+// The reference's trace for one slos_trace_job (include/slos_trace.h layout).
+int32_t slos_ref_trace(const slos_trace_job* job, slos_trace* out) {
+  std::memset(out, 0, sizeof *out);
+  const slos_scenario& s = *job->scenario;
+  ScenarioConfig sc;
+  sc.name = "ref";
+  sc.shape = s.shape == SLOS_SHAPE_SINGLE ? "single"
+             : s.shape == SLOS_SHAPE_REASONING ? "reasoning"
+             : s.shape == SLOS_SHAPE_TOOL ? "tool" : "unknown";
+  sc.arrival.process = s.process == SLOS_ARRIVAL_POISSON ? "poisson" : s.process == SLOS_ARRIVAL_BURSTY ? "bursty" : "other";
+  sc.arrival.rate_per_s = s.rate_per_s;
+  sc.arrival.on_multiplier = s.on_multiplier;
+  sc.arrival.mean_on_s = s.mean_on_s;
+  sc.arrival.mean_off_s = s.mean_off_s;
+  sc.prompt_tokens = {s.prompt_mean, s.prompt_std};
+  sc.output_tokens = {s.output_mean, s.output_std};
+  sc.think_tokens = {s.think_mean, s.think_std};
+  sc.response_tokens = {s.response_mean, s.response_std};
+  sc.prefill_tier = s.prefill_tier;
+  sc.decode_tier = s.decode_tier;
+  sc.think_tier = s.think_tier;
+  sc.response_tier = s.response_tier;
+  sc.value = s.value;
+  sc.tool_pairs_mean = s.tool_pairs_mean;
+  sc.tool_pairs_std = s.tool_pairs_std;
+  sc.tool_delay_min_s = s.tool_delay_min_s;
+  sc.tool_delay_max_s = s.tool_delay_max_s;
+  sc.memory_overprovision = s.memory_overprovision;
+  sc.slo.tpot_tiers_s.assign(s.tpot_tiers_s, s.tpot_tiers_s + s.n_tiers);
+  sc.slo.ttft_slowdowns.assign(s.ttft_slowdowns, s.ttft_slowdowns + s.n_tiers);
+  sc.slo.tpot_window = s.tpot_window;
+  std::vector<RequestSpec> reqs;
+  try {
+    reqs = generate_trace(scale_scenario(sc, job->rate_scale), job->seed, job->duration_s);
+  } catch (const Error& e) {
+    const std::string c = e.code();
+    out->status = c == "invalid-distribution-parameters" ? SLOS_ERR_INVALID_DISTRIBUTION
+                  : c == "invariant-violation"           ? SLOS_ERR_INVARIANT
+                  : c == "invalid-parameters"            ? 1
+                                                         : 2;
+    return out->status;
+  }
+  size_t ns = 0;
+  for (const auto& r : reqs) ns += r.stages.size();
+  out->stages = (slos_trace_stage*)std::malloc(std::max<size_t>(1, ns * sizeof(slos_trace_stage)));
+  out->requests = (slos_trace_request*)std::malloc(std::max<size_t>(1, reqs.size() * sizeof(slos_trace_request)));
+  size_t x = 0;
+  for (size_t k = 0; k < reqs.size(); ++k) {
+    const RequestSpec& r = reqs[k];
+    slos_trace_request& q = out->requests[k];
+    q.arrival_s = r.arrival_s;
+    q.value = r.value;
+    q.memory_units = r.memory_units;
+    q.first_stage = (int32_t)x;
+    q.n_stages = (int32_t)r.stages.size();
+    for (const auto& st : r.stages) {
+      slos_trace_stage& o = out->stages[x++];
+      o.tokens = st.tokens;
+      o.external_delay_s = st.external_delay_s;
+      o.kind = st.kind == StageKind::kPrefill ? 0 : 1;
+      o.slo_tier = st.slo_tier;
+    }
+  }
+  out->n_requests = (int32_t)reqs.size();
+  out->n_stages = (int64_t)ns;
+  return 0;
+}
+
+void slos_ref_trace_free(slos_trace* t) {
+  std::free(t->stages);
+  std::free(t->requests);
+  std::memset(t, 0, sizeof *t);
 }
 
 }  // extern "C"

@@ -42,7 +42,7 @@ def build_product(force: bool = False, verbose: bool = False, defines=(), out: s
     (e.g. -DSLOS_DP_THREADS=128 into exp/, selected with SLOS_PRODUCT_LIB)."""
     out = out or os.path.join(PKG, "libslos_b200.so")
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
-        os.path.join(ROOT, "include", h) for h in ("slos_planner.h", "slos_plan_json.h", "slos_route.h")]
+        os.path.join(ROOT, "include", h) for h in ("slos_planner.h", "slos_plan_json.h", "slos_route.h", "slos_trace.h")]
     if not force and not _stale(out, deps):
         return out
     bdir = os.path.join(PKG, "build") if not defines else os.path.join(os.path.dirname(out), "build")
@@ -57,7 +57,9 @@ def build_product(force: bool = False, verbose: bool = False, defines=(), out: s
     _run(["g++", "-std=c++17", "-O2", "-fPIC", "-c", os.path.join(CSRC, "slos_json.cpp"), "-o", jo])
     ro = os.path.join(bdir, "slos_route.o")  # host-only: batched routing rounds over slos_plan_batch
     _run(["g++", "-std=c++17", "-O2", "-fPIC", "-c", os.path.join(CSRC, "slos_route.cpp"), "-o", ro])
-    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xlinker", "-Bsymbolic", ko, ho, jo, ro, "-o", out,
+    to = os.path.join(bdir, "slos_trace.o")  # host-only: batched trace generation (libstdc++ <random>)
+    _run(["g++", "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-c", os.path.join(CSRC, "slos_trace.cpp"), "-o", to])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xlinker", "-Bsymbolic", ko, ho, jo, ro, to, "-o", out,
           "-lpthread", "-ldl", "-lrt"])
     return out
 
