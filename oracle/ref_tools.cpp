@@ -10,6 +10,8 @@
 //   slos_ref_trace             slosim::scale_scenario + slosim::generate_trace (the
 //                              reference's own code) into include/slos_trace.h's layout,
 //                              the checker of the product's batched trace generator.
+//   slos_ref_perf_fit          slosim::PerfModel::fit (the reference's own), the checker of
+//                              the product's device fit (include/slos_fit.h).
 //   slos_ref_oracle_best_value / slos_ref_oracle_subset_feasible
 //                              tests/oracle.cpp:8-65 on such a record.
 
@@ -19,6 +21,8 @@
 
 #include "oracle.hpp"
 #include "slos_trace.h"
+#include "slos_fit.h"
+#include "slosim/perf_model.hpp"
 #include "slosim/common.hpp"
 #include "slosim/metrics.hpp"
 #include "slosim/workload.hpp"
@@ -194,6 +198,25 @@ void slos_ref_trace_free(slos_trace* t) {
   std::free(t->stages);
   std::free(t->requests);
   std::memset(t, 0, sizeof *t);
+}
+
+// The reference's PerfModel::fit on one profile set; terms in the model's order.
+int32_t slos_ref_perf_fit(const slos_profile_sample* x, int32_t n, int32_t num_terms, int32_t max_iters,
+                          slos_perf_term* out) {
+  std::vector<ProfileSample> s((size_t)std::max(0, n));
+  for (int i = 0; i < n; ++i) s[i] = ProfileSample{x[i].num_tokens, x[i].spec_step, x[i].latency_s};
+  try {
+    const PerfModel m = PerfModel::fit(s, num_terms, max_iters);
+    const auto& t = m.terms();
+    for (size_t q = 0; q < t.size(); ++q) out[q] = slos_perf_term{t[q].k1, t[q].k2, t[q].b};
+    return (int32_t)t.size() == num_terms ? 0 : 2;
+  } catch (const Error& e) {
+    const std::string c = e.code();
+    return c == "insufficient-samples" ? SLOS_ERR_INSUFFICIENT_SAMPLES
+           : c == "degenerate-samples" ? SLOS_ERR_DEGENERATE_SAMPLES
+           : c == "invalid-parameters" ? 1
+                                       : 2;
+  }
 }
 
 }  // extern "C"

@@ -42,7 +42,7 @@ def build_product(force: bool = False, verbose: bool = False, defines=(), out: s
     (e.g. -DSLOS_DP_THREADS=128 into exp/, selected with SLOS_PRODUCT_LIB)."""
     out = out or os.path.join(PKG, "libslos_b200.so")
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
-        os.path.join(ROOT, "include", h) for h in ("slos_planner.h", "slos_plan_json.h", "slos_route.h", "slos_trace.h")]
+        os.path.join(ROOT, "include", h) for h in ("slos_planner.h", "slos_plan_json.h", "slos_route.h", "slos_trace.h", "slos_fit.h")]
     if not force and not _stale(out, deps):
         return out
     bdir = os.path.join(PKG, "build") if not defines else os.path.join(os.path.dirname(out), "build")

@@ -220,6 +220,26 @@ struct GapOutDev {
 };
 
 // dp_kernel / anchor_kernel launch parameters (host and device share this layout).
+// PerfModel::fit on the device (slos_fit.cuh)
+struct FitSet {
+  int64_t off;  // first sample in the SoA arrays
+  int32_t n;    // samples
+  int32_t run;  // 0: skipped (the host already reported an error)
+};
+
+struct FitParams {
+  const FitSet* sets;
+  const int64_t* nt;   // num_tokens
+  const int64_t* ss;   // spec_step
+  const double* lat;   // latency_s
+  int32_t* assign;     // regime per sample (host: initial quantile bands)
+  double* e2;          // squared residual per sample (scratch)
+  double* out;         // per set: T x (k1, k2, b) of the best iteration
+  int32_t* ok;         // per set: 1 when an iteration recorded a best model
+  int T;
+  int max_iters;
+};
+
 struct DpParams {
   BatchArgs a;
   int Sc;              // per-warp slot capacity

@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <numeric>
+#include <set>
 #include <chrono>
 #include <condition_variable>
 #include <functional>
@@ -29,6 +31,7 @@
 #include "slos_dev.h"
 #include "slos_launch.h"
 #include "../../include/slos_planner.h"
+#include "../../include/slos_fit.h"
 
 namespace slos {
 struct GapBatchOut {
@@ -2472,4 +2475,121 @@ int slos_solve_spec_lengths(slos_planner* p, const int64_t* counts, int32_t n_ti
   return SLOS_OK;
 }
 
+
+// ---- PerfModel::fit on the device (include/slos_fit.h) ----------------------
+// The host checks the arguments (perf_model.cpp:134-140), forms the reference's
+// initial regimes -- contiguous quantile bands of the (num_tokens, spec_step) order,
+// the same std::sort call on the same input, hence the same permutation (:143-151)
+// -- and orders the best terms at the end (:193-198); the iterations run in
+// fit_kernel, one CTA per set.
+int slos_perf_fit_batch(const slos_profile_sample* const* sets, const int32_t* n_samples, int32_t n_sets,
+                        int32_t num_terms, int32_t max_iters, slos_perf_term* terms_out, int32_t* status) {
+  g_err.clear();
+  if (n_sets <= 0) return SLOS_OK;
+  if (!sets || !n_samples || !terms_out || !status) return set_err(SLOS_ERR_INVALID_PARAMETERS, "null argument");
+  if (num_terms < 1 || num_terms > SLOS_FIT_MAX_TERMS) {
+    for (int k = 0; k < n_sets; ++k) status[k] = SLOS_ERR_INVALID_PARAMETERS;
+    return set_err(SLOS_ERR_INVALID_PARAMETERS, "num_terms must be in [1, 32]");
+  }
+  Ctx& c = ctx();
+  std::lock_guard<std::mutex> g(c.mu);
+  int st = ensure_device(c);
+  if (st != SLOS_OK) {
+    for (int k = 0; k < n_sets; ++k) status[k] = st;
+    return set_err(st, c.why);
+  }
+  const int T = num_terms;
+  std::vector<FitSet> fs((size_t)n_sets);
+  int64_t total = 0;
+  for (int k = 0; k < n_sets; ++k) {
+    fs[k].off = total;
+    fs[k].n = std::max(0, n_samples[k]);
+    fs[k].run = 0;
+    total += fs[k].n;
+  }
+  std::vector<int64_t> nt((size_t)total), sp((size_t)total);
+  std::vector<double> lat((size_t)total);
+  std::vector<int32_t> assign((size_t)total);
+  for (int k = 0; k < n_sets; ++k) {
+    const int n = fs[k].n;
+    const slos_profile_sample* x = sets[k];
+    status[k] = SLOS_OK;
+    if (n < 3 * T) { status[k] = SLOS_ERR_INSUFFICIENT_SAMPLES; continue; }  // "need at least 3 samples per term"
+    std::set<int64_t> distinct;
+    for (int i = 0; i < n; ++i) distinct.insert(x[i].num_tokens);
+    if ((int)distinct.size() < T) { status[k] = SLOS_ERR_DEGENERATE_SAMPLES; continue; }
+    std::vector<int> order((size_t)n);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+      if (x[a].num_tokens != x[b].num_tokens) return x[a].num_tokens < x[b].num_tokens;
+      return x[a].spec_step < x[b].spec_step;
+    });
+    const int64_t o = fs[k].off;
+    for (size_t r = 0; r < order.size(); ++r) assign[o + order[r]] = static_cast<int>(r * T / order.size());
+    for (int i = 0; i < n; ++i) {
+      nt[o + i] = x[i].num_tokens;
+      sp[o + i] = x[i].spec_step;
+      lat[o + i] = x[i].latency_s;
+    }
+    fs[k].run = 1;
+  }
+  Blob b;
+  const size_t o_set = b.add<FitSet>(n_sets), o_nt = b.add<int64_t>(total), o_ss = b.add<int64_t>(total),
+               o_lat = b.add<double>(total), o_as = b.add<int32_t>(total), o_e2 = b.add<double>(total),
+               o_out = b.add<double>((size_t)n_sets * T * 3), o_ok = b.add<int32_t>(n_sets);
+  unsigned char* D = nullptr;
+  cudaError_t e = cudaMalloc(&D, b.bytes);
+  if (e != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  std::vector<unsigned char> H(o_e2);
+  std::memcpy(H.data() + o_set, fs.data(), sizeof(FitSet) * fs.size());
+  if (total) {
+    std::memcpy(H.data() + o_nt, nt.data(), 8 * (size_t)total);
+    std::memcpy(H.data() + o_ss, sp.data(), 8 * (size_t)total);
+    std::memcpy(H.data() + o_lat, lat.data(), 8 * (size_t)total);
+    std::memcpy(H.data() + o_as, assign.data(), 4 * (size_t)total);
+  }
+  cudaMemcpyAsync(D, H.data(), o_e2, cudaMemcpyHostToDevice, c.stream);
+  cudaMemsetAsync(D + o_ok, 0, 4 * (size_t)n_sets, c.stream);
+  FitParams prm;
+  prm.sets = (const FitSet*)(D + o_set);
+  prm.nt = (const int64_t*)(D + o_nt);
+  prm.ss = (const int64_t*)(D + o_ss);
+  prm.lat = (const double*)(D + o_lat);
+  prm.assign = (int32_t*)(D + o_as);
+  prm.e2 = (double*)(D + o_e2);
+  prm.out = (double*)(D + o_out);
+  prm.ok = (int32_t*)(D + o_ok);
+  prm.T = T;
+  prm.max_iters = max_iters;
+  e = launch_fit(prm, n_sets, c.stream);
+  std::vector<double> out((size_t)n_sets * T * 3);
+  std::vector<int32_t> ok((size_t)n_sets);
+  if (e == cudaSuccess) {
+    cudaMemcpyAsync(out.data(), D + o_out, 8 * out.size(), cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(ok.data(), D + o_ok, 4 * ok.size(), cudaMemcpyDeviceToHost, c.stream);
+    e = cudaStreamSynchronize(c.stream);
+  }
+  cudaFree(D);
+  if (e != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  for (int k = 0; k < n_sets; ++k) {
+    slos_perf_term* t = terms_out + (size_t)k * T;
+    if (status[k] != SLOS_OK || !ok[k]) {
+      // no iteration improved on +inf (NaN residuals): the reference's PerfModel
+      // rejects the empty term list as invalid parameters (perf_model.cpp:97)
+      if (status[k] == SLOS_OK) status[k] = SLOS_ERR_INVALID_PARAMETERS;
+      for (int q = 0; q < T; ++q) t[q] = slos_perf_term{0.0, 0.0, 0.0};
+      continue;
+    }
+    for (int q = 0; q < T; ++q) {
+      const double* x = &out[((size_t)k * T + q) * 3];
+      t[q] = slos_perf_term{x[0], x[1], x[2]};
+    }
+    std::sort(t, t + T, [](const slos_perf_term& a, const slos_perf_term& b) {
+      if (a.k1 != b.k1) return a.k1 < b.k1;
+      if (a.k2 != b.k2) return a.k2 < b.k2;
+      return a.b < b.b;
+    });
+  }
+  return SLOS_OK;
+}
 }  // extern "C"

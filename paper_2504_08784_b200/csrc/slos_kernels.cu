@@ -7,6 +7,7 @@
 
 #include "slos_build.cuh"
 #include "slos_dp.cuh"
+#include "slos_fit.cuh"
 #include "slos_launch.h"
 
 namespace slos {
@@ -169,6 +170,12 @@ cudaError_t launch_spec(const PlannerDev* P, const int64_t* counts, void* out, c
 }
 
 size_t spec_sol_bytes() { return sizeof(SpecSol); }
+
+cudaError_t launch_fit(const FitParams& prm, int n_sets, cudaStream_t s) {
+  if (n_sets <= 0) return cudaSuccess;
+  fit_kernel<<<n_sets, kFitThreads, 0, s>>>(prm);
+  return cudaGetLastError();
+}
 
 __global__ void records_kernel(const OutHdr* out, const int32_t* map, int nv, slos_record* rec) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;

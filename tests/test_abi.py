@@ -14,9 +14,14 @@ from paper_2504_08784_b200 import abi
 HEADER = os.path.join(abi.ROOT, "include", "slos_planner.h")
 
 
-def declared():
+# headers whose functions libslos_b200.so implements (slos_lockstep.h belongs to the
+# reference-side integration library, integration/)
+PRODUCT_HEADERS = ["slos_planner.h", "slos_plan_json.h", "slos_route.h", "slos_trace.h", "slos_fit.h"]
+
+
+def declared(header=HEADER):
     # header-only inline accessors (SLOS_ENTRY_FN) are not exported symbols
-    src = "\n".join(l for l in open(HEADER).read().splitlines() if not l.startswith("SLOS_ENTRY_FN") and "return " not in l)
+    src = "\n".join(l for l in open(header).read().splitlines() if not l.startswith("SLOS_ENTRY_FN") and "return " not in l)
     return sorted(set(re.findall(r"^[a-z_ ]*?[\w\*]+\s+\**(slos_\w+)\(", src, re.M)))
 
 
@@ -39,6 +44,14 @@ def test_every_declared_symbol_is_exported(path):
         pytest.skip(f"{path} not built")
     missing = [n for n in declared() if n not in exported(path)]
     assert not missing, missing
+
+
+@pytest.mark.parametrize("header", PRODUCT_HEADERS)
+def test_product_exports_every_header(header):
+    names = declared(os.path.join(abi.ROOT, "include", header))
+    assert names, header
+    missing = [n for n in names if n not in exported(abi.PRODUCT_LIB)]
+    assert not missing, (header, missing)
 
 
 def test_product_library_loads_and_identifies():
