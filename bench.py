@@ -645,6 +645,11 @@ def run_ours(args):
             c3 = leg_c3(lib, stream, max(3, args.steps // 2), args.warmup, with_cpu)
             if c3 is not None:
                 legs["C3"] = c3
+            # the callers either side of the planner
+            from paper_2504_08784_b200 import fit as fit_mod
+            from paper_2504_08784_b200 import trace as trace_mod
+            legs["trace"] = trace_mod.bench_leg(ROOT, max(3, args.steps // 2), args.warmup, with_cpu)
+            legs["fit"] = fit_mod.bench_leg(max(3, args.steps // 2), args.warmup, with_cpu)
         if world > 1:
             dist.barrier()
 

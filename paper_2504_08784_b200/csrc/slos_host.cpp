@@ -1686,6 +1686,10 @@ const char* slos_status_slug(int s) {
     case SLOS_ERR_NO_DEVICE: return "no-device";
     case SLOS_ERR_ALLOC: return "alloc";
     case SLOS_ERR_RANGE: return "range";
+    case 20: return "invalid-distribution-parameters";  // slos_trace.h
+    case 21: return "invariant-violation";
+    case 22: return "insufficient-samples";             // slos_fit.h
+    case 23: return "degenerate-samples";
     default: return "error";
   }
 }

@@ -55,3 +55,44 @@ def reference_fit(samples: np.ndarray, num_terms: int, max_iters: int = 100):  #
     out = (abi.PerfTerm * max(1, num_terms))()
     st = lib.slos_ref_perf_fit(a.ctypes.data, len(a), num_terms, max_iters, out)
     return np.array([[t.k1, t.k2, t.b] for t in out], dtype=np.float64), int(st)
+
+
+def bench_sets(count: int = 64, seed: int = 7):
+    """Profile sets shaped like the reference's fit criterion (acceptance_main.cpp:
+    629-648): n = 8..8192 step 64 x spec_step {0,2,5,8}, +-2% noise, two regimes
+    with per-set coefficients."""
+    rng = np.random.default_rng(seed)
+    n, s = np.meshgrid(np.arange(8, 8193, 64), [0, 2, 5, 8], indexing="ij")
+    n, s = n.ravel(), s.ravel()
+    out = []
+    for _ in range(count):
+        k1, k2, b = rng.uniform(1e-6, 5e-5), rng.uniform(1e-4, 3e-3), rng.uniform(1e-3, 1e-2)
+        floor = rng.uniform(0.005, 0.03)
+        lat = np.maximum(k1 * n + k2 * s + b, floor) * (1.0 + rng.uniform(-0.02, 0.02, len(n)))
+        out.append(as_samples(n, s, lat))
+    return out
+
+
+def bench_leg(steps: int, warmup: int, with_cpu: bool):
+    """f4 leg of bench.py: 64 two-regime fits per step through slos_perf_fit_batch
+    (one CTA per set), the reference's PerfModel::fit looped beside it."""
+    import time
+    sets = bench_sets()
+    for _ in range(max(1, warmup)):
+        terms, st = fit_batch(sets, 2)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        terms, st = fit_batch(sets, 2)
+    dt = (time.perf_counter() - t0) / steps
+    leg = {"workload": f"f4: PerfModel::fit, {len(sets)} profile sets x {len(sets[0])} samples, 2 terms, "
+                       "through the C-ABI (host bands + device iterations)",
+           "value": len(sets) / dt, "unit": "fits/s", "ms_per_step": dt * 1e3, "statuses_ok": bool((st == 0).all())}
+    if with_cpu:
+        sample = sets[:16]
+        t0 = time.perf_counter()
+        ref = [reference_fit(x, 2) for x in sample]
+        rdt = time.perf_counter() - t0
+        leg["cpu_baseline"] = {"value": len(sample) / rdt, "unit": "fits/s", "cores": 1, "kind": "reference",
+                               "sample": f"{len(sample)} sets through the reference's PerfModel::fit, {rdt:.2f} s wall"}
+        leg["identical_to_reference"] = all(terms[k].tobytes() == ref[k][0].tobytes() for k in range(len(sample)))
+    return leg

@@ -174,7 +174,7 @@ def generate_traces(points, threads: int = 0, lib=None):
     return res
 
 
-def reference_traces(points):  # test infrastructure only: the reference's generate_trace
+def reference_traces(points, timed: bool = False):  # test infrastructure only: the reference's generate_trace
     lib = abi.reference()
     if not getattr(lib, "_trace_ref_bound", False):
         lib.slos_ref_trace.argtypes = [C.POINTER(TraceJob), C.POINTER(Trace)]
@@ -182,11 +182,75 @@ def reference_traces(points):  # test infrastructure only: the reference's gener
         lib.slos_ref_trace_free.argtypes = [C.POINTER(Trace)]
         lib.slos_ref_trace_free.restype = None
         lib._trace_ref_bound = True
+    import time
     jobs, pts = make_jobs(points)
-    res = []
+    res, dt = [], 0.0
     for k in range(len(pts)):
         t = Trace()
+        t0 = time.perf_counter()
         lib.slos_ref_trace(C.byref(jobs[k]), C.byref(t))
+        dt += time.perf_counter() - t0
         res.append(to_numpy(t))
         lib.slos_ref_trace_free(C.byref(t))
-    return res
+    return (res, dt) if timed else res
+
+
+def bench_points(root: str, seeds: int = 16, horizon_s: float = 60.0):
+    """The C5 sweep's trace grid: every scenario file under
+    tests/golden/scenarios with bursty arrivals (coder.json's burst parameters) x
+    4 rate scales x `seeds` seeds."""
+    import glob
+    import os
+    pts = []
+    for p in sorted(glob.glob(os.path.join(root, "tests", "golden", "scenarios", "*.json"))):
+        d = json.load(open(p))
+        d["arrival"] = dict(d.get("arrival", {}), process="bursty", on_multiplier=4.0, mean_on_s=10.0,
+                            mean_off_s=30.0)
+        sc = scenario_from_json(d)
+        for scale in (0.5, 1.0, 2.0, 4.0):
+            for seed in range(seeds):
+                pts.append((sc, scale, seed, horizon_s))
+    return pts
+
+
+def bench_leg(root: str, steps: int, warmup: int, with_cpu: bool):
+    """f3 leg of bench.py: the whole trace grid per step through slos_trace_batch
+    (all host threads) and, beside it, the reference's generate_trace looped over a
+    bounded sample on one thread (it has no batched entry point)."""
+    import os
+    import time
+    pts = bench_points(root)
+    lib = _bind(abi.product())
+    jobs, _ = make_jobs(pts)
+    outs = (Trace * len(pts))()
+    dts = []
+    for it in range(max(1, warmup) + steps):  # timed: the C-ABI call (generation + result arrays)
+        t0 = time.perf_counter()
+        lib.slos_trace_batch(jobs, len(pts), 0, outs)
+        dt = time.perf_counter() - t0
+        if it >= max(1, warmup):
+            dts.append(dt)
+        if it + 1 < max(1, warmup) + steps:
+            for k in range(len(pts)):
+                lib.slos_trace_free(C.byref(outs[k]))
+    res = [to_numpy(outs[k]) for k in range(len(pts))]
+    for k in range(len(pts)):
+        lib.slos_trace_free(C.byref(outs[k]))
+    dt = sum(dts) / len(dts)
+    n_req = sum(len(r[1]) for r in res)
+    leg = {"workload": f"f3: batched trace generation, {len(pts)} traces (6 scenarios, bursty, 4 rate scales x "
+                       f"16 seeds, 60 s) = {n_req} requests per step",
+           "value": len(pts) / dt, "unit": "traces/s", "requests_per_s": n_req / dt, "ms_per_step": dt * 1e3,
+           "threads": os.cpu_count(), "statuses_ok": all(r[0] == 0 for r in res)}
+    if with_cpu:
+        idx = list(range(0, len(pts), 8))  # every 8th point: the grid's mix, bounded
+        sample = [pts[k] for k in idx]
+        ref, rdt = reference_traces(sample, timed=True)
+        n_ref = sum(len(r[1]) for r in ref)
+        leg["cpu_baseline"] = {"value": len(sample) / rdt, "unit": "traces/s", "requests_per_s": n_ref / rdt,
+                               "cores": 1, "kind": "reference",
+                               "sample": f"every 8th grid point ({len(sample)} traces, {n_ref} requests) through "
+                                         f"the reference's generate_trace, {rdt:.2f} s wall"}
+        leg["identical_to_reference"] = all(res[k][1].tobytes() == b[1].tobytes() and res[k][2].tobytes() == b[2].tobytes()
+                                            for k, b in zip(idx, ref))
+    return leg
