@@ -231,7 +231,10 @@ struct FitParams {
   const FitSet* sets;
   const int64_t* nt;   // num_tokens
   const int64_t* ss;   // spec_step
-  const double* lat;   // latency_s
+  double* lat;         // latency_s (HBM; also the unstaged path's working copy)
+  double* nd;          // num_tokens as double (unstaged path)
+  double* sd;          // spec_step as double (unstaged path)
+  int smem_samples;    // sets with at most this many samples run from shared memory
   int32_t* assign;     // regime per sample (host: initial quantile bands)
   double* e2;          // squared residual per sample (scratch)
   double* out;         // per set: T x (k1, k2, b) of the best iteration

@@ -21,10 +21,6 @@ namespace slos {
 constexpr int kFitThreads = 256;
 constexpr int kFitMaxTerms = 32;
 
-__device__ __forceinline__ double fit_col(int64_t nt, int64_t ss, int c) {
-  return c == 0 ? (double)nt : (c == 1 ? (double)ss : 1.0);
-}
-
 // term_value perf_model.cpp:92-94
 __device__ __forceinline__ double fit_term(double k1, double k2, double b, double n, double s) {
   return k1 * n + k2 * s + b;
@@ -34,11 +30,26 @@ __global__ void __launch_bounds__(kFitThreads) fit_kernel(FitParams prm) {
   const FitSet S = prm.sets[blockIdx.x];
   if (!S.run) return;
   const int n = S.n, T = prm.T;
+  // the set's samples as doubles (the reference converts each use, :28-31, exactly),
+  // staged in shared memory when they fit (prm.smem_samples), else read from HBM
+  extern __shared__ __align__(16) unsigned char fsm[];
+  const bool staged = n <= prm.smem_samples;
+  double* nd = staged ? (double*)fsm : prm.nd + S.off;
+  double* sd = staged ? nd + n : prm.sd + S.off;
+  double* lat = staged ? sd + n : prm.lat + S.off;
+  double* e2 = staged ? lat + n : prm.e2 + S.off;
+  int32_t* assign = staged ? (int32_t*)(e2 + n) : prm.assign + S.off;
   const int64_t* nt = prm.nt + S.off;
   const int64_t* ss = prm.ss + S.off;
-  const double* lat = prm.lat + S.off;
-  int32_t* assign = prm.assign + S.off;
-  double* e2 = prm.e2 + S.off;
+  for (int i = threadIdx.x; i < n; i += kFitThreads) {
+    nd[i] = (double)nt[i];
+    sd[i] = (double)ss[i];
+    if (staged) {
+      lat[i] = prm.lat[S.off + i];
+      assign[i] = prm.assign[S.off + i];
+    }
+  }
+  __syncthreads();
   __shared__ double tk1[kFitMaxTerms], tk2[kFitMaxTerms], tb[kFitMaxTerms];
   __shared__ double bk1[kFitMaxTerms], bk2[kFitMaxTerms], bb[kFitMaxTerms];
   __shared__ int first[kFitMaxTerms], uk1[kFitMaxTerms], uk2[kFitMaxTerms];
@@ -56,7 +67,7 @@ __global__ void __launch_bounds__(kFitThreads) fit_kernel(FitParams prm) {
     __syncthreads();
     for (int i = tid; i < n; i += kFitThreads) {
       const int g = assign[i], f = first[g];
-      if (nt[i] != nt[f]) uk1[g] = 1;
+      if (nt[i] != nt[f]) uk1[g] = 1;  // int64 compares, like the reference
       if (ss[i] != ss[f]) uk2[g] = 1;
     }
     __syncthreads();
@@ -75,10 +86,13 @@ __global__ void __launch_bounds__(kFitThreads) fit_kernel(FitParams prm) {
         if (lane < k * (k + 1)) {
           const int r = lane / (k + 1), c = lane % (k + 1);
           const int cr = cols[r], cc = c < k ? cols[c] : -1;
+          const double* xa = cr == 0 ? nd : (cr == 1 ? sd : nullptr);
+          const double* ya = cc == 0 ? nd : (cc == 1 ? sd : (cc == 2 ? nullptr : lat));
+#pragma unroll 4
           for (int i = 0; i < n; ++i) {
             if (assign[i] != g) continue;
-            const double xr = fit_col(nt[i], ss[i], cr);
-            acc += xr * (cc >= 0 ? fit_col(nt[i], ss[i], cc) : lat[i]);
+            const double xr = xa ? xa[i] : 1.0;
+            acc += xr * (ya ? ya[i] : 1.0);
           }
         }
         double a[3][4];
@@ -132,11 +146,11 @@ __global__ void __launch_bounds__(kFitThreads) fit_kernel(FitParams prm) {
     // (C) argmax regime of every sample (ties prefer the smaller intercept)
     int changed = 0;
     for (int i = tid; i < n; i += kFitThreads) {
-      const double nd = (double)nt[i], sd = (double)ss[i];
+      const double ni = nd[i], si = sd[i];
       int arg = 0;
-      double v = fit_term(tk1[0], tk2[0], tb[0], nd, sd);
+      double v = fit_term(tk1[0], tk2[0], tb[0], ni, si);
       for (int g = 1; g < T; ++g) {
-        const double vg = fit_term(tk1[g], tk2[g], tb[g], nd, sd);
+        const double vg = fit_term(tk1[g], tk2[g], tb[g], ni, si);
         if (vg > v + 1e-15 || (fabs(vg - v) <= 1e-15 && tb[g] < tb[arg])) {
           v = vg;
           arg = g;

@@ -134,8 +134,8 @@ struct Ctx {
   std::string why;
   cudaStream_t stream = nullptr;
   size_t smem_optin = 0;  // opt-in dynamic shared memory per CTA (227 KB on B200)
-  DevBuf d_in, d_scr, d_out, d_pack, d_wscr, d_small;
-  PinBuf h_in, h_small;
+  DevBuf d_in, d_scr, d_out, d_pack, d_wscr, d_small, d_fit;
+  PinBuf h_in, h_small, h_fit;
   std::mutex pool_mu;
   std::vector<ResultArena*> pool;
 };
@@ -2514,14 +2514,19 @@ int slos_perf_fit_batch(const slos_profile_sample* const* sets, const int32_t* n
   std::vector<int64_t> nt((size_t)total), sp((size_t)total);
   std::vector<double> lat((size_t)total);
   std::vector<int32_t> assign((size_t)total);
-  for (int k = 0; k < n_sets; ++k) {
+  // per set (independent; the host worker pool takes them): checks, initial bands
+  HostPool::get().run(n_sets, [&](int lo, int hi) {
+  for (int k = lo; k < hi; ++k) {
     const int n = fs[k].n;
     const slos_profile_sample* x = sets[k];
     status[k] = SLOS_OK;
     if (n < 3 * T) { status[k] = SLOS_ERR_INSUFFICIENT_SAMPLES; continue; }  // "need at least 3 samples per term"
-    std::set<int64_t> distinct;
-    for (int i = 0; i < n; ++i) distinct.insert(x[i].num_tokens);
-    if ((int)distinct.size() < T) { status[k] = SLOS_ERR_DEGENERATE_SAMPLES; continue; }
+    {  // distinct num_tokens (the reference's std::set, :137-140)
+      std::vector<int64_t> d((size_t)n);
+      for (int i = 0; i < n; ++i) d[i] = x[i].num_tokens;
+      std::sort(d.begin(), d.end());
+      if ((int)(std::unique(d.begin(), d.end()) - d.begin()) < T) { status[k] = SLOS_ERR_DEGENERATE_SAMPLES; continue; }
+    }
     std::vector<int> order((size_t)n);
     std::iota(order.begin(), order.end(), 0);
     std::sort(order.begin(), order.end(), [&](int a, int b) {
@@ -2537,44 +2542,54 @@ int slos_perf_fit_batch(const slos_profile_sample* const* sets, const int32_t* n
     }
     fs[k].run = 1;
   }
+  });
   Blob b;
   const size_t o_set = b.add<FitSet>(n_sets), o_nt = b.add<int64_t>(total), o_ss = b.add<int64_t>(total),
                o_lat = b.add<double>(total), o_as = b.add<int32_t>(total), o_e2 = b.add<double>(total),
+               o_nd = b.add<double>(total), o_sd = b.add<double>(total),
                o_out = b.add<double>((size_t)n_sets * T * 3), o_ok = b.add<int32_t>(n_sets);
-  unsigned char* D = nullptr;
-  cudaError_t e = cudaMalloc(&D, b.bytes);
-  if (e != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-  std::vector<unsigned char> H(o_e2);
-  std::memcpy(H.data() + o_set, fs.data(), sizeof(FitSet) * fs.size());
+  cudaError_t e;
+  if ((e = c.d_fit.ensure(b.bytes)) != cudaSuccess || (e = c.h_fit.ensure(b.bytes)) != cudaSuccess)
+    return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  unsigned char* D = (unsigned char*)c.d_fit.p;
+  unsigned char* H = (unsigned char*)c.h_fit.p;  // pinned: inputs in, best terms out
+  std::memcpy(H + o_set, fs.data(), sizeof(FitSet) * fs.size());
   if (total) {
-    std::memcpy(H.data() + o_nt, nt.data(), 8 * (size_t)total);
-    std::memcpy(H.data() + o_ss, sp.data(), 8 * (size_t)total);
-    std::memcpy(H.data() + o_lat, lat.data(), 8 * (size_t)total);
-    std::memcpy(H.data() + o_as, assign.data(), 4 * (size_t)total);
+    std::memcpy(H + o_nt, nt.data(), 8 * (size_t)total);
+    std::memcpy(H + o_ss, sp.data(), 8 * (size_t)total);
+    std::memcpy(H + o_lat, lat.data(), 8 * (size_t)total);
+    std::memcpy(H + o_as, assign.data(), 4 * (size_t)total);
   }
-  cudaMemcpyAsync(D, H.data(), o_e2, cudaMemcpyHostToDevice, c.stream);
+  cudaMemcpyAsync(D, H, o_e2, cudaMemcpyHostToDevice, c.stream);
   cudaMemsetAsync(D + o_ok, 0, 4 * (size_t)n_sets, c.stream);
   FitParams prm;
   prm.sets = (const FitSet*)(D + o_set);
   prm.nt = (const int64_t*)(D + o_nt);
   prm.ss = (const int64_t*)(D + o_ss);
-  prm.lat = (const double*)(D + o_lat);
+  prm.lat = (double*)(D + o_lat);
+  prm.nd = (double*)(D + o_nd);
+  prm.sd = (double*)(D + o_sd);
+  // per sample in shared memory: num_tokens, spec_step, latency, residual (f64) and regime (i32)
+  constexpr size_t kPerSample = 4 * sizeof(double) + sizeof(int32_t);
+  int max_n = 0;
+  for (const FitSet& f : fs) max_n = std::max(max_n, f.n);
+  const size_t cap = std::min<size_t>(c.smem_optin, 200 * 1024) / kPerSample;
+  prm.smem_samples = (int)std::min<size_t>((size_t)max_n, cap);
+  const size_t fit_smem = (size_t)prm.smem_samples * kPerSample + 16;
   prm.assign = (int32_t*)(D + o_as);
   prm.e2 = (double*)(D + o_e2);
   prm.out = (double*)(D + o_out);
   prm.ok = (int32_t*)(D + o_ok);
   prm.T = T;
   prm.max_iters = max_iters;
-  e = launch_fit(prm, n_sets, c.stream);
-  std::vector<double> out((size_t)n_sets * T * 3);
-  std::vector<int32_t> ok((size_t)n_sets);
+  e = launch_fit(prm, n_sets, fit_smem, c.stream);
   if (e == cudaSuccess) {
-    cudaMemcpyAsync(out.data(), D + o_out, 8 * out.size(), cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(ok.data(), D + o_ok, 4 * ok.size(), cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(H + o_out, D + o_out, b.bytes - o_out, cudaMemcpyDeviceToHost, c.stream);
     e = cudaStreamSynchronize(c.stream);
   }
-  cudaFree(D);
   if (e != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+  const double* out = (const double*)(H + o_out);
+  const int32_t* ok = (const int32_t*)(H + o_ok);
   for (int k = 0; k < n_sets; ++k) {
     slos_perf_term* t = terms_out + (size_t)k * T;
     if (status[k] != SLOS_OK || !ok[k]) {

@@ -171,9 +171,11 @@ cudaError_t launch_spec(const PlannerDev* P, const int64_t* counts, void* out, c
 
 size_t spec_sol_bytes() { return sizeof(SpecSol); }
 
-cudaError_t launch_fit(const FitParams& prm, int n_sets, cudaStream_t s) {
+cudaError_t launch_fit(const FitParams& prm, int n_sets, size_t smem, cudaStream_t s) {
   if (n_sets <= 0) return cudaSuccess;
-  fit_kernel<<<n_sets, kFitThreads, 0, s>>>(prm);
+  cudaError_t e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fit_kernel<<<n_sets, kFitThreads, smem, s>>>(prm);
   return cudaGetLastError();
 }
 

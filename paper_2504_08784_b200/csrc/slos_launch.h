@@ -48,7 +48,7 @@ cudaError_t launch_predict(const PlannerDev* P, int n, const int64_t* t, const i
                            double* out, int32_t* st, cudaStream_t s);
 cudaError_t launch_spec(const PlannerDev* P, const int64_t* counts, void* out, cudaStream_t s);
 size_t spec_sol_bytes();
-cudaError_t launch_fit(const FitParams& prm, int n_sets, cudaStream_t s);
+cudaError_t launch_fit(const FitParams& prm, int n_sets, size_t smem, cudaStream_t s);
 cudaError_t launch_records(const OutHdr* out, const int32_t* map, int nv, slos_record* rec, cudaStream_t s);
 
 }  // namespace slos
