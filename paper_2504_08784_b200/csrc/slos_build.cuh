@@ -194,7 +194,7 @@ __device__ inline int emit_gap(const BatchArgs& A, BuildShared& sh, double a, bo
 // (decoder order, then EDF prefill order) is rank-major and one group scan per batch
 // places every entry.
 template <class G>
-__device__ inline void group_edf_fallback(const BatchArgs& A, BuildShared& sh, Arena ar, OutHdr* out) {
+__device__ __noinline__ void group_edf_fallback(const BatchArgs& A, BuildShared& sh, Arena ar, OutHdr* out) {
   const int lane = G::rank();
   constexpr int NT = G::kSize;
   const InstDev& I = sh.I;

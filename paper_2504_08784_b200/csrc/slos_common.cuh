@@ -19,8 +19,12 @@ __device__ __forceinline__ int64_t imax(int64_t a, int64_t b) { return (a < b) ?
 __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return (b < a) ? b : a; }
 
 // PerfModel::predict perf_model.cpp:106-114 (term_value :92-94).
+// Code size matters here: predict is inlined at hundreds of sites of the
+// reconstruction engine, whose warp form (one instance per warp) stalled on
+// instruction fetch; the loop stays rolled.
 __device__ __forceinline__ double predict(const PlannerDev& P, int64_t n, int64_t s) {
   double best = 0.0;
+#pragma unroll 1
   for (int t = 0; t < P.n_terms; ++t) {
     const double v = P.k1[t] * (double)n + P.k2[t] * (double)s + P.b[t];
     best = dmax(best, v);
@@ -182,7 +186,7 @@ __device__ __forceinline__ int min_len_covering(const PlannerDev& P, double tpot
 }
 
 // solve_spec_lengths batch_planner.cpp:51-115 (sequential, one thread).
-__device__ inline SpecSol solve_spec(const PlannerDev& P, const int64_t* counts) {
+__device__ __noinline__ SpecSol solve_spec(const PlannerDev& P, const int64_t* counts) {
   SpecSol best;
   best.ok = false;
   const int L = P.L;

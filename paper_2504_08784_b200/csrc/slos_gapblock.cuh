@@ -256,7 +256,7 @@ __device__ inline void blk_sort_mrec(MRec* r, int n_pow2) {
 }
 
 // prefill_only (batch_planner.cpp:177-195), thread 0 writes batches.
-__device__ inline int gap_prefill_only(const PlannerDev& P, double gap, double min_slot,
+__device__ __noinline__ int gap_prefill_only(const PlannerDev& P, double gap, double min_slot,
                                        GapPlanBuf& o) {
   double t = 0.0;
   const int64_t Cfull = imin(P.max_chunk, P.max_batch);  // see prefill_only_budget
