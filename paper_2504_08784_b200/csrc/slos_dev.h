@@ -123,6 +123,7 @@ struct BatchArgs {
   int32_t n_inst;
   const int32_t* atask;  // anchor tasks (instance, anchor j) pairs, j = -1 .. N-2
   int32_t n_atask;
+  int32_t mixed_spec;    // both speculative and autoregressive planners in the batch
   // decoders
   const int32_t* dec_idx;
   const int32_t* dec_tier;

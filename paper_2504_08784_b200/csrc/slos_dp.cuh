@@ -109,7 +109,7 @@ __device__ inline int memo_find_insert(MemoEnt* T, int64_t cap, uint64_t k0, uin
 // Evaluate one memo key (counts c) of a group: tile_gap(gap, census, dh).prefill_budget.
 // `gv`/`ga` is the group's shared exact-census variant (built by the block); a
 // count vector whose tightest tier differs builds a private variant in `w`.
-__device__ inline EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D, const GapGroup& g,
+__device__ __noinline__ EvalOut warp_eval_counts(const PlannerDev& P, const DecView& D, const GapGroup& g,
                                            const Variant& gv, const GroupVar& ga, int Sc,
                                            const WarpScr& w, const int64_t* c, double min_slot,
                                            int* spill_out) {
@@ -1889,7 +1889,11 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
     out->status = 0;
     // plan-reconstruction queue: instances that fall back (a long sequential batch
     // loop) are queued from the front, the rest from the back
-    build_queue_push(A, inst, I.part, I.build_kind, best < 0);
+    // (a batch mixing speculative and autoregressive planners -- the C5 sweep --
+    // queues the speculative instances from the front and the rest from the back:
+    // the reconstruction CTAs then run one code path at a time, which halves the
+    // instruction footprint the SMs share; otherwise long fallbacks go first)
+    build_queue_push(A, inst, I.part, I.build_kind, A.mixed_spec ? P.speculative != 0 : best < 0);
   }
   SLOS_PHASE(11);  // 11: terminal selection + backtrack
   if (prm.phase_cycles && tid == 0) out->dbg_dp_cycles = clock64() - ph_start_;

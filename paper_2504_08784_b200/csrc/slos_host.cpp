@@ -1161,6 +1161,11 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   A.atask = (const int32_t*)(DI + Ly.atask);
   A.n_atask = (int32_t)Ly.n_atask;
   A.n_inst = nv;
+  {  // reconstruction queues split by planner kind when both are present (below)
+    bool any_spec = false, any_ar = false;
+    for (const slos_planner* pl : plist) (pl->dev.speculative ? any_spec : any_ar) = true;
+    A.mixed_spec = any_spec && any_ar ? 1 : 0;
+  }
   A.dec_idx = (const int32_t*)(DI + Ly.dec_idx);
   A.dec_tier = (const int32_t*)(DI + Ly.dec_tier);
   A.dec_next = (const double*)(DI + Ly.dec_next);
