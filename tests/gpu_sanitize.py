@@ -24,4 +24,18 @@ for fam, seeds in (("C2", range(120, 136)), ("C1", range(0, 24)), ("C3", range(0
     O = plan_many(ora, ho.ptr, b)
     bad = [k for k in range(b.n) if diff(P[k], O[k], counters=True)]
     print(fam, b.n, "mismatches", bad, flush=True)
+# the device PerfModel::fit: one set staged in shared memory, one read from HBM
+from paper_2504_08784_b200 import fit as FT  # noqa: E402
+import numpy as np  # noqa: E402
+rng = np.random.default_rng(5)
+sets = []
+for cnt in (300, 6000):
+    n = rng.integers(1, 8193, cnt)
+    s_ = rng.choice([0, 2, 5], cnt)
+    lat = np.maximum(2.5e-5 * n + 2e-3 * s_ + 0.006, 0.02) * (1 + rng.uniform(-0.01, 0.01, cnt))
+    sets.append(FT.as_samples(n, s_, lat))
+got, st = FT.fit_batch(sets, 2)
+ok = all(got[k].tobytes() == FT.reference_fit(sets[k], 2)[0].tobytes() for k in range(2)) \
+    if os.path.exists(abi.REF_LIB) else None
+print("fit", list(st), "identical to reference:", ok, flush=True)
 print("sanitize workload done")
