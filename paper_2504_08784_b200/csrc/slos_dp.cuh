@@ -792,28 +792,25 @@ __global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm
 // x is rejected iff an EARLIER candidate y weakly dominates it, unless they are
 // equal in (value, memory, budget) and y admits fewer; pm[k] collects the LATER
 // candidates that weakly dominate member k (it is pruned iff one is accepted).
-template <typename TV, typename TM>
+template <int K, typename TV, typename TM>
 __device__ __forceinline__ void bucket_pair_tests(int n, const int (&cn)[2], const TV (&v)[2], const TM (&m)[2],
                                                   const TM (&p)[2], bool (&acc)[2], uint64_t (&pm)[2]) {
   for (int y = 0; y < n; ++y) {
     const int src = y & 31;
-    const bool hi = y >= 32;  // warp-uniform
+    const bool hi = K > 1 && y >= 32;  // warp-uniform
     const int ycn = __shfl_sync(0xffffffffu, hi ? cn[1] : cn[0], src);
     const TV yv = __shfl_sync(0xffffffffu, hi ? v[1] : v[0], src);
     const TM ym = __shfl_sync(0xffffffffu, hi ? m[1] : m[0], src);
     const TM yp = __shfl_sync(0xffffffffu, hi ? p[1] : p[0], src);
     const int yc = ycn >> 8;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      if (yv >= v[k] && ym <= m[k] && yp >= p[k]) {
-        const int c = cn[k] >> 8;
-        if (yc < c) {
-          const bool equal = yv == v[k] && ym == m[k] && yp == p[k];
-          if (!equal || (ycn & 255) >= (cn[k] & 255)) acc[k] = false;
-        } else if (yc > c) {
-          pm[k] |= 1ull << y;
-        }
-      }
+    for (int k = 0; k < K; ++k) {  // predicated, no branches
+      const int c = cn[k] >> 8;
+      const bool w = (yv >= v[k]) & (ym <= m[k]) & (yp >= p[k]);
+      const bool equal = (yv == v[k]) & (ym == m[k]) & (yp == p[k]);
+      const bool rej = w & (yc < c) & (!equal | ((ycn & 255) >= (cn[k] & 255)));
+      acc[k] = acc[k] & !rej;
+      pm[k] |= (uint64_t)(w & (yc > c)) << y;
     }
   }
 }
@@ -1429,9 +1426,10 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
             const int v32[2] = {(int)xv[0], (int)xv[1]};
             const int m32[2] = {(int)xm[0], (int)xm[1]};
             const int p32[2] = {(int)xp[0], (int)xp[1]};
-            bucket_pair_tests(n, cn, v32, m32, p32, acc, pm);
+            if (n <= 32) bucket_pair_tests<1>(n, cn, v32, m32, p32, acc, pm);
+            else bucket_pair_tests<2>(n, cn, v32, m32, p32, acc, pm);
           } else {
-            bucket_pair_tests(n, cn, xv, xm, xp, acc, pm);
+            bucket_pair_tests<2>(n, cn, xv, xm, xp, acc, pm);
           }
           const uint64_t Am = (uint64_t)__ballot_sync(0xffffffffu, acc[0] && lane < n) |
                               ((uint64_t)__ballot_sync(0xffffffffu, acc[1] && 32 + lane < n) << 32);
