@@ -699,6 +699,9 @@ __global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm
   const BatchArgs& A = prm.a;
   const int task = prm.task0 + blockIdx.x;
   const int vi = A.atask[2 * task], j = A.atask[2 * task + 1];
+  // the grid is sized for the longest chain: a CTA past this anchor's pairs exits
+  // before staging the headers (about half of them for anchors late in the chain)
+  if ((int)blockIdx.y * kGroupWarps >= A.inst[vi].N - j - 1) return;
   block_copy_struct(sI, A.inst[vi], threadIdx.x, 32 * kGroupWarps);
   block_copy_struct(sP, A.planners[A.inst[vi].planner], threadIdx.x, 32 * kGroupWarps);
   __syncthreads();
