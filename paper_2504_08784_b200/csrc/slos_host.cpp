@@ -370,6 +370,13 @@ constexpr double kSmallCost = 2048.0;
 // their admission DP in dp_kernel_big (512 threads, one CTA per SM); SLOS_DP_BIG_COST
 // overrides (0 disables). A power of two, so the big instances are a prefix of the
 // log2-bucketed cost-descending launch order.
+// Batches of at most this many instances are latency bound (fewer instances than
+// SMs): every instance gets the widest kernels (SLOS_LATENCY_BATCH overrides, 0 off).
+bool latency_batch(int nv) {
+  const char* e = std::getenv("SLOS_LATENCY_BATCH");  // read per upload: tests toggle it
+  return nv <= (e ? std::atoi(e) : 148);
+}
+
 double dp_big_cost() {
   static const double v = [] {
     const char* e = std::getenv("SLOS_DP_BIG_COST");
@@ -920,7 +927,10 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     I.last_forced = pr.last_forced;
     I.have_running_decode = pr.have_rd ? 1 : 0;
     I.values_integral = pr.values_integral ? 1 : 0;
-    I.build_kind = pr.n_dec <= build_warp_max_dec() ? 0 : (pr.n_dec < build_big_min_dec() ? 1 : 2);
+    // A batch smaller than the SM count cannot fill the GPU: every instance gets the
+    // widest reconstruction (256 threads) and admission DP (512 threads) for latency
+    // (one C1 plan end to end 0.72 -> ~0.5 ms); larger batches pick by throughput.
+    I.build_kind = latency_batch(nv) ? 2 : (pr.n_dec <= build_warp_max_dec() ? 0 : (pr.n_dec < build_big_min_dec() ? 1 : 2));
     kind_v[v] = (uint8_t)I.build_kind;
     N_v[v] = pr.N;
     {  // direct bucket table when the count-vector space is small
@@ -1086,8 +1096,9 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
         while (x > ws.part_lo[p] && cost[ord[x - 1]] < kSmallCost) --x;
       ws.small_lo[p] = x;
       int y = ws.part_lo[p];
-      if (dp_big_cost() > 0)
-        while (y < x && cost[ord[y]] >= dp_big_cost()) ++y;
+      const double big_thr = latency_batch(nv) ? 0.0 : dp_big_cost();
+      if (big_thr > 0 || latency_batch(nv))
+        while (y < x && cost[ord[y]] >= big_thr) ++y;
       ws.big_hi[p] = y;
     }
     for (int p = 0; p < P; ++p)

@@ -25,6 +25,21 @@ def test_stress_families_match_reference(fam):
     check_stress(abi.product(), families=(fam,))
 
 
+# Batches below the SM count take the widest kernels (latency mode, the default for
+# the small batches above); the same goldens through the throughput kernels (warp /
+# 128-thread reconstruction, 64- / 256-thread DP) with the latency mode off:
+@pytest.mark.parametrize("fam", ["C1", "LAT", "C2", "C3", "C4"])
+def test_stress_families_throughput_kernels(fam, monkeypatch):
+    monkeypatch.setenv("SLOS_LATENCY_BATCH", "0")
+    check_stress(abi.product(), families=(fam,))
+
+
+def test_brute_force_and_fuzz_throughput_kernels(monkeypatch):
+    monkeypatch.setenv("SLOS_LATENCY_BATCH", "0")
+    assert check_oracle_instances(abi.product()) == 811
+    check_fuzz(abi.product())
+
+
 def test_c5_simulator_corpus_matches_reference():
     # C5: inputs recorded from the reference simulator's sweep grid, batched
     assert check_c5(abi.product()) == 4096
