@@ -809,20 +809,30 @@ __global__ void __launch_bounds__(kBuildThreads, SLOS_BUILD_MIN_BLOCKS) build_ke
                                            (int64_t)prm.smem_bytes, prm.phase_cycles);
 }
 
-// Very large instances (thousands of running decoders, the C4 family): twice the
-// threads per instance, one CTA per SM. (512 threads measured C4 x 64 1.46 -> 1.33 ms,
-// but the BlockShared capacity it needs (kBW = 16) slowed the C2 reconstruction by
-// ~0.1 ms, so the default stays at 256.)
+// Larger instances get wider CTAs, one per SM: build_kernel_big (256 threads: the
+// latency mode's choice below a thousand decoders) and build_kernel_huge (512
+// threads: thousands of running decoders, the C4 family; C4 x 64 1.35 -> 1.21 ms
+// against 256 threads, while 256 stays faster for a single C2-sized plan).
 #ifndef SLOS_BUILD_BIG_THREADS
 #define SLOS_BUILD_BIG_THREADS (2 * kBuildThreads)
 #endif
-static_assert(SLOS_BUILD_BIG_THREADS <= kBT, "BlockShared holds groups of at most kBT threads");
+#ifndef SLOS_BUILD_HUGE_THREADS
+#define SLOS_BUILD_HUGE_THREADS (4 * kBuildThreads)
+#endif
+static_assert(SLOS_BUILD_HUGE_THREADS <= kBT, "BlockShared holds groups of at most kBT threads");
 __global__ void __launch_bounds__(SLOS_BUILD_BIG_THREADS, 1) build_kernel_big(BuildParams prm) {
   const BatchArgs& A = prm.a;
   __shared__ BuildShared sh;
   extern __shared__ __align__(16) unsigned char bsm[];
   build_instance<BlockGrpT<SLOS_BUILD_BIG_THREADS>>(A, sh, A.bq[A.qbase[kBuildKinds * prm.part + 2] + blockIdx.x], bsm,
                                                (int64_t)prm.smem_big, prm.phase_cycles);
+}
+__global__ void __launch_bounds__(SLOS_BUILD_HUGE_THREADS, 1) build_kernel_huge(BuildParams prm) {
+  const BatchArgs& A = prm.a;
+  __shared__ BuildShared sh;
+  extern __shared__ __align__(16) unsigned char bsm[];
+  build_instance<BlockGrpT<SLOS_BUILD_HUGE_THREADS>>(A, sh, A.bq[A.qbase[kBuildKinds * prm.part + 3] + blockIdx.x],
+                                                     bsm, (int64_t)prm.smem_big, prm.phase_cycles);
 }
 
 // ---- standalone gap queries (slos_tile_gap_batch) ----------------------------

@@ -25,7 +25,7 @@ namespace slos {
 
 constexpr int kMaxTiers = 8;      // dp_scheduler.cpp:367
 constexpr int kMaxParts = 4;      // solve parts pipelined across streams
-constexpr int kBuildKinds = 3;    // warp / 128-thread CTA / 256-thread CTA reconstruction
+constexpr int kBuildKinds = 4;    // warp / 128- / 256- / 512-thread CTA reconstruction
 constexpr int kQueues = kBuildKinds * kMaxParts;
 constexpr int kMaxTerms = 8;      // PerfModel terms carried on device
 constexpr int kMaxSpecLen = 64;   // PlannerConfig::spec_max_len carried on device
@@ -62,7 +62,7 @@ struct InstDev {
   int32_t last_forced;
   int32_t have_running_decode;
   int32_t values_integral;  // all chain values integral -> eps ties impossible
-  int32_t build_kind;       // plan reconstruction: 0 one warp, 1 a 128-thread CTA, 2 a 256-thread CTA
+  int32_t build_kind;       // plan reconstruction: 0 one warp, 1 a 128-, 2 a 256-, 3 a 512-thread CTA
   int32_t part;             // solve part (dp + build launched per part, pipelined)
   int32_t direct;           // Pareto buckets through a direct count-vector table (dp_kernel)
   int32_t has_shared;       // some DP pair's memo key recurs: dp_kernel clears its memo slice
@@ -184,7 +184,7 @@ struct BatchArgs {
   int32_t* ccnt;               // per instance: canonical due counts [kMaxTiers]
   int32_t* bq;       // build queues: 2 counters per queue, then the queue segments; per
                      // queue, fallback instances from the front, the rest from the back
-  int32_t qbase[kQueues];  // queue q = 3*part + build_kind: segment offset in bq
+  int32_t qbase[kQueues];  // queue q = kBuildKinds*part + build_kind: segment offset in bq
   int32_t qn[kQueues];     // and length
   OutHdr* out;
 };
@@ -264,7 +264,7 @@ struct DpParams {
   int dtab;                 // direct bucket-table entries in shared memory (0: none)
 };
 
-// Push an instance onto its plan-reconstruction queue q = 3*part + build_kind (the
+// Push an instance onto its plan-reconstruction queue q = kBuildKinds*part + build_kind (the
 // counters are bq[2q], bq[2q+1]); fallback instances (a long sequential batch loop)
 // are taken first, from the front.
 __device__ __forceinline__ void build_queue_push(const BatchArgs& A, int inst, int part, int kind, bool front) {

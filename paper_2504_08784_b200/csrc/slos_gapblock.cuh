@@ -21,7 +21,10 @@
 
 namespace slos {
 
-constexpr int kBT = 256;  // block size of build / gap kernels
+#ifndef SLOS_BT
+#define SLOS_BT 512
+#endif
+constexpr int kBT = SLOS_BT;  // largest cooperating group of the build / gap kernels
 constexpr int kBW = kBT / 32;  // BlockShared capacity: groups of up to kBT threads
 
 struct MemBuf {  // exact census members (SoA), census order

@@ -930,7 +930,9 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     // A batch smaller than the SM count cannot fill the GPU: every instance gets the
     // widest reconstruction (256 threads) and admission DP (512 threads) for latency
     // (one C1 plan end to end 0.72 -> ~0.5 ms); larger batches pick by throughput.
-    I.build_kind = latency_batch(nv) ? 2 : (pr.n_dec <= build_warp_max_dec() ? 0 : (pr.n_dec < build_big_min_dec() ? 1 : 2));
+    I.build_kind = pr.n_dec >= build_big_min_dec() ? 3
+                   : latency_batch(nv)              ? 2
+                   : (pr.n_dec <= build_warp_max_dec() ? 0 : 1);
     kind_v[v] = (uint8_t)I.build_kind;
     N_v[v] = pr.N;
     {  // direct bucket table when the count-vector space is small
@@ -1438,7 +1440,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     cudaEventRecord(ws.ev_dp[p], sp);
     bp.part = p;
     const int q0 = kBuildKinds * p;
-    if ((e = launch_build(bp, ws.qn[q0], ws.qn[q0 + 1], ws.qn[q0 + 2], sp)) != cudaSuccess)
+    if ((e = launch_build(bp, ws.qn[q0], ws.qn[q0 + 1], ws.qn[q0 + 2], ws.qn[q0 + 3], sp)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     if (ws.part_collect) {  // this part's headers, as soon as its reconstruction ends
       if ((e = ws.h_hdr[p].ensure(sizeof(OutHdr) * nv)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));

@@ -108,7 +108,7 @@ cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, int n_big, cudaStream_t s) {
+cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, int n_big, int n_huge, cudaStream_t s) {
   cudaError_t e;
   if (n_small > 0) {
     if ((e = cudaFuncSetAttribute(build_kernel_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -129,6 +129,13 @@ cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, int n
                                   (int)prm.smem_big)) != cudaSuccess)
       return e;
     build_kernel_big<<<n_big, SLOS_BUILD_BIG_THREADS, prm.smem_big, s>>>(prm);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (n_huge > 0) {
+    if ((e = cudaFuncSetAttribute(build_kernel_huge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)prm.smem_big)) != cudaSuccess)
+      return e;
+    build_kernel_huge<<<n_huge, SLOS_BUILD_HUGE_THREADS, prm.smem_big, s>>>(prm);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -39,7 +39,7 @@ cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s
 size_t anchor_smem_bytes(int max_N, int Sc, int L, size_t* scr);
 cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_group(const DpParams& prm, int n_atask, int max_N, cudaStream_t s);
-cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, int n_big, cudaStream_t s);
+cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, int n_big, int n_huge, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& prm, int grid, cudaStream_t s);
 cudaError_t launch_gap(const GapParams& prm, int grid, cudaStream_t s);
 cudaError_t launch_time2bs(const PlannerDev* P, int n, const double* b, const int64_t* sp,
