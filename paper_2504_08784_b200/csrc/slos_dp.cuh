@@ -632,19 +632,20 @@ constexpr int kAnchorThreads = SLOS_ANCHOR_THREADS;
 #ifndef SLOS_ANCHOR_MIN_BLOCKS
 #define SLOS_ANCHOR_MIN_BLOCKS 8
 #endif
-__global__ void __launch_bounds__(kAnchorThreads, SLOS_ANCHOR_MIN_BLOCKS) anchor_kernel(DpParams prm) {
+template <int NT>
+__device__ __forceinline__ void anchor_body(const DpParams& prm) {
   extern __shared__ __align__(16) unsigned char asm_[];
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;
   __shared__ int ccnt[kMaxTiers];
   __shared__ double s_maxdl, s_minA;
-  __shared__ int64_t s_wsum[kAnchorThreads / 32 + 1];
+  __shared__ int64_t s_wsum[NT / 32 + 1];
   const BatchArgs& A = prm.a;
   const int tid = threadIdx.x;
   const int task = prm.task0 + blockIdx.x;
   const int v = A.atask[2 * task], j = A.atask[2 * task + 1];
-  block_copy_struct(sI, A.inst[v], tid, kAnchorThreads);
-  block_copy_struct(sP, A.planners[A.inst[v].planner], tid, kAnchorThreads);
+  block_copy_struct(sI, A.inst[v], tid, NT);
+  block_copy_struct(sP, A.planners[A.inst[v].planner], tid, NT);
   __syncthreads();
   const PlannerDev& P = sP;
   const InstDev& I = sI;
@@ -680,14 +681,29 @@ __global__ void __launch_bounds__(kAnchorThreads, SLOS_ANCHOR_MIN_BLOCKS) anchor
   const double pull = min_slot;
   const double a = (j < 0) ? I.now : ch_dl[j];
   const AnchorView av = anchor_view(A.anchors + I.off_anchor + (size_t)(j + 1) * I.anchor_stride, D.n, Sc, L);
-  block_build_anchor<kAnchorThreads>(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), Sc, ctime, ccnt,
+  block_build_anchor<NT>(P, D, av, a, I.now, pull, quantize_gap(dmax(0.0, s_maxdl - a)), Sc, ctime, ccnt,
                      min_slot, s_wsum);
-  block_anchor_dues<kAnchorThreads>(P, D, av, j, N, ch_dl, ch_fl, a, pull, min_slot, Sc, scr, prm.anchor_scr_bytes);
+  block_anchor_dues<NT>(P, D, av, j, N, ch_dl, ch_fl, a, pull, min_slot, Sc, scr, prm.anchor_scr_bytes);
   if (j < 0) {  // the instance's canonical due times, for group_kernel
     double* gct = A.ctime + (size_t)v * prm.Lmax * Sc;
-    for (int x = tid; x < L * Sc; x += kAnchorThreads) gct[x] = ctime[x];
+    for (int x = tid; x < L * Sc; x += NT) gct[x] = ctime[x];
     if (tid < kMaxTiers) A.ccnt[v * kMaxTiers + tid] = tid < L ? ccnt[tid] : 0;
   }
+}
+
+__global__ void __launch_bounds__(kAnchorThreads, SLOS_ANCHOR_MIN_BLOCKS) anchor_kernel(DpParams prm) {
+  anchor_body<kAnchorThreads>(prm);
+}
+
+// Anchors of the large-instance class (thousands of decoders: each anchor walks
+// every decoder's dues): 512 threads per anchor, since a few dozen such instances
+// fill the GPU with one wave of anchors and the walk's length is the stage.
+#ifndef SLOS_ANCHOR_BIG_THREADS
+#define SLOS_ANCHOR_BIG_THREADS 512
+#endif
+constexpr int kAnchorBigThreads = SLOS_ANCHOR_BIG_THREADS;
+__global__ void __launch_bounds__(kAnchorBigThreads, 2) anchor_kernel_big(DpParams prm) {
+  anchor_body<kAnchorBigThreads>(prm);
 }
 
 // Gap group records (the DP's E1/E2, off its critical path): one warp per pair

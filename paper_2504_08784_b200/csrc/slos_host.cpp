@@ -643,6 +643,7 @@ struct Workspace {
   int n_parts = 1;
   int part_lo[kMaxParts + 1] = {0};
   int atask_lo[kMaxParts + 1] = {0};  // anchor-task range of each part
+  int atask_big[kMaxParts] = {0};     // end of each part's big-instance anchor tasks
   cudaEvent_t ev_anc[kMaxParts] = {nullptr};
   int qbase[kQueues] = {0};
   int qn[kQueues] = {0};
@@ -1127,6 +1128,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     aoff[0] = 0;
     for (int y = 0; y < nv; ++y) aoff[y + 1] = aoff[y] + N_v[ord[y]];
     for (int p = 0; p <= P; ++p) ws.atask_lo[p] = (int)aoff[ws.part_lo[p]];
+    for (int p = 0; p < P; ++p) ws.atask_big[p] = (int)aoff[ws.big_hi[p]];
     HostPool::get().run(nv, [&](int lo, int hi) {
       for (int y = lo; y < hi; ++y) {
         const int v = ord[y];
@@ -1380,7 +1382,8 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   ws.launches = 0;  // kernels this solve launches (slos_workspace_launches)
   for (int p = 0; p < ws.n_parts; ++p) {
     const int nt = ws.atask_lo[p + 1] - ws.atask_lo[p];
-    ws.launches += (nt > 0) + (nt > 0 && ws.maxN > 0) + (ws.big_hi[p] > ws.part_lo[p]) + (ws.small_lo[p] > ws.big_hi[p]) +
+    ws.launches += (ws.atask_big[p] > ws.atask_lo[p]) + (ws.atask_lo[p + 1] > ws.atask_big[p]) +
+                   (nt > 0 && ws.maxN > 0) + (ws.big_hi[p] > ws.part_lo[p]) + (ws.small_lo[p] > ws.big_hi[p]) +
                    (ws.part_lo[p + 1] > ws.small_lo[p]);
     for (int kd = 0; kd < kBuildKinds; ++kd) ws.launches += ws.qn[kBuildKinds * p + kd] > 0;
   }
@@ -1413,10 +1416,15 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
   cudaStreamWaitEvent(ws.astream, ws.ev_fork, 0);
   for (int p = 0; p < ws.n_parts; ++p) {
     DpParams dpa = dp;
-    dpa.task0 = ws.atask_lo[p];
     const int nt = ws.atask_lo[p + 1] - ws.atask_lo[p];
-    if ((e = launch_anchor(dpa, nt, ws.anchor_smem, ws.astream)) != cudaSuccess)
+    // anchors of the big-instance prefix on 512-thread CTAs, the rest on 128
+    dpa.task0 = ws.atask_lo[p];
+    if ((e = launch_anchor(dpa, ws.atask_big[p] - ws.atask_lo[p], ws.anchor_smem, ws.astream, true)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    dpa.task0 = ws.atask_big[p];
+    if ((e = launch_anchor(dpa, ws.atask_lo[p + 1] - ws.atask_big[p], ws.anchor_smem, ws.astream)) != cudaSuccess)
+      return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    dpa.task0 = ws.atask_lo[p];
     if ((e = launch_group(dpa, nt, ws.maxN, ws.astream)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     cudaEventRecord(ws.ev_anc[p], ws.astream);

@@ -73,8 +73,14 @@ size_t anchor_smem_bytes(int max_N, int Sc, int L, size_t* scr) {
   return sizeof(double) * (size_t)L * S + b;
 }
 
-cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s) {
+cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s, bool big) {
   if (grid <= 0) return cudaSuccess;
+  if (big) {
+    cudaError_t e = cudaFuncSetAttribute(anchor_kernel_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    anchor_kernel_big<<<grid, kAnchorBigThreads, smem, s>>>(prm);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaFuncSetAttribute(anchor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   anchor_kernel<<<grid, kAnchorThreads, smem, s>>>(prm);

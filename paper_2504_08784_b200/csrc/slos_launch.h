@@ -37,7 +37,7 @@ size_t dp_anchor_stride(int R, int Sc, int L, int N);
 size_t dp_warp_scr_stride(int Sc, int L);
 cudaError_t launch_dp(const DpParams& prm, int grid, size_t smem, cudaStream_t s, int kind = 0);
 size_t anchor_smem_bytes(int max_N, int Sc, int L, size_t* scr);
-cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_anchor(const DpParams& prm, int grid, size_t smem, cudaStream_t s, bool big = false);
 cudaError_t launch_group(const DpParams& prm, int n_atask, int max_N, cudaStream_t s);
 cudaError_t launch_build(const BuildParams& prm, int n_small, int n_large, int n_big, int n_huge, cudaStream_t s);
 cudaError_t launch_compact(const CompactParams& prm, int grid, cudaStream_t s);
