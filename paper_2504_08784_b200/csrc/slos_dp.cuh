@@ -884,27 +884,37 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
   const double pull = min_slot;
 
   // ---- dynamic smem: chain, decoders, warp scratch ----
+  // The chain's request descriptors (deadline, prefill, memory, value, suffix budget,
+  // tier, forced, floor: N + 1 entries each, 16-byte aligned slices padded to 4
+  // entries by the host) arrive by TMA bulk copies on the staging mbarrier.
   unsigned char* p = dsm;
-  double* ch_dl = (double*)p; p += sizeof(double) * (N + 1);
-  int64_t* ch_pf = (int64_t*)p; p += sizeof(int64_t) * (N + 1);
-  int64_t* ch_mm = (int64_t*)p; p += sizeof(int64_t) * (N + 1);
-  double* ch_vl = (double*)p; p += sizeof(double) * (N + 1);
-  int64_t* ch_sf = (int64_t*)p; p += sizeof(int64_t) * (N + 2);
-  int32_t* ch_tr = (int32_t*)p; p += sizeof(int32_t) * (N + 2);
-  int32_t* ch_fc = (int32_t*)p; p += sizeof(int32_t) * (N + 2);
-  int32_t* ch_fl = (int32_t*)p; p += sizeof(int32_t) * (N + 2);
-  p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
-  for (int k = tid; k < N; k += kDpThreads) {
-    const int64_t o = I.off_chain + k;
-    ch_dl[k] = A.ch_deadline[o];
-    ch_pf[k] = A.ch_prefill[o];
-    ch_mm[k] = A.ch_memory[o];
-    ch_vl[k] = A.ch_value[o];
-    ch_tr[k] = A.ch_tier[o];
-    ch_fc[k] = A.ch_forced[o];
-    ch_fl[k] = A.ch_floor[o];
+  const uint32_t b8 = (uint32_t)((8 * (N + 1) + 15) & ~15), b4 = (uint32_t)((4 * (N + 1) + 15) & ~15);
+  double* ch_dl = (double*)p; p += b8;
+  int64_t* ch_pf = (int64_t*)p; p += b8;
+  int64_t* ch_mm = (int64_t*)p; p += b8;
+  double* ch_vl = (double*)p; p += b8;
+  int64_t* ch_sf = (int64_t*)p; p += b8;
+  int32_t* ch_tr = (int32_t*)p; p += b4;
+  int32_t* ch_fc = (int32_t*)p; p += b4;
+  int32_t* ch_fl = (int32_t*)p; p += b4;
+  if (tid == 0) {
+    const uint32_t mb = smem_u32(&s_mbar);
+    const int64_t o = I.off_chain;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(5 * b8 + 3 * b4) : "memory");
+    auto bulk = [&](void* dst, const void* src, uint32_t bytes) {
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(dst)), "l"(src), "r"(bytes), "r"(mb)
+                   : "memory");
+    };
+    bulk(ch_dl, A.ch_deadline + o, b8);
+    bulk(ch_pf, A.ch_prefill + o, b8);
+    bulk(ch_mm, A.ch_memory + o, b8);
+    bulk(ch_vl, A.ch_value + o, b8);
+    bulk(ch_sf, A.ch_suffix + o, b8);
+    bulk(ch_tr, A.ch_tier + o, b4);
+    bulk(ch_fc, A.ch_forced + o, b4);
+    bulk(ch_fl, A.ch_floor + o, b4);
   }
-  for (int k = tid; k <= N; k += kDpThreads) ch_sf[k] = A.ch_suffix[I.off_chain + k];
   // decoders: only the private-variant / speculative warp path reads them
   DecView D;
   D.n = I.have_running_decode ? I.n_dec : 0;
@@ -997,7 +1007,15 @@ __device__ __forceinline__ void dp_body(const DpParams& prm) {
 
   long long ph_t0_ = clock64();
   const long long ph_start_ = ph_t0_;
-  uint32_t mb_phase = 0;  // parity of the staging barrier's current phase
+  {  // the chain descriptors have landed (phase 0 of the staging barrier)
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(smem_u32(&s_mbar)), "r"(0u)
+                   : "memory");
+  }
+  uint32_t mb_phase = 1;  // parity of the staging barrier's current phase (levels)
   SLOS_PHASE(0);  // 0: instance load / setup
   for (int i = 0; i < N && !s_err; ++i) {
     const int jlo = ch_fl[i];

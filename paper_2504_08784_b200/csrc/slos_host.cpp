@@ -717,7 +717,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     pr.planner = pi;
     valid.push_back(q);
     TD += pr.n_dec;
-    TC += pr.N + 1;
+    TC += (pr.N + 1 + 3) & ~3;  // 16-byte aligned chain slices (the DP stages them by TMA)
     TP += pr.n_pre;
     TR += inputs[k].n_running;
     TS += caps[q].surv;
@@ -879,7 +879,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
         const slos_input* in = &inputs[jobs[q].k];
         Off& o = offs[v];
         o.D = pr.n_dec;
-        o.C = pr.N + 1;
+        o.C = (pr.N + 1 + 3) & ~3;
         o.P = pr.n_pre;
         o.R = in->n_running;
         o.S = cp.surv;

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) compact_kernel(CompactParams p) {
 size_t dp_smem_bytes(int max_N, int max_dec_staged, int Sc, int L, int Tsm, size_t* overlay, int dtab, int kind) {
   const int nwarps = kind == 1 ? kDpSmallThreads / 32 : (kind == 2 ? kDpBigThreads / 32 : kDpWarps);
   const size_t N = (size_t)max_N;
-  size_t b = 8 * (N + 1) * 4 + 8 * (N + 2) + 4 * (N + 2) * 3 + 16;   // chain
+  size_t b = 5 * ((8 * (N + 1) + 15) & ~(size_t)15) + 3 * ((4 * (N + 1) + 15) & ~(size_t)15) + 16;  // chain (TMA)
   b += (size_t)max_dec_staged * 28 + 16;                              // decoders
   b += 8 * (size_t)Sc * nwarps + 16;                                  // placement temporaries
   const size_t ov = (size_t)76 * (size_t)Tsm;
