@@ -40,6 +40,13 @@ def test_brute_force_and_fuzz_throughput_kernels(monkeypatch):
     check_fuzz(abi.product())
 
 
+@pytest.mark.parametrize("n", [1, 147, 148, 149, 300])
+def test_c5_batch_sizes_around_the_latency_mode_threshold(n):
+    """Batches up to the SM count (148) take the widest kernels, larger ones the
+    throughput kernels: both sides of the boundary against the reference."""
+    assert check_c5(abi.product(), limit=n) == 2 * n
+
+
 def test_c5_simulator_corpus_matches_reference():
     # C5: inputs recorded from the reference simulator's sweep grid, batched
     assert check_c5(abi.product()) == 4096
