@@ -591,8 +591,9 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
         d += tpot;
         ++issued;
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, y);
-      if (y >= 0 && lane_id() == __ffs(peers) - 1) atomicAdd(&sHc[y], __popc(peers));
+      // per-lane shared-memory atomics: same-cell lanes resolve in the atomic unit
+      // (a match_any + leader add measured ~2% slower over the whole anchor stage)
+      if (y >= 0) atomicAdd(&sHc[y], 1);
     }
   }
   lx = warp_sum(lx);

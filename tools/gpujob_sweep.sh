@@ -1,1 +1,4 @@
-for v in X=1 SLOS_PIPELINE_SPLIT=0.2 SLOS_PIPELINE_SPLIT=0.4 SLOS_PIPELINE_SPLIT=0.5 SLOS_PIPELINE_CHUNKS=1 SLOS_PIPELINE_CHUNKS=3; do echo "== $v"; env $v python tests/gpu_e2e.py C2 1024 2>&1 | tail -2; done
+for k in 1 2; do
+echo "== base"; SLOS_NO_PHASES=1 SLOS_SOLVES=4 python tests/gpu_phases.py C2 1024 2>&1 | tail -2
+echo "== atom"; SLOS_PRODUCT_LIB=exp/atom/libslos_b200.so SLOS_NO_PHASES=1 SLOS_SOLVES=4 python tests/gpu_phases.py C2 1024 2>&1 | tail -2
+done
