@@ -127,6 +127,7 @@ struct BatchArgs {
   // decoders
   const int32_t* dec_idx;
   const int32_t* dec_tier;
+  const int32_t* dec_bytier;   // per instance: decoder indices grouped by tier (anchor due walk)
   const double* dec_next;
   const int64_t* dec_backlog;
   const int64_t* dec_rem;

@@ -546,7 +546,7 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
   // the walk: lanes over members in lockstep (one due per lane per round)
   unsigned long long lx = 0;
   for (int base = 0; base < D.n; base += NT) {
-    const int k = base + tid;
+    const int k = base + tid < D.n ? D.bytier[base + tid] : D.n;  // members grouped by tier
     int64_t rem = 0, issued = 0;
     double d = 0.0, tpot = 0.0;
     bool act = false;
@@ -661,6 +661,7 @@ __device__ __forceinline__ void anchor_body(const DpParams& prm) {
   D.backlog = A.dec_backlog + I.off_dec;
   D.rem = A.dec_rem + I.off_dec;
   D.tier = A.dec_tier + I.off_dec;
+  D.bytier = A.dec_bytier + I.off_dec;
   double* ctime = (double*)asm_;
   unsigned char* scr = asm_ + sizeof(double) * (size_t)prm.Lmax * Sc;
   if (tid == 0) {

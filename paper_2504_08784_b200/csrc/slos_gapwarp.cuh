@@ -67,6 +67,7 @@ struct DecView {
   const int64_t* rem;
   const int32_t* tier;
   int n;
+  const int32_t* bytier = nullptr;  // anchor due walk: member order grouped by tier
 };
 
 // One gap (chain item i, anchor j): the exact census is members_at(a).

@@ -599,7 +599,7 @@ struct Job {
 };
 
 struct Layout {
-  size_t planners, inst, order, dec_idx, dec_tier, dec_next, dec_backlog, dec_rem;
+  size_t planners, inst, order, dec_idx, dec_tier, dec_bytier, dec_next, dec_backlog, dec_rem;
   size_t ch_deadline, ch_prefill, ch_tier, ch_memory, ch_value, ch_forced, ch_ref, ch_floor, ch_suffix;
   size_t pre_idx, pre_left, run_tier, recdef, recmap;
   size_t in_bytes;
@@ -764,6 +764,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   const size_t grec_stride = (grec_hdr + dp_group_stride(Sc, Lmax) + 127) & ~(size_t)127;
   Ly.dec_idx = bi.add<int32_t>(TD);
   Ly.dec_tier = bi.add<int32_t>(TD);
+  Ly.dec_bytier = bi.add<int32_t>(TD);
   Ly.dec_next = bi.add<double>(TD);
   Ly.dec_backlog = bi.add<int64_t>(TD);
   Ly.dec_rem = bi.add<int64_t>(TD);
@@ -838,6 +839,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   InstDev* hI = (InstDev*)hp(Ly.inst);
   int32_t* h_dec_idx = (int32_t*)hp(Ly.dec_idx);
   int32_t* h_dec_tier = (int32_t*)hp(Ly.dec_tier);
+  int32_t* h_dec_bytier = (int32_t*)hp(Ly.dec_bytier);
   double* h_dec_next = (double*)hp(Ly.dec_next);
   int64_t* h_dec_bl = (int64_t*)hp(Ly.dec_backlog);
   int64_t* h_dec_rem = (int64_t*)hp(Ly.dec_rem);
@@ -971,6 +973,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     I.anchor_stride = astride[q];
     I.off_pair = oPair;
     I.off_group = oPair * (int64_t)grec_stride;
+    const int64_t oD0 = oD;
     for (int i = 0; i < in->n_running; ++i) {
       const slos_running& r = in->running[i];
       h_run_tier[oR + i] = r.decode_tier;
@@ -982,6 +985,17 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
         h_dec_rem[oD] = r.decode_remaining;
         ++oD;
       }
+    }
+    {  // decoders grouped by tier: a warp of the anchor due walk then walks lines of
+       // one cadence (equal due counts) instead of the longest of mixed ones
+      int32_t* bt = h_dec_bytier + oD0;
+      int x = 0;
+      const int nd = (int)(oD - oD0);
+      for (int l = 0; l < kMaxTiers && x < nd; ++l)
+        for (int k = 0; k < nd; ++k)
+          if (h_dec_tier[oD0 + k] == l) bt[x++] = k;
+      for (int k = 0; k < nd && x < nd; ++k)  // tiers outside [0, kMaxTiers) (rejected upstream)
+        if (h_dec_tier[oD0 + k] < 0 || h_dec_tier[oD0 + k] >= kMaxTiers) bt[x++] = k;
     }
     for (int x = 0; x < pr.n_pre; ++x) {
       h_pre_idx[oP + x] = pr.pre[x];
@@ -1183,6 +1197,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   }
   A.dec_idx = (const int32_t*)(DI + Ly.dec_idx);
   A.dec_tier = (const int32_t*)(DI + Ly.dec_tier);
+  A.dec_bytier = (const int32_t*)(DI + Ly.dec_bytier);
   A.dec_next = (const double*)(DI + Ly.dec_next);
   A.dec_backlog = (const int64_t*)(DI + Ly.dec_backlog);
   A.dec_rem = (const int64_t*)(DI + Ly.dec_rem);
