@@ -524,12 +524,21 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
     l_off[y + 1] = n;
   }
   __syncthreads();
-  if (tid == 0) {
-    l_off[0] = 0;
-    int acc = 0;
-    for (int y = 0; y <= Kg; ++y) { const int n = l_off[y + 1]; l_off[y + 1] = acc + n; acc += n; }
-    s_nl = acc;
-    if (acc > lcap) s_ok = 0;
+  if (tid < 32) {  // list offsets: a warp scan over the cells
+    const int lane = lane_id();
+    int carry = 0;
+    for (int base = 0; base <= Kg; base += 32) {
+      const int y = base + lane;
+      const int n = y <= Kg ? l_off[y + 1] : 0;
+      const int inc = warp_incl_scan(n);
+      if (y <= Kg) l_off[y + 1] = carry + inc;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) {
+      l_off[0] = 0;
+      s_nl = carry;
+      if (carry > lcap) s_ok = 0;
+    }
   }
   __syncthreads();
   if (!s_ok) {
@@ -600,12 +609,20 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
   if (lane_id() == 0 && lx) atomicAdd(&s_lx, lx);
   __syncthreads();
   // publish: cumulative histogram, per-group tails, facts
-  if (tid == 0) {
-    int acc = 0;
-    av.hcum[0] = 0;
-    for (int y = 0; y <= Kg; ++y) { acc += sHc[y]; av.hcum[y + 1] = acc; }
-    F->Lx = (int64_t)s_lx;
-    F->dues_ok = 1;
+  if (tid < 32) {  // cumulative histogram: a warp scan over the cells
+    const int lane = lane_id();
+    int carry = 0;
+    for (int base = 0; base <= Kg; base += 32) {
+      const int y = base + lane;
+      const int inc = warp_incl_scan(y <= Kg ? sHc[y] : 0);
+      if (y <= Kg) av.hcum[y + 1] = carry + inc;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) {
+      av.hcum[0] = 0;
+      F->Lx = (int64_t)s_lx;
+      F->dues_ok = 1;
+    }
   }
   for (int gi = tid; gi < nG; gi += NT) {
     GroupTail t;
@@ -664,11 +681,17 @@ __device__ __forceinline__ void anchor_body(const DpParams& prm) {
   D.bytier = A.dec_bytier + I.off_dec;
   double* ctime = (double*)asm_;
   unsigned char* scr = asm_ + sizeof(double) * (size_t)prm.Lmax * Sc;
-  if (tid == 0) {
+  if (tid < 32) {  // deadline range: a warp reduction (max / min are order-free)
     double mx = I.now, mn = I.now;
-    for (int k = 0; k < N; ++k) { mx = dmax(mx, ch_dl[k]); mn = dmin(mn, ch_dl[k]); }
-    s_maxdl = mx;
-    s_minA = mn;
+    for (int k = tid; k < N; k += 32) { mx = dmax(mx, ch_dl[k]); mn = dmin(mn, ch_dl[k]); }
+    for (int o = 16; o; o >>= 1) {
+      mx = dmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = dmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (tid == 0) {
+      s_maxdl = mx;
+      s_minA = mn;
+    }
   }
   __syncthreads();
   if (tid < L) {  // instance-wide canonical due times per tier (batch_planner.cpp:216)
