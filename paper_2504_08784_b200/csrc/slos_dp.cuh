@@ -736,8 +736,11 @@ __global__ void __launch_bounds__(kAnchorBigThreads, 2) anchor_kernel_big(DpPara
 
 // Gap group records (the DP's E1/E2, off its critical path): one warp per pair
 // (j, i), i > j >= floor_at[i], built from anchor j's cache and written to HBM.
-constexpr int kGroupWarps = 4;
-__global__ void __launch_bounds__(32 * kGroupWarps, 8) group_kernel(DpParams prm) {
+#ifndef SLOS_GROUP_WARPS
+#define SLOS_GROUP_WARPS 4
+#endif
+constexpr int kGroupWarps = SLOS_GROUP_WARPS;
+__global__ void __launch_bounds__(32 * kGroupWarps, 32 / kGroupWarps) group_kernel(DpParams prm) {
   __shared__ PlannerDev sP;
   __shared__ InstDev sI;
   const BatchArgs& A = prm.a;

@@ -1,2 +1,1 @@
-for k in 1 2; do for v in cur anc64 anc64b anc32; do echo "== $v"; SLOS_PRODUCT_LIB=exp/$v/libslos_b200.so SLOS_NO_PHASES=1 SLOS_SOLVES=4 python tests/gpu_phases.py C2 1024 2>&1 | tail -1; done; done
-for v in cur anc64; do echo "== C5 $v"; SLOS_PRODUCT_LIB=exp/$v/libslos_b200.so SLOS_NO_PHASES=1 SLOS_SOLVES=3 python tests/gpu_phases_c5.py 2>&1 | tail -1; echo "== C1 $v"; SLOS_PRODUCT_LIB=exp/$v/libslos_b200.so SLOS_NO_PHASES=1 SLOS_SOLVES=3 python tests/gpu_phases.py C1 1024 2>&1 | tail -1; done
+for k in 1 2; do for v in cur grp2 grp8; do echo "== $v"; SLOS_PRODUCT_LIB=exp/$v/libslos_b200.so SLOS_NO_PHASES=1 SLOS_SOLVES=4 python tests/gpu_phases.py C2 1024 2>&1 | tail -1; done; done
