@@ -571,6 +571,8 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
       }
     }
     int cell = -2;  // grid cell of the previous due (-1: before e_0); -2: none yet
+    double nb = 0.0;  // the next cell boundary sge[cell + 1] (+inf past the grid)
+    int l0 = 0, l1 = 0;  // the group list of cell y = cell + 1
     for (;;) {
       act = act && time_le(d, hmax) && issued < rem;
       if (!__any_sync(0xffffffffu, act)) break;
@@ -579,10 +581,23 @@ __device__ inline void block_anchor_dues(const PlannerDev& P, const DecView& D, 
         if (d <= kTimeEps) {
           ++lx;
         } else {
-          if (cell == -2) cell = jit_search(sge, Kg, d);
-          else while (cell + 1 < Kg && time_le(sge[cell + 1], d)) ++cell;
+          // the cell only moves forward: its boundary and group list stay in
+          // registers until a due crosses it
+          if (cell == -2) {
+            cell = jit_search(sge, Kg, d);
+            nb = cell + 1 < Kg ? sge[cell + 1] : INFINITY;
+            l0 = l_off[cell + 1];
+            l1 = l_off[cell + 2];
+          } else if (time_le(nb, d)) {
+            do {
+              ++cell;
+              nb = cell + 1 < Kg ? sge[cell + 1] : INFINITY;
+            } while (time_le(nb, d));
+            l0 = l_off[cell + 1];
+            l1 = l_off[cell + 2];
+          }
           y = cell + 1;
-          for (int q = l_off[y]; q < l_off[y + 1]; ++q) {
+          for (int q = l0; q < l1; ++q) {
             const int gi = l_item[q];
             if (!time_le(d, g_hor[gi])) continue;
             const double gap = g_gap[gi];
