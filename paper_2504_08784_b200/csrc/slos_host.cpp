@@ -650,6 +650,7 @@ struct Workspace {
   cudaStream_t pstream[kMaxParts] = {nullptr};  // per-part streams, earlier parts higher priority
   cudaStream_t astream = nullptr;                // anchor / group kernels of every part
   cudaEvent_t ev_fork = nullptr, ev_dp[kMaxParts] = {nullptr}, ev_join[kMaxParts] = {nullptr};
+  cudaEvent_t ev_bend[kMaxParts] = {nullptr};  // end of a part's reconstruction (SLOS_HOST_TIMING)
   // per-part collection (plan_all): each part's headers are copied on its stream
   // right after its reconstruction, so its compaction and D2H overlap later parts
   bool part_collect = false;
@@ -1385,8 +1386,11 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     cudaStreamCreateWithPriority(&ws.astream, cudaStreamNonBlocking, hi);
+    static const bool rev = std::getenv("SLOS_PART_PRIO_REV") != nullptr;
     for (int p = 0; p < kMaxParts; ++p) {
-      cudaStreamCreateWithPriority(&ws.pstream[p], cudaStreamNonBlocking, std::min(lo, hi + 1 + p));
+      cudaStreamCreateWithPriority(&ws.pstream[p], cudaStreamNonBlocking,
+                                   rev ? std::max(hi + 1, lo - p) : std::min(lo, hi + 1 + p));
+      cudaEventCreate(&ws.ev_bend[p]);
       cudaEventCreate(&ws.ev_dp[p]);
       cudaEventCreate(&ws.ev_anc[p]);
       cudaEventCreateWithFlags(&ws.ev_join[p], cudaEventDisableTiming);
@@ -1462,6 +1466,8 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
     cudaEventRecord(ws.ev_dp[p], sp);
     bp.part = p;
+    static const bool build_after_next = std::getenv("SLOS_BUILD_AFTER_NEXT_ANC") != nullptr;
+    if (build_after_next && p + 1 < ws.n_parts) cudaStreamWaitEvent(sp, ws.ev_anc[p + 1], 0);
     const int q0 = kBuildKinds * p;
     if ((e = launch_build(bp, ws.qn[q0], ws.qn[q0 + 1], ws.qn[q0 + 2], ws.qn[q0 + 3], sp)) != cudaSuccess)
       return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
@@ -1471,6 +1477,7 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
       cudaMemcpyAsync(ws.h_hdr[p].p, DO + Ly.out, sizeof(OutHdr) * nv, cudaMemcpyDeviceToHost, sp);
       cudaEventRecord(ws.ev_hdr[p], sp);
     }
+    if (host_timing()) cudaEventRecord(ws.ev_bend[p], sp);
     cudaEventRecord(ws.ev_join[p], sp);
     cudaStreamWaitEvent(s, ws.ev_join[p], 0);
   }
@@ -2147,6 +2154,14 @@ int slos_workspace_stage_ms(slos_workspace* b, float* ms, int32_t n) {
       cudaEventElapsedTime(&x, ws.ev[0], ws.ev_anc[p]);
       t[0] = std::max(t[0], x);
     }
+    if (host_timing())
+      for (int p = 0; p < ws.n_parts; ++p) {
+        float a = 0.0f, d = 0.0f, b = 0.0f;
+        cudaEventElapsedTime(&a, ws.ev[0], ws.ev_anc[p]);
+        cudaEventElapsedTime(&d, ws.ev[0], ws.ev_dp[p]);
+        cudaEventElapsedTime(&b, ws.ev[0], ws.ev_bend[p]);
+        std::fprintf(stderr, "[slos stages] part %d: groups end %.3f, dp end %.3f, build end %.3f ms\n", p, a, d, b);
+      }
     const float dp_end = dp_end_ms(ws);  // last part's DP (parts overlap: stages are
     t[1] = dp_end - t[0];                // timed to their last part's end)
     t[2] = all - dp_end;
