@@ -2248,6 +2248,7 @@ void slos_broker_leave(slos_broker* b) {
 }
 
 int slos_broker_plan(slos_broker* b, slos_planner* p, const slos_input* in, slos_result* out) {
+  g_err.clear();  // a message always belongs to this call (the batch may run on another thread)
   std::unique_lock<std::mutex> lk(b->mu);
   slos_broker::Req r{p, *in, out, false};
   b->queue.push_back(&r);
