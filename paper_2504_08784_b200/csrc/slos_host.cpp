@@ -11,6 +11,7 @@
 // was too small. There is no CPU fallback: without an sm_100 device every entry
 // point returns SLOS_ERR_NO_DEVICE.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -157,9 +158,20 @@ class HostPool {
   // fn(lo, hi) over contiguous ranges of [0, n); runs inline for small n. Workers
   // spin for a short while after each job before sleeping, so the back-to-back
   // jobs of one upload do not pay a thread wake-up each.
+  // time spent in run() and the number of runs (SLOS_HOST_TIMING breakdowns)
+  double run_ms = 0.0;
+  int runs = 0;
   void run(int n, const std::function<void(int, int)>& fn) {
     const int T = (int)workers_.size() + 1;
     if (n < 64 || T == 1) { fn(0, n); return; }
+    struct Tm {
+      HostPool* h;
+      std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+      ~Tm() {
+        h->run_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        ++h->runs;
+      }
+    } tm_{this};
     fn_ = &fn;
     n_ = n;
     next_.store(0, std::memory_order_relaxed);
@@ -694,6 +706,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   int maxN = 0, maxDec = 0, Lmax = 1;
   double S_need = 16;
   const auto t_a = std::chrono::steady_clock::now();
+  if (host_timing()) { HostPool::get().runs = 0; HostPool::get().run_ms = 0.0; }
   HostPool::get().run(n, [&](int lo, int hi) {
     for (int q = lo; q < hi; ++q) {
       const int k = jobs[q].k;
@@ -702,64 +715,138 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       if (pr.status == SLOS_OK) caps[q] = estimate_caps(planners[k], &inputs[k], pr, jobs[q].grow);
     }
   });
-  for (int q = 0; q < n; ++q) {
-    const int k = jobs[q].k;
-    const slos_planner* P = planners[k];
-    Prep& pr = prep[q];
-    if (pr.status != SLOS_OK) {
-      std::memset(&outs[k], 0, sizeof(outs[k]));
-      outs[k].status = pr.status;
-      g_err = pr.why;
-      continue;
+  const auto t_a1 = std::chrono::steady_clock::now();
+  // Totals over the valid instances: fixed chunks reduced in parallel and folded in
+  // chunk order, so the valid list, the planner order (first appearance) and the
+  // reported error (the last failing instance) are those of one serial pass.
+  {
+    struct Red {
+      int64_t TD, TC, TP, TR, TS, TCd, TM, TW, TSel, TIds, TB, TE;
+      int maxN, maxDec, Lmax, nvalid, last_bad, off;
+      double S_need;
+      std::vector<const slos_planner*> pl;  // distinct planners, first appearance
+    };
+    const int chunks = n < 4096 ? 1 : 256;
+    thread_local std::vector<Red> red_tl;  // lambdas below see it through the reference
+    std::vector<Red>& red = red_tl;
+    red.resize((size_t)chunks);
+    auto lo_of = [&](int ch) { return (int)((int64_t)ch * n / chunks); };
+    auto reduce = [&](int ch) {
+      Red& r = red[ch];
+      r.TD = r.TC = r.TP = r.TR = r.TS = r.TCd = r.TM = r.TW = r.TSel = r.TIds = r.TB = r.TE = 0;
+      r.maxN = 0; r.maxDec = 0; r.Lmax = 1; r.nvalid = 0; r.last_bad = -1; r.S_need = 16;
+      r.pl.clear();
+      for (int q = lo_of(ch); q < lo_of(ch + 1); ++q) {
+        const int k = jobs[q].k;
+        const slos_planner* P = planners[k];
+        const Prep& pr = prep[q];
+        if (pr.status != SLOS_OK) {
+          std::memset(&outs[k], 0, sizeof(outs[k]));
+          outs[k].status = pr.status;
+          r.last_bad = q;
+          continue;
+        }
+        if (r.pl.empty() || r.pl.back() != P) {
+          bool seen = false;
+          for (const slos_planner* x : r.pl) if (x == P) { seen = true; break; }
+          if (!seen) r.pl.push_back(P);
+        }
+        ++r.nvalid;
+        r.TD += pr.n_dec;
+        r.TC += (pr.N + 1 + 3) & ~3;  // 16-byte aligned chain slices (the DP stages them by TMA)
+        r.TP += pr.n_pre;
+        r.TR += inputs[k].n_running;
+        r.TS += caps[q].surv;
+        r.TCd += caps[q].cand;
+        r.TM += caps[q].memo;
+        r.TW += (caps[q].work + 255) & ~(int64_t)255;
+        r.TSel += pr.N + 1;
+        r.TIds += 2 * (int64_t)inputs[k].n_pending + 1;
+        r.TB += caps[q].batch;
+        r.TE += caps[q].entry;
+        r.maxN = std::max(r.maxN, pr.N);
+        r.maxDec = std::max(r.maxDec, pr.n_dec);
+        r.Lmax = std::max(r.Lmax, P->L);
+        r.S_need = std::max(r.S_need, std::ceil(pr.span / P->tpot[0]) + 8);
+      }
+    };
+    if (chunks == 1) reduce(0);
+    else HostPool::get().run(chunks, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) reduce(ch); });
+    int last_bad = -1, nvalid = 0;
+    for (int ch = 0; ch < chunks; ++ch) {
+      Red& r = red[ch];
+      r.off = nvalid;
+      nvalid += r.nvalid;
+      if (r.last_bad >= 0) last_bad = r.last_bad;
+      for (const slos_planner* P : r.pl) {
+        bool seen = false;
+        for (const slos_planner* x : plist) if (x == P) { seen = true; break; }
+        if (!seen) plist.push_back(P);
+      }
+      TD += r.TD; TC += r.TC; TP += r.TP; TR += r.TR; TS += r.TS; TCd += r.TCd; TM += r.TM; TW += r.TW;
+      TSel += r.TSel; TIds += r.TIds; TB += r.TB; TE += r.TE;
+      maxN = std::max(maxN, r.maxN);
+      maxDec = std::max(maxDec, r.maxDec);
+      Lmax = std::max(Lmax, r.Lmax);
+      S_need = std::max(S_need, r.S_need);
     }
-    int pi = -1;
-    for (size_t x = 0; x < plist.size(); ++x) if (plist[x] == P) { pi = (int)x; break; }
-    if (pi < 0) { pi = (int)plist.size(); plist.push_back(P); }
-    pr.planner = pi;
-    valid.push_back(q);
-    TD += pr.n_dec;
-    TC += (pr.N + 1 + 3) & ~3;  // 16-byte aligned chain slices (the DP stages them by TMA)
-    TP += pr.n_pre;
-    TR += inputs[k].n_running;
-    TS += caps[q].surv;
-    TCd += caps[q].cand;
-    TM += caps[q].memo;
-    TW += (caps[q].work + 255) & ~(int64_t)255;
-    TSel += pr.N + 1;
-    TIds += 2 * (int64_t)inputs[k].n_pending + 1;
-    TB += caps[q].batch;
-    TE += caps[q].entry;
-    maxN = std::max(maxN, pr.N);
-    maxDec = std::max(maxDec, pr.n_dec);
-    Lmax = std::max(Lmax, P->L);
-    S_need = std::max(S_need, std::ceil(pr.span / P->tpot[0]) + 8);
+    if (last_bad >= 0) g_err = prep[last_bad].why;  // on the calling thread
+    valid.resize((size_t)nvalid);
+    auto place = [&](int ch) {
+      int x = red[ch].off;
+      const slos_planner* lastP = nullptr;
+      int lastpi = -1;
+      for (int q = lo_of(ch); q < lo_of(ch + 1); ++q) {
+        Prep& pr = prep[q];
+        if (pr.status != SLOS_OK) continue;
+        const slos_planner* P = planners[jobs[q].k];
+        if (P != lastP) {
+          lastP = P;
+          for (size_t y = 0; y < plist.size(); ++y) if (plist[y] == P) { lastpi = (int)y; break; }
+        }
+        pr.planner = lastpi;
+        valid[x++] = q;
+      }
+    };
+    if (chunks == 1) place(0);
+    else HostPool::get().run(chunks, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) place(ch); });
   }
   const auto t_b = std::chrono::steady_clock::now();
   const int nv = (int)valid.size();
   if (nv == 0) return SLOS_OK;
   const int Sc = (int)std::min<double>(S_need, 1 << 20);
-  int64_t TA = 0;
+  int64_t TA = 0, TT = 0, TPair = 0;  // anchor cache bytes, anchor tasks, pair records
   thread_local std::vector<int64_t> astride_tl;  // lambdas below see it through the reference
   std::vector<int64_t>& astride = astride_tl;
   astride.resize((size_t)n);
-  HostPool::get().run((int)valid.size(), [&](int lo, int hi) {
-    for (int x = lo; x < hi; ++x) {
-      const int q = valid[x];
-      astride[q] = (int64_t)dp_anchor_stride(prep[q].n_dec, Sc, Lmax, prep[q].N);
-    }
-  });
-  for (int q : valid) TA += astride[q] * (prep[q].N + 1);
+  {
+    const int chunks = nv < 4096 ? 1 : 256;
+    thread_local std::vector<std::array<int64_t, 3>> sums_tl;  // lambdas below see it through the reference
+    std::vector<std::array<int64_t, 3>>& sums = sums_tl;
+    sums.resize((size_t)chunks);
+    auto body = [&](int ch) {
+      int64_t a = 0, t = 0, pp = 0;
+      for (int x = (int)((int64_t)ch * nv / chunks); x < (int)((int64_t)(ch + 1) * nv / chunks); ++x) {
+        const int q = valid[x];
+        const int N = prep[q].N;
+        astride[q] = (int64_t)dp_anchor_stride(prep[q].n_dec, Sc, Lmax, N);
+        a += astride[q] * (N + 1);
+        t += N;
+        pp += (int64_t)N * (N + 1) / 2;
+      }
+      sums[ch] = {a, t, pp};
+    };
+    if (chunks == 1) body(0);
+    else HostPool::get().run(chunks, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) body(ch); });
+    for (int ch = 0; ch < chunks; ++ch) { TA += sums[ch][0]; TT += sums[ch][1]; TPair += sums[ch][2]; }
+  }
   const auto t_b1 = std::chrono::steady_clock::now();
   Layout& Ly = ws.Ly;
   Blob bi;
   Ly.planners = bi.add<PlannerDev>(plist.size());
   Ly.inst = bi.add<InstDev>(nv);
   Ly.order = bi.add<int32_t>(nv);
-  int64_t TT = 0;
-  for (int q : valid) TT += prep[q].N;
   Ly.atask = bi.add<int32_t>(2 * TT);
-  int64_t TPair = 0;
-  for (int q : valid) TPair += (int64_t)prep[q].N * (prep[q].N + 1) / 2;
   Ly.pair = bi.add<uint8_t>(TPair);
   const size_t grec_hdr = dp_group_hdr_bytes();
   const size_t grec_stride = (grec_hdr + dp_group_stride(Sc, Lmax) + 127) & ~(size_t)127;
@@ -872,38 +959,57 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   std::vector<Off>& offs = offs_tl;
   offs.resize((size_t)nv);
   {
-    // per-instance sizes in parallel (the inputs are scattered), then one compact
-    // serial exclusive scan
-    HostPool::get().run(nv, [&](int lo, int hi) {
-      for (int v = lo; v < hi; ++v) {
+    // per-instance sizes and a chunk-local exclusive scan in parallel (the inputs are
+    // scattered), the chunk bases folded in order, then the bases added in parallel
+    auto add = [](Off& a, const Off& x) {
+      a.D += x.D; a.C += x.C; a.P += x.P; a.R += x.R; a.S += x.S; a.Cd += x.Cd; a.M += x.M;
+      a.W += x.W; a.Sel += x.Sel; a.Ids += x.Ids; a.B += x.B; a.E += x.E; a.A += x.A; a.Pair += x.Pair;
+    };
+    const int chunks = nv < 4096 ? 1 : 256;
+    thread_local std::vector<Off> cbase_tl;  // lambdas below see it through the reference
+    std::vector<Off>& cbase = cbase_tl;
+    cbase.resize((size_t)chunks);
+    auto lo_of = [&](int ch) { return (int)((int64_t)ch * nv / chunks); };
+    auto sizes = [&](int ch) {
+      Off acc{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int v = lo_of(ch); v < lo_of(ch + 1); ++v) {
         const int q = valid[v];
         const Prep& pr = prep[q];
         const Caps& cp = caps[q];
         const slos_input* in = &inputs[jobs[q].k];
-        Off& o = offs[v];
-        o.D = pr.n_dec;
-        o.C = (pr.N + 1 + 3) & ~3;
-        o.P = pr.n_pre;
-        o.R = in->n_running;
-        o.S = cp.surv;
-        o.Cd = cp.cand;
-        o.M = cp.memo;
-        o.W = (cp.work + 255) & ~(int64_t)255;
-        o.Sel = pr.N + 1;
-        o.Ids = 2 * (int64_t)in->n_pending + 1;
-        o.B = cp.batch;
-        o.E = cp.entry;
-        o.A = astride[q] * (pr.N + 1);
-        o.Pair = (int64_t)pr.N * (pr.N + 1) / 2;
+        Off x;
+        x.D = pr.n_dec;
+        x.C = (pr.N + 1 + 3) & ~3;
+        x.P = pr.n_pre;
+        x.R = in->n_running;
+        x.S = cp.surv;
+        x.Cd = cp.cand;
+        x.M = cp.memo;
+        x.W = (cp.work + 255) & ~(int64_t)255;
+        x.Sel = pr.N + 1;
+        x.Ids = 2 * (int64_t)in->n_pending + 1;
+        x.B = cp.batch;
+        x.E = cp.entry;
+        x.A = astride[q] * (pr.N + 1);
+        x.Pair = (int64_t)pr.N * (pr.N + 1) / 2;
+        offs[v] = acc;
+        add(acc, x);
       }
-    });
+      cbase[ch] = acc;
+    };
+    if (chunks == 1) sizes(0);
+    else HostPool::get().run(chunks, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) sizes(ch); });
     Off o{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int v = 0; v < nv; ++v) {
-      const Off x = offs[v];
-      offs[v] = o;
-      o.D += x.D; o.C += x.C; o.P += x.P; o.R += x.R; o.S += x.S; o.Cd += x.Cd; o.M += x.M;
-      o.W += x.W; o.Sel += x.Sel; o.Ids += x.Ids; o.B += x.B; o.E += x.E; o.A += x.A; o.Pair += x.Pair;
+    for (int ch = 0; ch < chunks; ++ch) {
+      const Off t = cbase[ch];
+      cbase[ch] = o;
+      add(o, t);
     }
+    if (chunks > 1)
+      HostPool::get().run(chunks, [&](int c0, int c1) {
+        for (int ch = c0; ch < c1; ++ch)
+          for (int v = lo_of(ch); v < lo_of(ch + 1); ++v) add(offs[v], cbase[ch]);
+      });
   }
   const auto t_c = std::chrono::steady_clock::now();
   HostPool::get().run(nv, [&](int v_lo, int v_hi) {
@@ -1072,6 +1178,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   }
   });
   const auto t_d = std::chrono::steady_clock::now();
+  auto t_d1 = t_d, t_d2 = t_d;
   int32_t* h_order = (int32_t*)hp(Ly.order);
   {
     // launch order, heaviest first (load balance only: results do not depend on it).
@@ -1088,16 +1195,19 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       thread_local std::vector<uint8_t> key_tl;
       std::vector<uint8_t>& key = key_tl;
       key.resize((size_t)nv);
-      for (int v = 0; v < nv; ++v) {
-        const int e = std::min(kB - 1, std::max(0, std::ilogb(std::max(1.0, cost[v]))));
-        key[v] = (uint8_t)(kB - 1 - e);
-        ++cnt[key[v] + 1];
-      }
+      HostPool::get().run(nv, [&](int lo, int hi) {
+        for (int v = lo; v < hi; ++v) {
+          const int e = std::min(kB - 1, std::max(0, std::ilogb(std::max(1.0, cost[v]))));
+          key[v] = (uint8_t)(kB - 1 - e);
+        }
+      });
+      for (int v = 0; v < nv; ++v) ++cnt[key[v] + 1];
       for (int b = 0; b < kB; ++b) cnt[b + 1] += cnt[b];
       for (int v = 0; v < nv; ++v) ord[cnt[key[v]]++] = v;
     }
     std::memcpy(h_order, ord.data(), sizeof(int32_t) * (size_t)nv);
     ws.ord.assign(ord.begin(), ord.end());
+    t_d1 = std::chrono::steady_clock::now();
     // solve parts: contiguous ranges of the cost-descending order (every part gets
     // a share of the heavy instances); each part's DP and reconstruction are
     // launched on their own stream so one part's reconstruction overlaps the next
@@ -1136,6 +1246,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     }
     // anchor tasks (instance, anchor j), j = -1 .. N-2, grouped by solve part so each
     // part's anchor/group kernels run on its own stream ahead of its DP
+    t_d2 = std::chrono::steady_clock::now();
     int32_t* t = (int32_t*)hp(Ly.atask);
     thread_local std::vector<int64_t> aoff_tl;  // lambdas below see it through the reference
     std::vector<int64_t>& aoff = aoff_tl;  // first task of the instance at order position y
@@ -1176,9 +1287,13 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     auto ms = [](std::chrono::steady_clock::time_point x, std::chrono::steady_clock::time_point y) {
       return std::chrono::duration<double, std::milli>(y - x).count();
     };
-    std::fprintf(stderr, "[slos upload] n %d: prep %.3f, totals %.3f, layout %.3f (strides %.3f blobs %.3f ensure %.3f), fill %.3f, order/parts %.3f, h2d %.3f ms\n",
+    std::fprintf(stderr, "[slos upload] n %d: prep run %.3f totals loop %.3f | order sort %.3f parts %.3f tasks+rec %.3f\n", n,
+                 ms(t_a, t_a1), ms(t_a1, t_b), ms(t_d, t_d1), ms(t_d1, t_d2), ms(t_d2, t_e));
+    std::fprintf(stderr, "[slos upload] n %d: prep %.3f, totals %.3f, layout %.3f (strides %.3f blobs %.3f ensure %.3f), fill %.3f, order/parts %.3f, h2d %.3f ms; host pool %d runs %.3f ms\n",
                  n, ms(t_a, t_b), 0.0, ms(t_b, t_c), ms(t_b, t_b1), ms(t_b1, t_b2), ms(t_b2, t_b3), ms(t_c, t_d),
-                 ms(t_d, t_e), ms(t_e, t_f));
+                 ms(t_d, t_e), ms(t_e, t_f), HostPool::get().runs, HostPool::get().run_ms);
+    HostPool::get().runs = 0;
+    HostPool::get().run_ms = 0.0;
   }
   Ly.memo_bytes = sizeof(MemoEnt) * (size_t)TM;
   Ly.bkey_bytes = sizeof(uint64_t) * 2 * (size_t)TCd;
@@ -1668,32 +1783,35 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
 // With per-part headers (ws.part_collect, copied by ws_solve on each part's
 // stream) a part's compaction and D2H start as soon as ITS reconstruction ends,
 // under the later parts' kernels; otherwise one set over the whole workspace.
-int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry) {
+int ws_collect_finish(Workspace& ws);
+
+// The first half of a collection: headers, regrowth list, compaction and the async
+// D2H into the result arena, the result pointers. With per-part headers the D2H is
+// still in flight on return (ws_collect_finish waits for it), so the chunk pipeline
+// prepares the next chunk on the host meanwhile.
+int ws_collect_start(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry) {
   if (!ws.uploaded || ws.nv == 0) return SLOS_OK;
   const int nv = ws.nv;
   cudaError_t e;
   if (ws.part_collect) {
     for (int p = 0; p < ws.n_parts; ++p) {
+      const auto t0 = std::chrono::steady_clock::now();
       if ((e = cudaEventSynchronize(ws.ev_hdr[p])) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+      if (host_timing())
+        std::fprintf(stderr, "[slos collect] part %d: header wait %.3f ms\n", p,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
       g_d2h += (int64_t)(sizeof(OutHdr) * (size_t)nv);
       const int lo = ws.part_lo[p], n = ws.part_lo[p + 1] - lo;
+      const auto t1 = std::chrono::steady_clock::now();
       const int r = collect_set(c, ws, (const OutHdr*)ws.h_hdr[p].p, ws.ord.data() + lo, ws.A.order + lo, n,
                                 ws.h_offs[p], ws.d_packp[p], ws.pstream[p], outs, retry);
       if (r != SLOS_OK) return r;
+      if (host_timing())
+        std::fprintf(stderr, "[slos collect] part %d: collect_set %.3f ms (%d instances)\n", p,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count(), n);
       if (host_timing()) {
         if (!ws.ev_d2h[p]) cudaEventCreate(&ws.ev_d2h[p]);
         cudaEventRecord(ws.ev_d2h[p], ws.pstream[p]);
-      }
-    }
-    for (int p = 0; p < ws.n_parts; ++p)
-      if ((e = cudaStreamSynchronize(ws.pstream[p])) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
-    if (host_timing()) {
-      for (int p = 0; p < ws.n_parts; ++p) {
-        float a = 0.0f, b = 0.0f, d = 0.0f;
-        cudaEventElapsedTime(&a, ws.ev[0], ws.ev_dp[p]);
-        cudaEventElapsedTime(&b, ws.ev[0], ws.ev_d2h[p]);
-        cudaEventElapsedTime(&d, ws.ev[0], ws.ev[2]);
-        std::fprintf(stderr, "[slos collect] part %d: dp end %.3f ms, d2h end %.3f ms (solve end %.3f ms)\n", p, a, b, d);
       }
     }
     return SLOS_OK;
@@ -1715,6 +1833,39 @@ int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry
   if (r != SLOS_OK) return r;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
   return SLOS_OK;
+}
+
+// The second half: wait for the result D2H of every part (per-part collection).
+int ws_collect_finish(Workspace& ws) {
+  if (!ws.uploaded || ws.nv == 0 || !ws.part_collect) return SLOS_OK;
+  cudaError_t e;
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int p = 0; p < ws.n_parts; ++p)
+      if ((e = cudaStreamSynchronize(ws.pstream[p])) != cudaSuccess) return set_err(SLOS_ERR_CUDA, cudaGetErrorString(e));
+    if (host_timing())
+      std::fprintf(stderr, "[slos collect] d2h wait %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    if (host_timing()) {
+      for (int p = 0; p < ws.n_parts; ++p) {
+        float a = 0.0f, b = 0.0f, d = 0.0f;
+        cudaEventElapsedTime(&a, ws.ev[0], ws.ev_dp[p]);
+        cudaEventElapsedTime(&b, ws.ev[0], ws.ev_d2h[p]);
+        cudaEventElapsedTime(&d, ws.ev[0], ws.ev[2]);
+        std::fprintf(stderr, "[slos collect] part %d: dp end %.3f ms, d2h end %.3f ms (solve end %.3f ms)\n", p, a, b, d);
+      }
+    }
+  }
+  return SLOS_OK;
+}
+
+int ws_collect(Ctx& c, Workspace& ws, slos_result* outs, std::vector<Job>& retry) {
+  const int r = ws_collect_start(c, ws, outs, retry);
+  if (r != SLOS_OK) {
+    cudaDeviceSynchronize();  // no D2H may outlive a failed collection
+    return r;
+  }
+  return ws_collect_finish(ws);
 }
 
 }  // namespace
@@ -1815,11 +1966,12 @@ Workspace& default_ws() {
   return *w;
 }
 
-// Two pipeline workspaces with their own streams: chunk i+1's host preparation and
-// H2D overlap chunk i's kernels, and chunk i's compaction + D2H overlap chunk i+1's
-// kernels (copy engines vs SMs).
+// Three pipeline workspaces with their own streams (chunk i uses i % 3): chunk i+1's
+// host preparation and H2D overlap chunk i's kernels, and chunk i's compaction + D2H
+// overlap chunk i+1's kernels (copy engines vs SMs) and chunk i+2's host preparation.
+constexpr int kPipeWs = 3;
 Workspace& pipe_ws(int k) {
-  static Workspace* w[2] = {nullptr, nullptr};
+  static Workspace* w[kPipeWs] = {nullptr, nullptr, nullptr};
   if (!w[k]) {
     w[k] = new Workspace();
     // the earlier chunk runs at higher priority so its D2H starts while the next
@@ -1838,9 +1990,10 @@ int pipeline_chunks(int n) {
   }();
   if (env > 0) return std::min(env, std::max(1, n));
   // measured: C2 x 1024 (heavy instances, GPU-bound): 2 chunks best; C5 x 65,536 (tiny
-  // instances, host-preparation-bound): 4 chunks 9.2 ms, 3: 9.4, 2: 10.7, 6: 9.9
+  // instances, host-preparation-bound; collection split around the next chunk's
+  // preparation): 3 chunks 7.05-7.18 ms, 4: 7.25-7.33, 5: 7.4-7.5, 6: 7.7, 8: 8.3-8.6
   if (n < 512) return 1;
-  return n < 32768 ? 2 : std::min(8, n / 16384);
+  return n < 40000 ? 2 : std::min(8, n / 20000);
 }
 
 bool part_collect_enabled() {  // SLOS_PART_COLLECT=0: one collection per workspace
@@ -1936,6 +2089,7 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
              int32_t unit_value, slos_result* outs, cudaStream_t stream) {
   g_h2d = 0;
   g_d2h = 0;
+  const auto t_p0 = std::chrono::steady_clock::now();
   std::vector<Job> jobs, retry;
   std::vector<std::pair<double, int>> wide;
   {
@@ -1945,6 +2099,9 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
     HostPool::get().run(n, [&](int lo, int hi) {
       for (int k = lo; k < hi; ++k) need[k] = slot_need(planners[k], &inputs[k]);
     });
+    if (host_timing())
+      std::fprintf(stderr, "[slos pipeline] slot needs: %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_p0).count());
     const double lim = narrow_slots();
     jobs.reserve((size_t)n);
     for (int k = 0; k < n; ++k) {
@@ -1974,32 +2131,40 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
       return e ? std::atof(e) : 0.3;  // measured C2 x 1024: 0.3 -> 4.5 ms, 0.5 -> 4.9 ms, 0.7 -> 5.2 ms
     }();
     std::vector<std::vector<Job>> chunk(K);
+    for (auto& ch : chunk) ch.reserve((size_t)n / K + 1);
     for (int k = 0; k < n; ++k) {
       int ci = (int)((int64_t)k * K / n);
       if (K == 2) ci = k < (int)(split * n) ? 0 : 1;
       chunk[ci].push_back(jobs[k]);
     }  // (jobs[k].k: the caller's instance index)
-    int prev = -1;
-    for (int i = 0; i <= K; ++i) {
+    if (host_timing())
+      std::fprintf(stderr, "[slos pipeline] before the chunks: %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_p0).count());
+    // step i: upload + solve chunk i, start chunk i-1's collection (headers, compaction,
+    // D2H enqueued), finish chunk i-2's (its D2H ran under chunk i's host preparation)
+    auto fail = [&](int r) {
+      cudaDeviceSynchronize();  // no D2H may outlive a failed call
+      for (const Job& j : jobs) outs[j.k].status = r;
+      return r;
+    };
+    for (int i = 0; i <= K + 1; ++i) {
       const auto t_a = std::chrono::steady_clock::now();
       if (i < K) {
-        Workspace& w = pipe_ws(i & 1);
+        Workspace& w = pipe_ws(i % kPipeWs);
         cudaStreamWaitEvent(w.own_stream, ev0, 0);
         w.part_collect = part_collect_enabled();
         int r = ws_upload(c, w, planners, inputs, unit_value, chunk[i], outs, w.own_stream);
         if (r == SLOS_OK) r = ws_solve(w, w.own_stream);
-        if (r != SLOS_OK) {
-          for (const Job& j : jobs) outs[j.k].status = r;
-          return r;
-        }
+        if (r != SLOS_OK) return fail(r);
       }
       const auto t_b = std::chrono::steady_clock::now();
-      if (prev >= 0) {
-        const int r = ws_collect(c, pipe_ws(prev & 1), outs, retry);
-        if (r != SLOS_OK) {
-          for (const Job& j : jobs) outs[j.k].status = r;
-          return r;
-        }
+      if (i >= 1 && i - 1 < K) {
+        const int r = ws_collect_start(c, pipe_ws((i - 1) % kPipeWs), outs, retry);
+        if (r != SLOS_OK) return fail(r);
+      }
+      if (i >= 2) {
+        const int r = ws_collect_finish(pipe_ws((i - 2) % kPipeWs));
+        if (r != SLOS_OK) return fail(r);
       }
       if (std::getenv("SLOS_HOST_TIMING")) {
         const auto t_c = std::chrono::steady_clock::now();
@@ -2007,7 +2172,6 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
                      std::chrono::duration<double, std::milli>(t_b - t_a).count(),
                      std::chrono::duration<double, std::milli>(t_c - t_b).count());
       }
-      prev = i;
     }
     jobs.swap(retry);
     retry.clear();
@@ -2024,9 +2188,14 @@ extern "C" {
 int slos_plan_batch(slos_planner* const* planners, int32_t n, const slos_input* inputs,
                     int32_t unit_value, slos_result* outs, void* stream) {
   g_err.clear();  // a message always belongs to this call
-  for (int k = 0; k < n; ++k) std::memset(&outs[k], 0, sizeof(outs[k]));
   Ctx& c = ctx();
-  std::lock_guard<std::mutex> g(c.mu);
+  std::lock_guard<std::mutex> g(c.mu);  // (the host pool serves one call at a time)
+  const auto t0 = std::chrono::steady_clock::now();
+  if (n > 0)
+    HostPool::get().run(n, [&](int lo, int hi) { std::memset(outs + lo, 0, sizeof(*outs) * (size_t)(hi - lo)); });
+  if (host_timing())
+    std::fprintf(stderr, "[slos plan_batch] clear %d results: %.3f ms\n", n,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   const int st = ensure_device(c);
   if (st != SLOS_OK) {
     set_err(st, c.why);
