@@ -1689,28 +1689,68 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
   boff.assign((size_t)n, 0);
   eoff.assign((size_t)n, 0);
   ioff.assign((size_t)n, 0);
-  size_t packed = 0;
-  int good = 0;
-  for (int x = 0; x < n; ++x) {
-    const int v = vof(x);
-    const int q = valid[v];
-    const OutHdr& h = hdr[v];
-    if (h.status == SLOS_ERR_CAPACITY && jobs[q].grow < 6) {
-      retry.push_back({jobs[q].k, jobs[q].grow + 1});
-      continue;
+  // packed layout per planned instance, from a 16-byte aligned start: batches,
+  // entries, ids, each 16-byte aligned; the next instance starts at the next 16-byte
+  // boundary. Chunk-local offsets in parallel, chunk bases folded in order.
+  const int chunks = n < 4096 ? 1 : 128;
+  struct CRed { size_t bytes; int good; size_t last_end; std::vector<Job> retry; };
+  thread_local std::vector<CRed> cred_tl;  // lambdas below see it through the reference
+  std::vector<CRed>& cred = cred_tl;
+  cred.resize((size_t)chunks);
+  auto lo_of = [&](int ch) { return (int)((int64_t)ch * n / chunks); };
+  auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  auto local = [&](int ch) {
+    CRed& r = cred[ch];
+    r.bytes = 0; r.good = 0; r.last_end = 0;
+    r.retry.clear();
+    size_t at = 0;  // aligned start of the next instance, relative to the chunk
+    for (int x = lo_of(ch); x < lo_of(ch + 1); ++x) {
+      const int v = vof(x);
+      const int q = valid[v];
+      const OutHdr& h = hdr[v];
+      if (h.status == SLOS_ERR_CAPACITY && jobs[q].grow < 6) {
+        r.retry.push_back({jobs[q].k, jobs[q].grow + 1});
+        continue;
+      }
+      if (h.status != SLOS_OK) continue;
+      ++r.good;
+      boff[x] = (int64_t)at;
+      size_t e = a16(at + sizeof(slos_batch) * (size_t)h.n_batches);
+      eoff[x] = (int64_t)e;
+      e = a16(e + sizeof(slos_entry) * (size_t)h.n_entries);
+      ioff[x] = (int64_t)e;
+      r.last_end = e + sizeof(int32_t) * (size_t)(h.n_admitted + h.n_declined);
+      at = a16(r.last_end);
     }
-    if (h.status != SLOS_OK) continue;
-    ++good;
-    packed = (packed + 15) & ~(size_t)15;
-    boff[x] = (int64_t)packed;
-    packed += sizeof(slos_batch) * (size_t)h.n_batches;
-    packed = (packed + 15) & ~(size_t)15;
-    eoff[x] = (int64_t)packed;
-    packed += sizeof(slos_entry) * (size_t)h.n_entries;
-    packed = (packed + 15) & ~(size_t)15;
-    ioff[x] = (int64_t)packed;
-    packed += sizeof(int32_t) * (size_t)(h.n_admitted + h.n_declined);
+    r.bytes = at;
+  };
+  if (chunks == 1) local(0);
+  else HostPool::get().run(chunks, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) local(ch); });
+  size_t packed = 0, base = 0;
+  int good = 0;
+  thread_local std::vector<size_t> cbase_tl;
+  std::vector<size_t>& cbase = cbase_tl;
+  cbase.resize((size_t)chunks);
+  for (int ch = 0; ch < chunks; ++ch) {
+    CRed& r = cred[ch];
+    cbase[ch] = base;
+    if (r.good) packed = base + r.last_end;  // the end of the last planned instance
+    base += r.bytes;
+    good += r.good;
+    retry.insert(retry.end(), r.retry.begin(), r.retry.end());
   }
+  if (chunks > 1)
+    HostPool::get().run(chunks, [&](int c0, int c1) {
+      for (int ch = c0; ch < c1; ++ch) {
+        const int64_t b = (int64_t)cbase[ch];
+        if (b == 0) continue;
+        for (int x = lo_of(ch); x < lo_of(ch + 1); ++x) {
+          boff[x] += b;
+          eoff[x] += b;
+          ioff[x] += b;
+        }
+      }
+    });
   ResultArena* ra = nullptr;
   if (good) {
     const size_t offs_bytes = sizeof(int64_t) * 3 * (size_t)n;
@@ -2090,7 +2130,12 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
   g_h2d = 0;
   g_d2h = 0;
   const auto t_p0 = std::chrono::steady_clock::now();
-  std::vector<Job> jobs, retry;
+  // per-call job lists kept across calls (fresh 0.5 MB vectors page-fault on every
+  // C5-size call)
+  thread_local std::vector<Job> jobs_tl;
+  std::vector<Job>& jobs = jobs_tl;
+  jobs.clear();
+  std::vector<Job> retry;
   std::vector<std::pair<double, int>> wide;
   {
     thread_local std::vector<double> need_tl;  // the workers see it through the reference
@@ -2103,12 +2148,22 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
       std::fprintf(stderr, "[slos pipeline] slot needs: %.3f ms\n",
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_p0).count());
     const double lim = narrow_slots();
-    jobs.reserve((size_t)n);
-    for (int k = 0; k < n; ++k) {
-      if (need[k] > lim) wide.push_back({need[k], k});
-      else jobs.push_back({k, 0});
+    bool any_wide = false;
+    for (int k = 0; k < n; ++k) any_wide |= need[k] > lim;
+    if (!any_wide) {  // (the common case: the job list is the identity, filled in parallel)
+      jobs.resize((size_t)n);
+      HostPool::get().run(n, [&](int lo, int hi) { for (int k = lo; k < hi; ++k) jobs[k] = {k, 0}; });
+    } else {
+      jobs.reserve((size_t)n);
+      for (int k = 0; k < n; ++k) {
+        if (need[k] > lim) wide.push_back({need[k], k});
+        else jobs.push_back({k, 0});
+      }
     }
   }
+  if (host_timing())
+    std::fprintf(stderr, "[slos pipeline] %zu wide instances (job list at %.3f ms)\n", wide.size(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_p0).count());
   if (!wide.empty()) {
     const int r = solve_wide(c, ws, planners, inputs, unit_value, outs, stream, wide);
     if (r != SLOS_OK) {
@@ -2123,6 +2178,9 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
     static cudaEvent_t ev0 = nullptr;
     if (!ev0) cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
     cudaEventRecord(ev0, stream ? stream : c.stream);
+    if (host_timing())
+      std::fprintf(stderr, "[slos pipeline] ev0 at %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_p0).count());
     // chunk boundaries: with 2 chunks the first is the smaller (SLOS_PIPELINE_SPLIT):
     // the GPU starts after a short host preparation, the second chunk's preparation
     // overlaps the first's kernels, and both chunks' kernels then share the SMs
@@ -2130,13 +2188,15 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
       const char* e = std::getenv("SLOS_PIPELINE_SPLIT");
       return e ? std::atof(e) : 0.3;  // measured C2 x 1024: 0.3 -> 4.5 ms, 0.5 -> 4.9 ms, 0.7 -> 5.2 ms
     }();
-    std::vector<std::vector<Job>> chunk(K);
-    for (auto& ch : chunk) ch.reserve((size_t)n / K + 1);
-    for (int k = 0; k < n; ++k) {
-      int ci = (int)((int64_t)k * K / n);
-      if (K == 2) ci = k < (int)(split * n) ? 0 : 1;
-      chunk[ci].push_back(jobs[k]);
-    }  // (jobs[k].k: the caller's instance index)
+    thread_local std::vector<std::vector<Job>> chunk_tl;
+    std::vector<std::vector<Job>>& chunk = chunk_tl;
+    if ((int)chunk.size() < K) chunk.resize((size_t)K);
+    // chunk i = jobs[ceil(i n / K), ceil((i+1) n / K)) (contiguous; jobs[k].k is the
+    // caller's instance index)
+    for (int i = 0; i < K; ++i) {
+      auto lo = [&](int x) { return x == 0 ? 0 : x == K ? n : K == 2 ? (int)(split * n) : (int)(((int64_t)x * n + K - 1) / K); };
+      chunk[i].assign(jobs.begin() + lo(i), jobs.begin() + lo(i + 1));
+    }
     if (host_timing())
       std::fprintf(stderr, "[slos pipeline] before the chunks: %.3f ms\n",
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_p0).count());
@@ -2173,11 +2233,11 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
                      std::chrono::duration<double, std::milli>(t_c - t_b).count());
       }
     }
-    jobs.swap(retry);
+    jobs.assign(retry.begin(), retry.end());  // (keeps the reused buffer)
     retry.clear();
     if (std::getenv("SLOS_HOST_TIMING")) std::fprintf(stderr, "[slos pipeline] %d chunks, %zu retried\n", K, jobs.size());
   }
-  const int r = solve_rounds(c, ws, planners, inputs, unit_value, outs, stream, std::move(jobs));
+  const int r = solve_rounds(c, ws, planners, inputs, unit_value, outs, stream, std::vector<Job>(jobs));
   if (r == SLOS_ERR_RANGE) return SLOS_OK;  // per-instance statuses already set
   return r;
 }
