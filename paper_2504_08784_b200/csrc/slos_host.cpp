@@ -2193,8 +2193,19 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
     if ((int)chunk.size() < K) chunk.resize((size_t)K);
     // chunk i = jobs[ceil(i n / K), ceil((i+1) n / K)) (contiguous; jobs[k].k is the
     // caller's instance index)
+    // With 3+ chunks the last one takes `tail` of an equal share (SLOS_PIPELINE_TAIL):
+    // its kernels, D2H and collection are the part of the call nothing overlaps.
+    static const double tail = [] {
+      const char* e = std::getenv("SLOS_PIPELINE_TAIL");
+      return e ? std::atof(e) : 1.0;
+    }();
     for (int i = 0; i < K; ++i) {
-      auto lo = [&](int x) { return x == 0 ? 0 : x == K ? n : K == 2 ? (int)(split * n) : (int)(((int64_t)x * n + K - 1) / K); };
+      auto lo = [&](int x) {
+        if (x == 0) return 0;
+        if (x == K) return n;
+        if (K == 2) return (int)(split * n);
+        return (int)((double)n * x / (K - 1 + tail));
+      };
       chunk[i].assign(jobs.begin() + lo(i), jobs.begin() + lo(i + 1));
     }
     if (host_timing())
