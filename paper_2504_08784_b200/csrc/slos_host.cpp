@@ -366,8 +366,12 @@ int solve_parts(int nv) {
     const char* e = std::getenv("SLOS_SOLVE_PARTS");
     return e ? std::atoi(e) : 2;
   }();
+  static const int per = [] {  // fewest instances per part (SLOS_PART_MIN)
+    const char* e = std::getenv("SLOS_PART_MIN");
+    return e ? std::max(1, std::atoi(e)) : 128;
+  }();
   int P = std::max(1, std::min(env, kMaxParts));
-  if (nv < 128 * P) P = std::max(1, nv / 128);
+  if (nv < per * P) P = std::max(1, nv / per);
   return std::max(1, P);
 }
 
