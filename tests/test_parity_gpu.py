@@ -249,3 +249,43 @@ def test_long_deadline_span_is_isolated():
     for x, k in enumerate(keep):
         assert not diff(P[k], O[x], counters=True), (k, diff(P[k], O[x], counters=True))
     assert P[4]["status"] == abi.SLOS_ERR_RANGE
+
+
+def test_invalid_instances_inside_a_pipelined_batch():
+    """Instances failing validation spread over the chunks of a 3-chunk pipelined batch
+    (65,536 C5 instances; the upload's parallel reductions and the split collection):
+    they get the status code, every other instance still matches the reference, and
+    slos_last_error names the last failing instance's fault."""
+    import gzip
+    import json
+    import os
+
+    import numpy as np
+    from golden_checks import _cmp
+    from paper_2504_08784_b200.planner import PerfTerm, PlannerConfig
+    GOLDEN = os.path.join(abi.ROOT, "tests", "golden")
+    meta = json.load(gzip.open(os.path.join(GOLDEN, "c5.json.gz"), "rt"))
+    G = meta["groups"]["ar"]
+    base = W.load_corpus(os.path.join(GOLDEN, "c5_ar.bin.gz"))
+    b = base.tiled(32)
+    bad = np.zeros(1, abi.PENDING_DTYPE)
+    bad[0]["prefill_deadline"] = 1e9
+    bad[0]["prefill_tokens"] = 10
+    bad[0]["decode_tier"] = 7  # out of range for two tiers
+    bad[0]["memory_units"] = 1
+    bad[0]["id"] = b._blob.ctypes.data  # any valid C string
+    broken = [5, 21845, 21846, 40000, 65535]
+    for k in broken:
+        b.inputs[k]["pending"] = bad.ctypes.data
+        b.inputs[k]["n_pending"] = 1
+    prod = abi.product()
+    cfg = PlannerConfig(max_chunk_tokens=2048, max_batch_tokens=16384, speculative=G["speculative"],
+                        spec_alpha=0.8, spec_max_len=8, plan_margin=0.0)
+    h = _Handle(prod, [PerfTerm(*t) for t in meta["model"]], W.TWO_TIER_SLO, cfg)
+    res = plan_many(prod, h.ptr, b)
+    assert b"tier" in prod.slos_last_error()
+    for k, got in enumerate(res):
+        if k in broken:
+            assert got["status"] == abi.SLOS_ERR_INVALID_PARAMETERS, (k, got["status"])
+        else:
+            _cmp(got, G["ref"][k % base.n], f"c5 ar tiled instance {k}")
