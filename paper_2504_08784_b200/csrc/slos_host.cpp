@@ -1504,7 +1504,8 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     cudaEventCreateWithFlags(&ws.ev_fork, cudaEventDisableTiming);
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&ws.astream, cudaStreamNonBlocking, hi);
+    // (SLOS_ANCHOR_PRIO_LOW: anchor/group kernels below the parts' DP and reconstruction)
+    cudaStreamCreateWithPriority(&ws.astream, cudaStreamNonBlocking, std::getenv("SLOS_ANCHOR_PRIO_LOW") ? lo : hi);
     static const bool rev = std::getenv("SLOS_PART_PRIO_REV") != nullptr;
     for (int p = 0; p < kMaxParts; ++p) {
       cudaStreamCreateWithPriority(&ws.pstream[p], cudaStreamNonBlocking,
