@@ -1205,9 +1205,34 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
           key[v] = (uint8_t)(kB - 1 - e);
         }
       });
-      for (int v = 0; v < nv; ++v) ++cnt[key[v] + 1];
-      for (int b = 0; b < kB; ++b) cnt[b + 1] += cnt[b];
-      for (int v = 0; v < nv; ++v) ord[cnt[key[v]]++] = v;
+      // stable counting sort over fixed chunks: per-chunk histograms in parallel,
+      // positions by (bucket, chunk), scatter in parallel (each chunk in order)
+      (void)cnt;
+      constexpr int kCh = 128;
+      thread_local std::vector<std::array<int, kB>> hist_tl;  // lambdas below see it through the reference
+      std::vector<std::array<int, kB>>& hist = hist_tl;
+      hist.resize(kCh);
+      auto clo = [&](int ch) { return (int)((int64_t)ch * nv / kCh); };
+      HostPool::get().run(kCh, [&](int c0, int c1) {
+        for (int ch = c0; ch < c1; ++ch) {
+          std::array<int, kB>& h = hist[ch];
+          h.fill(0);
+          for (int v = clo(ch); v < clo(ch + 1); ++v) ++h[key[v]];
+        }
+      });
+      int run = 0;
+      for (int b = 0; b < kB; ++b)
+        for (int ch = 0; ch < kCh; ++ch) {
+          const int x = hist[ch][b];
+          hist[ch][b] = run;
+          run += x;
+        }
+      HostPool::get().run(kCh, [&](int c0, int c1) {
+        for (int ch = c0; ch < c1; ++ch) {
+          std::array<int, kB>& h = hist[ch];
+          for (int v = clo(ch); v < clo(ch + 1); ++v) ord[h[key[v]]++] = v;
+        }
+      });
     }
     std::memcpy(h_order, ord.data(), sizeof(int32_t) * (size_t)nv);
     ws.ord.assign(ord.begin(), ord.end());
@@ -1233,15 +1258,28 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
         while (y < x && cost[ord[y]] >= big_thr) ++y;
       ws.big_hi[p] = y;
     }
-    for (int p = 0; p < P; ++p)
-      for (int x = ws.part_lo[p]; x < ws.part_lo[p + 1]; ++x) ++qcount[kBuildKinds * p + kind_v[ord[x]]];
-    HostPool::get().run(nv, [&](int lo, int hi) {
-      int p = 0;
-      for (int x = lo; x < hi; ++x) {
-        while (x >= ws.part_lo[p + 1]) ++p;
-        hI[ord[x]].part = p;
-      }
-    });
+    {  // queue sizes (per part and reconstruction kind) and each instance's part, over
+       // fixed chunks of the order in parallel
+      constexpr int kCh = 128;
+      thread_local std::vector<std::array<int, kQueues>> qc_tl;  // lambdas below see it through the reference
+      std::vector<std::array<int, kQueues>>& qc = qc_tl;
+      qc.resize(kCh);
+      auto clo = [&](int ch) { return (int)((int64_t)ch * nv / kCh); };
+      auto body = [&](int ch) {
+        std::array<int, kQueues>& c = qc[ch];
+        c.fill(0);
+        int p = 0;
+        for (int x = clo(ch); x < clo(ch + 1); ++x) {
+          while (x >= ws.part_lo[p + 1]) ++p;
+          hI[ord[x]].part = p;
+          ++c[kBuildKinds * p + kind_v[ord[x]]];
+        }
+      };
+      if (nv < 4096) { for (int ch = 0; ch < kCh; ++ch) body(ch); }
+      else HostPool::get().run(kCh, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) body(ch); });
+      for (int ch = 0; ch < kCh; ++ch)
+        for (int q = 0; q < kQueues; ++q) qcount[q] += qc[ch][q];
+    }
     int qb = 2 * kQueues;  // the counters come first
     for (int q = 0; q < kQueues; ++q) {
       ws.qbase[q] = qb;
@@ -1255,8 +1293,30 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     thread_local std::vector<int64_t> aoff_tl;  // lambdas below see it through the reference
     std::vector<int64_t>& aoff = aoff_tl;  // first task of the instance at order position y
     aoff.resize((size_t)nv + 1);
-    aoff[0] = 0;
-    for (int y = 0; y < nv; ++y) aoff[y + 1] = aoff[y] + N_v[ord[y]];
+    {  // exclusive scan of the chain lengths in launch order, over fixed chunks
+      constexpr int kCh = 128;
+      thread_local std::vector<int64_t> cs_tl;  // lambdas below see it through the reference
+      std::vector<int64_t>& cs = cs_tl;
+      cs.resize(kCh + 1);
+      auto clo = [&](int ch) { return (int)((int64_t)ch * nv / kCh); };
+      auto sum = [&](int ch) {
+        int64_t a = 0;
+        for (int y = clo(ch); y < clo(ch + 1); ++y) a += N_v[ord[y]];
+        cs[ch + 1] = a;
+      };
+      auto fill = [&](int ch) {
+        int64_t a = cs[ch];
+        for (int y = clo(ch); y < clo(ch + 1); ++y) { aoff[y] = a; a += N_v[ord[y]]; }
+      };
+      const bool par = nv >= 4096;
+      if (par) HostPool::get().run(kCh, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) sum(ch); });
+      else for (int ch = 0; ch < kCh; ++ch) sum(ch);
+      cs[0] = 0;
+      for (int ch = 0; ch < kCh; ++ch) cs[ch + 1] += cs[ch];
+      if (par) HostPool::get().run(kCh, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) fill(ch); });
+      else for (int ch = 0; ch < kCh; ++ch) fill(ch);
+      aoff[nv] = cs[kCh];
+    }
     for (int p = 0; p <= P; ++p) ws.atask_lo[p] = (int)aoff[ws.part_lo[p]];
     for (int p = 0; p < P; ++p) ws.atask_big[p] = (int)aoff[ws.big_hi[p]];
     HostPool::get().run(nv, [&](int lo, int hi) {
