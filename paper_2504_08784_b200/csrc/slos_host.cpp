@@ -161,9 +161,11 @@ class HostPool {
   // time spent in run() and the number of runs (SLOS_HOST_TIMING breakdowns)
   double run_ms = 0.0;
   int runs = 0;
-  void run(int n, const std::function<void(int, int)>& fn) {
+  // min_grain: fewest items per piece (16 for cheap items; 1 for items heavy enough
+  // that even a few of them are worth every core, e.g. 2,000-decoder instances)
+  void run(int n, const std::function<void(int, int)>& fn, int min_grain = 16) {
     const int T = (int)workers_.size() + 1;
-    if (n < 64 || T == 1) { fn(0, n); return; }
+    if (n < (min_grain < 16 ? 2 : 64) || T == 1) { fn(0, n); return; }
     struct Tm {
       HostPool* h;
       std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
@@ -177,7 +179,7 @@ class HostPool {
     next_.store(0, std::memory_order_relaxed);
     // chunks: ~8 per thread, at least 16 items (one shared counter: small chunks of
     // cheap items would serialise on it)
-    grain_ = std::max(16, n / (8 * T));
+    grain_ = std::max(std::max(1, min_grain), n / (8 * T));
     busy_.store((int)workers_.size(), std::memory_order_relaxed);
     {
       std::lock_guard<std::mutex> l(mu_);
@@ -711,6 +713,14 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   double S_need = 16;
   const auto t_a = std::chrono::steady_clock::now();
   if (host_timing()) { HostPool::get().runs = 0; HostPool::get().run_ms = 0.0; }
+  // instances with hundreds of requests each: per-instance pieces, so a batch of a few
+  // dozen (C4: 64 x 2,048 requests) still spreads over every core
+  int grain = 16;
+  if (n < 1024) {
+    int64_t reqs = 0;
+    for (int q = 0; q < n; ++q) reqs += (int64_t)inputs[jobs[q].k].n_running + inputs[jobs[q].k].n_pending;
+    if (reqs >= 256 * (int64_t)n) grain = 1;
+  }
   HostPool::get().run(n, [&](int lo, int hi) {
     for (int q = lo; q < hi; ++q) {
       const int k = jobs[q].k;
@@ -718,7 +728,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       pr.status = prep_instance(planners[k], &inputs[k], unit_value, pr);
       if (pr.status == SLOS_OK) caps[q] = estimate_caps(planners[k], &inputs[k], pr, jobs[q].grow);
     }
-  });
+  }, grain);
   const auto t_a1 = std::chrono::steady_clock::now();
   // Totals over the valid instances: fixed chunks reduced in parallel and folded in
   // chunk order, so the valid list, the planner order (first appearance) and the
@@ -1180,7 +1190,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     for (int x = pr.N - 1; x >= 0; --x) h_sf[oC + x] = h_sf[oC + x + 1] + h_pf[oC + x];
     cost[v] = (double)(pr.n_dec + 8) * (double)(pr.N + 1) * (double)(pr.N + 1);
   }
-  });
+  }, grain);
   const auto t_d = std::chrono::steady_clock::now();
   auto t_d1 = t_d, t_d2 = t_d;
   int32_t* h_order = (int32_t*)hp(Ly.order);
@@ -1195,7 +1205,6 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
     } else {
       constexpr int kB = 64;
-      int cnt[kB + 1] = {0};
       thread_local std::vector<uint8_t> key_tl;
       std::vector<uint8_t>& key = key_tl;
       key.resize((size_t)nv);
@@ -1207,7 +1216,6 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       });
       // stable counting sort over fixed chunks: per-chunk histograms in parallel,
       // positions by (bucket, chunk), scatter in parallel (each chunk in order)
-      (void)cnt;
       constexpr int kCh = 128;
       thread_local std::vector<std::array<int, kB>> hist_tl;  // lambdas below see it through the reference
       std::vector<std::array<int, kB>>& hist = hist_tl;
