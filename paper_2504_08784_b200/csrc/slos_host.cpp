@@ -716,7 +716,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   // instances with hundreds of requests each: per-instance pieces, so a batch of a few
   // dozen (C4: 64 x 2,048 requests) still spreads over every core
   int grain = 16;
-  if (n < 1024) {
+  if (n < 256) {  // (larger batches already make >= 16 pieces of 16)
     int64_t reqs = 0;
     for (int q = 0; q < n; ++q) reqs += (int64_t)inputs[jobs[q].k].n_running + inputs[jobs[q].k].n_pending;
     if (reqs >= 256 * (int64_t)n) grain = 1;
