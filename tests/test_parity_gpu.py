@@ -289,3 +289,15 @@ def test_invalid_instances_inside_a_pipelined_batch():
             assert got["status"] == abi.SLOS_ERR_INVALID_PARAMETERS, (k, got["status"])
         else:
             _cmp(got, G["ref"][k % base.n], f"c5 ar tiled instance {k}")
+
+
+def test_forced_three_chunk_pipeline_matches_reference():
+    """Small batches through three forced pipeline chunks (tests/gpu_forced_chunks.py,
+    its own process: the chunk count is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(abi.ROOT, "tests", "gpu_forced_chunks.py")],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "C2 12 mismatches []" in r.stdout and "forced chunks done" in r.stdout, r.stdout[-2000:]
