@@ -672,6 +672,9 @@ struct Workspace {
   // per-part collection (plan_all): each part's headers are copied on its stream
   // right after its reconstruction, so its compaction and D2H overlap later parts
   bool part_collect = false;
+  // default records of every input (slos_workspace_records): uploaded only for the
+  // workspace API; slos_plan_batch's pipeline and regrowth rounds do not read them
+  bool records = true;
   std::vector<int32_t> ord;  // instance order: part p = ord[part_lo[p] .. part_lo[p+1])
   PinBuf h_hdr[kMaxParts], h_offs[kMaxParts];
   DevBuf d_packp[kMaxParts];
@@ -882,8 +885,8 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
   Ly.pre_idx = bi.add<int32_t>(TP);
   Ly.pre_left = bi.add<int64_t>(TP);
   Ly.run_tier = bi.add<int32_t>(TR);
-  Ly.recdef = bi.add<slos_record>(n);
-  Ly.recmap = bi.add<int32_t>(nv);
+  Ly.recdef = ws.records ? bi.add<slos_record>(n) : 0;
+  Ly.recmap = ws.records ? bi.add<int32_t>(nv) : 0;
   Ly.in_bytes = bi.bytes;
   Blob bs;
   Ly.s_counts = bs.add<uint64_t>(TS);
@@ -1336,7 +1339,7 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     });
     Ly.n_atask = aoff[nv];
   }
-  {
+  if (ws.records) {
     slos_record* rd = (slos_record*)hp(Ly.recdef);
     HostPool::get().run(n, [&](int lo, int hi) {
       std::memset(rd + lo, 0, sizeof(slos_record) * (size_t)(hi - lo));
@@ -2152,6 +2155,7 @@ int solve_rounds(Ctx& c, Workspace& ws, slos_planner* const* planners, const slo
                  int32_t unit_value, slos_result* outs, cudaStream_t stream, std::vector<Job> jobs) {
   std::vector<Job> retry;
   ws.part_collect = part_collect_enabled();
+  ws.records = false;
   for (int round = 0; round < 8 && !jobs.empty(); ++round) {
     retry.clear();
     int r = ws_upload(c, ws, planners, inputs, unit_value, jobs, outs, stream);
@@ -2297,6 +2301,7 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
         Workspace& w = pipe_ws(i % kPipeWs);
         cudaStreamWaitEvent(w.own_stream, ev0, 0);
         w.part_collect = part_collect_enabled();
+        w.records = false;
         int r = ws_upload(c, w, planners, inputs, unit_value, chunk[i], outs, w.own_stream);
         if (r == SLOS_OK) r = ws_solve(w, w.own_stream);
         if (r != SLOS_OK) return fail(r);
@@ -2426,7 +2431,7 @@ int slos_workspace_records(slos_workspace* b, slos_record* out, void* stream) {
   Ctx& c = ctx();
   std::lock_guard<std::mutex> g(c.mu);
   Workspace& ws = b->ws;
-  if (!ws.uploaded) return set_err(SLOS_ERR_INVALID_PARAMETERS, "nothing uploaded");
+  if (!ws.uploaded || !ws.records) return set_err(SLOS_ERR_INVALID_PARAMETERS, "nothing uploaded");
   const cudaStream_t s = stream ? (cudaStream_t)stream : ws.stream;
   unsigned char* DI = (unsigned char*)ws.d_in.p;
   cudaError_t e = cudaMemcpyAsync(out, DI + ws.Ly.recdef, sizeof(slos_record) * (size_t)ws.n_total,
