@@ -1753,6 +1753,7 @@ void print_phase_debug(Workspace& ws, const std::vector<OutHdr>& hdr) {
 // fills the slos_result of each instance (the caller synchronises `s`).
 int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h, const int32_t* vlist_d, int n,
                 PinBuf& h_offs, DevBuf& d_pack, cudaStream_t s, slos_result* outs, std::vector<Job>& retry) {
+  const auto tcs = std::chrono::steady_clock::now();
   const std::vector<int>& valid = ws.valid;
   const std::vector<Job>& jobs = ws.jobs;
   const BatchArgs& A = ws.A;
@@ -1762,9 +1763,9 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
   std::vector<int64_t>& boff = boff_tl;  // the pool's lambdas see them through these references
   std::vector<int64_t>& eoff = eoff_tl;
   std::vector<int64_t>& ioff = ioff_tl;
-  boff.assign((size_t)n, 0);
-  eoff.assign((size_t)n, 0);
-  ioff.assign((size_t)n, 0);
+  boff.resize((size_t)n);  // every entry is written below (0 for unplanned instances)
+  eoff.resize((size_t)n);
+  ioff.resize((size_t)n);
   // packed layout per planned instance, from a 16-byte aligned start: batches,
   // entries, ids, each 16-byte aligned; the next instance starts at the next 16-byte
   // boundary. Chunk-local offsets in parallel, chunk bases folded in order.
@@ -1784,6 +1785,7 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
       const int v = vof(x);
       const int q = valid[v];
       const OutHdr& h = hdr[v];
+      boff[x] = eoff[x] = ioff[x] = 0;
       if (h.status == SLOS_ERR_CAPACITY && jobs[q].grow < 6) {
         r.retry.push_back({jobs[q].k, jobs[q].grow + 1});
         continue;
@@ -1827,6 +1829,7 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
         }
       }
     });
+  const auto tc0 = std::chrono::steady_clock::now();
   ResultArena* ra = nullptr;
   if (good) {
     const size_t offs_bytes = sizeof(int64_t) * 3 * (size_t)n;
@@ -1858,6 +1861,7 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
     g_d2h += (int64_t)packed;
     g_h2d += (int64_t)offs_bytes;
   }
+  const auto tc1 = std::chrono::steady_clock::now();
   if (ra) ra->refs += good;  // one reference per result that points into the arena
   HostPool::get().run(n, [&](int lo, int hi) {
   for (int x = lo; x < hi; ++x) {
@@ -1892,6 +1896,13 @@ int collect_set(Ctx& c, Workspace& ws, const OutHdr* hdr, const int32_t* vlist_h
     r.owner_ = ra;
   }
   });
+  if (host_timing()) {
+    auto ms = [](std::chrono::steady_clock::time_point x, std::chrono::steady_clock::time_point y) {
+      return std::chrono::duration<double, std::milli>(y - x).count();
+    };
+    std::fprintf(stderr, "[slos collect_set] n %d: offsets %.3f, copies+compaction %.3f, results %.3f ms\n", n,
+                 ms(tcs, tc0), ms(tc0, tc1), ms(tc1, std::chrono::steady_clock::now()));
+  }
   return SLOS_OK;
 }
 
