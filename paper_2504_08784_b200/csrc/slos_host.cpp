@@ -2110,7 +2110,7 @@ Workspace& pipe_ws(int k) {
   return *w[k];
 }
 
-int pipeline_chunks(int n) {
+int pipeline_chunks(int n, double reqs_per_instance) {
   static const int env = [] {
     const char* e = std::getenv("SLOS_PIPELINE_CHUNKS");
     return e ? std::atoi(e) : 0;
@@ -2120,7 +2120,12 @@ int pipeline_chunks(int n) {
   // instances, host-preparation-bound; collection split around the next chunk's
   // preparation): 3 chunks 7.05-7.18 ms, 4: 7.25-7.33, 5: 7.4-7.5, 6: 7.7, 8: 8.3-8.6
   if (n < 512) return 1;
-  return n < 40000 ? 2 : std::min(8, n / 20000);
+  if (n < 40000) return 2;
+  // Three workspaces are live at once: chunks of instances with many requests (device
+  // scratch grows with them: ~2 MB per C2 instance) stay at <= 10,923 instances so
+  // the pipeline's footprint is no larger than two 16k-instance workspaces were.
+  if (reqs_per_instance >= 64.0) return std::min(16, (n + 10922) / 10923);
+  return std::min(8, n / 20000);
 }
 
 bool part_collect_enabled() {  // SLOS_PART_COLLECT=0: one collection per workspace
@@ -2260,7 +2265,12 @@ int plan_all(Ctx& c, Workspace& ws, slos_planner* const* planners, int32_t n, co
     }
   }
   n = (int32_t)jobs.size();
-  const int K = pipeline_chunks(n);
+  double reqs = 0.0;  // mean requests per instance (chunk sizing)
+  if (n >= 40000) {
+    for (int k = 0; k < n; ++k) reqs += (double)inputs[jobs[k].k].n_running + inputs[jobs[k].k].n_pending;
+    reqs /= n;
+  }
+  const int K = pipeline_chunks(n, reqs);
   if (K > 1) {
     // order after the caller's prior work on `stream`
     static cudaEvent_t ev0 = nullptr;
