@@ -1211,12 +1211,6 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
       thread_local std::vector<uint8_t> key_tl;
       std::vector<uint8_t>& key = key_tl;
       key.resize((size_t)nv);
-      HostPool::get().run(nv, [&](int lo, int hi) {
-        for (int v = lo; v < hi; ++v) {
-          const int e = std::min(kB - 1, std::max(0, std::ilogb(std::max(1.0, cost[v]))));
-          key[v] = (uint8_t)(kB - 1 - e);
-        }
-      });
       // stable counting sort over fixed chunks: per-chunk histograms in parallel,
       // positions by (bucket, chunk), scatter in parallel (each chunk in order)
       constexpr int kCh = 128;
@@ -1228,7 +1222,11 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
         for (int ch = c0; ch < c1; ++ch) {
           std::array<int, kB>& h = hist[ch];
           h.fill(0);
-          for (int v = clo(ch); v < clo(ch + 1); ++v) ++h[key[v]];
+          for (int v = clo(ch); v < clo(ch + 1); ++v) {
+            const int e = std::min(kB - 1, std::max(0, std::ilogb(std::max(1.0, cost[v]))));
+            key[v] = (uint8_t)(kB - 1 - e);
+            ++h[key[v]];
+          }
         }
       });
       int run = 0;
@@ -1269,9 +1267,15 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
         while (y < x && cost[ord[y]] >= big_thr) ++y;
       ws.big_hi[p] = y;
     }
+    // chain lengths per chunk of the order (the anchor-task scan below), summed in the
+    // same pass as the queue sizes
+    constexpr int kOrdCh = 128;
+    thread_local std::vector<int64_t> cs_tl;  // lambdas below see it through the reference
+    std::vector<int64_t>& cs = cs_tl;
+    cs.resize(kOrdCh + 1);
     {  // queue sizes (per part and reconstruction kind) and each instance's part, over
        // fixed chunks of the order in parallel
-      constexpr int kCh = 128;
+      constexpr int kCh = kOrdCh;
       thread_local std::vector<std::array<int, kQueues>> qc_tl;  // lambdas below see it through the reference
       std::vector<std::array<int, kQueues>>& qc = qc_tl;
       qc.resize(kCh);
@@ -1280,11 +1284,15 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
         std::array<int, kQueues>& c = qc[ch];
         c.fill(0);
         int p = 0;
+        int64_t a = 0;
         for (int x = clo(ch); x < clo(ch + 1); ++x) {
           while (x >= ws.part_lo[p + 1]) ++p;
-          hI[ord[x]].part = p;
-          ++c[kBuildKinds * p + kind_v[ord[x]]];
+          const int v = ord[x];
+          hI[v].part = p;
+          ++c[kBuildKinds * p + kind_v[v]];
+          a += N_v[v];
         }
+        cs[ch + 1] = a;
       };
       if (nv < 4096) { for (int ch = 0; ch < kCh; ++ch) body(ch); }
       else HostPool::get().run(kCh, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) body(ch); });
@@ -1304,39 +1312,26 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     thread_local std::vector<int64_t> aoff_tl;  // lambdas below see it through the reference
     std::vector<int64_t>& aoff = aoff_tl;  // first task of the instance at order position y
     aoff.resize((size_t)nv + 1);
-    {  // exclusive scan of the chain lengths in launch order, over fixed chunks
-      constexpr int kCh = 128;
-      thread_local std::vector<int64_t> cs_tl;  // lambdas below see it through the reference
-      std::vector<int64_t>& cs = cs_tl;
-      cs.resize(kCh + 1);
+    {  // exclusive scan of the chain lengths in launch order (chunk sums from the pass
+       // above), each chunk then writing its offsets and its anchor tasks
+      constexpr int kCh = kOrdCh;
       auto clo = [&](int ch) { return (int)((int64_t)ch * nv / kCh); };
-      auto sum = [&](int ch) {
-        int64_t a = 0;
-        for (int y = clo(ch); y < clo(ch + 1); ++y) a += N_v[ord[y]];
-        cs[ch + 1] = a;
-      };
       auto fill = [&](int ch) {
         int64_t a = cs[ch];
-        for (int y = clo(ch); y < clo(ch + 1); ++y) { aoff[y] = a; a += N_v[ord[y]]; }
+        for (int y = clo(ch); y < clo(ch + 1); ++y) {
+          const int v = ord[y];
+          aoff[y] = a;
+          for (int j = -1; j < N_v[v] - 1; ++j, ++a) { t[2 * a] = v; t[2 * a + 1] = j; }
+        }
       };
-      const bool par = nv >= 4096;
-      if (par) HostPool::get().run(kCh, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) sum(ch); });
-      else for (int ch = 0; ch < kCh; ++ch) sum(ch);
       cs[0] = 0;
       for (int ch = 0; ch < kCh; ++ch) cs[ch + 1] += cs[ch];
-      if (par) HostPool::get().run(kCh, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) fill(ch); });
+      if (nv >= 4096) HostPool::get().run(kCh, [&](int c0, int c1) { for (int ch = c0; ch < c1; ++ch) fill(ch); });
       else for (int ch = 0; ch < kCh; ++ch) fill(ch);
       aoff[nv] = cs[kCh];
     }
     for (int p = 0; p <= P; ++p) ws.atask_lo[p] = (int)aoff[ws.part_lo[p]];
     for (int p = 0; p < P; ++p) ws.atask_big[p] = (int)aoff[ws.big_hi[p]];
-    HostPool::get().run(nv, [&](int lo, int hi) {
-      for (int y = lo; y < hi; ++y) {
-        const int v = ord[y];
-        int64_t x = aoff[y];
-        for (int j = -1; j < N_v[v] - 1; ++j, ++x) { t[2 * x] = v; t[2 * x + 1] = j; }
-      }
-    });
     Ly.n_atask = aoff[nv];
   }
   if (ws.records) {
