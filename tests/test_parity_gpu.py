@@ -301,3 +301,27 @@ def test_forced_three_chunk_pipeline_matches_reference():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "C2 12 mismatches []" in r.stdout and "forced chunks done" in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("n", [511, 512, 513, 39999, 40000, 40001])
+def test_c5_batch_sizes_around_the_pipeline_chunk_thresholds(n):
+    """Batch sizes at the chunk-count thresholds of the end-to-end pipeline (1 -> 2
+    chunks at 512, 2 -> n / 20k chunks at 40,000): every instance matches the reference."""
+    import gzip
+    import json
+    import os
+    from golden_checks import _cmp
+    from paper_2504_08784_b200.planner import PerfTerm, PlannerConfig
+    GOLDEN = os.path.join(abi.ROOT, "tests", "golden")
+    meta = json.load(gzip.open(os.path.join(GOLDEN, "c5.json.gz"), "rt"))
+    G = meta["groups"]["ar"]
+    base = W.load_corpus(os.path.join(GOLDEN, "c5_ar.bin.gz"))
+    b = base.tiled((n + base.n - 1) // base.n).subset(range(n))
+    prod = abi.product()
+    cfg = PlannerConfig(max_chunk_tokens=2048, max_batch_tokens=16384, speculative=G["speculative"],
+                        spec_alpha=0.8, spec_max_len=8, plan_margin=0.0)
+    h = _Handle(prod, [PerfTerm(*t) for t in meta["model"]], W.TWO_TIER_SLO, cfg)
+    res = plan_many(prod, h.ptr, b)
+    assert len(res) == n
+    for k, got in enumerate(res):
+        _cmp(got, G["ref"][k % base.n], f"c5 ar batch of {n}, instance {k}")
