@@ -325,3 +325,29 @@ def test_c5_batch_sizes_around_the_pipeline_chunk_thresholds(n):
     assert len(res) == n
     for k, got in enumerate(res):
         _cmp(got, G["ref"][k % base.n], f"c5 ar batch of {n}, instance {k}")
+
+
+def test_large_heavy_batch_equals_small_batches():
+    """43,690 C2 instances (64 seeds repeated) in one slos_plan_batch: the heavy-instance
+    chunking (four chunks of <= 10,923 over three rotating workspaces) returns, for every
+    sampled instance, exactly the plan the same input gets in a 64-instance batch (itself
+    pinned to the reference by the tests above)."""
+    import ctypes as C
+    from parity import canon_c
+    F = W.FAMILIES["C2"]
+    n = 43690
+    prod = abi.product()
+    h = _Handle(prod, F["model"], W.TWO_TIER_SLO, F["cfg"])
+    small = plan_many(prod, h.ptr, W.InstanceBatch.stress(F["spec"], range(64)))
+    b = W.InstanceBatch.stress(F["spec"], range(64)).tiled((n + 63) // 64).subset(range(n))
+    hs = (C.c_void_p * n)(*([h.ptr] * n))
+    outs = (abi.Result * n)()
+    assert prod.slos_plan_batch(hs, n, C.c_void_p(b.inputs_ptr()), 0, outs, None) == abi.SLOS_OK
+    try:
+        assert all(outs[k].status == abi.SLOS_OK for k in range(n))
+        for k in range(0, n, 97):
+            d = diff(canon_c(outs[k]), small[k % 64], counters=True)
+            assert not d, (k, d)
+    finally:
+        for k in range(n):
+            prod.slos_result_free(C.byref(outs[k]))
