@@ -675,6 +675,7 @@ struct Workspace {
   // default records of every input (slos_workspace_records): uploaded only for the
   // workspace API; slos_plan_batch's pipeline and regrowth rounds do not read them
   bool records = true;
+  int prio_shift = 0;  // pipeline workspaces after the first: streams this much lower
   std::vector<int32_t> ord;  // instance order: part p = ord[part_lo[p] .. part_lo[p+1])
   PinBuf h_hdr[kMaxParts], h_offs[kMaxParts];
   DevBuf d_packp[kMaxParts];
@@ -1571,11 +1572,12 @@ int ws_solve(Workspace& ws, cudaStream_t stream) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     // (SLOS_ANCHOR_PRIO_LOW: anchor/group kernels below the parts' DP and reconstruction)
-    cudaStreamCreateWithPriority(&ws.astream, cudaStreamNonBlocking, std::getenv("SLOS_ANCHOR_PRIO_LOW") ? lo : hi);
+    cudaStreamCreateWithPriority(&ws.astream, cudaStreamNonBlocking,
+                                 std::getenv("SLOS_ANCHOR_PRIO_LOW") ? lo : std::min(lo, hi + ws.prio_shift));
     static const bool rev = std::getenv("SLOS_PART_PRIO_REV") != nullptr;
     for (int p = 0; p < kMaxParts; ++p) {
       cudaStreamCreateWithPriority(&ws.pstream[p], cudaStreamNonBlocking,
-                                   rev ? std::max(hi + 1, lo - p) : std::min(lo, hi + 1 + p));
+                                   rev ? std::max(hi + 1, lo - p) : std::min(lo, hi + 1 + p + ws.prio_shift));
       cudaEventCreate(&ws.ev_bend[p]);
       cudaEventCreate(&ws.ev_dp[p]);
       cudaEventCreate(&ws.ev_anc[p]);
@@ -2096,6 +2098,10 @@ Workspace& pipe_ws(int k) {
   static Workspace* w[kPipeWs] = {nullptr, nullptr, nullptr};
   if (!w[k]) {
     w[k] = new Workspace();
+    {  // SLOS_CHUNK_PRIO=n: later chunks' kernel streams n priority levels lower
+      const char* e = std::getenv("SLOS_CHUNK_PRIO");
+      w[k]->prio_shift = (e && k > 0) ? std::atoi(e) : 0;
+    }
     // the earlier chunk runs at higher priority so its D2H starts while the next
     // chunk's kernels still run
     int lo = 0, hi = 0;
