@@ -1257,15 +1257,24 @@ int ws_upload(Ctx& c, Workspace& ws, slos_planner* const* planners, const slos_i
     for (int p = 0; p <= P; ++p) ws.part_lo[p] = (int)((int64_t)p * nv / P);
     // the small instances are a suffix of each part (cost-descending order; the
     // bucketed order keys on ilogb(cost) and kSmallCost is a power of two)
+    // (cost is non-increasing along the order at power-of-two thresholds, so both
+    // boundaries are partition points: binary searches instead of scans of the part)
+    auto first_where = [&](int lo, int hi, auto pred) {  // first x in [lo, hi) with pred(x), else hi
+      while (lo < hi) {
+        const int mid = lo + (hi - lo) / 2;
+        if (pred(mid)) hi = mid; else lo = mid + 1;
+      }
+      return lo;
+    };
     for (int p = 0; p < P; ++p) {
       int x = ws.part_lo[p + 1];
       if (dp_small_enabled())
-        while (x > ws.part_lo[p] && cost[ord[x - 1]] < kSmallCost) --x;
+        x = first_where(ws.part_lo[p], x, [&](int z) { return cost[ord[z]] < kSmallCost; });
       ws.small_lo[p] = x;
       int y = ws.part_lo[p];
       const double big_thr = latency_batch(nv) ? 0.0 : dp_big_cost();
       if (big_thr > 0 || latency_batch(nv))
-        while (y < x && cost[ord[y]] >= big_thr) ++y;
+        y = first_where(y, x, [&](int z) { return !(cost[ord[z]] >= big_thr); });
       ws.big_hi[p] = y;
     }
     // chain lengths per chunk of the order (the anchor-task scan below), summed in the
